@@ -1,0 +1,186 @@
+/* sparselex_b200.h — C-ABI of the B200-native eager sparse BM25 path.
+ *
+ * The reference (paths relative to its root) has no index/retrieval code, only the
+ * SPEC's C++ operations plus proj/include/sparselex/bm25.hpp. Each entry point
+ * below replaces one of those operations for token-id input:
+ *
+ *   sl_index_build      <- build_index(corpus, BM25Params, TokenizerConfig)  SPEC.md [MODULE] index
+ *                          (token ids instead of text; pass 1/2 on the GPU; DF + length
+ *                          all-reduce over NCCL when a communicator is given)
+ *   sl_index_export     <- the ScoreMatrix / SearchIndex fields                SPEC.md [MODULE] index
+ *                          (indptr.bin u64, docids.bin u32, values.bin f32, df.bin u32,
+ *                          theta.bin f32, doclens.bin u32 of "External Interfaces")
+ *   sl_retrieve_batch   <- retrieve_batch(index, queries, k, ordered, workers) SPEC.md [MODULE] retrieval
+ *                          = score_query + top_k per query, k x G candidates merged on rank 0
+ *   sl_score_query      <- score_query(index, query) -> dense |C| vector       SPEC.md [MODULE] retrieval
+ *   sl_top_k            <- top_k(scores, k, ordered)                           SPEC.md [MODULE] retrieval
+ *   sl_params_validate  <- BM25Params::validate                                proj/src/scoring.cpp:47-58
+ *   sl_index_destroy / sl_last_error : ownership + error plumbing (the reference throws
+ *                          std::invalid_argument with fixed messages, scoring.cpp:15-138;
+ *                          here a status code + thread-local message).
+ *
+ * Conventions: plain pointers and sizes only. `mem` says whether caller buffers live
+ * in host memory (SL_MEM_HOST: the call copies in/out) or on the index's device
+ * (SL_MEM_DEVICE). The index owns all device memory; inputs are borrowed for the
+ * duration of the call. Built indexes are immutable and safe for concurrent
+ * sl_retrieve_batch calls (each call uses its own scratch and stream).
+ * Variant numbering follows proj/include/sparselex/bm25.hpp:16-23.
+ * There is no CPU fallback: every compute entry point runs CUDA kernels for sm_100a
+ * and fails with SL_ECUDA if no device is usable.
+ */
+#ifndef SPARSELEX_B200_H
+#define SPARSELEX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SL_ABI_VERSION 1
+
+typedef enum {
+  SL_OK = 0,
+  SL_EINVAL = 1,   /* contract violation (reference: std::invalid_argument) */
+  SL_ECUDA = 2,    /* CUDA runtime / launch failure or no device */
+  SL_ENCCL = 3,    /* NCCL failure */
+  SL_ENOMEM = 4,   /* device allocation failed */
+  SL_ECORRUPT = 5, /* structural invariant violated */
+  SL_EUNSUPPORTED = 6
+} sl_status;
+
+typedef enum {
+  SL_ROBERTSON = 0,
+  SL_ATIRE = 1,
+  SL_LUCENE = 2,
+  SL_BM25L = 3,
+  SL_BM25PLUS = 4,
+  SL_TFLDP = 5
+} sl_variant;
+
+typedef enum { SL_MEM_HOST = 0, SL_MEM_DEVICE = 1 } sl_mem;
+
+/* BM25Params (bm25.hpp:31-47). */
+typedef struct {
+  int32_t variant;
+  double k1;
+  double b;
+  double delta;
+} sl_params;
+
+typedef struct sl_index sl_index;
+typedef struct sl_comm sl_comm;
+
+/* One rank's shard of a document-sharded corpus. With comm == NULL the
+ * shard is the whole corpus. Documents are contiguous: this rank owns global doc ids
+ * [doc_base, doc_base + num_docs). */
+typedef struct {
+  const uint64_t* doc_offsets; /* [num_docs + 1], token offsets; doc_offsets[0] may be nonzero */
+  const uint32_t* token_ids;   /* token_ids[doc_offsets[0] .. doc_offsets[num_docs]) */
+  uint32_t num_docs;           /* local |C_r| */
+  uint32_t vocab_size;         /* |V| (global, identical on all ranks) */
+  uint32_t doc_base;           /* global id of local doc 0 */
+  int32_t mem;                 /* sl_mem of doc_offsets / token_ids */
+  sl_params params;
+  int32_t device;              /* CUDA device ordinal */
+  int32_t keep_tf;             /* keep per-nonzero tf for sl_index_export (debug/parity) */
+  float dense_min_density;     /* rows with global df >= density * N_global get a dense
+                                  query-side copy; <= 0 selects the default (0.25) */
+  sl_comm* comm;               /* NULL = single shard */
+} sl_build_desc;
+
+/* Index statistics (global unless marked local). */
+typedef struct {
+  uint32_t num_docs_local;
+  uint32_t num_docs_global;
+  uint32_t vocab_size;
+  uint32_t doc_base;
+  uint64_t nnz_local;
+  uint64_t total_len_global; /* Σ|D| */
+  double avg_len;            /* L_avg = Σ|D| / N */
+  uint32_t dense_rows;       /* rows with a dense query-side copy */
+  uint32_t skip_rows;        /* rows with a per-tile skip table */
+  uint32_t tile_docs;        /* docs per scoring tile */
+  uint32_t num_tiles;
+  uint64_t device_bytes;     /* device memory held by the index */
+  float build_ms;            /* device time of the last build (CUDA events) */
+} sl_index_info;
+
+int32_t sl_abi_version(void);
+const char* sl_last_error(void);
+const char* sl_status_string(int32_t status);
+
+int32_t sl_params_validate(const sl_params* p);
+double sl_default_delta(int32_t variant); /* bm25.hpp:37-39 / scoring.cpp:34-41 */
+
+/* Index build (SPEC build_index). Token ids must be < vocab_size; num_docs >= 1; the
+ * corpus must not be all-empty ("degenerate corpus"). */
+int32_t sl_index_build(const sl_build_desc* desc, sl_index** out);
+void sl_index_destroy(sl_index* index);
+int32_t sl_index_get_info(const sl_index* index, sl_index_info* info);
+
+/* Export any subset of the SearchIndex arrays (NULL = skip). Sizes: indptr V+1,
+ * docids/values/tf nnz_local, df/theta V, doclens num_docs_local. df is the GLOBAL
+ * document frequency; docids are LOCAL (add doc_base for global ids). tf requires
+ * keep_tf at build time. */
+int32_t sl_index_export(const sl_index* index, int32_t mem, uint64_t* indptr, uint32_t* docids,
+                        float* values, uint32_t* df, float* theta, uint32_t* doclens, uint32_t* tf);
+
+/* Batched retrieval (SPEC retrieve_batch): for each query b, the min(k, N_global) best
+ * documents by B(Q,D) = Σ S^Δ + Σ S^θ, score descending, ties -> smaller global doc id.
+ * Outputs are [num_queries x k]; slots beyond min(k, N) hold id 0xFFFFFFFF, score -inf.
+ * Query tokens with global df = 0 are dropped (SPEC OOV rule); ids >= |V| are an error.
+ * `ordered` is accepted for API parity; results are always sorted (a valid order for
+ * ordered == 0 as well). With a communicator, every rank passes the same queries and
+ * the merged result is written on rank 0 only (other ranks may pass NULL outputs). */
+int32_t sl_retrieve_batch(const sl_index* index, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                          uint32_t num_queries, uint32_t k, int32_t ordered, int32_t mem,
+                          uint32_t* out_ids, float* out_scores);
+
+/* Device-timed variant used by the bench harness: same as sl_retrieve_batch with
+ * mem == SL_MEM_DEVICE, and reports the device time of the scoring kernel and the whole
+ * call (CUDA events on the call's stream) plus the algorithmic posting bytes read. */
+typedef struct {
+  float total_ms;
+  float score_kernel_ms;
+  float merge_ms;
+  uint64_t posting_bytes;   /* Σ_q Σ_{t in q} 8 * nnz_local(t) */
+  uint64_t scorevec_bytes;  /* Σ_q 4 * N_local */
+  uint64_t unique_posting_bytes; /* 8 * Σ_{t in union of batch} nnz_local(t) */
+  uint32_t kernels_launched;
+} sl_retrieve_stats;
+
+int32_t sl_retrieve_batch_timed(const sl_index* index, const uint64_t* q_offsets,
+                                const uint32_t* q_tokens, uint32_t num_queries, uint32_t k,
+                                int32_t mem, uint32_t* out_ids, float* out_scores,
+                                sl_retrieve_stats* stats);
+
+/* Dense score vector of one query over the LOCAL shard (SPEC score_query; f32).
+ * out_scores has num_docs_local entries and includes the Σ S^θ constant. */
+int32_t sl_score_query(const sl_index* index, const uint32_t* q_tokens, uint32_t q_len, int32_t mem,
+                       float* out_scores);
+
+/* SPEC top_k over an arbitrary f32 vector (GPU radix select). Returns min(k, n) results,
+ * padded as in sl_retrieve_batch. */
+int32_t sl_top_k(const float* scores, uint32_t n, uint32_t k, int32_t ordered, int32_t mem,
+                 int32_t device, uint32_t* out_ids, float* out_scores);
+
+/* Multi-GPU (one process per GPU). The unique id (128 bytes) is created on rank 0 and
+ * shipped to every rank by the caller (any transport), then each rank joins. */
+int32_t sl_comm_unique_id(uint8_t out_id[128]);
+int32_t sl_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                     sl_comm** out);
+void sl_comm_destroy(sl_comm* comm);
+
+/* Synthetic corpus generation on the device (bench/test input only; bit-identical to
+ * the host generator in libsl_synth): token_ids[i] = Zipf token at global position
+ * begin + i, using the f64 CDF `cdf` (host or device per mem). */
+int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed, uint64_t begin,
+                               uint64_t count, int32_t cdf_mem, uint32_t* token_ids_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSELEX_B200_H */

@@ -1,0 +1,696 @@
+// sl_build.cu — index build on the device (SPEC.md [MODULE] index, build_index).
+//
+// Token ids arrive flat, doc-major (u32[T] + u64 offsets[N+1]). The reference's two
+// passes (pass 1: count_terms + DF + lengths, tokenizer.cpp:162-168 /
+// vocabulary.hpp:38; pass 2: S^Δ per nonzero, scoring.cpp:116-145) become:
+//   K1  doc expansion + stable LSD radix sort of (token, doc) by token   -> (t,d) order
+//   K1' run-length encoding of equal (t,d) runs -> tf, doc ids, indptr (row starts)
+//   K2  df = row lengths (+ NCCL all-reduce of df, Σ|D|, N across shards)
+//   K3  idf(t), S^θ(t) in f64 (scoring.cpp:60-79, 125-145)
+//   K4  values[p] = f32(idf * tf_component - S^θ)  (scoring.cpp:81-123)
+// followed by the query-side structures (dense copies of the highest-df rows and
+// per-tile skip offsets) that sl_query.cu consumes.
+// Everything is HBM-streaming integer work; no tensor cores are involved.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "sl_index.cuh"
+
+namespace sl {
+
+// ============================================================== scan (u32, exclusive)
+namespace {
+constexpr int kScanThreads = 256;
+constexpr int kScanIPT = 8;
+constexpr int kScanTile = kScanThreads * kScanIPT;
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// exclusive block scan; sw needs 33 entries
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sw, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t incl = warp_incl_scan(v);
+  if (lane == 31) sw[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = lane < nw ? sw[lane] : 0u;
+    const uint32_t xi = warp_incl_scan(x);
+    if (lane < nw) sw[lane] = xi - x;
+    if (lane == 31) sw[32] = xi;
+  }
+  __syncthreads();
+  const uint32_t r = sw[w] + incl - v;
+  if (total) *total = sw[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_reduce_tiles(const uint32_t* in, uint64_t n,
+                                                               uint32_t* sums) {
+  __shared__ uint32_t sw[33];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j) {
+    const uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
+    if (i < n) s += in[i];
+  }
+  uint32_t tot;
+  block_excl_scan(s, sw, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* in, uint32_t* out,
+                                                             uint64_t n, const uint32_t* offs) {
+  __shared__ uint32_t sw[33];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanIPT;
+  uint32_t v[kScanIPT];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j) {
+    const uint64_t i = base + j;
+    v[j] = i < n ? in[i] : 0u;
+    s += v[j];
+  }
+  uint32_t run = block_excl_scan(s, sw, nullptr) + (offs ? offs[blockIdx.x] : 0u);
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j) {
+    const uint64_t i = base + j;
+    if (i < n) out[i] = run;
+    run += v[j];
+  }
+}
+}  // namespace
+
+// in-place safe (each block reads its whole tile before writing it)
+int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st,
+                           uint32_t* total_host) {
+  if (n == 0) {
+    if (total_host) *total_host = 0;
+    return SL_OK;
+  }
+  uint32_t last_in = 0;
+  if (total_host) SL_CUDA_TRY(cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, st));
+  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb == 1) {
+    k_scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
+  } else {
+    uint32_t* sums = nullptr;
+    SL_CUDA_TRY(cudaMallocAsync(&sums, nb * 4, st));
+    k_reduce_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
+    SL_TRY(exclusive_scan_u32(sums, sums, nb, st, nullptr));
+    k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+    SL_CUDA_TRY(cudaFreeAsync(sums, st));
+  }
+  SL_CUDA_TRY(cudaGetLastError());
+  if (total_host) {
+    uint32_t last_out = 0;
+    SL_CUDA_TRY(cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    *total_host = last_out + last_in;
+  }
+  return SL_OK;
+}
+
+// ============================================================== build kernels
+namespace {
+
+constexpr uint32_t kErrOffsets = 1u, kErrToken = 2u, kErrDocLen = 4u;
+
+// doc id per token position (warp per document) + |D| (tokenizer.cpp:166)
+__global__ void k_doc_expand(const uint64_t* __restrict__ off, uint32_t N, uint64_t o0,
+                             uint32_t* __restrict__ docs, uint32_t* __restrict__ doclens,
+                             uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t d = gw; d < N; d += nw) {
+    const uint64_t b = off[d], e = off[d + 1];
+    if (e < b) {
+      if (lane == 0) atomicOr(err, kErrOffsets);
+      continue;
+    }
+    if (lane == 0) {
+      if (e - b > 0xFFFFFFFFull) atomicOr(err, kErrDocLen);
+      doclens[d] = (uint32_t)(e - b);
+    }
+    for (uint64_t i = b - o0 + lane; i < e - o0; i += 32) docs[i] = (uint32_t)d;
+  }
+}
+
+__global__ void k_check_tokens(const uint32_t* __restrict__ keys, uint64_t n, uint32_t V,
+                               uint32_t* err) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (keys[i] >= V) atomicOr(err, kErrToken);
+}
+
+constexpr int kSortThreads = 256;
+constexpr int kSortIPT = 16;
+constexpr int kSortTile = kSortThreads * kSortIPT;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// per-tile digit histogram (warp-aggregated with match.any), digit-major output
+__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __restrict__ keys,
+                                                             uint64_t n, int shift, uint32_t mask,
+                                                             uint32_t* __restrict__ hist,
+                                                             uint32_t n_tiles, uint32_t V,
+                                                             uint32_t* err) {
+  __shared__ uint32_t sh[256];
+  for (int i = threadIdx.x; i < 256; i += kSortThreads) sh[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+  bool bad = false;
+#pragma unroll 4
+  for (int j = 0; j < kSortIPT; ++j) {
+    const uint64_t i = base + (uint64_t)j * kSortThreads + threadIdx.x;
+    const bool valid = i < n;
+    uint32_t k = valid ? keys[i] : 0u;
+    bad |= valid && k >= V;
+    const uint32_t dg = valid ? ((k >> shift) & mask) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[dg], (uint32_t)__popc(peers));
+  }
+  if (err && bad) atomicOr(err, kErrToken);
+  __syncthreads();
+  for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) hist[(uint64_t)dg * n_tiles + blockIdx.x] = sh[dg];
+}
+
+// stable scatter: warp w owns a contiguous 32*IPT sub-tile; ranks via match.any
+__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
+    uint32_t n_tiles) {
+  constexpr int NW = kSortThreads / 32;
+  __shared__ uint32_t wc[NW][256];
+  for (int i = threadIdx.x; i < NW * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile + (uint64_t)w * 32 * kSortIPT;
+  const uint32_t lt = lanemask_lt();
+  uint32_t kk[kSortIPT], vv[kSortIPT], rr[kSortIPT];
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    const bool valid = i < n;
+    kk[j] = valid ? kin[i] : 0u;
+    vv[j] = valid ? vin[i] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    const bool valid = i < n;
+    const uint32_t dg = valid ? ((kk[j] >> shift) & mask) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t before = valid ? wc[w][dg] : 0u;
+    rr[j] = before + __popc(peers & lt);
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wc[w][dg] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) {
+    uint32_t run = offs[(uint64_t)dg * n_tiles + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) {
+      const uint32_t c = wc[ww][dg];
+      wc[ww][dg] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const uint64_t i = base + (uint64_t)j * 32 + lane;
+    if (i < n) {
+      const uint32_t dg = (kk[j] >> shift) & mask;
+      const uint32_t pos = wc[w][dg] + rr[j];
+      kout[pos] = kk[j];
+      vout[pos] = vv[j];
+    }
+  }
+}
+
+__device__ __forceinline__ bool run_head(const uint32_t* k, const uint32_t* v, uint64_t i) {
+  return i == 0 || k[i] != k[i - 1] || v[i] != v[i - 1];
+}
+
+__global__ void k_rle_flags(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v, uint64_t n,
+                            uint32_t* __restrict__ flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    flags[i] = run_head(k, v, i) ? 1u : 0u;
+}
+
+// one nonzero per (t,d) run: doc id, row id, run start; row starts fill indptr
+__global__ void k_rle_emit(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v,
+                           const uint32_t* __restrict__ pos, uint64_t n, uint64_t nnz, uint32_t V,
+                           uint32_t* __restrict__ docids, uint32_t* __restrict__ rows,
+                           uint32_t* __restrict__ runstart, uint64_t* __restrict__ indptr) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = k[i];
+    if (run_head(k, v, i)) {
+      const uint32_t p = pos[i];
+      docids[p] = v[i];
+      rows[p] = t;
+      runstart[p] = (uint32_t)i;
+      if (i == 0 || k[i - 1] != t) {
+        const int64_t prev = i == 0 ? -1 : (int64_t)k[i - 1];
+        for (int64_t x = prev + 1; x <= (int64_t)t; ++x) indptr[x] = p;
+      }
+    }
+    if (i == n - 1) {
+      for (uint64_t x = (uint64_t)t + 1; x <= V; ++x) indptr[x] = nnz;
+      runstart[nnz] = (uint32_t)n;
+    }
+  }
+}
+
+__global__ void k_tf(const uint32_t* __restrict__ runstart, uint64_t nnz, uint32_t* __restrict__ tf) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (uint64_t)gridDim.x * blockDim.x)
+    tf[p] = runstart[p + 1] - runstart[p];
+}
+
+__global__ void k_df_from_indptr(const uint64_t* __restrict__ indptr, uint32_t V, uint32_t* __restrict__ df) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x)
+    df[t] = (uint32_t)(indptr[t + 1] - indptr[t]);
+}
+
+// K3: idf and S^θ per token (df = 0 -> empty row, theta 0)
+__global__ void k_token_stats(const uint32_t* __restrict__ df, uint32_t V, uint32_t Ng, sl_params p,
+                              double* __restrict__ idf64, double* __restrict__ theta64,
+                              float* __restrict__ theta) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x) {
+    const uint32_t d = df[t];
+    double i = 0.0, th = 0.0;
+    if (d > 0) {
+      i = d_idf(p.variant, (double)Ng, (double)d);
+      if (!is_sparse_variant(p.variant)) th = d_nonoccurrence(p.variant, i, p.k1, p.delta);
+    }
+    idf64[t] = i;
+    theta64[t] = th;
+    theta[t] = (float)th;
+  }
+}
+
+// K4: S^Δ = idf * tf_component - S^θ in f64, narrowed to f32 (SPEC index pass 2)
+__global__ void k_values(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ docids,
+                         const uint32_t* __restrict__ tf, const uint32_t* __restrict__ doclens,
+                         const double* __restrict__ idf64, const double* __restrict__ theta64,
+                         uint64_t nnz, sl_params p, double avg, float* __restrict__ values) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = rows[i];
+    const double tfc = d_tf_component(p.variant, (double)tf[i], (double)doclens[docids[i]], avg, p.k1,
+                                      p.b, p.delta);
+    const double s = __dmul_rn(idf64[t], tfc);
+    values[i] = __double2float_rn(__dsub_rn(s, theta64[t]));
+  }
+}
+
+__global__ void k_dense_fill(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ docids,
+                             const float* __restrict__ values, const uint32_t* __restrict__ slot_tok,
+                             uint32_t n_slots, uint32_t n_pad, float* __restrict__ dense) {
+  for (uint32_t s = blockIdx.y; s < n_slots; s += gridDim.y) {
+    const uint32_t t = slot_tok[s];
+    const uint64_t b = indptr[t], e = indptr[t + 1];
+    float* row = dense + (uint64_t)s * n_pad;
+    for (uint64_t i = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e;
+         i += (uint64_t)gridDim.x * blockDim.x)
+      row[docids[i]] = values[i];
+  }
+}
+
+// skip[s][tile] = first row-relative posting with doc >= tile * kTileDocs
+__global__ void k_skip_fill(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ docids,
+                            const uint32_t* __restrict__ slot_tok, uint32_t n_slots, uint32_t n_tiles,
+                            uint32_t* __restrict__ skip) {
+  for (uint32_t s = blockIdx.y; s < n_slots; s += gridDim.y) {
+    const uint32_t t = slot_tok[s];
+    const uint64_t b = indptr[t];
+    const uint32_t len = (uint32_t)(indptr[t + 1] - b);
+    uint32_t* tab = skip + (uint64_t)s * (n_tiles + 1);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < len; j += gridDim.x * blockDim.x) {
+      const int64_t tile = docids[b + j] / kTileDocs;
+      const int64_t prev = j == 0 ? -1 : (int64_t)(docids[b + j - 1] / kTileDocs);
+      for (int64_t x = prev + 1; x <= tile; ++x) tab[x] = j;
+      if (j == len - 1)
+        for (int64_t x = tile + 1; x <= (int64_t)n_tiles; ++x) tab[x] = len;
+    }
+  }
+}
+
+int grid_for(uint64_t n, int threads, int max_blocks = 148 * 32) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > (uint64_t)max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+int32_t host_validate(const sl_params& p) {
+  if (p.variant < 0 || p.variant > 5) SL_FAIL(SL_EINVAL, "invalid Variant value");
+  if (!(p.k1 > 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: k1 must be > 0");
+  if (!(p.b >= 0.0 && p.b <= 1.0)) SL_FAIL(SL_EINVAL, "BM25Params: b must be in [0, 1]");
+  if (!(p.delta >= 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: delta must be >= 0");
+  if (p.variant == SL_TFLDP && !(p.delta > std::exp(-1.0)))
+    SL_FAIL(SL_EINVAL, "BM25Params: tfldp requires delta > exp(-1)");
+  return SL_OK;
+}
+
+// RAII set of stream-ordered temporaries
+struct Temps {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Temps(cudaStream_t s) : st(s) {}
+  template <class T>
+  int32_t alloc(T** p, uint64_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMallocAsync((void**)p, count * sizeof(T), st);
+    if (e != cudaSuccess) {
+      set_error(std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
+                " bytes failed: " + cudaGetErrorString(e));
+      return SL_ENOMEM;
+    }
+    ptrs.push_back(*p);
+    return SL_OK;
+  }
+  void release(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) {
+        cudaFreeAsync(q, st);
+        q = nullptr;
+      }
+  }
+  ~Temps() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, st);
+  }
+};
+
+}  // namespace
+
+int32_t nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return SL_OK;
+  set_error(std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+  return SL_ENCCL;
+}
+
+void free_index(sl_index* ix) {
+  if (!ix) return;
+  cudaSetDevice(ix->device);
+  void* ps[] = {ix->indptr, ix->docids, ix->values, ix->df_global, ix->theta,
+                ix->doclens, ix->tf, ix->tokinfo, ix->dense, ix->skiptab};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  delete ix;
+}
+
+namespace {
+template <class T>
+int32_t dalloc(sl_index* ix, T** p, uint64_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    set_error(std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
+              " bytes failed: " + cudaGetErrorString(e));
+    return SL_ENOMEM;
+  }
+  ix->device_bytes += count * sizeof(T);
+  return SL_OK;
+}
+
+int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
+  const uint32_t N = d->num_docs, V = d->vocab_size;
+  // ---- inputs on the device
+  uint64_t o0 = 0, oN = 0;
+  if (d->mem == SL_MEM_HOST) {
+    o0 = d->doc_offsets[0];
+    oN = d->doc_offsets[N];
+  } else {
+    SL_CUDA_TRY(cudaMemcpyAsync(&o0, d->doc_offsets, 8, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(&oN, d->doc_offsets + N, 8, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (oN < o0) SL_FAIL(SL_EINVAL, "build_index: doc offsets must be non-decreasing");
+  const uint64_t T = oN - o0;
+  if (T == 0) SL_FAIL(SL_EINVAL, "build_index: degenerate corpus (all documents empty)");
+  if (T >= 0xFFFFFFFFull)
+    SL_FAIL(SL_EUNSUPPORTED, "build_index: a shard must hold fewer than 2^32-1 tokens; shard further");
+
+  Temps tmp(st);
+  const uint64_t* off = d->doc_offsets;
+  const uint32_t* tokens = d->token_ids + o0;
+  if (d->mem == SL_MEM_HOST) {
+    uint64_t* doff;
+    uint32_t* dtok;
+    SL_TRY(tmp.alloc(&doff, (uint64_t)N + 1));
+    SL_TRY(tmp.alloc(&dtok, T));
+    SL_CUDA_TRY(cudaMemcpyAsync(doff, off, ((uint64_t)N + 1) * 8, cudaMemcpyHostToDevice, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(dtok, tokens, T * 4, cudaMemcpyHostToDevice, st));
+    off = doff;
+    tokens = dtok;
+  }
+
+  cudaEvent_t ev0, ev1;
+  SL_CUDA_TRY(cudaEventCreate(&ev0));
+  SL_CUDA_TRY(cudaEventCreate(&ev1));
+  SL_CUDA_TRY(cudaEventRecord(ev0, st));
+
+  uint32_t* err;
+  SL_TRY(tmp.alloc(&err, 1));
+  SL_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+
+  // ---- K1: doc expansion
+  uint32_t *docs, *kb0, *kb1, *vb1;
+  SL_TRY(tmp.alloc(&docs, T));
+  SL_TRY(dalloc(ix, &ix->doclens, N));
+  k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err);
+
+  // ---- K1: stable LSD radix sort of (token, doc) by token
+  int bits = 0;
+  while (bits < 32 && (V - 1) >> bits) ++bits;
+  const int passes = (bits + 7) / 8;
+  const uint32_t* ksorted = tokens;
+  const uint32_t* vsorted = docs;
+  if (passes == 0) {
+    k_check_tokens<<<grid_for(T, 256), 256, 0, st>>>(tokens, T, V, err);
+  } else {
+    const int width = (bits + passes - 1) / passes;
+    const uint32_t mask = (1u << width) - 1u;
+    const uint64_t n_tiles = (T + kSortTile - 1) / kSortTile;
+    if (n_tiles > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "build_index: too many sort tiles");
+    uint32_t* hist;
+    SL_TRY(tmp.alloc(&kb0, T));
+    SL_TRY(tmp.alloc(&kb1, T));
+    SL_TRY(tmp.alloc(&vb1, T));
+    SL_TRY(tmp.alloc(&hist, n_tiles * (uint64_t)(mask + 1)));
+    uint32_t* kbuf[2] = {kb0, kb1};
+    uint32_t* vbuf[2] = {vb1, docs};
+    const uint32_t* kin = tokens;
+    const uint32_t* vin = docs;
+    for (int p = 0; p < passes; ++p) {
+      const int shift = p * width;
+      uint32_t* kout = kbuf[p & 1];
+      uint32_t* vout = vbuf[p & 1];
+      k_radix_hist<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(kin, T, shift, mask, hist,
+                                                               (uint32_t)n_tiles, V,
+                                                               p == 0 ? err : nullptr);
+      SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
+      k_radix_scatter<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, T, shift, mask,
+                                                                  hist, (uint32_t)n_tiles);
+      kin = kout;
+      vin = vout;
+    }
+    ksorted = kin;
+    vsorted = vin;
+    tmp.release(hist);
+  }
+  SL_CUDA_TRY(cudaGetLastError());
+  uint32_t herr = 0;
+  SL_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  if (herr & kErrOffsets) SL_FAIL(SL_EINVAL, "build_index: doc offsets must be non-decreasing");
+  if (herr & kErrToken) SL_FAIL(SL_EINVAL, "build_index: token id >= vocab size");
+  if (herr & kErrDocLen) SL_FAIL(SL_EUNSUPPORTED, "build_index: document longer than 2^32-1 tokens");
+
+  // ---- K1': run-length encode (t,d) runs
+  uint32_t *flags, *pos;
+  SL_TRY(tmp.alloc(&flags, T));
+  SL_TRY(tmp.alloc(&pos, T));
+  k_rle_flags<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, T, flags);
+  uint32_t nnz32 = 0;
+  SL_TRY(exclusive_scan_u32(flags, pos, T, st, &nnz32));
+  const uint64_t nnz = nnz32;
+  ix->nnz = nnz;
+  uint32_t* rows = flags;  // flags are recomputed by the emit kernel; reuse the buffer
+  uint32_t* runstart;
+  SL_TRY(tmp.alloc(&runstart, nnz + 1));
+  SL_TRY(dalloc(ix, &ix->docids, nnz));
+  SL_TRY(dalloc(ix, &ix->indptr, (uint64_t)V + 1));
+  k_rle_emit<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, pos, T, nnz, V, ix->docids, rows,
+                                               runstart, ix->indptr);
+  uint32_t* tf;
+  if (d->keep_tf) {
+    SL_TRY(dalloc(ix, &ix->tf, nnz));
+    tf = ix->tf;
+  } else {
+    SL_TRY(tmp.alloc(&tf, nnz));
+  }
+  k_tf<<<grid_for(nnz, 256), 256, 0, st>>>(runstart, nnz, tf);
+  tmp.release(runstart);
+  tmp.release(pos);
+  if (passes > 0) {
+    tmp.release(kb0);
+    tmp.release(kb1);
+    tmp.release(vb1);
+  }
+  tmp.release(docs);
+
+  // ---- K2: df (global via NCCL), N, Σ|D|
+  SL_TRY(dalloc(ix, &ix->df_global, V));
+  k_df_from_indptr<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, ix->df_global);
+  uint64_t stats[2] = {T, N};
+  if (d->comm && d->comm->nranks > 1) {
+    uint64_t* dstats;
+    SL_TRY(tmp.alloc(&dstats, 2));
+    SL_CUDA_TRY(cudaMemcpyAsync(dstats, stats, 16, cudaMemcpyHostToDevice, st));
+    SL_TRY(nccl_check(nccl().AllReduce(ix->df_global, ix->df_global, V, ncclUint32, ncclSum, d->comm->comm, st),
+                      "ncclAllReduce(df)"));
+    SL_TRY(nccl_check(nccl().AllReduce(dstats, dstats, 2, ncclUint64, ncclSum, d->comm->comm, st),
+                      "ncclAllReduce(sum_len, N)"));
+    SL_CUDA_TRY(cudaMemcpyAsync(stats, dstats, 16, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (stats[1] > 0xFFFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "build_index: more than 2^32-1 documents");
+  ix->total_len = stats[0];
+  ix->N_global = (uint32_t)stats[1];
+  ix->avg_len = (double)stats[0] / (double)stats[1];  // SPEC L_avg = Σ|D| / N
+
+  // ---- K3 + K4
+  double *idf64, *theta64;
+  SL_TRY(tmp.alloc(&idf64, V));
+  SL_TRY(tmp.alloc(&theta64, V));
+  SL_TRY(dalloc(ix, &ix->theta, V));
+  k_token_stats<<<grid_for(V, 256), 256, 0, st>>>(ix->df_global, V, ix->N_global, d->params, idf64, theta64,
+                                                 ix->theta);
+  SL_TRY(dalloc(ix, &ix->values, nnz));
+  k_values<<<grid_for(nnz, 256), 256, 0, st>>>(rows, ix->docids, tf, ix->doclens, idf64, theta64, nnz,
+                                               d->params, ix->avg_len, ix->values);
+  SL_CUDA_TRY(cudaGetLastError());
+
+  // ---- query-side structures: dense copies of high-df rows, per-tile skip offsets
+  ix->num_tiles = (N + kTileDocs - 1) / kTileDocs;
+  ix->n_pad = ix->num_tiles * kTileDocs;
+  std::vector<uint32_t> h_df(V);
+  std::vector<uint64_t> h_ptr((size_t)V + 1);
+  SL_CUDA_TRY(cudaMemcpyAsync(h_df.data(), ix->df_global, (uint64_t)V * 4, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaMemcpyAsync(h_ptr.data(), ix->indptr, ((uint64_t)V + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  const double density = d->dense_min_density > 0.f ? (double)d->dense_min_density : 0.25;
+  const double dense_thr = density * (double)ix->N_global;
+  const uint64_t skip_thr = 32ull * ix->num_tiles;
+  std::vector<int32_t> info(V, -1);
+  std::vector<uint32_t> dense_tok, skip_tok;
+  for (uint32_t t = 0; t < V; ++t) {
+    const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
+    if (dl == 0 || h_df[t] == 0) continue;
+    if ((double)h_df[t] >= dense_thr && density <= 1.0) {
+      info[t] = (int32_t)dense_tok.size();
+      dense_tok.push_back(t);
+    } else if (dl >= skip_thr) {
+      info[t] = -2 - (int32_t)skip_tok.size();
+      skip_tok.push_back(t);
+    }
+  }
+  ix->dense_rows = (uint32_t)dense_tok.size();
+  ix->skip_rows = (uint32_t)skip_tok.size();
+  SL_TRY(dalloc(ix, &ix->tokinfo, V));
+  SL_CUDA_TRY(cudaMemcpyAsync(ix->tokinfo, info.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+  uint32_t* slot_tok;
+  SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
+  if (!dense_tok.empty())
+    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok, dense_tok.data(), dense_tok.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!skip_tok.empty())
+    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
+                                cudaMemcpyHostToDevice, st));
+  if (ix->dense_rows) {
+    SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
+    SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
+    dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
+    k_dense_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok, ix->dense_rows, ix->n_pad,
+                                    ix->dense);
+  }
+  if (ix->skip_rows) {
+    SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
+    dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
+    k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
+                                   ix->num_tiles, ix->skiptab);
+  }
+  SL_CUDA_TRY(cudaGetLastError());
+  SL_CUDA_TRY(cudaEventRecord(ev1, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  SL_CUDA_TRY(cudaEventElapsedTime(&ix->build_ms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  return SL_OK;
+}
+}  // namespace
+
+int32_t build_index_impl(const sl_build_desc* d, sl_index** out) {
+  if (!d || !out) SL_FAIL(SL_EINVAL, "sl_index_build: null argument");
+  *out = nullptr;
+  SL_TRY(host_validate(d->params));
+  if (d->num_docs == 0) SL_FAIL(SL_EINVAL, "build_index: empty corpus");
+  if (d->vocab_size == 0) SL_FAIL(SL_EINVAL, "build_index: empty vocabulary");
+  if (!d->doc_offsets || !d->token_ids) SL_FAIL(SL_EINVAL, "build_index: null corpus pointers");
+  if (d->mem != SL_MEM_HOST && d->mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "build_index: bad mem kind");
+  if ((uint64_t)d->doc_base + d->num_docs > 0xFFFFFFFFull)
+    SL_FAIL(SL_EUNSUPPORTED, "build_index: global doc ids must fit in 32 bits");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    SL_FAIL(SL_ECUDA, "sl_index_build: no CUDA device available (there is no CPU fallback)");
+  SL_CUDA_TRY(cudaSetDevice(d->device));
+  auto* ix = new sl_index();
+  ix->device = d->device;
+  ix->params = d->params;
+  ix->N = d->num_docs;
+  ix->V = d->vocab_size;
+  ix->doc_base = d->doc_base;
+  ix->comm = d->comm;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ix;
+    SL_FAIL(SL_ECUDA, "sl_index_build: stream creation failed");
+  }
+  const int32_t rc = build_body(d, ix, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc != SL_OK) {
+    free_index(ix);
+    return rc;
+  }
+  *out = ix;
+  return SL_OK;
+}
+
+}  // namespace sl

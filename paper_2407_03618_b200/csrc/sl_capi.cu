@@ -1,0 +1,194 @@
+// sl_capi.cu — the extern "C" boundary declared in include/sparselex_b200.h.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "sl_index.cuh"
+#include "sl_synth.h"
+
+namespace sl {
+namespace {
+thread_local std::string t_error;
+}
+void set_error(const std::string& msg) { t_error = msg; }
+const std::string& get_error() { return t_error; }
+
+int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
+                      uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats);
+int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t q_len, int32_t mem, float* out);
+int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int32_t device, uint32_t* out_ids,
+                   float* out_scores);
+
+namespace {
+__global__ void k_synth_tokens(const double* __restrict__ cdf, uint32_t V, uint32_t seed, uint64_t begin,
+                               uint64_t count, uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = sl_corpus_token(cdf, V, seed, begin + i);
+}
+}  // namespace
+}  // namespace sl
+
+using namespace sl;
+
+extern "C" {
+
+int32_t sl_abi_version(void) { return SL_ABI_VERSION; }
+
+const char* sl_last_error(void) { return get_error().c_str(); }
+
+const char* sl_status_string(int32_t s) {
+  switch (s) {
+    case SL_OK: return "ok";
+    case SL_EINVAL: return "invalid argument";
+    case SL_ECUDA: return "CUDA error";
+    case SL_ENCCL: return "NCCL error";
+    case SL_ENOMEM: return "out of device memory";
+    case SL_ECORRUPT: return "corrupt index";
+    case SL_EUNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+int32_t sl_params_validate(const sl_params* p) {
+  if (!p) SL_FAIL(SL_EINVAL, "null params");
+  if (p->variant < 0 || p->variant > 5) SL_FAIL(SL_EINVAL, "invalid Variant value");
+  if (!(p->k1 > 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: k1 must be > 0");
+  if (!(p->b >= 0.0 && p->b <= 1.0)) SL_FAIL(SL_EINVAL, "BM25Params: b must be in [0, 1]");
+  if (!(p->delta >= 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: delta must be >= 0");
+  if (p->variant == SL_TFLDP && !(p->delta > std::exp(-1.0)))
+    SL_FAIL(SL_EINVAL, "BM25Params: tfldp requires delta > exp(-1)");
+  return SL_OK;
+}
+
+double sl_default_delta(int32_t v) {
+  switch (v) {
+    case SL_BM25L: return 0.5;
+    case SL_BM25PLUS: return 1.0;
+    case SL_TFLDP: return 0.5;
+    default: return 0.0;
+  }
+}
+
+int32_t sl_index_build(const sl_build_desc* desc, sl_index** out) { return build_index_impl(desc, out); }
+
+void sl_index_destroy(sl_index* index) { free_index(index); }
+
+int32_t sl_index_get_info(const sl_index* ix, sl_index_info* info) {
+  if (!ix || !info) SL_FAIL(SL_EINVAL, "sl_index_get_info: null argument");
+  info->num_docs_local = ix->N;
+  info->num_docs_global = ix->N_global;
+  info->vocab_size = ix->V;
+  info->doc_base = ix->doc_base;
+  info->nnz_local = ix->nnz;
+  info->total_len_global = ix->total_len;
+  info->avg_len = ix->avg_len;
+  info->dense_rows = ix->dense_rows;
+  info->skip_rows = ix->skip_rows;
+  info->tile_docs = kTileDocs;
+  info->num_tiles = ix->num_tiles;
+  info->device_bytes = ix->device_bytes;
+  info->build_ms = ix->build_ms;
+  return SL_OK;
+}
+
+int32_t sl_index_export(const sl_index* ix, int32_t mem, uint64_t* indptr, uint32_t* docids, float* values,
+                        uint32_t* df, float* theta, uint32_t* doclens, uint32_t* tf) {
+  if (!ix) SL_FAIL(SL_EINVAL, "sl_index_export: null index");
+  if (tf && !ix->tf) SL_FAIL(SL_EINVAL, "sl_index_export: tf requested but the index was built without keep_tf");
+  SL_CUDA_TRY(cudaSetDevice(ix->device));
+  const cudaMemcpyKind kind = mem == SL_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  struct {
+    void* dst;
+    const void* src;
+    uint64_t bytes;
+  } items[] = {{indptr, ix->indptr, ((uint64_t)ix->V + 1) * 8}, {docids, ix->docids, ix->nnz * 4},
+               {values, ix->values, ix->nnz * 4},           {df, ix->df_global, (uint64_t)ix->V * 4},
+               {theta, ix->theta, (uint64_t)ix->V * 4},     {doclens, ix->doclens, (uint64_t)ix->N * 4},
+               {tf, ix->tf, ix->nnz * 4}};
+  for (auto& it : items)
+    if (it.dst && it.bytes) SL_CUDA_TRY(cudaMemcpy(it.dst, it.src, it.bytes, kind));
+  return SL_OK;
+}
+
+int32_t sl_retrieve_batch(const sl_index* index, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                          uint32_t num_queries, uint32_t k, int32_t ordered, int32_t mem, uint32_t* out_ids,
+                          float* out_scores) {
+  (void)ordered;
+  return retrieve_impl(index, q_offsets, q_tokens, num_queries, k, mem, out_ids, out_scores, nullptr);
+}
+
+int32_t sl_retrieve_batch_timed(const sl_index* index, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                                uint32_t num_queries, uint32_t k, int32_t mem, uint32_t* out_ids,
+                                float* out_scores, sl_retrieve_stats* stats) {
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  return retrieve_impl(index, q_offsets, q_tokens, num_queries, k, mem, out_ids, out_scores, stats);
+}
+
+int32_t sl_score_query(const sl_index* index, const uint32_t* q_tokens, uint32_t q_len, int32_t mem,
+                       float* out_scores) {
+  return score_query_impl(index, q_tokens, q_len, mem, out_scores);
+}
+
+int32_t sl_top_k(const float* scores, uint32_t n, uint32_t k, int32_t ordered, int32_t mem, int32_t device,
+                 uint32_t* out_ids, float* out_scores) {
+  (void)ordered;
+  return top_k_impl(scores, n, k, mem, device, out_ids, out_scores);
+}
+
+int32_t sl_comm_unique_id(uint8_t out_id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!nccl().ok) SL_FAIL(SL_ENCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  SL_TRY(nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId"));
+  std::memcpy(out_id, &id, 128);
+  return SL_OK;
+}
+
+int32_t sl_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, sl_comm** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) SL_FAIL(SL_EINVAL, "sl_comm_init: bad arguments");
+  if (!nccl().ok) SL_FAIL(SL_ENCCL, "libnccl.so.2 could not be loaded");
+  SL_CUDA_TRY(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  auto* c = new sl_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  const int32_t rc = nccl_check(nccl().CommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+  if (rc != SL_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return SL_OK;
+}
+
+void sl_comm_destroy(sl_comm* c) {
+  if (!c) return;
+  if (c->comm) nccl().CommDestroy(c->comm);
+  delete c;
+}
+
+int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed, uint64_t begin, uint64_t count,
+                               int32_t cdf_mem, uint32_t* token_ids_dev) {
+  if (!cdf || !token_ids_dev || vocab == 0) SL_FAIL(SL_EINVAL, "sl_synth_tokens_device: bad arguments");
+  const double* dcdf = cdf;
+  double* tmp = nullptr;
+  if (cdf_mem == SL_MEM_HOST) {
+    SL_CUDA_TRY(cudaMalloc(&tmp, (uint64_t)vocab * 8));
+    SL_CUDA_TRY(cudaMemcpy(tmp, cdf, (uint64_t)vocab * 8, cudaMemcpyHostToDevice));
+    dcdf = tmp;
+  }
+  uint64_t blocks = (count + 255) / 256;
+  if (blocks > 148ull * 64) blocks = 148ull * 64;
+  if (blocks == 0) blocks = 1;
+  k_synth_tokens<<<(unsigned)blocks, 256>>>(dcdf, vocab, seed, begin, count, token_ids_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (tmp) cudaFree(tmp);
+  if (e != cudaSuccess) SL_FAIL(SL_ECUDA, std::string("sl_synth_tokens_device: ") + cudaGetErrorString(e));
+  return SL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// sl_index.cuh — the device-resident SearchIndex shard behind the opaque sl_index handle.
+#pragma once
+
+#include <nccl.h>
+
+#include "sl_nccl.cuh"
+
+#include "sl_internal.cuh"
+
+struct sl_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1;
+  int rank = 0;
+  int device = 0;
+};
+
+// SPEC.md [MODULE] index, SearchIndex: matrix (indptr/docids/values), stats, params,
+// theta; plus the query-side acceleration structures this design adds (dense copies of
+// the highest-df rows, per-tile skip offsets for long rows).
+struct sl_index {
+  int device = 0;
+  sl_params params{};
+  uint32_t N = 0;          // local docs
+  uint32_t N_global = 0;
+  uint32_t V = 0;
+  uint32_t doc_base = 0;
+  uint64_t nnz = 0;        // local nonzeros
+  uint64_t total_len = 0;  // global Σ|D|
+  double avg_len = 0.0;
+  sl_comm* comm = nullptr;  // borrowed
+
+  uint64_t* indptr = nullptr;     // [V+1]
+  uint32_t* docids = nullptr;     // [nnz]
+  float* values = nullptr;        // [nnz]
+  uint32_t* df_global = nullptr;  // [V]
+  float* theta = nullptr;         // [V]
+  uint32_t* doclens = nullptr;    // [N]
+  uint32_t* tf = nullptr;         // [nnz] (keep_tf only)
+
+  int32_t* tokinfo = nullptr;     // [V]
+  float* dense = nullptr;         // [dense_rows * n_pad]
+  uint32_t dense_rows = 0;
+  uint32_t* skiptab = nullptr;    // [skip_rows * (num_tiles + 1)]
+  uint32_t skip_rows = 0;
+  uint32_t num_tiles = 0;
+  uint32_t n_pad = 0;
+
+  uint64_t device_bytes = 0;
+  float build_ms = 0.f;
+
+  sl::IndexView view() const {
+    sl::IndexView v;
+    v.indptr = indptr;
+    v.docids = docids;
+    v.values = values;
+    v.df_global = df_global;
+    v.theta = theta;
+    v.tokinfo = tokinfo;
+    v.dense = dense;
+    v.skiptab = skiptab;
+    v.V = V;
+    v.N = N;
+    v.n_pad = n_pad;
+    v.num_tiles = num_tiles;
+    v.doc_base = doc_base;
+    return v;
+  }
+};
+
+namespace sl {
+int32_t build_index_impl(const sl_build_desc* desc, sl_index** out);
+void free_index(sl_index* ix);
+int32_t nccl_check(ncclResult_t r, const char* what);
+}  // namespace sl

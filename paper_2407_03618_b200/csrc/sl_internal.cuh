@@ -1,0 +1,166 @@
+// sl_internal.cuh — shared device/host internals of libsparselex_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "sparselex_b200.h"
+
+namespace sl {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+const std::string& get_error();
+
+struct Status {
+  int32_t code = SL_OK;
+  bool ok() const { return code == SL_OK; }
+};
+
+#define SL_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) {                                                                \
+      ::sl::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                  \
+      return _e == cudaErrorMemoryAllocation ? SL_ENOMEM : SL_ECUDA;                        \
+    }                                                                                       \
+  } while (0)
+
+#define SL_TRY(expr)                 \
+  do {                               \
+    int32_t _s = (expr);             \
+    if (_s != SL_OK) return _s;      \
+  } while (0)
+
+#define SL_FAIL(code, msg)     \
+  do {                         \
+    ::sl::set_error(msg);      \
+    return (code);             \
+  } while (0)
+
+// ---------------------------------------------------------------- constants
+constexpr int kTileDocs = 2048;        // docs per scoring tile (f32 accumulator = 8 KB smem)
+constexpr int kScoreThreads = 256;     // threads per scoring CTA
+constexpr int kQMax = 256;             // max query tokens handled per query
+constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path
+constexpr uint64_t kInvalidKey = 0ull; // never produced by a real (score, doc) key
+
+// ---------------------------------------------------------------- BM25 math (f64)
+// Exact restatement of proj/src/scoring.cpp:60-145 with every operation explicitly
+// rounded (no FMA contraction), matching the reference's C++ expression trees.
+__device__ __forceinline__ double d_idf(int v, double n, double d) {
+  switch (v) {
+    case SL_LUCENE:  // log(1.0 + (n - d + 0.5) / (d + 0.5))
+      return log(__dadd_rn(1.0, __ddiv_rn(__dadd_rn(__dsub_rn(n, d), 0.5), __dadd_rn(d, 0.5))));
+    case SL_ROBERTSON:  // log((n - d + 0.5) / (d + 0.5))
+      return log(__ddiv_rn(__dadd_rn(__dsub_rn(n, d), 0.5), __dadd_rn(d, 0.5)));
+    case SL_ATIRE:  // log(n / d)
+      return log(__ddiv_rn(n, d));
+    case SL_BM25L:  // log((n + 1.0) / (d + 0.5))
+      return log(__ddiv_rn(__dadd_rn(n, 1.0), __dadd_rn(d, 0.5)));
+    default:  // bm25plus, tfldp: log((n + 1.0) / d)
+      return log(__ddiv_rn(__dadd_rn(n, 1.0), d));
+  }
+}
+
+// scoring.cpp:81-114 (preconditions validated on the host)
+__device__ __forceinline__ double d_tf_component(int v, double tf, double dl, double avg, double k1,
+                                                 double b, double delta) {
+  // norm = 1.0 - b + b * doc_len / avg_len  ==  ((1.0 - b) + ((b * dl) / avg))
+  const double norm = __dadd_rn(__dsub_rn(1.0, b), __ddiv_rn(__dmul_rn(b, dl), avg));
+  switch (v) {
+    case SL_LUCENE:
+      return __ddiv_rn(tf, __dadd_rn(tf, __dmul_rn(k1, norm)));
+    case SL_ROBERTSON:
+    case SL_ATIRE:
+      return __ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), tf), __dadd_rn(tf, __dmul_rn(k1, norm)));
+    case SL_BM25L: {
+      const double c = __ddiv_rn(tf, norm);
+      return __ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), __dadd_rn(c, delta)),
+                       __dadd_rn(__dadd_rn(k1, c), delta));
+    }
+    case SL_BM25PLUS: {
+      const double c = __ddiv_rn(tf, norm);
+      return __dadd_rn(__ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), c), __dadd_rn(k1, c)), delta);
+    }
+    default: {  // tfldp
+      const double c = __ddiv_rn(tf, norm);
+      const double inner = __dadd_rn(1.0, log(__dadd_rn(c, delta)));
+      return __dadd_rn(1.0, log(inner));
+    }
+  }
+}
+
+// scoring.cpp:125-145 given idf
+__device__ __forceinline__ double d_nonoccurrence(int v, double idf, double k1, double delta) {
+  switch (v) {
+    case SL_BM25L:  // i * ((k1 + 1.0) * delta) / (k1 + delta)
+      return __ddiv_rn(__dmul_rn(idf, __dmul_rn(__dadd_rn(k1, 1.0), delta)), __dadd_rn(k1, delta));
+    case SL_BM25PLUS:
+      return __dmul_rn(idf, delta);
+    case SL_TFLDP:
+      return __dmul_rn(idf, __dadd_rn(1.0, log(__dadd_rn(1.0, log(delta)))));
+    default:
+      return 0.0;
+  }
+}
+
+__host__ __device__ __forceinline__ bool is_sparse_variant(int v) {
+  return v == SL_ROBERTSON || v == SL_ATIRE || v == SL_LUCENE;
+}
+
+// ---------------------------------------------------------------- top-k keys
+// key = orderable(score) << 32 | ~doc : larger key = better; equal scores -> smaller doc.
+__host__ __device__ __forceinline__ uint32_t float_to_ord(float f) {
+  f = f + 0.0f;  // -0 -> +0 so that both zeros tie
+#ifdef __CUDA_ARCH__
+  uint32_t u = __float_as_uint(f);
+#else
+  uint32_t u;
+  memcpy(&u, &f, 4);
+#endif
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float ord_to_float(uint32_t o) {
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+__host__ __device__ __forceinline__ uint64_t make_key(float score, uint32_t doc) {
+  return ((uint64_t)float_to_ord(score) << 32) | (uint64_t)(~doc);
+}
+__host__ __device__ __forceinline__ uint32_t key_doc(uint64_t key) { return ~(uint32_t)key; }
+__host__ __device__ __forceinline__ float key_score(uint64_t key) {
+  return ord_to_float((uint32_t)(key >> 32));
+}
+
+// ---------------------------------------------------------------- device views
+struct IndexView {
+  const uint64_t* indptr;     // [V+1]
+  const uint32_t* docids;     // [nnz] local doc ids
+  const float* values;        // [nnz] S^Δ
+  const uint32_t* df_global;  // [V]
+  const float* theta;         // [V]
+  const int32_t* tokinfo;     // [V] >=0 dense slot, -1 short row, <=-2 skip slot -(x+2)
+  const float* dense;         // [dense_rows][n_pad]
+  const uint32_t* skiptab;    // [skip_rows][num_tiles+1]
+  uint32_t V;
+  uint32_t N;        // local docs
+  uint32_t n_pad;    // num_tiles * kTileDocs
+  uint32_t num_tiles;
+  uint32_t doc_base;
+};
+
+// host launchers (sl_build.cu / sl_query.cu / sl_synth_dev.cu)
+struct BuildScratch;
+int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st,
+                           uint32_t* total_host);
+
+}  // namespace sl

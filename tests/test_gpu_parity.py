@@ -1,0 +1,234 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (north_star): TF/DF counts, CSC structure and doc ids bit-exact; values and scores
+within 1e-5 relative; top-k ids identical except where scores tie within 1e-5.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2407_03618_b200 import BM25Params, Variant, build_index, retrieve_batch, score_query, synth, top_k
+from tests.helpers import TOL, assert_topk_match, csr, query_scale
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [
+    BM25Params(Variant.lucene, 1.5, 0.75, 0.0),
+    BM25Params(Variant.robertson, 1.5, 0.75, 0.0),
+    BM25Params(Variant.atire, 1.5, 0.75, 0.0),
+    BM25Params(Variant.bm25l, 1.5, 0.75, 0.5),
+    BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5),
+    BM25Params(Variant.bm25plus, 1.5, 0.75, 1.0),
+    BM25Params(Variant.tfldp, 1.5, 0.75, 0.5),
+]
+
+
+@pytest.fixture(scope="module")
+def c1():
+    cfg = synth.config(1)
+    corp = synth.corpus_host(cfg)
+    qoff, qtok = synth.queries(cfg, corp.cdf)
+    return cfg, corp, qoff, qtok
+
+
+def _oracle(corp, V, p):
+    return oracle.OracleIndex(corp.offsets, corp.tokens, V, int(p.variant), p.k1, p.b, p.delta)
+
+
+def assert_index_equal(gx, ox, what=""):
+    for key in ("indptr", "docids", "df", "doclens", "tf"):
+        assert np.array_equal(gx[key], ox[key]), f"{what}: {key} differs"
+    assert gx["avg_len"] == ox["avg_len"], what
+    rel = np.abs(gx["values"].astype(np.float64) - ox["values"]) / np.maximum(np.abs(ox["values"]), 1e-30)
+    assert rel.max(initial=0) <= TOL, f"{what}: values rel err {rel.max()}"
+    relt = np.abs(gx["theta"].astype(np.float64) - ox["theta"]) / np.maximum(np.abs(ox["theta"]), 1e-30)
+    assert relt.max(initial=0) <= TOL, f"{what}: theta rel err {relt.max()}"
+    return int(np.count_nonzero(gx["values"] != ox["values"]))
+
+
+def test_device_generator_matches_host(cuda_ok, c1):
+    import torch
+    cfg, corp, _, _ = c1
+    T = int(corp.offsets[-1])
+    out = torch.empty(T, dtype=torch.uint32, device="cuda")
+    from paper_2407_03618_b200._lib import check, lib, SL_MEM_HOST
+    check(lib().sl_synth_tokens_device(corp.cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, 0, T, SL_MEM_HOST,
+                                       out.data_ptr()))
+    assert np.array_equal(out.cpu().numpy(), corp.tokens)
+
+
+@pytest.mark.parametrize("p", VARIANTS, ids=lambda p: f"{p.variant.name}-d{p.delta}")
+def test_build_c1_bitexact(cuda_ok, c1, p):
+    cfg, corp, _, _ = c1
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p, keep_tf=True) as gi:
+        gx = gi.export(tf=True)
+    ox = _oracle(corp, cfg.vocab, p).export()
+    n_diff = assert_index_equal(gx, ox, p.variant.name)
+    # f64 log may differ from glibc by an ulp; after f32 narrowing almost always identical
+    assert n_diff <= max(3, len(ox["values"]) // 100000), f"{n_diff} values not bit-identical"
+
+
+@pytest.mark.parametrize("k", [10, 100, 1000])
+def test_retrieve_c1_lucene(cuda_ok, c1, k):
+    cfg, corp, qoff, qtok = c1
+    p = BM25Params(Variant.lucene, 1.5, 0.75)
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    rid, rsc = ox.retrieve_batch(qoff, qtok, k, True, 8)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        gid, gsc = retrieve_batch(gi, (qoff, qtok), k, as_arrays=True)
+    q = lambda b: qtok[int(qoff[b]):int(qoff[b + 1])]  # noqa: E731
+    assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(q(b)),
+                      lambda b: query_scale(exp, q(b)), f"c1 k={k}")
+
+
+@pytest.mark.parametrize("p", VARIANTS, ids=lambda p: f"{p.variant.name}-d{p.delta}")
+def test_retrieve_c1_variants(cuda_ok, c1, p):
+    cfg, corp, qoff, qtok = c1
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    rid, rsc = ox.retrieve_batch(qoff, qtok, 10, True, 8)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        gid, gsc = retrieve_batch(gi, (qoff, qtok), 10, as_arrays=True)
+    q = lambda b: qtok[int(qoff[b]):int(qoff[b + 1])]  # noqa: E731
+    assert_topk_match(gid, gsc, rid, rsc, 10, cfg.num_docs, lambda b: ox.score_query(q(b)),
+                      lambda b: query_scale(exp, q(b)), p.variant.name)
+
+
+@pytest.mark.parametrize("density", [0.0001, 0.25, 2.0])
+def test_dense_rows_do_not_change_results(cuda_ok, c1, density):
+    """Dense query-side row copies are an access path, not a numeric change: identical output."""
+    cfg, corp, qoff, qtok = c1
+    p = BM25Params(Variant.lucene)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as a:
+        ia, sa = retrieve_batch(a, (qoff, qtok), 100, as_arrays=True)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p, dense_min_density=density) as b:
+        ib, sb = retrieve_batch(b, (qoff, qtok), 100, as_arrays=True)
+    np.testing.assert_array_equal(sa, sb)
+    np.testing.assert_array_equal(ia, ib)
+
+
+def test_score_query_dense_vector(cuda_ok, c1):
+    cfg, corp, qoff, qtok = c1
+    for p in VARIANTS:
+        ox = _oracle(corp, cfg.vocab, p)
+        exp = ox.export()
+        with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+            for b in range(0, 1000, 97):
+                q = qtok[int(qoff[b]):int(qoff[b + 1])]
+                g = score_query(gi, q).astype(np.float64)
+                r = ox.score_query(q)
+                tol = TOL * np.maximum(np.abs(r), query_scale(exp, q)) + 1e-30
+                assert np.all(np.abs(g - r) <= tol), (p.variant.name, b)
+
+
+def test_edge_queries(cuda_ok):
+    # toy corpus of SPEC index examples: ["cat sat", "dog ran", "cat cat cat"], ids cat=0 sat=1 dog=2 ran=3, 4=unused
+    off = np.array([0, 2, 4, 7], np.uint64)
+    tok = np.array([0, 1, 2, 3, 0, 0, 0], np.uint32)
+    for p in VARIANTS:
+        ox = oracle.OracleIndex(off, tok, 5, int(p.variant), p.k1, p.b, p.delta)
+        exp = ox.export()
+        queries = [[], [0], [0, 0], [4], [4, 1], [0, 1, 2, 3], [3, 3, 1]]
+        qo, qt = csr(queries)
+        for k in (1, 2, 3, 5):
+            rid, rsc = ox.retrieve_batch(qo, qt, k, True, 1)
+            with build_index(off, tok, 5, p) as gi:
+                gid, gsc = retrieve_batch(gi, (qo, qt), k, as_arrays=True)
+            assert_topk_match(gid, gsc, rid, rsc, k, 3, lambda b: ox.score_query(queries[b]),
+                              lambda b: query_scale(exp, queries[b]), f"toy {p.variant.name} k={k}")
+
+
+def test_toy_corpus_golden(cuda_ok):
+    """SURVEY.md §4 values verified with the reference's own scoring.cpp."""
+    off = np.array([0, 2, 4, 7], np.uint64)
+    tok = np.array([0, 1, 2, 3, 0, 0, 0], np.uint32)
+    with build_index(off, tok, 4, BM25Params(Variant.lucene)) as gi:
+        e = gi.export()
+    assert e["indptr"].tolist() == [0, 2, 3, 4, 5]  # 5 nonzeros (SPEC.md:207 says 6: erratum)
+    assert e["docids"].tolist() == [0, 2, 0, 1, 1]
+    np.testing.assert_array_equal(e["values"], np.array([0.200917587, 0.292446703, 0.419285774, 0.419285774,
+                                                         0.419285774], np.float32))
+    assert e["avg_len"] == 7 / 3
+    with build_index(off, tok, 4, BM25Params(Variant.bm25plus, 1.5, 0.75, 1.0)) as gi:
+        e = gi.export()
+    assert np.float32(e["theta"][0]) == np.float32(0.693147181)
+    np.testing.assert_array_equal(e["values"][:2], np.array([0.740767956, 1.07822895], np.float32))
+
+
+def test_errors(cuda_ok):
+    off = np.array([0, 2, 4, 7], np.uint64)
+    tok = np.array([0, 1, 2, 3, 0, 0, 0], np.uint32)
+    with pytest.raises(ValueError, match="token id >= vocab size"):
+        build_index(off, tok, 3)
+    with pytest.raises(ValueError, match="degenerate corpus"):
+        build_index(np.zeros(3, np.uint64), np.zeros(0, np.uint32), 4)
+    with pytest.raises(ValueError, match="empty corpus"):
+        build_index(np.zeros(1, np.uint64), np.zeros(0, np.uint32), 4)
+    with pytest.raises(ValueError, match="k1 must be > 0"):
+        build_index(off, tok, 4, BM25Params(Variant.lucene, 0.0))
+    with pytest.raises(ValueError, match="tfldp requires"):
+        build_index(off, tok, 4, BM25Params(Variant.tfldp, 1.5, 0.75, 0.3))
+    with build_index(off, tok, 4) as gi:
+        with pytest.raises(ValueError, match="token id >= vocab size"):
+            retrieve_batch(gi, [[9]], 2)
+        with pytest.raises(ValueError, match="k must be >= 1"):
+            retrieve_batch(gi, [[0]], 0)
+
+
+def test_empty_docs_and_unused_tokens(cuda_ok):
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 6, 300)
+    lens[:7] = 0
+    off = np.zeros(301, np.uint64)
+    off[1:] = np.cumsum(lens)
+    tok = rng.integers(0, 40, int(off[-1])).astype(np.uint32) * 3  # ids ≡ 0 mod 3: most of V=150 unused
+    queries = [list(rng.integers(0, 150, rng.integers(0, 6))) for _ in range(200)]
+    qo, qt = csr(queries)
+    for p in VARIANTS:
+        ox = oracle.OracleIndex(off, tok, 150, int(p.variant), p.k1, p.b, p.delta)
+        exp = ox.export()
+        with build_index(off, tok, 150, p, keep_tf=True) as gi:
+            assert_index_equal(gi.export(tf=True), exp, p.variant.name)
+            for k in (1, 7, 300, 400):
+                gid, gsc = retrieve_batch(gi, (qo, qt), k, as_arrays=True)
+                rid, rsc = ox.retrieve_batch(qo, qt, k, True, 2)
+                assert_topk_match(gid, gsc, rid, rsc, k, 300, lambda b: ox.score_query(queries[b]),
+                                  lambda b: query_scale(exp, queries[b]), f"ragged {p.variant.name} k={k}")
+
+
+def test_random_corpora_ac1(cuda_ok):
+    """SPEC acceptance criterion 1 on the GPU path: random corpora x all variants x 20 queries
+    vs the naive dense scorer (B(Q,D) from raw tf/df/lengths)."""
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        N = int(rng.integers(10, 201))
+        V = int(rng.integers(5, 301))
+        lens = rng.integers(1, 51, N)
+        off = np.zeros(N + 1, np.uint64)
+        off[1:] = np.cumsum(lens)
+        tok = rng.integers(0, V, int(off[-1])).astype(np.uint32)
+        queries = [list(rng.integers(0, V, rng.integers(1, 6))) for _ in range(20)]
+        for p in VARIANTS:
+            with build_index(off, tok, V, p) as gi:
+                for q in queries:
+                    dense = oracle.dense_score(off, tok, V, q, int(p.variant), p.k1, p.b, p.delta)
+                    g = score_query(gi, q).astype(np.float64)
+                    scale = np.abs(dense).max() + 1e-12
+                    assert np.all(np.abs(g - dense) <= TOL * np.maximum(np.abs(dense), scale)), (trial, p)
+
+
+def test_top_k_random_vectors_ac3(cuda_ok):
+    """SPEC acceptance criterion 3: 1000-vector sweep scaled down; duplicate-heavy included."""
+    rng = np.random.default_rng(3)
+    for i in range(200):
+        n = int(rng.integers(1, 10001))
+        if i % 3 == 0:
+            s = rng.integers(0, 4, n).astype(np.float32)  # duplicate-heavy
+        else:
+            s = rng.standard_normal(n).astype(np.float32)
+        k = int(rng.integers(1, 300))
+        gi, gs = top_k(s, k)
+        ri, rs = oracle.top_k(s.astype(np.float64), k)
+        assert np.array_equal(gi.astype(np.int64), ri.astype(np.int64)), i
+        assert np.array_equal(gs, rs.astype(np.float32)), i
