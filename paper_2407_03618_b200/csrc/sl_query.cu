@@ -13,9 +13,8 @@
 //   * remaining rows are gathered per tile from the CSC slice [s, e) found through a
 //     per-tile skip table (long rows) or a warp ballot over a cursor (short rows), and
 //     added to the shared accumulator one token at a time (doc ids are unique within a
-//     row, so no atomics are needed and the per-document summation order is fixed:
-//     dense tokens in query order, then the rest in query order — identical for any
-//     split or GPU count);
+//     row, so no atomics are needed). Every document sums its terms in query order
+//     whatever the dense/gathered split, tile split or GPU count: bit-identical results;
 //   * fused top-k: each CTA keeps its running best keys (u64 = orderable(score)<<32 |
 //     ~doc) in shared memory behind a threshold; overflow triggers an in-CTA MSD radix
 //     select; the per-split winners are merged per query by k_merge (also the rank-0
@@ -198,12 +197,18 @@ struct QueryArgs {
 };
 
 // Score one tile of one query into s.acc (local doc d0 .. d0+TILE).
-__device__ __forceinline__ void score_tile(const IndexView& ix, const Smem& s, int nd, int ns,
-                                           uint32_t tile, uint32_t d0) {
+// Entries are the query's tokens in QUERY ORDER: dense copies (dslot >= 0) are streamed
+// as float4 and accumulated in registers; a CSC-gathered token (dslot < 0) spills the
+// registers to the shared accumulator, scatters its slice, and reloads. Every document
+// therefore sums its terms in query order, whatever the dense/gathered split, tile split
+// or GPU count (bit-identical results across all of them).
+__device__ __forceinline__ void score_tile(const IndexView& ix, const Smem& s, int ne, uint32_t tile,
+                                           uint32_t d0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t d1 = d0 + TILE;
-  // ranges of the CSC-gathered rows within this tile (one warp per row)
-  for (int e = warp; e < ns; e += NW) {
+  // slice [rs, re) of every gathered row within this tile (one warp per row)
+  for (int e = warp; e < ne; e += NW) {
+    if (s.dslot[e] >= 0) continue;
     uint32_t sb, se;
     const int32_t sk = s.skip[e];
     if (sk >= 0) {
@@ -230,36 +235,51 @@ __device__ __forceinline__ void score_tile(const IndexView& ix, const Smem& s, i
       s.re[e] = se;
     }
   }
-  // dense rows: coalesced float4 stream, accumulated in registers (query order)
   float4 a[F4];
 #pragma unroll
   for (int r = 0; r < F4; ++r) a[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int i = 0; i < nd; ++i) {
-    const float4* row = reinterpret_cast<const float4*>(ix.dense + (uint64_t)s.dslot[i] * ix.n_pad + d0);
-#pragma unroll
-    for (int r = 0; r < F4; ++r) {
-      const float4 v = __ldg(row + threadIdx.x + r * NT);
-      a[r].x += v.x;
-      a[r].y += v.y;
-      a[r].z += v.z;
-      a[r].w += v.w;
-    }
-  }
   float4* acc4 = reinterpret_cast<float4*>(s.acc);
+  bool in_smem = false;
+  for (int e = 0; e < ne; ++e) {
+    const int32_t slot = s.dslot[e];
+    if (slot >= 0) {
+      if (in_smem) {
 #pragma unroll
-  for (int r = 0; r < F4; ++r) acc4[threadIdx.x + r * NT] = a[r];
-  __syncthreads();
-  // gathered rows, one at a time (unique docs within a row -> plain smem RMW)
-  for (int e = 0; e < ns; ++e) {
-    const uint32_t sb = s.rs[e], se = s.re[e];
-    if (sb == se) continue;
-    const uint64_t base = s.row_start[e];
-    for (uint32_t p = sb + threadIdx.x; p < se; p += NT) {
-      const uint32_t doc = __ldg(ix.docids + base + p);
-      s.acc[doc - d0] += __ldg(ix.values + base + p);
+        for (int r = 0; r < F4; ++r) a[r] = acc4[threadIdx.x + r * NT];
+        in_smem = false;
+      }
+      const float4* row = reinterpret_cast<const float4*>(ix.dense + (uint64_t)slot * ix.n_pad + d0);
+#pragma unroll
+      for (int r = 0; r < F4; ++r) {
+        const float4 v = __ldg(row + threadIdx.x + r * NT);
+        a[r].x += v.x;
+        a[r].y += v.y;
+        a[r].z += v.z;
+        a[r].w += v.w;
+      }
+    } else {
+      if (!in_smem) {
+#pragma unroll
+        for (int r = 0; r < F4; ++r) acc4[threadIdx.x + r * NT] = a[r];
+        in_smem = true;
+        __syncthreads();
+      }
+      const uint32_t sb = s.rs[e], se = s.re[e];
+      if (sb == se) continue;
+      const uint64_t base = s.row_start[e];
+      // doc ids are unique within a row: plain shared-memory RMW, no atomics
+      for (uint32_t p = sb + threadIdx.x; p < se; p += NT) {
+        const uint32_t doc = __ldg(ix.docids + base + p);
+        s.acc[doc - d0] += __ldg(ix.values + base + p);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
+  if (!in_smem) {
+#pragma unroll
+    for (int r = 0; r < F4; ++r) acc4[threadIdx.x + r * NT] = a[r];
+  }
+  __syncthreads();
 }
 
 template <int MODE>
@@ -274,38 +294,32 @@ __global__ void __launch_bounds__(NT) k_score_topk(IndexView ix, QueryArgs qa) {
   const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * n_tiles / qa.n_splits);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  int nd = 0, ns = 0;
+  int ne = 0;
   if constexpr (MODE != MODE_VECTOR) {
-    // classify the query's tokens: dense copies first, then CSC-gathered rows, each in
-    // query order (this fixes the per-document summation order).
+    // the query's tokens in query order (OOV / locally empty rows dropped)
     if (threadIdx.x == 0) {
       const uint64_t qb = qa.q_off[q], qe = qa.q_off[q + 1];
-      int cd = 0, cs = 0;
+      int c = 0;
       for (uint64_t j = qb; j < qe; ++j) {
         const uint32_t t = qa.q_tok[j];
         if (t >= ix.V || ix.df_global[t] == 0) continue;  // OOV drop (SPEC tokenizer decisions)
         const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
         if (rb == re) continue;  // no local postings
         const int32_t info = ix.tokinfo[t];
-        if (info >= 0) {
-          s.dslot[cd++] = info;
-        } else {
-          s.row_start[cs] = rb;
-          s.row_len[cs] = (uint32_t)(re - rb);
-          s.skip[cs] = info <= -2 ? -2 - info : -1;
-          ++cs;
-        }
+        s.dslot[c] = info >= 0 ? info : -1;
+        s.row_start[c] = rb;
+        s.row_len[c] = (uint32_t)(re - rb);
+        s.skip[c] = info <= -2 ? -2 - info : -1;
+        ++c;
       }
-      s.counts[0] = cd;
-      s.counts[1] = cs;
+      s.counts[0] = c;
     }
     __syncthreads();
-    nd = s.counts[0];
-    ns = s.counts[1];
+    ne = s.counts[0];
     // cursors of short rows at the split's first doc (lower_bound, one lane per row)
     const uint32_t dstart = t0 * TILE;
-    for (int e = warp; e < ns; e += NW) {
-      if (lane == 0 && s.skip[e] < 0) {
+    for (int e = warp; e < ne; e += NW) {
+      if (lane == 0 && s.dslot[e] < 0 && s.skip[e] < 0) {
         const uint32_t* ids = ix.docids + s.row_start[e];
         uint32_t lo = 0, hi = s.row_len[e];
         while (lo < hi) {
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(NT) k_score_topk(IndexView ix, QueryArgs qa) {
       for (uint32_t i = threadIdx.x; i < TILE; i += NT) s.acc[i] = i < nvalid ? qa.vec[d0 + i] : 0.f;
       __syncthreads();
     } else {
-      score_tile(ix, s, nd, ns, tile, d0);
+      score_tile(ix, s, ne, tile, d0);
     }
     if constexpr (MODE == MODE_DENSE) {
       for (uint32_t i = threadIdx.x; i < nvalid; i += NT)
@@ -345,11 +359,11 @@ __global__ void __launch_bounds__(NT) k_score_topk(IndexView ix, QueryArgs qa) {
       for (int r = 0; r < F4; ++r) {
         const uint32_t dl = 4 * (threadIdx.x + r * NT);
         const float4 v = reinterpret_cast<const float4*>(s.acc)[threadIdx.x + r * NT];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (dl + c < nvalid) {
-            const uint64_t key = make_key(vv[c], gdoc0 + dl + c);
+            const float x = c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+            const uint64_t key = make_key(x, gdoc0 + dl + c);
             if (key >= thr) f(key);
           }
         }
