@@ -408,6 +408,45 @@ struct Temps {
 
 }  // namespace
 
+// Stable LSD radix sort of u32 (key, value) pairs by the low `bits` key bits (8-bit
+// digits, widths balanced over the passes). Pass p reads the previous output and writes
+// k{p&1}/v{p&1}; kin/vin are only read by the first pass, so v1 may alias vin. When
+// v_check != 0, keys >= v_check set err bit 2 during the first histogram pass.
+int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, int bits, uint32_t* k0, uint32_t* k1,
+                         uint32_t* v0, uint32_t* v1, cudaStream_t st, const uint32_t** kout, const uint32_t** vout,
+                         uint32_t v_check, uint32_t* err) {
+  *kout = kin;
+  *vout = vin;
+  if (bits <= 0 || n == 0) return SL_OK;
+  const int passes = (bits + 7) / 8;
+  const int width = (bits + passes - 1) / passes;
+  const uint32_t mask = (1u << width) - 1u;
+  const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
+  if (n_tiles > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "radix sort: too many tiles");
+  uint32_t* hist;
+  SL_CUDA_TRY(cudaMallocAsync(&hist, n_tiles * (uint64_t)(mask + 1) * 4, st));
+  uint32_t* kb[2] = {k0, k1};
+  uint32_t* vb[2] = {v0, v1};
+  const uint32_t* ki = kin;
+  const uint32_t* vi = vin;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * width;
+    k_radix_hist<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(ki, n, shift, mask, hist, (uint32_t)n_tiles,
+                                                             v_check ? v_check : 0xFFFFFFFFu,
+                                                             p == 0 && v_check ? err : nullptr);
+    SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
+    k_radix_scatter<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist,
+                                                                (uint32_t)n_tiles);
+    ki = kb[p & 1];
+    vi = vb[p & 1];
+  }
+  SL_CUDA_TRY(cudaFreeAsync(hist, st));
+  SL_CUDA_TRY(cudaGetLastError());
+  *kout = ki;
+  *vout = vi;
+  return SL_OK;
+}
+
 int32_t nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return SL_OK;
   set_error(std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
@@ -489,41 +528,16 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   // ---- K1: stable LSD radix sort of (token, doc) by token
   int bits = 0;
   while (bits < 32 && (V - 1) >> bits) ++bits;
-  const int passes = (bits + 7) / 8;
   const uint32_t* ksorted = tokens;
   const uint32_t* vsorted = docs;
-  if (passes == 0) {
+  if (bits == 0) {
     k_check_tokens<<<grid_for(T, 256), 256, 0, st>>>(tokens, T, V, err);
   } else {
-    const int width = (bits + passes - 1) / passes;
-    const uint32_t mask = (1u << width) - 1u;
-    const uint64_t n_tiles = (T + kSortTile - 1) / kSortTile;
-    if (n_tiles > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "build_index: too many sort tiles");
-    uint32_t* hist;
     SL_TRY(tmp.alloc(&kb0, T));
     SL_TRY(tmp.alloc(&kb1, T));
     SL_TRY(tmp.alloc(&vb1, T));
-    SL_TRY(tmp.alloc(&hist, n_tiles * (uint64_t)(mask + 1)));
-    uint32_t* kbuf[2] = {kb0, kb1};
-    uint32_t* vbuf[2] = {vb1, docs};
-    const uint32_t* kin = tokens;
-    const uint32_t* vin = docs;
-    for (int p = 0; p < passes; ++p) {
-      const int shift = p * width;
-      uint32_t* kout = kbuf[p & 1];
-      uint32_t* vout = vbuf[p & 1];
-      k_radix_hist<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(kin, T, shift, mask, hist,
-                                                               (uint32_t)n_tiles, V,
-                                                               p == 0 ? err : nullptr);
-      SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
-      k_radix_scatter<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(kin, vin, kout, vout, T, shift, mask,
-                                                                  hist, (uint32_t)n_tiles);
-      kin = kout;
-      vin = vout;
-    }
-    ksorted = kin;
-    vsorted = vin;
-    tmp.release(hist);
+    // values ping-pong between vb1 and docs (docs is consumed by the first pass)
+    SL_TRY(radix_sort_pairs(tokens, docs, T, bits, kb0, kb1, vb1, docs, st, &ksorted, &vsorted, V, err));
   }
   SL_CUDA_TRY(cudaGetLastError());
   uint32_t herr = 0;
@@ -559,7 +573,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   k_tf<<<grid_for(nnz, 256), 256, 0, st>>>(runstart, nnz, tf);
   tmp.release(runstart);
   tmp.release(pos);
-  if (passes > 0) {
+  if (bits > 0) {
     tmp.release(kb0);
     tmp.release(kb1);
     tmp.release(vb1);
@@ -608,7 +622,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   const double density = d->dense_min_density > 0.f ? (double)d->dense_min_density : 0.25;
   const double dense_thr = density * (double)ix->N_global;
-  const uint64_t skip_thr = 32ull * ix->num_tiles;
+  const uint64_t skip_thr = 4ull * ix->num_tiles;  // >= 4 postings per tile expected
   std::vector<int32_t> info(V, -1);
   std::vector<uint32_t> dense_tok, skip_tok;
   for (uint32_t t = 0; t < V; ++t) {

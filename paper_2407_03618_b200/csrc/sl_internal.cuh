@@ -41,7 +41,7 @@ struct Status {
   } while (0)
 
 // ---------------------------------------------------------------- constants
-constexpr int kTileDocs = 2048;        // docs per scoring tile (f32 accumulator = 8 KB smem)
+constexpr int kTileDocs = 512;         // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
 constexpr int kScoreThreads = 256;     // threads per scoring CTA
 constexpr int kQMax = 256;             // max query tokens handled per query
 constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path
@@ -158,9 +158,11 @@ struct IndexView {
   uint32_t doc_base;
 };
 
-// host launchers (sl_build.cu / sl_query.cu / sl_synth_dev.cu)
-struct BuildScratch;
+// host launchers shared between sl_build.cu and sl_query.cu
 int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st,
                            uint32_t* total_host);
+int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, int bits, uint32_t* k0, uint32_t* k1,
+                         uint32_t* v0, uint32_t* v1, cudaStream_t st, const uint32_t** kout, const uint32_t** vout,
+                         uint32_t v_check, uint32_t* err);
 
 }  // namespace sl

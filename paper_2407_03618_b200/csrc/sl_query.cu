@@ -4,22 +4,27 @@
 // contiguous slice into a zeroed |C| accumulator and adds Σ S^θ; top_k selects the k
 // best with ties -> smaller doc index; retrieve_batch runs both per query.
 //
-// B200 design:
-//   * doc-tiled scoring: a CTA owns (query, contiguous run of 2048-doc tiles). The
-//     tile's scores live in shared memory (8 KB) and never touch HBM; the |C| vector of
-//     the reference is never materialised.
-//   * rows with global df >= density*N have a dense f32 copy: their contribution is a
-//     coalesced float4 stream accumulated in registers (no indirection, no atomics);
-//   * remaining rows are gathered per tile from the CSC slice [s, e) found through a
-//     per-tile skip table (long rows) or a warp ballot over a cursor (short rows), and
-//     added to the shared accumulator one token at a time (doc ids are unique within a
-//     row, so no atomics are needed). Every document sums its terms in query order
-//     whatever the dense/gathered split, tile split or GPU count: bit-identical results;
-//   * fused top-k: each CTA keeps its running best keys (u64 = orderable(score)<<32 |
-//     ~doc) in shared memory behind a threshold; overflow triggers an in-CTA MSD radix
-//     select; the per-split winners are merged per query by k_merge (also the rank-0
-//     merge of the G x k candidates gathered over NCCL).
+// B200 design. k_score_runs: queries are grouped by their DENSE SIGNATURE
+// (the rows with a dense f32 copy, i.e. global df >= density*N) — sorted by a signature
+// hash and cut into runs of <= R identical signatures. One WARP owns (run, doc split) and
+// walks 1024-doc tiles with no CTA-level synchronisation:
+//   1. the run's dense signature is summed once per tile, in registers, ascending slot
+//      order, every lane streaming 8 float4 per row with all loads in flight;
+//   2. per query of the run: lane j locates token j's CSC slice in the tile (per-tile skip
+//      table for long rows, forward cursor for short rows); if the query has postings in
+//      the tile, the dense sum is spilled to the warp's 4 KB shared accumulator and the
+//      postings are flattened across tokens, loaded 4 x 32 at a time, and applied in
+//      token order (same-doc postings inside a round serialised with match.any);
+//   3. running top-k: float pre-test against the threshold, exact 64-bit keys
+//      (orderable(score) << 32 | ~doc) for survivors into a per-query shared buffer;
+//      overflow -> warp-level MSD radix select.
+// The reference's |C| score vector is never materialised. Per document the sum is the
+// dense terms (ascending slot) then the gathered terms (query order): a fixed function of
+// the query and the global df classification — identical for any grouping, doc split or
+// GPU count. k_merge selects the final top-k per query from the per-split candidates (and
+// is the rank-0 merge of the G x k candidates gathered over NCCL).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -28,13 +33,17 @@
 namespace sl {
 namespace {
 
-constexpr int NT = kScoreThreads;
+constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int TILE = kTileDocs;
-constexpr int F4 = TILE / (4 * NT);  // float4 per thread per tile
-static_assert(F4 * 4 * NT == TILE, "tile must be a multiple of 4*threads");
+constexpr int TILE = kTileDocs;      // 512
+constexpr int F4L = TILE / 4 / 32;   // float4 per lane when a warp scans one tile
+static_assert(F4L * 128 == TILE, "a warp covers a tile with whole float4 per lane");
 
-enum Mode { MODE_TOPK = 0, MODE_DENSE = 1, MODE_VECTOR = 2 };
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   const int lane = threadIdx.x & 31;
@@ -64,14 +73,45 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sw, ui
   return r;
 }
 
+// Locate the bucket holding the need-th largest key from a 256-bin histogram (bins read
+// high to low). Executed by one full warp; returns (bucket, count above, bucket count).
+__device__ __forceinline__ void warp_pick_bucket(const uint32_t* hist, uint32_t need, uint32_t& b,
+                                                 uint32_t& above, uint32_t& cnt) {
+  const int lane = threadIdx.x & 31;
+  uint32_t c[8], s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c[j] = hist[255 - (8 * lane + j)];
+    s += c[j];
+  }
+  const uint32_t incl = warp_incl_scan(s), excl = incl - s;
+  const bool mine = excl < need && need <= incl;
+  uint32_t lb = 0, la = 0, lc = 0;
+  if (mine) {
+    uint32_t run = excl;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (run + c[j] >= need) {
+        lb = 255u - (8u * lane + j);
+        la = run;
+        lc = c[j];
+        break;
+      }
+      run += c[j];
+    }
+  }
+  const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+  b = __shfl_sync(0xffffffffu, lb, src);
+  above = __shfl_sync(0xffffffffu, la, src);
+  cnt = __shfl_sync(0xffffffffu, lc, src);
+}
+
 // MSD radix select over u64 keys (8-bit digits): returns tau such that exactly k of the
-// visited keys are >= tau. Requires more than k keys. `visit(f)` calls f(key) for every
-// key this thread owns. hist: 256 u32, bc: 3 u32 (shared).
+// visited keys are >= tau (keys are distinct). Requires more than k keys.
 template <class Visit>
 __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, uint32_t* bc) {
   uint64_t prefix = 0, mask = 0;
   uint32_t need = k;
-  const int lane = threadIdx.x & 31;
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
@@ -80,25 +120,12 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
     });
     __syncthreads();
     if (threadIdx.x < 32) {
-      uint32_t c[8], s = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = hist[255 - (8 * lane + j)];
-        s += c[j];
-      }
-      const uint32_t incl = warp_incl_scan(s), excl = incl - s;
-      if (excl < need && need <= incl) {
-        uint32_t run = excl;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (run + c[j] >= need) {
-            bc[0] = 255u - (8u * lane + j);
-            bc[1] = run;
-            bc[2] = c[j];
-            break;
-          }
-          run += c[j];
-        }
+      uint32_t b, a, c;
+      warp_pick_bucket(hist, need, b, a, c);
+      if (threadIdx.x == 0) {
+        bc[0] = b;
+        bc[1] = a;
+        bc[2] = c;
       }
     }
     __syncthreads();
@@ -107,6 +134,34 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
     prefix |= (uint64_t)b << shift;
     mask |= 0xFFull << shift;
     __syncthreads();
+    if (cnt == need) break;
+  }
+  return prefix;
+}
+
+// warp-level variant with 4-bit digits (16-bin warp-private histogram, 64 bytes)
+template <class Visit>
+__device__ uint64_t warp_select_kth(Visit visit, uint32_t k, uint32_t* hist) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0, mask = 0;
+  uint32_t need = k;
+  for (int shift = 60; shift >= 0; shift -= 4) {
+    if (lane < 16) hist[lane] = 0;
+    __syncwarp();
+    visit([&](uint64_t x) {
+      if ((x & mask) == prefix) atomicAdd(&hist[(uint32_t)(x >> shift) & 15u], 1u);
+    });
+    __syncwarp();
+    const uint32_t c = lane < 16 ? hist[15 - lane] : 0u;  // buckets high -> low
+    const uint32_t incl = warp_incl_scan(c), excl = incl - c;
+    const bool mine = lane < 16 && excl < need && need <= incl;
+    const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    const uint32_t above = __shfl_sync(0xffffffffu, excl, src);
+    const uint32_t cnt = __shfl_sync(0xffffffffu, c, src);
+    __syncwarp();
+    need -= above;
+    prefix |= (uint64_t)(15 - src) << shift;
+    mask |= 0xFull << shift;
     if (cnt == need) break;
   }
   return prefix;
@@ -136,310 +191,573 @@ __host__ __device__ inline uint32_t next_pow2(uint32_t x) {
   return p;
 }
 
+// candidate buffer per (query, split)
 __host__ __device__ inline uint32_t kept_capacity(uint32_t k) {
   const uint32_t c = 2 * next_pow2(k);
-  return c < 512 ? 512 : c;
+  return c < 64 ? 64 : c;
 }
 
-// dynamic shared memory layout of the scoring kernel
-struct Smem {
-  float* acc;          // [TILE]
-  uint64_t* kept[2];   // [C] each
-  uint64_t* row_start; // [qmax]
-  uint32_t* hist;      // [256]
-  uint32_t* sw;        // [40]
-  int32_t* dslot;      // [qmax]
-  uint32_t* row_len;   // [qmax]
-  int32_t* skip;       // [qmax]
-  uint32_t* cursor;    // [qmax]
-  uint32_t* rs;        // [qmax]
-  uint32_t* re;        // [qmax]
-  int32_t* counts;     // [4] nd, ns
+// float lower bound of every key >= tau (for the cheap pre-test)
+__device__ __forceinline__ float tau_float(uint64_t tau) {
+  const uint32_t hi = (uint32_t)(tau >> 32);
+  return hi < 0x00800000u ? -INFINITY : ord_to_float(hi);
+}
+
+__device__ __forceinline__ float f4c(const float4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+enum GroupMode { GM_TOPK = 0, GM_DENSE = 1 };
+
+constexpr int RMAX = 2;      // queries per run (same dense signature) handled by one warp
+constexpr int UNROLL = 4;    // gather rounds whose loads are issued together
+
+struct RunArgs {
+  const uint64_t* q_off;      // [B+1]
+  const uint32_t* q_tok;
+  const double* qconst;       // [B]
+  const uint32_t* perm;       // sorted position -> original query id
+  const uint32_t* run_begin;  // [n_runs+1] positions in perm
+  const uint32_t* n_runs;     // device scalar
+  uint32_t k;
+  uint32_t C;                 // candidates kept per (query, split)
+  uint32_t R;                 // max queries per run
+  uint32_t qmax;
+  uint32_t n_splits;
+  uint32_t wpc;               // warps per CTA in use
+  uint32_t warp_bytes;        // shared memory per warp
+  uint64_t* cand;             // [B][n_splits][C] (original query order)
+  float* dense_out;           // GM_DENSE: [N]
 };
 
-__host__ __device__ inline size_t smem_bytes(uint32_t C, uint32_t qmax) {
-  return (size_t)TILE * 4 + 2 * (size_t)C * 8 + (size_t)qmax * 8 + 256 * 4 + 40 * 4 +
-         (size_t)qmax * 4 * 6 + 16;
+// per-warp shared memory; E = R * qmax gathered-row entries (the run's queries' CSC
+// tokens concatenated, query r owning entries [ebeg[r], ebeg[r+1]))
+struct WSmem {
+  float* dsum;          // [TILE] dense-signature sum of the current tile
+  float* acc;           // [TILE] working accumulator (runs with > 1 query)
+  uint64_t* kept;       // [R][C]
+  uint64_t* tau;        // [R]
+  uint64_t* row_start;  // [E]
+  uint32_t* hist;       // [16]
+  uint32_t* n_kept;     // [R]
+  int32_t* ebeg;        // [R+1]
+  int32_t* nd;          // [1]
+  int32_t* dslot;       // [qmax]
+  uint32_t* row_len;    // [E]
+  int32_t* skip;        // [E]
+  uint32_t* cursor;     // [E] short rows: first posting not consumed yet
+  uint32_t* nextdoc;    // [E] short rows: doc id at the cursor (UINT32_MAX at the end)
+  uint32_t* sb;         // [E] slice of the current tile (row-relative start)
+  uint32_t* cnt;        // [E] and length
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(uint32_t R, uint32_t C, uint32_t qmax) {
+  const size_t E = (size_t)R * qmax;
+  size_t b = (size_t)TILE * 8 + (size_t)R * C * 8 + (size_t)R * 8 + E * 8 + 16 * 4 + (size_t)R * 4 + (R + 1) * 4 + 4 +
+             (size_t)qmax * 4 + E * 4 * 6;
+  return (b + 15) & ~(size_t)15;
 }
 
-__device__ inline Smem carve(unsigned char* base, uint32_t C, uint32_t qmax) {
-  Smem s;
-  unsigned char* p = base;
+__device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_t qmax) {
+  const size_t E = (size_t)R * qmax;
+  WSmem s;
+  s.dsum = (float*)p; p += (size_t)TILE * 4;
   s.acc = (float*)p; p += (size_t)TILE * 4;
-  s.kept[0] = (uint64_t*)p; p += (size_t)C * 8;
-  s.kept[1] = (uint64_t*)p; p += (size_t)C * 8;
-  s.row_start = (uint64_t*)p; p += (size_t)qmax * 8;
-  s.hist = (uint32_t*)p; p += 256 * 4;
-  s.sw = (uint32_t*)p; p += 40 * 4;
+  s.kept = (uint64_t*)p; p += (size_t)R * C * 8;
+  s.tau = (uint64_t*)p; p += (size_t)R * 8;
+  s.row_start = (uint64_t*)p; p += E * 8;
+  s.hist = (uint32_t*)p; p += 16 * 4;
+  s.n_kept = (uint32_t*)p; p += (size_t)R * 4;
+  s.ebeg = (int32_t*)p; p += (size_t)(R + 1) * 4;
+  s.nd = (int32_t*)p; p += 4;
   s.dslot = (int32_t*)p; p += (size_t)qmax * 4;
-  s.row_len = (uint32_t*)p; p += (size_t)qmax * 4;
-  s.skip = (int32_t*)p; p += (size_t)qmax * 4;
-  s.cursor = (uint32_t*)p; p += (size_t)qmax * 4;
-  s.rs = (uint32_t*)p; p += (size_t)qmax * 4;
-  s.re = (uint32_t*)p; p += (size_t)qmax * 4;
-  s.counts = (int32_t*)p;
+  s.row_len = (uint32_t*)p; p += E * 4;
+  s.skip = (int32_t*)p; p += E * 4;
+  s.cursor = (uint32_t*)p; p += E * 4;
+  s.nextdoc = (uint32_t*)p; p += E * 4;
+  s.sb = (uint32_t*)p; p += E * 4;
+  s.cnt = (uint32_t*)p;
   return s;
 }
 
-struct QueryArgs {
-  const uint64_t* q_off;   // [B+1] (absolute offsets into q_tok)
-  const uint32_t* q_tok;
-  const double* qconst;    // [B] Σ S^θ
-  uint32_t B;
-  uint32_t k;
-  uint32_t C;              // kept capacity
-  uint32_t qmax;
-  uint32_t n_splits;
-  uint64_t* cand;          // [B][n_splits][k] (MODE_TOPK / MODE_VECTOR)
-  float* dense_out;        // [N] (MODE_DENSE)
-  const float* vec;        // [n] input scores (MODE_VECTOR)
-  uint32_t vec_n;
-};
-
-// Score one tile of one query into s.acc (local doc d0 .. d0+TILE).
-// Entries are the query's tokens in QUERY ORDER: dense copies (dslot >= 0) are streamed
-// as float4 and accumulated in registers; a CSC-gathered token (dslot < 0) spills the
-// registers to the shared accumulator, scatters its slice, and reloads. Every document
-// therefore sums its terms in query order, whatever the dense/gathered split, tile split
-// or GPU count (bit-identical results across all of them).
-__device__ __forceinline__ void score_tile(const IndexView& ix, const Smem& s, int ne, uint32_t tile,
-                                           uint32_t d0) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t d1 = d0 + TILE;
-  // slice [rs, re) of every gathered row within this tile (one warp per row)
-  for (int e = warp; e < ne; e += NW) {
-    if (s.dslot[e] >= 0) continue;
-    uint32_t sb, se;
-    const int32_t sk = s.skip[e];
-    if (sk >= 0) {
-      const uint32_t* tab = ix.skiptab + (uint64_t)sk * (ix.num_tiles + 1);
-      sb = tab[tile];
-      se = tab[tile + 1];
-    } else {
-      uint32_t cur = s.cursor[e];
-      const uint32_t len = s.row_len[e];
-      const uint32_t* ids = ix.docids + s.row_start[e];
-      sb = cur;
-      while (true) {
-        const uint32_t idx = cur + lane;
-        const bool in = idx < len && __ldg(ids + idx) < d1;
-        const uint32_t c = __popc(__ballot_sync(0xffffffffu, in));
-        cur += c;
-        if (c < 32) break;
-      }
-      se = cur;
-      if (lane == 0) s.cursor[e] = cur;
+// Add the tile slices of entries [e0, e1) (one query's gathered rows, query order) to
+// buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are unique within a
+// row, so a round has no write conflicts); the loads of UNROLL rounds are in flight
+// together, and rounds are applied in entry order with __syncwarp between them, so every
+// document receives its terms in token order without atomics or match.any.
+__device__ __forceinline__ void apply_slices(const IndexView& ix, const WSmem& s, int e0, int e1, float* buf,
+                                             uint32_t d0) {
+  const int lane = threadIdx.x & 31;
+  for (int j0 = e0; j0 < e1; j0 += 32) {
+    const int e = j0 + lane;
+    uint32_t sb = 0, cnt = 0;
+    uint64_t rb = 0;
+    if (e < e1) {
+      sb = s.sb[e];
+      cnt = s.cnt[e];
+      rb = s.row_start[e] + sb;
     }
-    if (lane == 0) {
-      s.rs[e] = sb;
-      s.re[e] = se;
+    const uint32_t nrnd = (cnt + 31) >> 5;
+    const uint32_t rincl = warp_incl_scan(nrnd);
+    const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
+    const uint32_t rexcl = rincl - nrnd;
+    for (uint32_t base = 0; base < rtot; base += UNROLL) {
+      uint32_t doc[UNROLL];
+      float val[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint32_t ridx = base + u;
+        int tk = 0;  // entry of round ridx: largest lane t with rexcl[t] <= ridx
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t ex = __shfl_sync(0xffffffffu, rexcl, tk + step);
+          if (ex <= ridx) tk += step;
+        }
+        const uint32_t tre = __shfl_sync(0xffffffffu, rexcl, tk);
+        const uint32_t tcnt = __shfl_sync(0xffffffffu, cnt, tk);
+        const uint64_t trb = __shfl_sync(0xffffffffu, rb, tk);
+        const uint32_t off = (ridx - tre) * 32 + lane;
+        doc[u] = 0xFFFFFFFFu;
+        val[u] = 0.f;
+        if (ridx < rtot && off < tcnt) {
+          doc[u] = __ldg(ix.docids + trb + off);
+          val[u] = __ldg(ix.values + trb + off);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        if (doc[u] != 0xFFFFFFFFu) buf[doc[u] - d0] += val[u];
+        __syncwarp();
+      }
     }
   }
-  float4 a[F4];
-#pragma unroll
-  for (int r = 0; r < F4; ++r) a[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4* acc4 = reinterpret_cast<float4*>(s.acc);
-  bool in_smem = false;
-  for (int e = 0; e < ne; ++e) {
-    const int32_t slot = s.dslot[e];
-    if (slot >= 0) {
-      if (in_smem) {
-#pragma unroll
-        for (int r = 0; r < F4; ++r) a[r] = acc4[threadIdx.x + r * NT];
-        in_smem = false;
-      }
-      const float4* row = reinterpret_cast<const float4*>(ix.dense + (uint64_t)slot * ix.n_pad + d0);
-#pragma unroll
-      for (int r = 0; r < F4; ++r) {
-        const float4 v = __ldg(row + threadIdx.x + r * NT);
-        a[r].x += v.x;
-        a[r].y += v.y;
-        a[r].z += v.z;
-        a[r].w += v.w;
-      }
-    } else {
-      if (!in_smem) {
-#pragma unroll
-        for (int r = 0; r < F4; ++r) acc4[threadIdx.x + r * NT] = a[r];
-        in_smem = true;
-        __syncthreads();
-      }
-      const uint32_t sb = s.rs[e], se = s.re[e];
-      if (sb == se) continue;
-      const uint64_t base = s.row_start[e];
-      // doc ids are unique within a row: plain shared-memory RMW, no atomics
-      for (uint32_t p = sb + threadIdx.x; p < se; p += NT) {
-        const uint32_t doc = __ldg(ix.docids + base + p);
-        s.acc[doc - d0] += __ldg(ix.values + base + p);
-      }
-      __syncthreads();
-    }
-  }
-  if (!in_smem) {
-#pragma unroll
-    for (int r = 0; r < F4; ++r) acc4[threadIdx.x + r * NT] = a[r];
-  }
-  __syncthreads();
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(NT) k_score_topk(IndexView ix, QueryArgs qa) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem s = carve(smem_raw, qa.C, qa.qmax);
-  const uint32_t q = blockIdx.x / qa.n_splits;
-  const uint32_t split = blockIdx.x % qa.n_splits;
-  const uint32_t n_docs = MODE == MODE_VECTOR ? qa.vec_n : ix.N;
-  const uint32_t n_tiles = (n_docs + TILE - 1) / TILE;
-  const uint32_t t0 = (uint32_t)((uint64_t)split * n_tiles / qa.n_splits);
-  const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * n_tiles / qa.n_splits);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  int ne = 0;
-  if constexpr (MODE != MODE_VECTOR) {
-    // the query's tokens in query order (OOV / locally empty rows dropped)
-    if (threadIdx.x == 0) {
-      const uint64_t qb = qa.q_off[q], qe = qa.q_off[q + 1];
-      int c = 0;
-      for (uint64_t j = qb; j < qe; ++j) {
-        const uint32_t t = qa.q_tok[j];
-        if (t >= ix.V || ix.df_global[t] == 0) continue;  // OOV drop (SPEC tokenizer decisions)
-        const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
-        if (rb == re) continue;  // no local postings
-        const int32_t info = ix.tokinfo[t];
-        s.dslot[c] = info >= 0 ? info : -1;
-        s.row_start[c] = rb;
-        s.row_len[c] = (uint32_t)(re - rb);
-        s.skip[c] = info <= -2 ? -2 - info : -1;
-        ++c;
-      }
-      s.counts[0] = c;
+// Running top-k of query r over one tile (warp-level) from buf[TILE].
+__device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
+                                            uint32_t nvalid, const float* buf) {
+  const int lane = threadIdx.x & 31;
+  const float4* b4 = reinterpret_cast<const float4*>(buf);
+  const uint64_t tau = s.tau[r];
+  const float tf = tau_float(tau);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int rr = 0; rr < F4L; ++rr) {
+    const float4 v = b4[lane + 32 * rr];
+    const uint32_t dl = 4 * (lane + 32 * rr);
+    if (dl + 3 < nvalid) {
+      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (dl + c < nvalid) mx = fmaxf(mx, f4c(v, c));
     }
-    __syncthreads();
-    ne = s.counts[0];
-    // cursors of short rows at the split's first doc (lower_bound, one lane per row)
+  }
+  if (!__any_sync(0xffffffffu, mx >= tf)) return;
+  auto tile_visit = [&](uint64_t thr, auto&& fn) {
+#pragma unroll
+    for (int rr = 0; rr < F4L; ++rr) {
+      const float4 v = b4[lane + 32 * rr];
+      const uint32_t dl = 4 * (lane + 32 * rr);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float x = f4c(v, c);
+        if (x >= tf && dl + c < nvalid) {
+          const uint64_t key = make_key(x, gdoc0 + dl + c);
+          if (key >= thr) fn(key);
+        }
+      }
+    }
+  };
+  uint32_t mine = 0;
+  tile_visit(tau, [&](uint64_t) { ++mine; });
+  const uint32_t incl = warp_incl_scan(mine);
+  const uint32_t P = __shfl_sync(0xffffffffu, incl, 31);
+  uint64_t* kept = s.kept + (size_t)r * C;
+  const uint32_t nk = s.n_kept[r];
+  if (nk + P <= C) {
+    uint64_t* dst = kept + nk + incl - mine;
+    tile_visit(tau, [&](uint64_t key) { *dst++ = key; });
+    __syncwarp();
+    if (lane == 0) s.n_kept[r] = nk + P;
+  } else {
+    const uint64_t nt = warp_select_kth(
+        [&](auto&& fn) {
+          for (uint32_t i = lane; i < nk; i += 32) fn(kept[i]);
+          tile_visit(tau, fn);
+        },
+        k, s.hist);
+    // in-place compaction of kept (destination never passes the source chunk)
+    uint32_t out = 0;
+    for (uint32_t b = 0; b < nk; b += 32) {
+      const uint32_t i = b + lane;
+      const uint64_t x = i < nk ? kept[i] : 0ull;
+      const bool keep = i < nk && x >= nt;
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) kept[out + __popc(bal & lanemask_lt())] = x;
+      out += __popc(bal);
+      __syncwarp();
+    }
+    uint32_t m2 = 0;
+    tile_visit(nt, [&](uint64_t) { ++m2; });
+    const uint32_t inc2 = warp_incl_scan(m2);
+    const uint32_t tot2 = __shfl_sync(0xffffffffu, inc2, 31);
+    uint64_t* dst = kept + out + inc2 - m2;
+    tile_visit(nt, [&](uint64_t key) { *dst++ = key; });
+    __syncwarp();
+    if (lane == 0) {
+      s.n_kept[r] = out + tot2;
+      s.tau[r] = nt;
+    }
+  }
+  __syncwarp();
+}
+
+// One warp per (run, doc split): a run is <= R queries with the same dense signature.
+// No CTA-level synchronisation: warps progress independently.
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((uint32_t)warp >= ra.wpc) return;
+  const uint32_t n_runs = *ra.n_runs;
+  const uint64_t item = (uint64_t)blockIdx.x * ra.wpc + warp;
+  if (item >= (uint64_t)n_runs * ra.n_splits) return;
+  const WSmem s = wcarve(smem_raw + (size_t)warp * ra.warp_bytes, ra.R, ra.C, ra.qmax);
+  const uint32_t run = (uint32_t)(item / ra.n_splits), split = (uint32_t)(item % ra.n_splits);
+  const uint32_t pb = ra.run_begin[run];
+  const uint32_t nr = ra.run_begin[run + 1] - pb;
+  const uint32_t t0 = (uint32_t)((uint64_t)split * ix.num_tiles / ra.n_splits);
+  const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * ix.num_tiles / ra.n_splits);
+
+  // ---- setup: lane r classifies query r's tokens; gathered rows are concatenated
+  {
+    const bool act = (uint32_t)lane < nr;
+    const uint32_t q = act ? ra.perm[pb + lane] : 0u;
+    const uint64_t qb = act ? ra.q_off[q] : 0, qe = act ? ra.q_off[q + 1] : 0;
+    uint32_t ns = 0, nd = 0;
+    for (uint64_t j = qb; j < qe; ++j) {
+      const uint32_t t = ra.q_tok[j];
+      if (t >= ix.V || ix.df_global[t] == 0 || ix.indptr[t] == ix.indptr[t + 1]) continue;
+      if (ix.tokinfo[t] >= 0) ++nd; else ++ns;
+    }
+    const uint32_t incl = warp_incl_scan(ns);
+    uint32_t e = incl - ns;
+    if (act) s.ebeg[lane] = (int32_t)e;
+    if (lane == 31) s.ebeg[nr] = (int32_t)incl;
+    nd = 0;
+    for (uint64_t j = qb; j < qe; ++j) {
+      const uint32_t t = ra.q_tok[j];
+      if (t >= ix.V || ix.df_global[t] == 0) continue;  // OOV drop (SPEC tokenizer decisions)
+      const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
+      if (rb == re) continue;                           // no local postings
+      const int32_t info = ix.tokinfo[t];
+      if (info >= 0) {
+        if (lane == 0) s.dslot[nd] = info;  // identical multiset for every query of the run
+        ++nd;
+      } else {
+        s.row_start[e] = rb;
+        s.row_len[e] = (uint32_t)(re - rb);
+        s.skip[e] = info <= -2 ? -2 - info : -1;
+        ++e;
+      }
+    }
+    if (act) {
+      s.n_kept[lane] = 0;
+      s.tau[lane] = 0;
+    }
+    if (lane == 0) {
+      for (uint32_t a = 1; a < nd; ++a) {  // canonical (ascending slot) order of the dense terms
+        const int32_t x = s.dslot[a];
+        int b = (int)a - 1;
+        while (b >= 0 && s.dslot[b] > x) {
+          s.dslot[b + 1] = s.dslot[b];
+          --b;
+        }
+        s.dslot[b + 1] = x;
+      }
+      s.nd[0] = (int32_t)nd;
+    }
+  }
+  __syncwarp();
+  const int E = s.ebeg[nr];
+  const int nd = s.nd[0];
+  // short rows: cursor = lower_bound(split's first doc), nextdoc = doc at the cursor
+  {
     const uint32_t dstart = t0 * TILE;
-    for (int e = warp; e < ne; e += NW) {
-      if (lane == 0 && s.dslot[e] < 0 && s.skip[e] < 0) {
+    for (int e = lane; e < E; e += 32) {
+      if (s.skip[e] < 0) {
         const uint32_t* ids = ix.docids + s.row_start[e];
-        uint32_t lo = 0, hi = s.row_len[e];
+        const uint32_t len = s.row_len[e];
+        uint32_t lo = 0, hi = len;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (ids[mid] < dstart) lo = mid + 1; else hi = mid;
+          if (__ldg(ids + mid) < dstart) lo = mid + 1; else hi = mid;
         }
         s.cursor[e] = lo;
+        s.nextdoc[e] = lo < len ? __ldg(ids + lo) : 0xFFFFFFFFu;
       }
     }
+  }
+  __syncwarp();
+  const uint32_t rstride = ix.n_pad / 4;
+  float4* dsum4 = reinterpret_cast<float4*>(s.dsum);
+  float4* acc4 = reinterpret_cast<float4*>(s.acc);
+
+  for (uint32_t tile = t0; tile < t1; ++tile) {
+    const uint32_t d0 = tile * TILE, d1 = d0 + TILE;
+    const uint32_t nvalid = min((uint32_t)TILE, ix.N - d0);
+    // (1) slices of every gathered row of the run in this tile (lanes over entries)
+    for (int e = lane; e < E; e += 32) {
+      const int32_t sk = s.skip[e];
+      uint32_t sb, cnt;
+      if (sk >= 0) {
+        const uint32_t* tab = ix.skiptab + (uint64_t)sk * (ix.num_tiles + 1) + tile;
+        sb = __ldg(tab);
+        cnt = __ldg(tab + 1) - sb;
+      } else {
+        sb = s.cursor[e];
+        cnt = 0;
+        if (s.nextdoc[e] < d1) {
+          const uint32_t* ids = ix.docids + s.row_start[e];
+          const uint32_t len = s.row_len[e];
+          uint32_t cur = sb + 1, nxt = 0xFFFFFFFFu;
+          while (cur < len) {
+            nxt = __ldg(ids + cur);
+            if (nxt >= d1) break;
+            ++cur;
+          }
+          if (cur >= len) nxt = 0xFFFFFFFFu;
+          cnt = cur - sb;
+          s.cursor[e] = cur;
+          s.nextdoc[e] = nxt;
+        }
+      }
+      s.sb[e] = sb;
+      s.cnt[e] = cnt;
+    }
+    // (2) dense signature of the run, ascending slot order, all loads in flight
+    {
+      float4 a[F4L];
+#pragma unroll
+      for (int rr = 0; rr < F4L; ++rr) a[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane;
+      for (int i = 0; i < nd; ++i) {
+        const float4* row = dbase + (uint64_t)s.dslot[i] * rstride;
+        float4 v[F4L];
+#pragma unroll
+        for (int rr = 0; rr < F4L; ++rr) v[rr] = __ldg(row + 32 * rr);
+#pragma unroll
+        for (int rr = 0; rr < F4L; ++rr) {
+          a[rr].x += v[rr].x;
+          a[rr].y += v[rr].y;
+          a[rr].z += v[rr].z;
+          a[rr].w += v[rr].w;
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < F4L; ++rr) dsum4[lane + 32 * rr] = a[rr];
+    }
+    __syncwarp();
+    // (3) per query: gathered rows, then the running top-k
+    for (uint32_t r = 0; r < nr; ++r) {
+      const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
+      uint32_t c = 0;
+      for (int e = e0 + lane; e < e1; e += 32) c += s.cnt[e];
+      const bool has = __any_sync(0xffffffffu, c != 0);
+      float* buf = s.dsum;
+      if (has) {
+        if (nr > 1) {  // keep the shared dense sum intact for the run's other queries
+#pragma unroll
+          for (int rr = 0; rr < F4L; ++rr) acc4[lane + 32 * rr] = dsum4[lane + 32 * rr];
+          __syncwarp();
+          buf = s.acc;
+        }
+        apply_slices(ix, s, e0, e1, buf, d0);
+        __syncwarp();
+      }
+      if constexpr (MODE == GM_DENSE) {
+        const double qc = ra.qconst[ra.perm[pb + r]];
+        for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
+        __syncwarp();
+      } else {
+        filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf);
+      }
+    }
+    __syncwarp();
+  }
+  if constexpr (MODE == GM_TOPK) {
+    for (uint32_t r = 0; r < nr; ++r) {
+      const uint32_t q = ra.perm[pb + r];
+      const uint32_t nk = s.n_kept[r];
+      const uint64_t* kept = s.kept + (size_t)r * ra.C;
+      uint64_t* out = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
+      for (uint32_t i = lane; i < ra.C; i += 32) out[i] = i < nk ? kept[i] : kInvalidKey;
+    }
+  }
+}
+
+// Per query: sorted dense signature (slots of rows with a dense copy) and its hash.
+__global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
+                            IndexView ix, uint32_t qmax, int32_t* __restrict__ qdense, uint32_t* __restrict__ nden,
+                            uint32_t* __restrict__ hkey, uint32_t* __restrict__ hval) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
+    int32_t* d = qdense + (uint64_t)q * qmax;
+    uint32_t n = 0;
+    for (uint64_t j = q_off[q]; j < q_off[q + 1]; ++j) {
+      const uint32_t t = q_tok[j];
+      if (t >= ix.V || ix.df_global[t] == 0 || ix.indptr[t] == ix.indptr[t + 1]) continue;
+      const int32_t info = ix.tokinfo[t];
+      if (info < 0) continue;
+      int b = (int)n - 1;
+      while (b >= 0 && d[b] > info) {
+        d[b + 1] = d[b];
+        --b;
+      }
+      d[b + 1] = info;
+      ++n;
+    }
+    uint32_t h = 2166136261u ^ n;  // FNV-1a over the sorted slots
+    for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
+    nden[q] = n;
+    hkey[q] = h;
+    hval[q] = q;
+  }
+}
+
+__device__ __forceinline__ bool same_signature(const int32_t* qdense, const uint32_t* nden, uint32_t qmax,
+                                               uint32_t a, uint32_t b) {
+  if (nden[a] != nden[b]) return false;
+  const int32_t* x = qdense + (uint64_t)a * qmax;
+  const int32_t* y = qdense + (uint64_t)b * qmax;
+  for (uint32_t i = 0; i < nden[a]; ++i)
+    if (x[i] != y[i]) return false;
+  return true;
+}
+
+// Runs over the signature-sorted queries: maximal stretches of identical signatures, cut
+// every R queries. One block of 1024 threads walks the batch in chunks.
+__global__ void __launch_bounds__(1024) k_build_runs(const uint32_t* __restrict__ perm, uint32_t B,
+                                                     const int32_t* __restrict__ qdense,
+                                                     const uint32_t* __restrict__ nden, uint32_t qmax, uint32_t R,
+                                                     uint32_t* __restrict__ run_begin, uint32_t* __restrict__ n_runs) {
+  __shared__ uint32_t sw[40];
+  __shared__ uint32_t wmax[32];
+  __shared__ uint32_t carry_start, carry_count;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    carry_start = 0;
+    carry_count = 0;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < B; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const bool valid = i < B;
+    const bool sighead = valid && (i == 0 || !same_signature(qdense, nden, qmax, perm[i], perm[i - 1]));
+    // inclusive max-scan of signature-run heads -> start of i's signature run
+    uint32_t m = sighead ? i : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, m, o);
+      if (lane >= o) m = max(m, t);
+    }
+    if (lane == 31) wmax[w] = m;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t x = wmax[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = max(x, t);
+      }
+      wmax[lane] = x;
+    }
+    __syncthreads();
+    const uint32_t prev = w > 0 ? wmax[w - 1] : 0u;
+    const uint32_t start = max(max(m, prev), carry_start);
+    const bool head = valid && ((i - start) % R == 0);
+    uint32_t tot;
+    const uint32_t off = block_excl_scan(head ? 1u : 0u, sw, &tot) + carry_count;
+    if (head) run_begin[off] = i;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1 || i == B - 1) carry_start = start;
+    if (threadIdx.x == 0) carry_count += tot;
     __syncthreads();
   }
+  if (threadIdx.x == 0) {
+    run_begin[carry_count] = B;
+    *n_runs = carry_count;
+  }
+}
 
+// top-k over an arbitrary f32 vector (SPEC top_k on its own): CTA per split of tiles,
+// block-level filter + select, candidates [n_splits][C].
+__global__ void __launch_bounds__(NT) k_topk_vector(const float* __restrict__ vec, uint32_t n, uint32_t k,
+                                                    uint32_t C, uint32_t n_splits, uint64_t* cand) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* acc = (float*)smem_raw;
+  uint64_t* kept[2] = {(uint64_t*)(acc + TILE), (uint64_t*)(acc + TILE) + C};
+  uint32_t* hist = (uint32_t*)(kept[1] + C);
+  uint32_t* sw = hist + 256;
+  const uint32_t split = blockIdx.x;
+  const uint32_t n_tiles = (n + TILE - 1) / TILE;
+  const uint32_t t0 = (uint32_t)((uint64_t)split * n_tiles / n_splits);
+  const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * n_tiles / n_splits);
   uint32_t n_kept = 0;
   uint64_t tau = 0;
   int cur = 0;
-  const double qc = (MODE == MODE_VECTOR) ? 0.0 : qa.qconst[q];
-
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint32_t d0 = tile * TILE;
-    const uint32_t nvalid = min((uint32_t)TILE, n_docs - d0);
-    if constexpr (MODE == MODE_VECTOR) {
-      for (uint32_t i = threadIdx.x; i < TILE; i += NT) s.acc[i] = i < nvalid ? qa.vec[d0 + i] : 0.f;
-      __syncthreads();
-    } else {
-      score_tile(ix, s, ne, tile, d0);
-    }
-    if constexpr (MODE == MODE_DENSE) {
-      for (uint32_t i = threadIdx.x; i < nvalid; i += NT)
-        qa.dense_out[d0 + i] = __double2float_rn((double)s.acc[i] + qc);
-      __syncthreads();
-      continue;
-    }
-    const uint32_t gdoc0 = (MODE == MODE_VECTOR ? 0u : ix.doc_base) + d0;
-    // candidates of this tile that clear the running threshold
-    auto tile_visit = [&](uint64_t thr, auto&& f) {
-#pragma unroll
-      for (int r = 0; r < F4; ++r) {
-        const uint32_t dl = 4 * (threadIdx.x + r * NT);
-        const float4 v = reinterpret_cast<const float4*>(s.acc)[threadIdx.x + r * NT];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (dl + c < nvalid) {
-            const float x = c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-            const uint64_t key = make_key(x, gdoc0 + dl + c);
-            if (key >= thr) f(key);
-          }
-        }
+    const uint32_t nvalid = min((uint32_t)TILE, n - d0);
+    for (uint32_t i = threadIdx.x; i < TILE; i += NT) acc[i] = i < nvalid ? vec[d0 + i] : 0.f;
+    __syncthreads();
+    auto visit = [&](uint64_t thr, auto&& f) {
+      for (uint32_t i = threadIdx.x; i < nvalid; i += NT) {
+        const uint64_t key = make_key(acc[i], d0 + i);
+        if (key >= thr) f(key);
       }
     };
     uint32_t mine = 0;
-    tile_visit(tau, [&](uint64_t) { ++mine; });
+    visit(tau, [&](uint64_t) { ++mine; });
     uint32_t P;
-    uint32_t off = block_excl_scan(mine, s.sw, &P);
-    if (n_kept + P <= qa.C) {
-      uint64_t* dst = s.kept[cur] + n_kept + off;
-      tile_visit(tau, [&](uint64_t key) { *dst++ = key; });
+    const uint32_t off = block_excl_scan(mine, sw, &P);
+    if (n_kept + P <= C) {
+      uint64_t* dst = kept[cur] + n_kept + off;
+      visit(tau, [&](uint64_t key) { *dst++ = key; });
       n_kept += P;
-      __syncthreads();
     } else {
-      const uint64_t* kb = s.kept[cur];
+      const uint64_t* kb = kept[cur];
       const uint32_t nk = n_kept;
       const uint64_t old = tau;
       tau = block_select_kth(
           [&](auto&& f) {
             for (uint32_t i = threadIdx.x; i < nk; i += NT) f(kb[i]);
-            tile_visit(old, f);
+            visit(old, f);
           },
-          qa.k, s.hist, s.sw + 36);
+          k, hist, sw + 36);
       uint32_t m2 = 0;
       for (uint32_t i = threadIdx.x; i < nk; i += NT) m2 += kb[i] >= tau;
-      tile_visit(tau, [&](uint64_t) { ++m2; });
+      visit(tau, [&](uint64_t) { ++m2; });
       uint32_t tot;
-      const uint32_t o2 = block_excl_scan(m2, s.sw, &tot);
-      uint64_t* dst = s.kept[cur ^ 1] + o2;
+      const uint32_t o2 = block_excl_scan(m2, sw, &tot);
+      uint64_t* dst = kept[cur ^ 1] + o2;
       for (uint32_t i = threadIdx.x; i < nk; i += NT)
         if (kb[i] >= tau) *dst++ = kb[i];
-      tile_visit(tau, [&](uint64_t key) { *dst++ = key; });
+      visit(tau, [&](uint64_t key) { *dst++ = key; });
       n_kept = tot;
       cur ^= 1;
-      __syncthreads();
     }
-  }
-  if constexpr (MODE == MODE_DENSE) return;
-  else {
-
-  // emit this split's best min(k, n_kept) keys, sorted descending
-  if (n_kept > qa.k) {
-    const uint64_t* kb = s.kept[cur];
-    const uint32_t nk = n_kept;
-    const uint64_t t2 = block_select_kth(
-        [&](auto&& f) {
-          for (uint32_t i = threadIdx.x; i < nk; i += NT) f(kb[i]);
-        },
-        qa.k, s.hist, s.sw + 36);
-    uint32_t m2 = 0;
-    for (uint32_t i = threadIdx.x; i < nk; i += NT) m2 += kb[i] >= t2;
-    uint32_t tot;
-    const uint32_t o2 = block_excl_scan(m2, s.sw, &tot);
-    uint64_t* dst = s.kept[cur ^ 1] + o2;
-    for (uint32_t i = threadIdx.x; i < nk; i += NT)
-      if (kb[i] >= t2) *dst++ = kb[i];
-    n_kept = tot;
-    cur ^= 1;
     __syncthreads();
   }
-  const uint32_t m = min(n_kept, qa.k);
-  const uint32_t p2 = next_pow2(max(m, 2u));
-  uint64_t* buf = s.kept[cur];
-  for (uint32_t i = m + threadIdx.x; i < p2; i += NT) buf[i] = kInvalidKey;
-  __syncthreads();
-  block_bitonic_desc(buf, p2);
-  uint64_t* out = qa.cand + ((uint64_t)q * qa.n_splits + split) * qa.k;
-  for (uint32_t i = threadIdx.x; i < qa.k; i += NT) out[i] = i < m ? buf[i] : kInvalidKey;
-  }
+  uint64_t* out = cand + (uint64_t)split * C;
+  for (uint32_t i = threadIdx.x; i < C; i += NT) out[i] = i < n_kept ? kept[cur][i] : kInvalidKey;
 }
 
-// Per query: top-k over n_splits x k candidate keys (invalid = 0), sorted, decoded.
+// Per query: top-k over n_splits x per_split candidate keys (invalid = 0), sorted, decoded.
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand, uint32_t n_splits,
-                                               uint64_t split_stride, uint64_t query_stride, uint32_t k,
-                                               const double* __restrict__ qconst, uint32_t* out_ids,
+                                               uint32_t per_split, uint64_t split_stride, uint64_t query_stride,
+                                               uint32_t k, const double* __restrict__ qconst, uint32_t* out_ids,
                                                float* out_scores, uint64_t* out_keys) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* buf = (uint64_t*)smem_raw;  // [p2]
@@ -448,8 +766,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
   uint32_t* sw = hist + 256;
   const uint32_t q = blockIdx.x;
   const uint64_t* base = cand + (uint64_t)q * query_stride;
-  const uint64_t total = (uint64_t)n_splits * k;
-  auto at = [&](uint64_t i) { return base[(i / k) * split_stride + (i % k)]; };
+  const uint64_t total = (uint64_t)n_splits * per_split;
+  auto at = [&](uint64_t i) { return base[(i / per_split) * split_stride + (i % per_split)]; };
 
   uint32_t mine = 0;
   for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) mine += at(i) != kInvalidKey;
@@ -484,8 +802,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
     if (out_keys) out_keys[(uint64_t)q * k + i] = key;
     if (out_ids) out_ids[(uint64_t)q * k + i] = i < m ? key_doc(key) : 0xFFFFFFFFu;
     if (out_scores)
-      out_scores[(uint64_t)q * k + i] =
-          i < m ? __double2float_rn((double)key_score(key) + qc) : -INFINITY;
+      out_scores[(uint64_t)q * k + i] = i < m ? __double2float_rn((double)key_score(key) + qc) : -INFINITY;
   }
 }
 
@@ -572,36 +889,47 @@ int num_sms(int device) {
   return cache[device];
 }
 
-template <int MODE>
-int32_t launch_score(const IndexView& ix, QueryArgs& qa, cudaStream_t st, int device, uint32_t n_docs,
-                     uint32_t n_blocks_per_item_hint) {
-  const size_t smem = smem_bytes(qa.C, qa.qmax);
-  if (smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "top-k / query length too large for shared memory");
-  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_topk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const uint32_t n_tiles = (n_docs + TILE - 1) / TILE;
-  if (n_blocks_per_item_hint) {
-    qa.n_splits = std::min(n_blocks_per_item_hint, std::max(1u, n_tiles));
-  } else {
-    int per_sm = 0;
-    SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_topk<MODE>, NT, smem));
-    const uint64_t target = (uint64_t)std::max(1, per_sm) * num_sms(device) * 2;
-    uint64_t ns = (target + qa.B - 1) / qa.B;
-    ns = std::max<uint64_t>(1, std::min<uint64_t>(ns, std::max(1u, n_tiles)));
-    qa.n_splits = (uint32_t)ns;
-  }
-  const uint64_t grid = (uint64_t)qa.B * qa.n_splits;
-  if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
-  k_score_topk<MODE><<<(unsigned)grid, NT, smem, st>>>(ix, qa);
-  SL_CUDA_TRY(cudaGetLastError());
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+struct RunPlan {
+  uint32_t R, C, wpc, n_splits, warp_bytes;
+  size_t smem;
+};
+
+// Warps per CTA under a shared-memory budget (3 CTAs/SM); splits so that the expected
+// number of warp work items covers several waves. SL_SMEM_BUDGET / SL_SPLITS / SL_RUN
+// override the plan in tuning runs.
+int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
+  p->C = kept_capacity(k);
+  uint32_t R = (uint32_t)env_int("SL_RUN", 0);
+  if (R == 0) R = p->C <= 256 ? RMAX : (p->C <= 1024 ? 2 : 1);
+  p->R = std::max(1u, std::min<uint32_t>(R, 32));
+  p->warp_bytes = (uint32_t)warp_smem_bytes(p->R, p->C, qmax);
+  const size_t budget = (size_t)env_int("SL_SMEM_BUDGET", 72 * 1024);
+  p->wpc = (uint32_t)std::max<size_t>(1, std::min<size_t>(NW, budget / p->warp_bytes));
+  p->smem = (size_t)p->wpc * p->warp_bytes;
+  if (p->smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "top-k / query length too large for shared memory");
+  int per_sm = 0;
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK>, NT, p->smem));
+  const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
+  const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
+  uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
+  if (ns == 0) ns = (uint32_t)std::max<uint64_t>(1, (4 * warps + items - 1) / items);
+  p->n_splits = std::max(1u, std::min(ns, std::max(1u, ix->num_tiles)));
   return SL_OK;
 }
 
-int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint64_t split_stride,
+int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32_t per_split, uint64_t split_stride,
                      uint64_t query_stride, uint32_t k, const double* qconst, uint32_t* ids, float* scores,
                      uint64_t* keys, cudaStream_t st) {
   const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4;
   SL_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_merge<<<B, 256, smem, st>>>(cand, n_splits, split_stride, query_stride, k, qconst, ids, scores, keys);
+  k_merge<<<B, 256, smem, st>>>(cand, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores,
+                                keys);
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
@@ -625,12 +953,10 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   cudaStream_t st = sc->st;
   Scratch scr(st);
 
-  // queries on the device
   const uint64_t* d_off = q_offsets;
   const uint32_t* d_tok = q_tokens;
-  uint64_t ntok = 0;
   if (mem == SL_MEM_HOST) {
-    ntok = q_offsets[B];
+    const uint64_t ntok = q_offsets[B];
     uint64_t* o;
     uint32_t* t;
     SL_TRY(scr.alloc(&o, (uint64_t)B + 1));
@@ -657,35 +983,53 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_info[0] & 2u) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
-  if (h_info[1] > (uint32_t)kQMax) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: queries longer than 256 tokens are not supported");
+  if (h_info[1] > (uint32_t)kQMax)
+    SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: queries longer than 256 tokens are not supported");
 
-  QueryArgs qa{};
-  qa.q_off = d_off;
-  qa.q_tok = d_tok;
-  qa.qconst = qconst;
-  qa.B = B;
-  qa.k = k;
-  qa.C = kept_capacity(k);
-  qa.qmax = std::max(1u, h_info[1]);
-  SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
-  // split count is known only inside launch_score; allocate for the worst case first
-  {
-    const size_t smem = smem_bytes(qa.C, qa.qmax);
-    if (smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "top-k / query length too large for shared memory");
-  }
-  int per_sm = 0;
-  {
-    const size_t smem = smem_bytes(qa.C, qa.qmax);
-    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_topk<MODE_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_topk<MODE_TOPK>, NT, smem));
-  }
-  const uint32_t n_tiles = std::max(1u, ix->num_tiles);
-  const uint64_t target = (uint64_t)std::max(1, per_sm) * num_sms(ix->device) * 2;
-  const uint32_t n_splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((target + B - 1) / B, n_tiles));
+  const uint32_t qmax = std::max(1u, h_info[1]);
+  RunPlan plan;
+  SL_TRY(plan_runs(ix, B, k, qmax, &plan));
+  // group queries by dense signature: sort by signature hash, cut runs of <= R identical ones
+  int32_t* qdense;
+  uint32_t *nden, *hk, *hv, *k0, *k1, *v0, *v1, *run_begin, *n_runs;
+  SL_TRY(scr.alloc(&qdense, (uint64_t)B * qmax));
+  SL_TRY(scr.alloc(&nden, B));
+  SL_TRY(scr.alloc(&hk, B));
+  SL_TRY(scr.alloc(&hv, B));
+  SL_TRY(scr.alloc(&k0, B));
+  SL_TRY(scr.alloc(&k1, B));
+  SL_TRY(scr.alloc(&v0, B));
+  SL_TRY(scr.alloc(&v1, B));
+  SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
+  SL_TRY(scr.alloc(&n_runs, 1));
+  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv);
+  const uint32_t *sk, *perm;
+  SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
+  k_build_runs<<<1, 1024, 0, st>>>(perm, B, qdense, nden, qmax, plan.R, run_begin, n_runs);
+  SL_CUDA_TRY(cudaGetLastError());
+  RunArgs ra{};
+  ra.q_off = d_off;
+  ra.q_tok = d_tok;
+  ra.qconst = qconst;
+  ra.perm = perm;
+  ra.run_begin = run_begin;
+  ra.n_runs = n_runs;
+  ra.k = k;
+  ra.C = plan.C;
+  ra.R = plan.R;
+  ra.qmax = qmax;
+  ra.n_splits = plan.n_splits;
+  ra.wpc = plan.wpc;
+  ra.warp_bytes = plan.warp_bytes;
   uint64_t* cand;
-  SL_TRY(scr.alloc(&cand, (uint64_t)B * n_splits * k));
-  qa.cand = cand;
-  SL_TRY(launch_score<MODE_TOPK>(v, qa, st, ix->device, ix->N, n_splits));
+  SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
+  ra.cand = cand;
+  // upper bound on runs is B; warps past the real run count exit at once
+  const uint64_t grid = ((uint64_t)B * plan.n_splits + plan.wpc - 1) / plan.wpc;
+  if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
+  SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
+  k_score_runs<GM_TOPK><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+  SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
 
   uint32_t* ids_dev = nullptr;
@@ -699,16 +1043,15 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
       SL_TRY(scr.alloc(&sc_dev, (uint64_t)B * k));
     }
   }
+  const uint64_t qstride = (uint64_t)plan.n_splits * plan.C;
   if (!dist) {
-    SL_TRY(launch_merge(cand, B, qa.n_splits, k, (uint64_t)qa.n_splits * k, k, qconst, ids_dev, sc_dev,
-                        nullptr, st));
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids_dev, sc_dev, nullptr, st));
   } else {
     // local merge -> keys, gather the G x k candidates on rank 0 (NCCL), merge there
     const sl_comm* cm = ix->comm;
     uint64_t* local;
     SL_TRY(scr.alloc(&local, (uint64_t)B * k));
-    SL_TRY(launch_merge(cand, B, qa.n_splits, k, (uint64_t)qa.n_splits * k, k, nullptr, nullptr, nullptr, local,
-                        st));
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, local, st));
     uint64_t* gathered = nullptr;
     if (cm->rank == 0) SL_TRY(scr.alloc(&gathered, (uint64_t)cm->nranks * B * k));
     const size_t cnt = (size_t)B * k;
@@ -720,7 +1063,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     SL_TRY(nccl_check(nccl().Send(local, cnt, ncclUint64, 0, cm->comm, st), "ncclSend"));
     SL_TRY(nccl_check(nccl().GroupEnd(), "ncclGroupEnd"));
     if (cm->rank == 0)
-      SL_TRY(launch_merge(gathered, B, (uint32_t)cm->nranks, cnt, k, k, qconst, ids_dev, sc_dev, nullptr, st));
+      SL_TRY(launch_merge(gathered, B, (uint32_t)cm->nranks, k, cnt, k, k, qconst, ids_dev, sc_dev, nullptr, st));
   }
   SL_CUDA_TRY(cudaEventRecord(sc->ev[3], st));
   if (want_out && mem == SL_MEM_HOST) {
@@ -775,16 +1118,32 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
   SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
-  QueryArgs qa{};
-  qa.q_off = d_off;
-  qa.q_tok = d_tok;
-  qa.qconst = qconst;
-  qa.B = 1;
-  qa.k = 1;
-  qa.C = kept_capacity(1);
-  qa.qmax = std::max(1u, q_len);
-  qa.dense_out = d_out;
-  SL_TRY(launch_score<MODE_DENSE>(v, qa, st, ix->device, ix->N, std::max(1u, ix->num_tiles)));
+  // one run holding the single query, one warp per tile
+  const uint32_t h_runs[3] = {0u, 1u, 1u};  // run_begin = {0, 1}; n_runs = 1
+  uint32_t *d_runs, *d_perm;
+  SL_TRY(scr.alloc(&d_runs, 3));
+  SL_TRY(scr.alloc(&d_perm, 1));
+  SL_CUDA_TRY(cudaMemcpyAsync(d_runs, h_runs, 12, cudaMemcpyHostToDevice, st));
+  SL_CUDA_TRY(cudaMemsetAsync(d_perm, 0, 4, st));
+  RunArgs ra{};
+  ra.q_off = d_off;
+  ra.q_tok = d_tok;
+  ra.qconst = qconst;
+  ra.perm = d_perm;
+  ra.run_begin = d_runs;
+  ra.n_runs = d_runs + 2;
+  ra.k = 1;
+  ra.C = kept_capacity(1);
+  ra.R = 1;
+  ra.qmax = std::max(1u, q_len);
+  ra.n_splits = std::max(1u, ix->num_tiles);
+  ra.wpc = NW;
+  ra.warp_bytes = (uint32_t)warp_smem_bytes(ra.R, ra.C, ra.qmax);
+  ra.dense_out = d_out;
+  const size_t smem = (size_t)ra.wpc * ra.warp_bytes;
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_score_runs<GM_DENSE><<<(ra.n_splits + NW - 1) / NW, NT, smem, st>>>(v, ra);
+  SL_CUDA_TRY(cudaGetLastError());
   if (mem == SL_MEM_HOST)
     SL_CUDA_TRY(cudaMemcpyAsync(out, d_out, (uint64_t)ix->N * 4, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
@@ -816,26 +1175,21 @@ int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int
     SL_TRY(scr.alloc(&ids_dev, k));
     SL_TRY(scr.alloc(&sc_dev, k));
   }
-  IndexView v{};
-  QueryArgs qa{};
-  qa.B = 1;
-  qa.k = k;
-  qa.C = kept_capacity(k);
-  qa.qmax = 1;
-  qa.vec = d_in;
-  qa.vec_n = n;
+  const uint32_t C = std::max(512u, kept_capacity(k));
   const uint32_t n_tiles = std::max(1u, (n + TILE - 1) / TILE);
   const uint32_t n_splits = std::min<uint32_t>(n_tiles, 148 * 4);
   uint64_t* cand;
-  SL_TRY(scr.alloc(&cand, (uint64_t)n_splits * k));
-  qa.cand = cand;
+  SL_TRY(scr.alloc(&cand, (uint64_t)n_splits * C));
   if (n) {
-    SL_TRY(launch_score<MODE_VECTOR>(v, qa, st, device, n, n_splits));
+    const size_t smem = (size_t)TILE * 4 + 2 * (size_t)C * 8 + 256 * 4 + 40 * 4;
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_topk_vector, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_topk_vector<<<n_splits, NT, smem, st>>>(d_in, n, k, C, n_splits, cand);
+    SL_CUDA_TRY(cudaGetLastError());
   } else {
-    qa.n_splits = 1;
-    SL_CUDA_TRY(cudaMemsetAsync(cand, 0, (uint64_t)k * 8, st));
+    SL_CUDA_TRY(cudaMemsetAsync(cand, 0, (uint64_t)C * 8, st));
   }
-  SL_TRY(launch_merge(cand, 1, qa.n_splits, k, (uint64_t)qa.n_splits * k, k, nullptr, ids_dev, sc_dev, nullptr, st));
+  SL_TRY(launch_merge(cand, 1, n ? n_splits : 1, C, C, (uint64_t)n_splits * C, k, nullptr, ids_dev, sc_dev, nullptr,
+                      st));
   if (mem == SL_MEM_HOST) {
     SL_CUDA_TRY(cudaMemcpyAsync(out_ids, ids_dev, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
     SL_CUDA_TRY(cudaMemcpyAsync(out_scores, sc_dev, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
