@@ -43,7 +43,7 @@ struct Status {
 // ---------------------------------------------------------------- constants
 constexpr int kTileDocs = 512;         // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
 constexpr int kScoreThreads = 256;     // threads per scoring CTA
-constexpr int kQMax = 256;             // max query tokens handled per query
+constexpr int kQMax = 32;              // max query tokens (one lane per gathered row)
 constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path
 constexpr uint64_t kInvalidKey = 0ull; // never produced by a real (score, doc) key
 

@@ -280,55 +280,47 @@ __device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_
   return s;
 }
 
-// Add the tile slices of entries [e0, e1) (one query's gathered rows, query order) to
-// buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are unique within a
-// row, so a round has no write conflicts); the loads of UNROLL rounds are in flight
-// together, and rounds are applied in entry order with __syncwarp between them, so every
-// document receives its terms in token order without atomics or match.any.
-__device__ __forceinline__ void apply_slices(const IndexView& ix, const WSmem& s, int e0, int e1, float* buf,
-                                             uint32_t d0) {
+// Add the tile slices of the query owning lanes [e0, e1) (lane = gathered-row entry, in
+// query order) to buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are
+// unique within a row, so a round has no write conflicts); the loads of UNROLL rounds
+// are in flight together, and rounds are applied in entry order with __syncwarp between
+// them, so every document receives its terms in token order without atomics.
+// sb/cnt/rbase are this lane's entry slice (ignored outside [e0, e1)).
+__device__ __forceinline__ void apply_slices(const IndexView& ix, int e0, int e1, uint32_t cnt, uint64_t rbase,
+                                             float* buf, uint32_t d0) {
   const int lane = threadIdx.x & 31;
-  for (int j0 = e0; j0 < e1; j0 += 32) {
-    const int e = j0 + lane;
-    uint32_t sb = 0, cnt = 0;
-    uint64_t rb = 0;
-    if (e < e1) {
-      sb = s.sb[e];
-      cnt = s.cnt[e];
-      rb = s.row_start[e] + sb;
+  const bool mine = lane >= e0 && lane < e1;
+  const uint32_t nrnd = mine ? (cnt + 31) >> 5 : 0u;
+  const uint32_t rincl = warp_incl_scan(nrnd);
+  const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
+  const uint32_t rexcl = rincl - nrnd;
+  for (uint32_t base = 0; base < rtot; base += UNROLL) {
+    uint32_t doc[UNROLL];
+    float val[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint32_t ridx = base + u;
+      int tk = 0;  // entry of round ridx: largest lane t with rexcl[t] <= ridx
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t ex = __shfl_sync(0xffffffffu, rexcl, tk + step);
+        if (ex <= ridx) tk += step;
+      }
+      const uint32_t tre = __shfl_sync(0xffffffffu, rexcl, tk);
+      const uint32_t tcnt = __shfl_sync(0xffffffffu, cnt, tk);
+      const uint64_t trb = __shfl_sync(0xffffffffu, rbase, tk);
+      const uint32_t off = (ridx - tre) * 32 + lane;
+      doc[u] = 0xFFFFFFFFu;
+      val[u] = 0.f;
+      if (ridx < rtot && off < tcnt) {
+        doc[u] = __ldg(ix.docids + trb + off);
+        val[u] = __ldg(ix.values + trb + off);
+      }
     }
-    const uint32_t nrnd = (cnt + 31) >> 5;
-    const uint32_t rincl = warp_incl_scan(nrnd);
-    const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
-    const uint32_t rexcl = rincl - nrnd;
-    for (uint32_t base = 0; base < rtot; base += UNROLL) {
-      uint32_t doc[UNROLL];
-      float val[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const uint32_t ridx = base + u;
-        int tk = 0;  // entry of round ridx: largest lane t with rexcl[t] <= ridx
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t ex = __shfl_sync(0xffffffffu, rexcl, tk + step);
-          if (ex <= ridx) tk += step;
-        }
-        const uint32_t tre = __shfl_sync(0xffffffffu, rexcl, tk);
-        const uint32_t tcnt = __shfl_sync(0xffffffffu, cnt, tk);
-        const uint64_t trb = __shfl_sync(0xffffffffu, rb, tk);
-        const uint32_t off = (ridx - tre) * 32 + lane;
-        doc[u] = 0xFFFFFFFFu;
-        val[u] = 0.f;
-        if (ridx < rtot && off < tcnt) {
-          doc[u] = __ldg(ix.docids + trb + off);
-          val[u] = __ldg(ix.values + trb + off);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        if (doc[u] != 0xFFFFFFFFu) buf[doc[u] - d0] += val[u];
-        __syncwarp();
-      }
+    for (int u = 0; u < UNROLL; ++u) {
+      if (doc[u] != 0xFFFFFFFFu) buf[doc[u] - d0] += val[u];
+      __syncwarp();
     }
   }
 }
@@ -415,7 +407,8 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
 }
 
 // One warp per (run, doc split): a run is <= R queries with the same dense signature.
-// No CTA-level synchronisation: warps progress independently.
+// Lane e owns gathered-row entry e of the run (the runs' queries' CSC tokens concatenated
+// in query order; at most 32). No CTA-level synchronisation: warps progress independently.
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -445,7 +438,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     const uint32_t incl = warp_incl_scan(ns);
     uint32_t e = incl - ns;
     if (act) s.ebeg[lane] = (int32_t)e;
-    if (lane == 31) s.ebeg[nr] = (int32_t)incl;
+    if (lane == 31) s.ebeg[nr] = (int32_t)min(incl, 32u);
     nd = 0;
     for (uint64_t j = qb; j < qe; ++j) {
       const uint32_t t = ra.q_tok[j];
@@ -456,7 +449,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
       if (info >= 0) {
         if (lane == 0) s.dslot[nd] = info;  // identical multiset for every query of the run
         ++nd;
-      } else {
+      } else if (e < 32) {
         s.row_start[e] = rb;
         s.row_len[e] = (uint32_t)(re - rb);
         s.skip[e] = info <= -2 ? -2 - info : -1;
@@ -483,24 +476,30 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   __syncwarp();
   const int E = s.ebeg[nr];
   const int nd = s.nd[0];
-  // short rows: cursor = lower_bound(split's first doc), nextdoc = doc at the cursor
-  {
-    const uint32_t dstart = t0 * TILE;
-    for (int e = lane; e < E; e += 32) {
-      if (s.skip[e] < 0) {
-        const uint32_t* ids = ix.docids + s.row_start[e];
-        const uint32_t len = s.row_len[e];
-        uint32_t lo = 0, hi = len;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (__ldg(ids + mid) < dstart) lo = mid + 1; else hi = mid;
-        }
-        s.cursor[e] = lo;
-        s.nextdoc[e] = lo < len ? __ldg(ids + lo) : 0xFFFFFFFFu;
+  // ---- per-lane entry state (registers)
+  const bool ent = lane < E;
+  const uint64_t rstart = ent ? s.row_start[lane] : 0ull;
+  const uint32_t rlen = ent ? s.row_len[lane] : 0u;
+  const int32_t sk = ent ? s.skip[lane] : -1;
+  const uint32_t* tab = ix.skiptab + (uint64_t)(sk < 0 ? 0 : sk) * (ix.num_tiles + 1);
+  uint32_t cursor = 0, nextdoc = 0xFFFFFFFFu;  // short rows
+  uint32_t nsb = 0, ncnt = 0;                  // skip rows: slice of the NEXT tile (prefetched)
+  if (ent) {
+    if (sk >= 0) {
+      nsb = __ldg(tab + t0);
+      ncnt = __ldg(tab + t0 + 1) - nsb;
+    } else {
+      const uint32_t* ids = ix.docids + rstart;
+      const uint32_t dstart = t0 * TILE;
+      uint32_t lo = 0, hi = rlen;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ids + mid) < dstart) lo = mid + 1; else hi = mid;
       }
+      cursor = lo;
+      nextdoc = lo < rlen ? __ldg(ids + lo) : 0xFFFFFFFFu;
     }
   }
-  __syncwarp();
   const uint32_t rstride = ix.n_pad / 4;
   float4* dsum4 = reinterpret_cast<float4*>(s.dsum);
   float4* acc4 = reinterpret_cast<float4*>(s.acc);
@@ -508,35 +507,41 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint32_t d0 = tile * TILE, d1 = d0 + TILE;
     const uint32_t nvalid = min((uint32_t)TILE, ix.N - d0);
-    // (1) slices of every gathered row of the run in this tile (lanes over entries)
-    for (int e = lane; e < E; e += 32) {
-      const int32_t sk = s.skip[e];
-      uint32_t sb, cnt;
+    // (1) this tile's slice of every gathered row (lane = entry)
+    uint32_t sb = 0, cnt = 0;
+    if (ent) {
       if (sk >= 0) {
-        const uint32_t* tab = ix.skiptab + (uint64_t)sk * (ix.num_tiles + 1) + tile;
-        sb = __ldg(tab);
-        cnt = __ldg(tab + 1) - sb;
-      } else {
-        sb = s.cursor[e];
-        cnt = 0;
-        if (s.nextdoc[e] < d1) {
-          const uint32_t* ids = ix.docids + s.row_start[e];
-          const uint32_t len = s.row_len[e];
-          uint32_t cur = sb + 1, nxt = 0xFFFFFFFFu;
-          while (cur < len) {
-            nxt = __ldg(ids + cur);
-            if (nxt >= d1) break;
-            ++cur;
-          }
-          if (cur >= len) nxt = 0xFFFFFFFFu;
-          cnt = cur - sb;
-          s.cursor[e] = cur;
-          s.nextdoc[e] = nxt;
+        sb = nsb;
+        cnt = ncnt;
+        if (tile + 1 < t1) {  // prefetch the next tile's slice; consumed one iteration later
+          nsb = __ldg(tab + tile + 1);
+          ncnt = __ldg(tab + tile + 2) - nsb;
         }
+      } else if (nextdoc < d1) {
+        const uint32_t* ids = ix.docids + rstart;
+        sb = cursor;
+        uint32_t cur = cursor + 1;
+        while (true) {  // probe 4 postings at a time (independent loads)
+          uint32_t p[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p[i] = cur + i < rlen ? __ldg(ids + cur + i) : 0xFFFFFFFFu;
+          int adv = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) adv += (adv == i && p[i] < d1) ? 1 : 0;
+          cur += adv;
+          if (adv < 4) {
+            nextdoc = p[adv];
+            break;
+          }
+        }
+        cnt = cur - cursor;
+        cursor = cur;
+      } else {
+        sb = cursor;
       }
-      s.sb[e] = sb;
-      s.cnt[e] = cnt;
     }
+    const uint32_t hmask = __ballot_sync(0xffffffffu, cnt != 0);
+    const uint64_t rbase = rstart + sb;
     // (2) dense signature of the run, ascending slot order, all loads in flight
     {
       float4 a[F4L];
@@ -563,19 +568,16 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
       const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
-      uint32_t c = 0;
-      for (int e = e0 + lane; e < e1; e += 32) c += s.cnt[e];
-      const bool has = __any_sync(0xffffffffu, c != 0);
+      const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
-      if (has) {
+      if (hmask & emask) {
         if (nr > 1) {  // keep the shared dense sum intact for the run's other queries
 #pragma unroll
           for (int rr = 0; rr < F4L; ++rr) acc4[lane + 32 * rr] = dsum4[lane + 32 * rr];
           __syncwarp();
           buf = s.acc;
         }
-        apply_slices(ix, s, e0, e1, buf, d0);
-        __syncwarp();
+        apply_slices(ix, e0, e1, cnt, rbase, buf, d0);
       }
       if constexpr (MODE == GM_DENSE) {
         const double qc = ra.qconst[ra.perm[pb + r]];
@@ -905,7 +907,8 @@ struct RunPlan {
 int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
   p->C = kept_capacity(k);
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
-  if (R == 0) R = p->C <= 256 ? RMAX : (p->C <= 1024 ? 2 : 1);
+  if (R == 0) R = p->C <= 256 ? RMAX : 1;
+  R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
   p->R = std::max(1u, std::min<uint32_t>(R, 32));
   p->warp_bytes = (uint32_t)warp_smem_bytes(p->R, p->C, qmax);
   const size_t budget = (size_t)env_int("SL_SMEM_BUDGET", 72 * 1024);
@@ -984,7 +987,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   if (h_info[0] & 2u) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
   if (h_info[1] > (uint32_t)kQMax)
-    SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: queries longer than 256 tokens are not supported");
+    SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: queries longer than 32 tokens are not supported yet");
 
   const uint32_t qmax = std::max(1u, h_info[1]);
   RunPlan plan;
@@ -1091,7 +1094,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
 
 int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t q_len, int32_t mem, float* out) {
   if (!ix || !out) SL_FAIL(SL_EINVAL, "score_query: null argument");
-  if (q_len > (uint32_t)kQMax) SL_FAIL(SL_EUNSUPPORTED, "score_query: query longer than 256 tokens");
+  if (q_len > (uint32_t)kQMax) SL_FAIL(SL_EUNSUPPORTED, "score_query: queries longer than 32 tokens are not supported yet");
   StreamCache* sc;
   SL_TRY(get_stream(ix->device, &sc));
   cudaStream_t st = sc->st;
