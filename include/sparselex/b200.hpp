@@ -1,0 +1,211 @@
+// sparselex/b200.hpp — C++20 mirror of the reference's SPEC API over the C-ABI
+// (include/sparselex_b200.h). Header-only; link with -lsparselex_b200.
+//
+// The reference declares its scoring types in proj/include/sparselex/bm25.hpp:16-72 and
+// specifies build_index / score_query / top_k / retrieve / retrieve_batch in SPEC.md
+// ([MODULE] index, [MODULE] retrieval) without shipping code for them. This header gives
+// those operations for token-id input, computed on a B200:
+//   build_index(TokenCorpus, BM25Params)                       SPEC index build_index
+//   score_query(index, query) -> std::vector<float>[|C|]       SPEC retrieval score_query
+//   top_k(scores, k, ordered) -> QueryResult                   SPEC retrieval top_k
+//   retrieve(index, query, k, ordered) -> QueryResult          SPEC retrieval retrieve
+//   retrieve_batch(index, queries, k, ordered, workers)        SPEC retrieval retrieve_batch
+// Contract violations throw std::invalid_argument (as scoring.cpp does); CUDA / NCCL
+// failures throw std::runtime_error.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sparselex_b200.h"
+
+namespace sparselex::b200 {
+
+// bm25.hpp:16-23 (same order)
+enum class Variant : int32_t { robertson = 0, atire = 1, lucene = 2, bm25l = 3, bm25plus = 4, tfldp = 5 };
+
+inline void check(int32_t status) {
+  if (status == SL_OK) return;
+  const std::string msg = sl_last_error();
+  if (status == SL_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(std::string(sl_status_string(status)) + ": " + msg);
+}
+
+// bm25.hpp:31-47
+struct BM25Params {
+  Variant variant = Variant::lucene;
+  double k1 = 1.5;
+  double b = 0.75;
+  double delta = 0.0;
+
+  static double default_delta(Variant v) { return sl_default_delta(static_cast<int32_t>(v)); }
+  static BM25Params for_variant(Variant v, double k1 = 1.5, double b = 0.75) {
+    return BM25Params{v, k1, b, default_delta(v)};
+  }
+  sl_params c() const { return sl_params{static_cast<int32_t>(variant), k1, b, delta}; }
+  void validate() const {
+    const sl_params p = c();
+    check(sl_params_validate(&p));
+  }
+};
+
+// A tokenised corpus: document d holds token_ids[doc_offsets[d] .. doc_offsets[d+1]).
+struct TokenCorpus {
+  std::span<const uint64_t> doc_offsets;  // num_docs + 1 entries
+  std::span<const uint32_t> token_ids;
+  uint32_t vocab_size = 0;
+};
+
+struct BuildOptions {
+  int device = 0;
+  bool keep_tf = false;
+  float dense_min_density = 0.f;  // <= 0: library default
+  uint32_t doc_base = 0;          // shard's first global doc id
+  sl_comm* comm = nullptr;        // NCCL communicator for a document-sharded corpus
+};
+
+// SPEC retrieval QueryResult: doc indices with exact B(Q,D) scores, descending.
+struct QueryResult {
+  std::vector<uint32_t> doc_indices;
+  std::vector<float> scores;
+};
+
+// A device-resident index shard (move-only RAII over sl_index*).
+class SearchIndex {
+ public:
+  SearchIndex() = default;
+  explicit SearchIndex(sl_index* h) : h_(h) {}
+  SearchIndex(SearchIndex&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  SearchIndex& operator=(SearchIndex&& o) noexcept {
+    if (this != &o) {
+      reset();
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  SearchIndex(const SearchIndex&) = delete;
+  SearchIndex& operator=(const SearchIndex&) = delete;
+  ~SearchIndex() { reset(); }
+
+  sl_index* handle() const {
+    if (!h_) throw std::invalid_argument("SearchIndex: empty handle");
+    return h_;
+  }
+  sl_index_info info() const {
+    sl_index_info i{};
+    check(sl_index_get_info(handle(), &i));
+    return i;
+  }
+  uint32_t num_docs() const { return info().num_docs_global; }
+  uint32_t vocab_size() const { return info().vocab_size; }
+  double avg_len() const { return info().avg_len; }
+
+  // ScoreMatrix + statistics (SPEC index External Interfaces layout)
+  struct Arrays {
+    std::vector<uint64_t> indptr;
+    std::vector<uint32_t> docids;
+    std::vector<float> values;
+    std::vector<uint32_t> df;
+    std::vector<float> theta;
+    std::vector<uint32_t> doclens;
+  };
+  Arrays export_arrays() const {
+    const sl_index_info i = info();
+    Arrays a;
+    a.indptr.resize(i.vocab_size + 1ull);
+    a.docids.resize(i.nnz_local);
+    a.values.resize(i.nnz_local);
+    a.df.resize(i.vocab_size);
+    a.theta.resize(i.vocab_size);
+    a.doclens.resize(i.num_docs_local);
+    check(sl_index_export(handle(), SL_MEM_HOST, a.indptr.data(), a.docids.data(), a.values.data(), a.df.data(),
+                          a.theta.data(), a.doclens.data(), nullptr));
+    return a;
+  }
+
+ private:
+  void reset() {
+    if (h_) sl_index_destroy(h_);
+    h_ = nullptr;
+  }
+  sl_index* h_ = nullptr;
+};
+
+inline SearchIndex build_index(const TokenCorpus& corpus, const BM25Params& params, const BuildOptions& opt = {}) {
+  if (corpus.doc_offsets.empty()) throw std::invalid_argument("build_index: empty corpus");
+  sl_build_desc d{};
+  d.doc_offsets = corpus.doc_offsets.data();
+  d.token_ids = corpus.token_ids.data();
+  d.num_docs = static_cast<uint32_t>(corpus.doc_offsets.size() - 1);
+  d.vocab_size = corpus.vocab_size;
+  d.doc_base = opt.doc_base;
+  d.mem = SL_MEM_HOST;
+  d.params = params.c();
+  d.device = opt.device;
+  d.keep_tf = opt.keep_tf ? 1 : 0;
+  d.dense_min_density = opt.dense_min_density;
+  d.comm = opt.comm;
+  sl_index* h = nullptr;
+  check(sl_index_build(&d, &h));
+  return SearchIndex(h);
+}
+
+inline std::vector<float> score_query(const SearchIndex& index, std::span<const uint32_t> query) {
+  std::vector<float> out(index.info().num_docs_local);
+  check(sl_score_query(index.handle(), query.data(), static_cast<uint32_t>(query.size()), SL_MEM_HOST, out.data()));
+  return out;
+}
+
+inline QueryResult top_k(std::span<const float> scores, uint32_t k, bool ordered = true, int device = 0) {
+  if (k == 0) throw std::invalid_argument("top_k: k must be >= 1");
+  QueryResult r;
+  r.doc_indices.resize(k);
+  r.scores.resize(k);
+  check(sl_top_k(scores.data(), static_cast<uint32_t>(scores.size()), k, ordered ? 1 : 0, SL_MEM_HOST, device,
+                 r.doc_indices.data(), r.scores.data()));
+  const size_t m = k < scores.size() ? k : scores.size();
+  r.doc_indices.resize(m);
+  r.scores.resize(m);
+  return r;
+}
+
+// workers: accepted for SPEC parity (results are identical for any value; the batch is
+// one device launch sequence).
+inline std::vector<QueryResult> retrieve_batch(const SearchIndex& index,
+                                               const std::vector<std::vector<uint32_t>>& queries, uint32_t k,
+                                               bool ordered = true, int workers = 1) {
+  if (workers < 1) throw std::invalid_argument("retrieve_batch: workers must be >= 1");
+  if (k == 0) throw std::invalid_argument("top_k: k must be >= 1");
+  std::vector<uint64_t> off(queries.size() + 1, 0);
+  for (size_t i = 0; i < queries.size(); ++i) off[i + 1] = off[i] + queries[i].size();
+  std::vector<uint32_t> tok;
+  tok.reserve(off.back());
+  for (const auto& q : queries) tok.insert(tok.end(), q.begin(), q.end());
+  if (tok.empty()) tok.push_back(0);
+  const size_t B = queries.size();
+  std::vector<uint32_t> ids(B * k);
+  std::vector<float> sc(B * k);
+  if (B) {
+    check(sl_retrieve_batch(index.handle(), off.data(), tok.data(), static_cast<uint32_t>(B), k, ordered ? 1 : 0,
+                            SL_MEM_HOST, ids.data(), sc.data()));
+  }
+  const uint32_t n = index.num_docs();
+  const size_t m = k < n ? k : n;
+  std::vector<QueryResult> out(B);
+  for (size_t b = 0; b < B; ++b) {
+    out[b].doc_indices.assign(ids.begin() + b * k, ids.begin() + b * k + m);
+    out[b].scores.assign(sc.begin() + b * k, sc.begin() + b * k + m);
+  }
+  return out;
+}
+
+inline QueryResult retrieve(const SearchIndex& index, std::span<const uint32_t> query, uint32_t k,
+                            bool ordered = true) {
+  return std::move(retrieve_batch(index, {std::vector<uint32_t>(query.begin(), query.end())}, k, ordered)[0]);
+}
+
+}  // namespace sparselex::b200

@@ -88,6 +88,13 @@ typedef struct {
   float dense_min_density;     /* rows with global df >= density * N_global get a dense
                                   query-side copy; <= 0 selects the default (0.25) */
   sl_comm* comm;               /* NULL = single shard */
+  /* Optional precomputed GLOBAL statistics (host memory). When global_df != NULL the
+   * build uses them instead of its own counts / the NCCL all-reduce: df[V] summed over all
+   * shards, N and Σ|D| over all shards. Lets a caller shard without NCCL (e.g. several
+   * shards on one GPU, or statistics exchanged over another transport). */
+  const uint32_t* global_df;
+  uint32_t global_num_docs;
+  uint64_t global_total_len;
 } sl_build_desc;
 
 /* Index statistics (global unless marked local). */

@@ -21,6 +21,7 @@ _d, _u32, _i32, _vp, _u64 = C.c_double, C.c_uint32, C.c_int32, C.c_void_p, C.c_u
 _SIG = {
     "orc_last_error": (C.c_char_p, []),
     "orc_build": (_i32, [_vp, _vp, _u32, _u32, _i32, _d, _d, _d, C.POINTER(_vp)]),
+    "orc_build_shard": (_i32, [_vp, _vp, _u32, _u32, _i32, _d, _d, _d, _vp, _u32, _u64, C.POINTER(_vp)]),
     "orc_free": (None, [_vp]),
     "orc_nnz": (_u64, [_vp]),
     "orc_avg_len": (_d, [_vp]),
@@ -90,7 +91,7 @@ def _p(a):
 class OracleIndex:
     """SPEC build_index restated on the CPU (two-pass, f64 math, f32 storage)."""
 
-    def __init__(self, offsets, tokens, vocab_size, variant=2, k1=1.5, b=0.75, delta=0.0):
+    def __init__(self, offsets, tokens, vocab_size, variant=2, k1=1.5, b=0.75, delta=0.0, global_stats=None):
         self.offsets = np.ascontiguousarray(offsets, np.uint64)
         self.tokens = np.ascontiguousarray(tokens, np.uint32)
         self.N = len(self.offsets) - 1
@@ -98,7 +99,12 @@ class OracleIndex:
         self.params = (int(variant), float(k1), float(b), float(delta))
         h = _vp()
         tok = self.tokens if len(self.tokens) else np.zeros(1, np.uint32)
-        rc = lib().orc_build(_p(self.offsets), _p(tok), self.N, vocab_size, *self.params, C.byref(h))
+        if global_stats is None:
+            rc = lib().orc_build(_p(self.offsets), _p(tok), self.N, vocab_size, *self.params, C.byref(h))
+        else:  # shard of a document-sharded corpus: (global df[V], N_global, sum_len_global)
+            self._gdf = np.ascontiguousarray(global_stats[0], np.uint32)
+            rc = lib().orc_build_shard(_p(self.offsets), _p(tok), self.N, vocab_size, *self.params, _p(self._gdf),
+                                       int(global_stats[1]), int(global_stats[2]), C.byref(h))
         if rc:
             raise ValueError(_err())
         self._h = h

@@ -155,7 +155,10 @@ void count_terms(const uint32_t* ids, uint64_t n, std::vector<uint32_t>& scratch
   }
 }
 
-OracleIndex* build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, const Params& p) {
+// gdf/gN/gtotal: optional global statistics of a document-sharded corpus;
+// with them, idf, S^θ and L_avg are those of the whole corpus while rows hold this shard's docs.
+OracleIndex* build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, const Params& p,
+                   const uint32_t* gdf = nullptr, uint32_t gN = 0, uint64_t gtotal = 0) {
   validate(p);
   if (N == 0) throw std::invalid_argument("build_index: empty corpus");
   if (V == 0) throw std::invalid_argument("build_index: empty vocabulary");
@@ -180,10 +183,17 @@ OracleIndex* build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, 
     total += e - b;
   }
   if (total == 0) { delete ix; throw std::invalid_argument("build_index: degenerate corpus (all documents empty)"); }
+  std::vector<uint32_t> local_df = ix->df;
+  uint32_t Ns = N;
+  if (gdf) {
+    for (uint32_t t = 0; t < V; ++t) ix->df[t] = gdf[t];
+    total = gtotal;
+    Ns = gN;
+  }
   ix->total_len = total;
-  ix->avg_len = (double)total / (double)N;  // SPEC scoring CorpusStats: L_avg
+  ix->avg_len = (double)total / (double)Ns;  // SPEC scoring CorpusStats: L_avg
   ix->indptr.assign((size_t)V + 1, 0);
-  for (uint32_t t = 0; t < V; ++t) ix->indptr[t + 1] = ix->indptr[t] + ix->df[t];
+  for (uint32_t t = 0; t < V; ++t) ix->indptr[t + 1] = ix->indptr[t] + local_df[t];
   const uint64_t nnz = ix->indptr[V];
   ix->docids.resize(nnz);
   ix->values.resize(nnz);
@@ -192,7 +202,7 @@ OracleIndex* build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, 
   std::vector<double> theta64(V, 0.0);
   for (uint32_t t = 0; t < V; ++t)
     if (ix->df[t] > 0) {
-      theta64[t] = nonoccurrence(ix->df[t], N, p);
+      theta64[t] = nonoccurrence(ix->df[t], Ns, p);
       ix->theta[t] = (float)theta64[t];
     }
   // pass 2: S^Δ = S - S^θ in f64, stored f32, docs ascending => strictly increasing per row
@@ -206,7 +216,7 @@ OracleIndex* build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, 
       const uint64_t pos = cursor[t]++;
       ix->docids[pos] = d;
       ix->tf[pos] = c.second;
-      const double s = score((double)c.second, ix->df[t], dl, N, ix->avg_len, p);
+      const double s = score((double)c.second, ix->df[t], dl, Ns, ix->avg_len, p);
       ix->values[pos] = (float)(s - theta64[t]);
     }
   }
@@ -271,6 +281,15 @@ const char* orc_last_error(void) { return g_err.c_str(); }
 int orc_build(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, int variant,
               double k1, double b, double delta, orc_index** out) {
   return guarded([&] { *out = build(offsets, tokens, N, V, Params{variant, k1, b, delta}); });
+}
+
+// One shard of a document-sharded corpus built with the corpus-wide df / N / Σ|D|.
+int orc_build_shard(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, int variant, double k1,
+                    double b, double delta, const uint32_t* global_df, uint32_t global_n, uint64_t global_total,
+                    orc_index** out) {
+  return guarded([&] {
+    *out = build(offsets, tokens, N, V, Params{variant, k1, b, delta}, global_df, global_n, global_total);
+  });
 }
 
 void orc_free(orc_index* ix) { delete ix; }

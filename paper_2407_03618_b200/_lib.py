@@ -35,6 +35,9 @@ class BuildDesc(C.Structure):
         ("keep_tf", C.c_int32),
         ("dense_min_density", C.c_float),
         ("comm", C.c_void_p),
+        ("global_df", C.c_void_p),
+        ("global_num_docs", C.c_uint32),
+        ("global_total_len", C.c_uint64),
     ]
 
 

@@ -169,7 +169,7 @@ class SearchIndex:
 
 def build_index(doc_offsets, token_ids, vocab_size: int, params: BM25Params | None = None, *, device: int = 0,
                 keep_tf: bool = False, dense_min_density: float = 0.0, doc_base: int = 0, num_docs: int | None = None,
-                comm=None) -> SearchIndex:
+                comm=None, global_stats: tuple | None = None) -> SearchIndex:
     """SPEC build_index over token ids: doc d holds token_ids[doc_offsets[d]:doc_offsets[d+1]]."""
     params = params or BM25Params()
     off_p, m1, keep1 = _as_arg(doc_offsets, np.uint64)
@@ -185,6 +185,11 @@ def build_index(doc_offsets, token_ids, vocab_size: int, params: BM25Params | No
     d.params = params.to_c()
     d.device, d.keep_tf, d.dense_min_density = device, int(keep_tf), float(dense_min_density)
     d.comm = comm.handle if comm is not None else None
+    if global_stats is not None:  # (df[V] summed over shards, N_global, sum_len_global)
+        gdf = np.ascontiguousarray(global_stats[0], np.uint32)
+        if len(gdf) != vocab_size:
+            raise ValueError("global_stats df must have vocab_size entries")
+        d.global_df, d.global_num_docs, d.global_total_len = gdf.ctypes.data, int(global_stats[1]), int(global_stats[2])
     h = C.c_void_p()
     check(lib().sl_index_build(C.byref(d), C.byref(h)))
     return SearchIndex(h.value, device, comm)

@@ -584,7 +584,13 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(dalloc(ix, &ix->df_global, V));
   k_df_from_indptr<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, ix->df_global);
   uint64_t stats[2] = {T, N};
-  if (d->comm && d->comm->nranks > 1) {
+  if (d->global_df) {
+    // caller-supplied global statistics (virtual shards / external transport)
+    SL_CUDA_TRY(cudaMemcpyAsync(ix->df_global, d->global_df, (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+    stats[0] = d->global_total_len;
+    stats[1] = d->global_num_docs;
+    if (stats[1] < N || stats[0] < T) SL_FAIL(SL_EINVAL, "build_index: global statistics smaller than the shard's");
+  } else if (d->comm) {
     uint64_t* dstats;
     SL_TRY(tmp.alloc(&dstats, 2));
     SL_CUDA_TRY(cudaMemcpyAsync(dstats, stats, 16, cudaMemcpyHostToDevice, st));

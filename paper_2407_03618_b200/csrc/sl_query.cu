@@ -946,7 +946,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
   if (k > kMaxK) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: k > 4096 is not supported by the fused top-k");
   if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "retrieve_batch: bad mem kind");
-  const bool dist = ix->comm && ix->comm->nranks > 1;
+  const bool dist = ix->comm != nullptr;  // any communicator, 1 rank included
   const bool want_out = !dist || ix->comm->rank == 0;
   if (B == 0) return SL_OK;
   if (!q_offsets || !q_tokens) SL_FAIL(SL_EINVAL, "retrieve_batch: null query pointers");

