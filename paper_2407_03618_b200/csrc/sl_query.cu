@@ -282,39 +282,39 @@ __device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_
 
 // Add the tile slices of the query owning lanes [e0, e1) (lane = gathered-row entry, in
 // query order) to buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are
-// unique within a row, so a round has no write conflicts); the loads of UNROLL rounds
-// are in flight together, and rounds are applied in entry order with __syncwarp between
-// them, so every document receives its terms in token order without atomics.
-// sb/cnt/rbase are this lane's entry slice (ignored outside [e0, e1)).
-__device__ __forceinline__ void apply_slices(const IndexView& ix, int e0, int e1, uint32_t cnt, uint64_t rbase,
+// unique within a row, so a round has no write conflicts). A warp-uniform iterator walks
+// the non-empty entries in lane (= token) order; the loads of UNROLL rounds are in flight
+// together and the rounds are applied in order with __syncwarp between them, so every
+// document receives its terms in token order without atomics.
+// cnt/rbase are this lane's entry slice (length, absolute start).
+__device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask, uint32_t cnt, uint64_t rbase,
                                              float* buf, uint32_t d0) {
   const int lane = threadIdx.x & 31;
-  const bool mine = lane >= e0 && lane < e1;
-  const uint32_t nrnd = mine ? (cnt + 31) >> 5 : 0u;
-  const uint32_t rincl = warp_incl_scan(nrnd);
-  const uint32_t rtot = __shfl_sync(0xffffffffu, rincl, 31);
-  const uint32_t rexcl = rincl - nrnd;
-  for (uint32_t base = 0; base < rtot; base += UNROLL) {
+  uint32_t m = __ballot_sync(0xffffffffu, cnt != 0) & emask;  // entries with postings here
+  int tk = m ? __ffs(m) - 1 : 32;
+  uint32_t c = 0;                                             // next 32-posting chunk of entry tk
+  uint32_t tcnt = __shfl_sync(0xffffffffu, cnt, tk & 31);
+  uint64_t trb = __shfl_sync(0xffffffffu, rbase, tk & 31);
+  while (tk < 32) {
     uint32_t doc[UNROLL];
     float val[UNROLL];
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const uint32_t ridx = base + u;
-      int tk = 0;  // entry of round ridx: largest lane t with rexcl[t] <= ridx
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t ex = __shfl_sync(0xffffffffu, rexcl, tk + step);
-        if (ex <= ridx) tk += step;
-      }
-      const uint32_t tre = __shfl_sync(0xffffffffu, rexcl, tk);
-      const uint32_t tcnt = __shfl_sync(0xffffffffu, cnt, tk);
-      const uint64_t trb = __shfl_sync(0xffffffffu, rbase, tk);
-      const uint32_t off = (ridx - tre) * 32 + lane;
       doc[u] = 0xFFFFFFFFu;
       val[u] = 0.f;
-      if (ridx < rtot && off < tcnt) {
-        doc[u] = __ldg(ix.docids + trb + off);
-        val[u] = __ldg(ix.values + trb + off);
+      if (tk < 32) {
+        const uint32_t off = c * 32 + lane;
+        if (off < tcnt) {
+          doc[u] = __ldg(ix.docids + trb + off);
+          val[u] = __ldg(ix.values + trb + off);
+        }
+        if ((++c) * 32 >= tcnt) {  // entry exhausted: move to the next non-empty one
+          m &= m - 1;
+          tk = m ? __ffs(m) - 1 : 32;
+          c = 0;
+          tcnt = __shfl_sync(0xffffffffu, cnt, tk & 31);
+          trb = __shfl_sync(0xffffffffu, rbase, tk & 31);
+        }
       }
     }
 #pragma unroll
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
           __syncwarp();
           buf = s.acc;
         }
-        apply_slices(ix, e0, e1, cnt, rbase, buf, d0);
+        apply_slices(ix, emask, cnt, rbase, buf, d0);
       }
       if constexpr (MODE == GM_DENSE) {
         const double qc = ra.qconst[ra.perm[pb + r]];
