@@ -289,7 +289,12 @@ def run_ours(args):
                        "dense_rows": int(info.dense_rows), "skip_rows": int(info.skip_rows),
                        "tile_docs": int(info.tile_docs)},
             "index_tokens_per_s": T_total / (build_ms / 1e3),
-            "index_build_ms": build_ms,
+            "index_build": {
+                "ms": build_ms, "tokens": T_total, "nnz": int(info.nnz_local),
+                # SURVEY §8d floor: read ids + offsets, write CSC, indptr, doclens, df, theta
+                "algorithmic_bytes": 4 * T_total + 8 * (cfg.num_docs + 1) + 8 * int(info.nnz_local)
+                                     + 8 * (cfg.vocab + 1) + 4 * cfg.num_docs + 8 * cfg.vocab,
+            },
             "score_kernel_ms_per_step": ker_ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_source": hbm_src, "traffic": traffic,
@@ -304,6 +309,9 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        bb = line["index_build"]["algorithmic_bytes"]
+        line["index_build"]["achieved_GBps"] = bb / (build_ms / 1e3) / 1e9
+        line["index_build"]["frac"] = line["index_build"]["achieved_GBps"] / hbm
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
             r = cpu_reference_run(args.config, k, 1, 1, args.cpu_sample, cores)

@@ -459,15 +459,20 @@ void free_index(sl_index* ix) {
   void* ps[] = {ix->indptr, ix->docids, ix->values, ix->df_global, ix->theta,
                 ix->doclens, ix->tf, ix->tokinfo, ix->dense, ix->skiptab};
   for (void* p : ps)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);  // back to the stream-ordered pool
+  cudaStreamSynchronize(0);
   delete ix;
 }
 
 namespace {
+// persistent index arrays come from the device's stream-ordered pool (kept mapped across
+// builds by the release threshold set in get_stream), so rebuilding does not pay page mapping
+thread_local cudaStream_t t_build_stream = nullptr;
+
 template <class T>
 int32_t dalloc(sl_index* ix, T** p, uint64_t count) {
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  cudaError_t e = cudaMallocAsync((void**)p, count * sizeof(T), t_build_stream);
   if (e != cudaSuccess) {
     *p = nullptr;
     set_error(std::string("device allocation of ") + std::to_string(count * sizeof(T)) +
@@ -702,7 +707,16 @@ int32_t build_index_impl(const sl_build_desc* d, sl_index** out) {
     delete ix;
     SL_FAIL(SL_ECUDA, "sl_index_build: stream creation failed");
   }
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  t_build_stream = st;
   const int32_t rc = build_body(d, ix, st);
+  t_build_stream = nullptr;
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   if (rc != SL_OK) {
