@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparselex_b200.so")
+LIB_PATH = os.environ.get("SPARSELEX_LIB") or os.path.join(_HERE, "libsparselex_b200.so")  # env: tuning variants
 SYNTH_PATH = os.path.join(_HERE, "libsl_synth.so")
 
 SL_OK, SL_EINVAL, SL_ECUDA, SL_ENCCL, SL_ENOMEM, SL_ECORRUPT, SL_EUNSUPPORTED = range(7)

@@ -41,7 +41,10 @@ struct Status {
   } while (0)
 
 // ---------------------------------------------------------------- constants
-constexpr int kTileDocs = 512;         // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
+#ifndef SL_TILE_DOCS
+#define SL_TILE_DOCS 512
+#endif
+constexpr int kTileDocs = SL_TILE_DOCS;  // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
 constexpr int kScoreThreads = 256;     // threads per scoring CTA
 constexpr int kQMax = 32;              // max query tokens (one lane per gathered row)
 constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path

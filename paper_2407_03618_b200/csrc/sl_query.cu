@@ -228,6 +228,7 @@ struct RunArgs {
   uint32_t warp_bytes;        // shared memory per warp
   uint64_t* cand;             // [B][n_splits][C] (original query order)
   float* dense_out;           // GM_DENSE: [N]
+  uint32_t debug_skip;        // timing experiments only (SL_DEBUG_SKIP): 1 gather, 2 filter, 4 dense
 };
 
 // per-warp shared memory; E = R * qmax gathered-row entries (the run's queries' CSC
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     const uint32_t hmask = __ballot_sync(0xffffffffu, cnt != 0);
     const uint64_t rbase = rstart + sb;
     // (2) dense signature of the run, ascending slot order, all loads in flight
-    {
+    if (!(ra.debug_skip & 4)) {
       float4 a[F4L];
 #pragma unroll
       for (int rr = 0; rr < F4L; ++rr) a[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
       const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
       const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
-      if (hmask & emask) {
+      if ((hmask & emask) && !(ra.debug_skip & 1)) {
         if (nr > 1) {  // keep the shared dense sum intact for the run's other queries
 #pragma unroll
           for (int rr = 0; rr < F4L; ++rr) acc4[lane + 32 * rr] = dsum4[lane + 32 * rr];
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf);
+        if (!(ra.debug_skip & 2)) filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf);
       }
     }
     __syncwarp();
@@ -1024,6 +1025,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.n_splits = plan.n_splits;
   ra.wpc = plan.wpc;
   ra.warp_bytes = plan.warp_bytes;
+  ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
