@@ -229,6 +229,7 @@ struct RunArgs {
   uint64_t* cand;             // [B][n_splits][C] (original query order)
   float* dense_out;           // GM_DENSE: [N]
   uint32_t debug_skip;        // timing experiments only (SL_DEBUG_SKIP): 1 gather, 2 filter, 4 dense
+  uint32_t kept_global;       // large k: running candidates live in their cand slot (global/L2)
 };
 
 // per-warp shared memory; E = R * qmax gathered-row entries (the run's queries' CSC
@@ -252,6 +253,7 @@ struct WSmem {
   uint32_t* cnt;        // [E] and length
 };
 
+// C = candidates held in shared memory per query (0 when they live in global memory)
 __host__ __device__ inline size_t warp_smem_bytes(uint32_t R, uint32_t C, uint32_t qmax) {
   const size_t E = (size_t)R * qmax;
   size_t b = (size_t)TILE * 8 + (size_t)R * C * 8 + (size_t)R * 8 + E * 8 + 16 * 4 + (size_t)R * 4 + (R + 1) * 4 + 4 +
@@ -328,7 +330,7 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
 
 // Running top-k of query r over one tile (warp-level) from buf[TILE].
 __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
-                                            uint32_t nvalid, const float* buf) {
+                                            uint32_t nvalid, const float* buf, uint64_t* kept) {
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   const uint64_t tau = s.tau[r];
@@ -366,7 +368,6 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
   tile_visit(tau, [&](uint64_t) { ++mine; });
   const uint32_t incl = warp_incl_scan(mine);
   const uint32_t P = __shfl_sync(0xffffffffu, incl, 31);
-  uint64_t* kept = s.kept + (size_t)r * C;
   const uint32_t nk = s.n_kept[r];
   if (nk + P <= C) {
     uint64_t* dst = kept + nk + incl - mine;
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   const uint32_t n_runs = *ra.n_runs;
   const uint64_t item = (uint64_t)blockIdx.x * ra.wpc + warp;
   if (item >= (uint64_t)n_runs * ra.n_splits) return;
-  const WSmem s = wcarve(smem_raw + (size_t)warp * ra.warp_bytes, ra.R, ra.C, ra.qmax);
+  const WSmem s = wcarve(smem_raw + (size_t)warp * ra.warp_bytes, ra.R, ra.kept_global ? 0u : ra.C, ra.qmax);
   const uint32_t run = (uint32_t)(item / ra.n_splits), split = (uint32_t)(item % ra.n_splits);
   const uint32_t pb = ra.run_begin[run];
   const uint32_t nr = ra.run_begin[run + 1] - pb;
@@ -585,7 +586,10 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        if (!(ra.debug_skip & 2)) filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf);
+        uint64_t* kept = ra.kept_global
+                             ? ra.cand + ((uint64_t)ra.perm[pb + r] * ra.n_splits + split) * ra.C
+                             : s.kept + (size_t)r * ra.C;
+        if (!(ra.debug_skip & 2)) filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
       }
     }
     __syncwarp();
@@ -594,9 +598,13 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     for (uint32_t r = 0; r < nr; ++r) {
       const uint32_t q = ra.perm[pb + r];
       const uint32_t nk = s.n_kept[r];
-      const uint64_t* kept = s.kept + (size_t)r * ra.C;
       uint64_t* out = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
-      for (uint32_t i = lane; i < ra.C; i += 32) out[i] = i < nk ? kept[i] : kInvalidKey;
+      if (ra.kept_global) {  // candidates are already in place: pad the tail
+        for (uint32_t i = nk + lane; i < ra.C; i += 32) out[i] = kInvalidKey;
+      } else {
+        const uint64_t* kept = s.kept + (size_t)r * ra.C;
+        for (uint32_t i = lane; i < ra.C; i += 32) out[i] = i < nk ? kept[i] : kInvalidKey;
+      }
     }
   }
 }
@@ -898,7 +906,7 @@ int env_int(const char* name, int dflt) {
 }
 
 struct RunPlan {
-  uint32_t R, C, wpc, n_splits, warp_bytes;
+  uint32_t R, C, wpc, n_splits, warp_bytes, kept_global;
   size_t smem;
 };
 
@@ -907,11 +915,12 @@ struct RunPlan {
 // override the plan in tuning runs.
 int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
   p->C = kept_capacity(k);
+  p->kept_global = p->C > (uint32_t)env_int("SL_KEPT_SMEM_MAX", 0);  // large k: candidates in their global output slot (L2)
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
-  if (R == 0) R = p->C <= 256 ? RMAX : 1;
+  if (R == 0) R = RMAX;
   R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
   p->R = std::max(1u, std::min<uint32_t>(R, 32));
-  p->warp_bytes = (uint32_t)warp_smem_bytes(p->R, p->C, qmax);
+  p->warp_bytes = (uint32_t)warp_smem_bytes(p->R, p->kept_global ? 0u : p->C, qmax);
   const size_t budget = (size_t)env_int("SL_SMEM_BUDGET", 72 * 1024);
   p->wpc = (uint32_t)std::max<size_t>(1, std::min<size_t>(NW, budget / p->warp_bytes));
   p->smem = (size_t)p->wpc * p->warp_bytes;
@@ -1026,6 +1035,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.wpc = plan.wpc;
   ra.warp_bytes = plan.warp_bytes;
   ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
+  ra.kept_global = plan.kept_global;
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
