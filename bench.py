@@ -173,9 +173,14 @@ def run_ours(args):
     cfg = synth.config(args.config)
     cdf = synth.zipf_cdf(cfg)
     offsets = synth.doc_offsets(cfg)
-    d0, d1 = shard_ranges(offsets, world)[rank]
+    if args.shard_of > 1:  # one GPU builds shard `shard_index` of a shard_of-way sharding (c5 memory plan)
+        d0, d1 = shard_ranges(offsets, args.shard_of)[args.shard_index]
+    else:
+        d0, d1 = shard_ranges(offsets, world)[rank]
     o0, o1 = int(offsets[d0]), int(offsets[d1])
     T_local, T_total = o1 - o0, int(offsets[-1])
+    if args.shard_of > 1:
+        T_total = T_local
     tok = torch.empty(max(1, T_local), dtype=torch.uint32, device="cuda")
     check(L.sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, o0, T_local, SL_MEM_HOST,
                                    tok.data_ptr()))
@@ -287,13 +292,16 @@ def run_ours(args):
                        "tokens": T_total, "nnz_local": int(info.nnz_local), "queries_per_step": B, "k": k,
                        "parallelism": f"doc-shard x{world}", "l2": "flushed between steps (256 MiB memset)",
                        "dense_rows": int(info.dense_rows), "skip_rows": int(info.skip_rows),
-                       "tile_docs": int(info.tile_docs)},
+                       "tile_docs": int(info.tile_docs),
+                       **({"simulated_shard": f"{args.shard_index} of {args.shard_of} (docs {d0}..{d1}; "
+                                              "shard-local df/N statistics; value is per-GPU)"}
+                          if args.shard_of > 1 else {})},
             "index_tokens_per_s": T_total / (build_ms / 1e3),
             "index_build": {
                 "ms": build_ms, "tokens": T_total, "nnz": int(info.nnz_local),
                 # SURVEY §8d floor: read ids + offsets, write CSC, indptr, doclens, df, theta
-                "algorithmic_bytes": 4 * T_total + 8 * (cfg.num_docs + 1) + 8 * int(info.nnz_local)
-                                     + 8 * (cfg.vocab + 1) + 4 * cfg.num_docs + 8 * cfg.vocab,
+                "algorithmic_bytes": 4 * T_total + 8 * (int(info.num_docs_local) + 1) + 8 * int(info.nnz_local)
+                                     + 8 * (cfg.vocab + 1) + 4 * int(info.num_docs_local) + 8 * cfg.vocab,
             },
             "score_kernel_ms_per_step": ker_ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -342,6 +350,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--ref-sample", type=int, default=128)
+    ap.add_argument("--shard-of", type=int, default=1, help="build one shard of an N-way doc sharding (1 GPU)")
+    ap.add_argument("--shard-index", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 violates the timing rules; using 3", file=sys.stderr)

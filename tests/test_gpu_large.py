@@ -61,7 +61,8 @@ def _run(cfg, corp, qoff, qtok, p, ks, nsample, seed):
         # full batch: structural properties + score recomputation on the device
         gid, gsc = retrieve_batch(gi, (qoff, qtok), ks[0], as_arrays=True)
         assert np.all(np.diff(gsc.astype(np.float64), axis=1) <= 0)
-        assert all(len(set(r.tolist())) == ks[0] for r in gid)
+        srt = np.sort(gid.astype(np.int64), axis=1)
+        assert np.all(np.diff(srt, axis=1) > 0)  # k distinct ids per query
         for b in range(0, len(qoff) - 1, 997):
             q = qtok[int(qoff[b]):int(qoff[b + 1])]
             s = score_query(gi, q)
@@ -79,3 +80,12 @@ def test_c2_lucene(cuda_ok, c2):
 def test_c3_variant_sweep(cuda_ok, c2, p):
     cfg, corp, qoff, qtok = c2  # c3 = c2's corpus shapes with the variant sweep
     _run(cfg, corp, qoff, qtok, p, (10,), 300, 3)
+
+
+def test_c4_csc_and_top1000(cuda_ok):
+    """c4 (8.8M passages, V=1M, ~4.9e8 tokens): full 1-GPU CSC vs the oracle and top-1000 parity
+    on a 128-query sample of the first 8,192-query batch (SURVEY.md §8d parity plan)."""
+    cfg = synth.config(4)
+    corp = synth.corpus_host(cfg, threads=32)
+    qoff, qtok = synth.queries(cfg, corp.cdf, 0, 8192)
+    _run(cfg, corp, qoff, qtok, BM25Params(Variant.lucene, 1.5, 0.75), (1000,), 128, 4)
