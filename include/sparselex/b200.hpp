@@ -154,6 +154,16 @@ inline SearchIndex build_index(const TokenCorpus& corpus, const BM25Params& para
   return SearchIndex(h);
 }
 
+// SPEC save_index / load_index (9-file layout)
+inline void save_index(const SearchIndex& index, const std::string& directory) {
+  check(sl_index_save(index.handle(), directory.c_str()));
+}
+inline SearchIndex load_index(const std::string& directory, int device = 0) {
+  sl_index* h = nullptr;
+  check(sl_index_load(directory.c_str(), device, 0.f, &h));
+  return SearchIndex(h);
+}
+
 inline std::vector<float> score_query(const SearchIndex& index, std::span<const uint32_t> query) {
   std::vector<float> out(index.info().num_docs_local);
   check(sl_score_query(index.handle(), query.data(), static_cast<uint32_t>(query.size()), SL_MEM_HOST, out.data()));

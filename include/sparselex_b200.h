@@ -15,6 +15,8 @@
  *   sl_score_query      <- score_query(index, query) -> dense |C| vector       SPEC.md [MODULE] retrieval
  *   sl_top_k            <- top_k(scores, k, ordered)                           SPEC.md [MODULE] retrieval
  *   sl_params_validate  <- BM25Params::validate                                proj/src/scoring.cpp:47-58
+ *   sl_index_save       <- save_index(index, directory)                        SPEC.md [MODULE] index
+ *   sl_index_load       <- load_index(directory)                               SPEC.md [MODULE] index
  *   sl_index_destroy / sl_last_error : ownership + error plumbing (the reference throws
  *                          std::invalid_argument with fixed messages, scoring.cpp:15-138;
  *                          here a status code + thread-local message).
@@ -47,7 +49,8 @@ typedef enum {
   SL_ENCCL = 3,    /* NCCL failure */
   SL_ENOMEM = 4,   /* device allocation failed */
   SL_ECORRUPT = 5, /* structural invariant violated */
-  SL_EUNSUPPORTED = 6
+  SL_EUNSUPPORTED = 6,
+  SL_EIO = 7       /* file I/O failure (message names the path) */
 } sl_status;
 
 typedef enum {
@@ -133,6 +136,15 @@ int32_t sl_index_get_info(const sl_index* index, sl_index_info* info);
  * keep_tf at build time. */
 int32_t sl_index_export(const sl_index* index, int32_t mem, uint64_t* indptr, uint32_t* docids,
                         float* values, uint32_t* df, float* theta, uint32_t* doclens, uint32_t* tf);
+
+/* SPEC save_index / load_index: the 9-file directory layout of SPEC.md [MODULE] index
+ * "External Interfaces" (meta.json, vocab.json, df.bin, theta.bin, indptr.bin, docids.bin,
+ * values.bin, doclens.bin, docs.json; little-endian). Token-id corpora store the id's decimal
+ * string as the vocabulary token and the global doc id as the external id. load validates
+ * every ScoreMatrix invariant: missing file -> SL_EIO (path in the message), corrupt lengths /
+ * invariants -> SL_ECORRUPT, format version mismatch -> SL_EUNSUPPORTED. */
+int32_t sl_index_save(const sl_index* index, const char* directory);
+int32_t sl_index_load(const char* directory, int32_t device, float dense_min_density, sl_index** out);
 
 /* Batched retrieval (SPEC retrieve_batch): for each query b, the min(k, N_global) best
  * documents by B(Q,D) = Σ S^Δ + Σ S^θ, score descending, ties -> smaller global doc id.

@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SPARSELEX_LIB") or os.path.join(_HERE, "libsparselex_b200.so")  # env: tuning variants
 SYNTH_PATH = os.path.join(_HERE, "libsl_synth.so")
 
-SL_OK, SL_EINVAL, SL_ECUDA, SL_ENCCL, SL_ENOMEM, SL_ECORRUPT, SL_EUNSUPPORTED = range(7)
+SL_OK, SL_EINVAL, SL_ECUDA, SL_ENCCL, SL_ENOMEM, SL_ECORRUPT, SL_EUNSUPPORTED, SL_EIO = range(8)
 SL_MEM_HOST, SL_MEM_DEVICE = 0, 1
 
 # name, restype, argtypes — every symbol declared in include/sparselex_b200.h
@@ -81,6 +81,8 @@ SIGNATURES = {
     "sl_index_destroy": (None, [_vp]),
     "sl_index_get_info": (_i32, [_vp, C.POINTER(IndexInfo)]),
     "sl_index_export": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sl_index_save": (_i32, [_vp, C.c_char_p]),
+    "sl_index_load": (_i32, [C.c_char_p, _i32, C.c_float, C.POINTER(C.c_void_p)]),
     "sl_retrieve_batch": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _i32, _vp, _vp]),
     "sl_retrieve_batch_timed": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _vp, _vp, C.POINTER(RetrieveStats)]),
     "sl_score_query": (_i32, [_vp, _vp, _u32, _i32, _vp]),
@@ -124,12 +126,18 @@ class SparselexInvalid(SparselexError, ValueError):
     """SL_EINVAL: the reference throws std::invalid_argument here."""
 
 
+class SparselexIOError(SparselexError, OSError):
+    """SL_EIO: file I/O failure (SPEC save_index / load_index)."""
+
+
 def check(status: int) -> None:
     if status == SL_OK:
         return
     msg = (lib().sl_last_error() or b"").decode(errors="replace")
     if status == SL_EINVAL:
         raise SparselexInvalid(status, msg)
+    if status == SL_EIO:
+        raise SparselexIOError(status, msg)
     raise SparselexError(status, msg)
 
 

@@ -149,6 +149,11 @@ class SearchIndex:
         out["doc_base"] = inf.doc_base
         return out
 
+    def save(self, directory: str) -> None:
+        """SPEC save_index: the 9-file layout (meta.json, vocab.json, df/theta/indptr/docids/
+        values/doclens .bin, docs.json)."""
+        check(lib().sl_index_save(self.handle, str(directory).encode()))
+
     def close(self) -> None:
         if self._h:
             lib().sl_index_destroy(self._h)
@@ -193,6 +198,13 @@ def build_index(doc_offsets, token_ids, vocab_size: int, params: BM25Params | No
     h = C.c_void_p()
     check(lib().sl_index_build(C.byref(d), C.byref(h)))
     return SearchIndex(h.value, device, comm)
+
+
+def load_index(directory: str, *, device: int = 0, dense_min_density: float = 0.0) -> SearchIndex:
+    """SPEC load_index: validates every ScoreMatrix invariant, uploads, rebuilds query structures."""
+    h = C.c_void_p()
+    check(lib().sl_index_load(str(directory).encode(), device, float(dense_min_density), C.byref(h)))
+    return SearchIndex(h.value, device)
 
 
 def _queries_to_csr(queries):

@@ -483,6 +483,64 @@ int32_t dalloc(sl_index* ix, T** p, uint64_t count) {
   return SL_OK;
 }
 
+// Query-side access structures from a finished CSC (ix->indptr/docids/values/df_global):
+// dense copies of the rows with global df >= density * N_global, per-tile skip offsets of
+// long rows, and the per-token dispatch table. Used by the build and by index loading.
+int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream_t st) {
+  Temps tmp(st);
+  const uint32_t N = ix->N, V = ix->V;
+  ix->num_tiles = (N + kTileDocs - 1) / kTileDocs;
+  ix->n_pad = ix->num_tiles * kTileDocs;
+  std::vector<uint32_t> h_df(V);
+  std::vector<uint64_t> h_ptr((size_t)V + 1);
+  SL_CUDA_TRY(cudaMemcpyAsync(h_df.data(), ix->df_global, (uint64_t)V * 4, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaMemcpyAsync(h_ptr.data(), ix->indptr, ((uint64_t)V + 1) * 8, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.25;
+  const double dense_thr = density * (double)ix->N_global;
+  const uint64_t skip_thr = 4ull * ix->num_tiles;  // >= 4 postings per tile expected
+  std::vector<int32_t> info(V, -1);
+  std::vector<uint32_t> dense_tok, skip_tok;
+  for (uint32_t t = 0; t < V; ++t) {
+    const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
+    if (dl == 0 || h_df[t] == 0) continue;
+    if ((double)h_df[t] >= dense_thr && density <= 1.0) {
+      info[t] = (int32_t)dense_tok.size();
+      dense_tok.push_back(t);
+    } else if (dl >= skip_thr) {
+      info[t] = -2 - (int32_t)skip_tok.size();
+      skip_tok.push_back(t);
+    }
+  }
+  ix->dense_rows = (uint32_t)dense_tok.size();
+  ix->skip_rows = (uint32_t)skip_tok.size();
+  SL_TRY(dalloc(ix, &ix->tokinfo, V));
+  SL_CUDA_TRY(cudaMemcpyAsync(ix->tokinfo, info.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+  uint32_t* slot_tok;
+  SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
+  if (!dense_tok.empty())
+    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok, dense_tok.data(), dense_tok.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!skip_tok.empty())
+    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
+                                cudaMemcpyHostToDevice, st));
+  if (ix->dense_rows) {
+    SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
+    SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
+    dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
+    k_dense_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok, ix->dense_rows, ix->n_pad,
+                                    ix->dense);
+  }
+  if (ix->skip_rows) {
+    SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
+    dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
+    k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
+                                   ix->num_tiles, ix->skiptab);
+  }
+  SL_CUDA_TRY(cudaGetLastError());
+  SL_CUDA_TRY(cudaGetLastError());
+  return SL_OK;
+}
+
 int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   const uint32_t N = d->num_docs, V = d->vocab_size;
   // ---- inputs on the device
@@ -623,55 +681,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
                                                d->params, ix->avg_len, ix->values);
   SL_CUDA_TRY(cudaGetLastError());
 
-  // ---- query-side structures: dense copies of high-df rows, per-tile skip offsets
-  ix->num_tiles = (N + kTileDocs - 1) / kTileDocs;
-  ix->n_pad = ix->num_tiles * kTileDocs;
-  std::vector<uint32_t> h_df(V);
-  std::vector<uint64_t> h_ptr((size_t)V + 1);
-  SL_CUDA_TRY(cudaMemcpyAsync(h_df.data(), ix->df_global, (uint64_t)V * 4, cudaMemcpyDeviceToHost, st));
-  SL_CUDA_TRY(cudaMemcpyAsync(h_ptr.data(), ix->indptr, ((uint64_t)V + 1) * 8, cudaMemcpyDeviceToHost, st));
-  SL_CUDA_TRY(cudaStreamSynchronize(st));
-  const double density = d->dense_min_density > 0.f ? (double)d->dense_min_density : 0.25;
-  const double dense_thr = density * (double)ix->N_global;
-  const uint64_t skip_thr = 4ull * ix->num_tiles;  // >= 4 postings per tile expected
-  std::vector<int32_t> info(V, -1);
-  std::vector<uint32_t> dense_tok, skip_tok;
-  for (uint32_t t = 0; t < V; ++t) {
-    const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
-    if (dl == 0 || h_df[t] == 0) continue;
-    if ((double)h_df[t] >= dense_thr && density <= 1.0) {
-      info[t] = (int32_t)dense_tok.size();
-      dense_tok.push_back(t);
-    } else if (dl >= skip_thr) {
-      info[t] = -2 - (int32_t)skip_tok.size();
-      skip_tok.push_back(t);
-    }
-  }
-  ix->dense_rows = (uint32_t)dense_tok.size();
-  ix->skip_rows = (uint32_t)skip_tok.size();
-  SL_TRY(dalloc(ix, &ix->tokinfo, V));
-  SL_CUDA_TRY(cudaMemcpyAsync(ix->tokinfo, info.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
-  uint32_t* slot_tok;
-  SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
-  if (!dense_tok.empty())
-    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok, dense_tok.data(), dense_tok.size() * 4, cudaMemcpyHostToDevice, st));
-  if (!skip_tok.empty())
-    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
-                                cudaMemcpyHostToDevice, st));
-  if (ix->dense_rows) {
-    SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
-    SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
-    dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
-    k_dense_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok, ix->dense_rows, ix->n_pad,
-                                    ix->dense);
-  }
-  if (ix->skip_rows) {
-    SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
-    dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
-    k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
-                                   ix->num_tiles, ix->skiptab);
-  }
-  SL_CUDA_TRY(cudaGetLastError());
+  SL_TRY(build_query_structures(ix, d->dense_min_density, st));
   SL_CUDA_TRY(cudaEventRecord(ev1, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   SL_CUDA_TRY(cudaEventElapsedTime(&ix->build_ms, ev0, ev1));
@@ -718,6 +728,105 @@ int32_t build_index_impl(const sl_build_desc* d, sl_index** out) {
   const int32_t rc = build_body(d, ix, st);
   t_build_stream = nullptr;
   cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc != SL_OK) {
+    free_index(ix);
+    return rc;
+  }
+  *out = ix;
+  return SL_OK;
+}
+
+// Device index from host CSC arrays (index loading, SPEC load_index): validates the
+// ScoreMatrix invariants on the device, uploads, rebuilds the query-side structures.
+namespace {
+__global__ void k_row_starts(const uint64_t* __restrict__ indptr, uint32_t V, uint8_t* __restrict__ start) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x)
+    if (indptr[t] < indptr[t + 1]) start[indptr[t]] = 1;
+}
+__global__ void k_check_rows(const uint32_t* __restrict__ docids, const uint8_t* __restrict__ start, uint64_t nnz,
+                             uint32_t N, uint32_t* err) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = docids[p];
+    if (d >= N || (!start[p] && p > 0 && d <= docids[p - 1])) atomicOr(err, 1u);
+  }
+}
+}  // namespace
+
+int32_t load_index_from_host(const HostIndex& h, int device, float dense_min_density, sl_index** out) {
+  *out = nullptr;
+  SL_TRY(host_validate(h.params));
+  const uint32_t V = h.V, N = h.N;
+  const uint64_t nnz = h.indptr.empty() ? 0 : h.indptr.back();
+  if (h.indptr.size() != (size_t)V + 1 || h.indptr[0] != 0)
+    SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (indptr length/origin)");
+  for (uint32_t t = 0; t < V; ++t)
+    if (h.indptr[t + 1] < h.indptr[t]) SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (indptr decreasing)");
+  if (h.docids.size() != nnz || h.values.size() != nnz)
+    SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (indptr[V] != number of stored entries)");
+  if (h.df.size() != V || h.theta.size() != V || h.doclens.size() != N)
+    SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (array length mismatch)");
+  for (uint32_t t = 0; t < V; ++t) {
+    const uint64_t rl = h.indptr[t + 1] - h.indptr[t];
+    if (h.df[t] < rl || (h.N_global == N && h.df[t] != rl))
+      SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (df does not match row lengths)");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    SL_FAIL(SL_ECUDA, "load_index: no CUDA device available (there is no CPU fallback)");
+  SL_CUDA_TRY(cudaSetDevice(device));
+  auto* ix = new sl_index();
+  ix->device = device;
+  ix->params = h.params;
+  ix->N = N;
+  ix->V = V;
+  ix->doc_base = h.doc_base;
+  ix->N_global = h.N_global;
+  ix->total_len = h.total_len;
+  ix->avg_len = h.avg_len;
+  ix->nnz = nnz;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ix;
+    SL_FAIL(SL_ECUDA, "load_index: stream creation failed");
+  }
+  t_build_stream = st;
+  auto body = [&]() -> int32_t {
+    SL_TRY(dalloc(ix, &ix->indptr, (uint64_t)V + 1));
+    SL_TRY(dalloc(ix, &ix->docids, nnz));
+    SL_TRY(dalloc(ix, &ix->values, nnz));
+    SL_TRY(dalloc(ix, &ix->df_global, V));
+    SL_TRY(dalloc(ix, &ix->theta, V));
+    SL_TRY(dalloc(ix, &ix->doclens, N));
+    SL_CUDA_TRY(cudaMemcpyAsync(ix->indptr, h.indptr.data(), ((uint64_t)V + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (nnz) {
+      SL_CUDA_TRY(cudaMemcpyAsync(ix->docids, h.docids.data(), nnz * 4, cudaMemcpyHostToDevice, st));
+      SL_CUDA_TRY(cudaMemcpyAsync(ix->values, h.values.data(), nnz * 4, cudaMemcpyHostToDevice, st));
+    }
+    SL_CUDA_TRY(cudaMemcpyAsync(ix->df_global, h.df.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(ix->theta, h.theta.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(ix->doclens, h.doclens.data(), (uint64_t)N * 4, cudaMemcpyHostToDevice, st));
+    if (nnz) {  // strictly increasing doc ids per row, all < N (SPEC ScoreMatrix invariants)
+      Temps tmp(st);
+      uint8_t* start;
+      uint32_t* err;
+      SL_TRY(tmp.alloc(&start, nnz));
+      SL_TRY(tmp.alloc(&err, 1));
+      SL_CUDA_TRY(cudaMemsetAsync(start, 0, nnz, st));
+      SL_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+      k_row_starts<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, start);
+      k_check_rows<<<grid_for(nnz, 256), 256, 0, st>>>(ix->docids, start, nnz, N, err);
+      uint32_t herr = 0;
+      SL_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+      if (herr) SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (doc ids not strictly increasing or >= num_docs)");
+    }
+    ix->build_ms = 0.f;
+    return build_query_structures(ix, dense_min_density, st);
+  };
+  const int32_t rc = body();
+  cudaStreamSynchronize(st);
+  t_build_stream = nullptr;
   cudaStreamDestroy(st);
   if (rc != SL_OK) {
     free_index(ix);

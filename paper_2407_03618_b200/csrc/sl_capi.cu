@@ -46,6 +46,7 @@ const char* sl_status_string(int32_t s) {
     case SL_ENOMEM: return "out of device memory";
     case SL_ECORRUPT: return "corrupt index";
     case SL_EUNSUPPORTED: return "unsupported";
+    case SL_EIO: return "I/O error";
     default: return "unknown status";
   }
 }

@@ -67,7 +67,20 @@ struct sl_index {
   }
 };
 
+#include <vector>
+
 namespace sl {
+// host copy of a SearchIndex shard (persistence)
+struct HostIndex {
+  sl_params params{};
+  uint32_t N = 0, V = 0, doc_base = 0, N_global = 0;
+  uint64_t total_len = 0;
+  double avg_len = 0.0;
+  std::vector<uint64_t> indptr;
+  std::vector<uint32_t> docids, df, doclens;
+  std::vector<float> values, theta;
+};
+int32_t load_index_from_host(const HostIndex& h, int device, float dense_min_density, sl_index** out);
 int32_t build_index_impl(const sl_build_desc* desc, sl_index** out);
 void free_index(sl_index* ix);
 int32_t nccl_check(ncclResult_t r, const char* what);
