@@ -13,6 +13,7 @@
 // Everything is HBM-streaming integer work; no tensor cores are involved.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -358,6 +359,68 @@ __global__ void k_skip_fill(const uint64_t* __restrict__ indptr, const uint32_t*
   }
 }
 
+// max(0, v) as order-preserving bits (non-negative floats order like their bit patterns)
+__device__ __forceinline__ uint32_t pos_bits(float v) { return __float_as_uint(v > 0.f ? v : 0.f); }
+
+// rowmax[t] = max(0, max S^Δ in row t); the row of posting p by binary search on indptr
+__global__ void k_row_max(const uint64_t* __restrict__ indptr, uint32_t V, const float* __restrict__ values,
+                          uint64_t nnz, uint32_t* __restrict__ rowmax_bits) {
+  const uint32_t full = 0xffffffffu;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < nnz; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = base + threadIdx.x;
+    const bool valid = p < nnz;
+    uint32_t row = 0xFFFFFFFFu, bits = 0;
+    if (valid) {
+      uint32_t lo = 0, hi = V;  // last t with indptr[t] <= p
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (indptr[mid] <= p) lo = mid; else hi = mid;
+      }
+      row = lo;
+      bits = pos_bits(values[p]);
+    }
+    const uint32_t peers = __match_any_sync(full, row);
+    const uint32_t m = __reduce_max_sync(peers, bits);
+    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1 && m) atomicMax(rowmax_bits + row, m);
+  }
+}
+
+// per-tile maxima of the dense copies: warp per (slot, tile)
+__global__ void k_dense_tile_max(const float* __restrict__ dense, uint32_t n_slots, uint32_t n_tiles, uint32_t n_pad,
+                                 float* __restrict__ dmax) {
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (uint64_t)n_slots * n_tiles) return;
+  const uint32_t slot = (uint32_t)(w / n_tiles), tile = (uint32_t)(w % n_tiles);
+  const float* p = dense + (uint64_t)slot * n_pad + (uint64_t)tile * kTileDocs;
+  float m = 0.f;
+  for (int i = lane; i < kTileDocs; i += 32) m = fmaxf(m, p[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) dmax[w] = m;
+}
+
+// per-tile maxima of the skip rows' slices (warp-aggregated by tile)
+__global__ void k_skip_tile_max(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ docids,
+                                const float* __restrict__ values, const uint32_t* __restrict__ slot_tok,
+                                uint32_t n_slots, uint32_t n_tiles, uint32_t* __restrict__ smax_bits) {
+  for (uint32_t s = blockIdx.y; s < n_slots; s += gridDim.y) {
+    const uint32_t t = slot_tok[s];
+    const uint64_t b = indptr[t];
+    const uint32_t len = (uint32_t)(indptr[t + 1] - b);
+    for (uint32_t base = blockIdx.x * blockDim.x; base < len; base += gridDim.x * blockDim.x) {
+      const uint32_t j = base + threadIdx.x;
+      const bool valid = j < len;
+      const uint32_t tile = valid ? docids[b + j] / kTileDocs : 0xFFFFFFFFu;
+      const uint32_t bits = valid ? pos_bits(values[b + j]) : 0u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+      const uint32_t m = __reduce_max_sync(peers, bits);
+      if (valid && (threadIdx.x & 31) == __ffs(peers) - 1 && m)
+        atomicMax(smax_bits + (uint64_t)s * n_tiles + tile, m);
+    }
+  }
+}
+
 int grid_for(uint64_t n, int threads, int max_blocks = 148 * 32) {
   uint64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -456,8 +519,8 @@ int32_t nccl_check(ncclResult_t r, const char* what) {
 void free_index(sl_index* ix) {
   if (!ix) return;
   cudaSetDevice(ix->device);
-  void* ps[] = {ix->indptr, ix->docids, ix->values, ix->df_global, ix->theta,
-                ix->doclens, ix->tf, ix->tokinfo, ix->dense, ix->skiptab};
+  void* ps[] = {ix->indptr, ix->docids, ix->values, ix->df_global, ix->theta, ix->doclens, ix->tf,
+                ix->tokinfo, ix->dense, ix->skiptab, ix->rowmax, ix->dmax, ix->smax};
   for (void* p : ps)
     if (p) cudaFreeAsync(p, 0);  // back to the stream-ordered pool
   cudaStreamSynchronize(0);
@@ -536,7 +599,30 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
                                    ix->num_tiles, ix->skiptab);
   }
-  SL_CUDA_TRY(cudaGetLastError());
+  // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
+  // DESIGN.md §8)
+  const char* bm = std::getenv("SL_BLOCKMAX");
+  if (!bm || std::atoi(bm) == 0) {
+    SL_CUDA_TRY(cudaGetLastError());
+    return SL_OK;
+  }
+  SL_TRY(dalloc(ix, &ix->rowmax, V));
+  SL_CUDA_TRY(cudaMemsetAsync(ix->rowmax, 0, (uint64_t)V * 4, st));
+  if (ix->nnz)
+    k_row_max<<<grid_for(ix->nnz, 256), 256, 0, st>>>(ix->indptr, V, ix->values, ix->nnz, (uint32_t*)ix->rowmax);
+  if (ix->dense_rows) {
+    SL_TRY(dalloc(ix, &ix->dmax, (uint64_t)ix->dense_rows * ix->num_tiles));
+    const uint64_t warps = (uint64_t)ix->dense_rows * ix->num_tiles;
+    k_dense_tile_max<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(ix->dense, ix->dense_rows, ix->num_tiles,
+                                                                         ix->n_pad, ix->dmax);
+  }
+  if (ix->skip_rows) {
+    SL_TRY(dalloc(ix, &ix->smax, (uint64_t)ix->skip_rows * ix->num_tiles));
+    SL_CUDA_TRY(cudaMemsetAsync(ix->smax, 0, (uint64_t)ix->skip_rows * ix->num_tiles * 4, st));
+    dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
+    k_skip_tile_max<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok + dense_tok.size(),
+                                       ix->skip_rows, ix->num_tiles, (uint32_t*)ix->smax);
+  }
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }

@@ -41,6 +41,10 @@ struct sl_index {
   float* dense = nullptr;         // [dense_rows * n_pad]
   uint32_t dense_rows = 0;
   uint32_t* skiptab = nullptr;    // [skip_rows * (num_tiles + 1)]
+  // block-max bounds (exact top-k pruning): max(0, S^Δ) over a row / a row's tile slice
+  float* rowmax = nullptr;        // [V]
+  float* dmax = nullptr;          // [dense_rows * num_tiles]
+  float* smax = nullptr;          // [skip_rows * num_tiles]
   uint32_t skip_rows = 0;
   uint32_t num_tiles = 0;
   uint32_t n_pad = 0;
@@ -58,6 +62,9 @@ struct sl_index {
     v.tokinfo = tokinfo;
     v.dense = dense;
     v.skiptab = skiptab;
+    v.rowmax = rowmax;
+    v.dmax = dmax;
+    v.smax = smax;
     v.V = V;
     v.N = N;
     v.n_pad = n_pad;

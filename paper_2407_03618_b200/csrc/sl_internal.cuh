@@ -154,6 +154,9 @@ struct IndexView {
   const int32_t* tokinfo;     // [V] >=0 dense slot, -1 short row, <=-2 skip slot -(x+2)
   const float* dense;         // [dense_rows][n_pad]
   const uint32_t* skiptab;    // [skip_rows][num_tiles+1]
+  const float* rowmax;        // [V]                       max(0, S^Δ) over the row
+  const float* dmax;          // [dense_rows][num_tiles]   max(0, S^Δ) over a dense row's tile
+  const float* smax;          // [skip_rows][num_tiles]    max(0, S^Δ) over a skip row's tile slice
   uint32_t V;
   uint32_t N;        // local docs
   uint32_t n_pad;    // num_tiles * kTileDocs

@@ -24,6 +24,7 @@
 // GPU count. k_merge selects the final top-k per query from the per-split candidates (and
 // is the rank-0 merge of the G x k candidates gathered over NCCL).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -230,6 +231,7 @@ struct RunArgs {
   float* dense_out;           // GM_DENSE: [N]
   uint32_t debug_skip;        // timing experiments only (SL_DEBUG_SKIP): 1 gather, 2 filter, 4 dense
   uint32_t kept_global;       // large k: running candidates live in their cand slot (global/L2)
+  uint32_t prune;             // exact block-max pruning of (query, tile) pairs
 };
 
 // per-warp shared memory; E = R * qmax gathered-row entries (the run's queries' CSC
@@ -251,13 +253,14 @@ struct WSmem {
   uint32_t* nextdoc;    // [E] short rows: doc id at the cursor (UINT32_MAX at the end)
   uint32_t* sb;         // [E] slice of the current tile (row-relative start)
   uint32_t* cnt;        // [E] and length
+  float* rmax;          // [E] row maximum max(0, S^Δ) (block-max bound of short rows)
 };
 
 // C = candidates held in shared memory per query (0 when they live in global memory)
 __host__ __device__ inline size_t warp_smem_bytes(uint32_t R, uint32_t C, uint32_t qmax) {
   const size_t E = (size_t)R * qmax;
   size_t b = (size_t)TILE * 8 + (size_t)R * C * 8 + (size_t)R * 8 + E * 8 + 16 * 4 + (size_t)R * 4 + (R + 1) * 4 + 4 +
-             (size_t)qmax * 4 + E * 4 * 6;
+             (size_t)qmax * 4 + E * 4 * 7;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -279,7 +282,8 @@ __device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_
   s.cursor = (uint32_t*)p; p += E * 4;
   s.nextdoc = (uint32_t*)p; p += E * 4;
   s.sb = (uint32_t*)p; p += E * 4;
-  s.cnt = (uint32_t*)p;
+  s.cnt = (uint32_t*)p; p += E * 4;
+  s.rmax = (float*)p;
   return s;
 }
 
@@ -452,9 +456,17 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
         if (lane == 0) s.dslot[nd] = info;  // identical multiset for every query of the run
         ++nd;
       } else if (e < 32) {
+#ifdef SL_DEBUG_CHECKS
+        if (e >= ra.R * ra.qmax) {
+          printf("entry overflow: run %u lane %d nr %u R %u qmax %u e %u incl %u ns %u q %u qlen %llu\n", run, lane, nr,
+                 ra.R, ra.qmax, e, incl, ns, q, (unsigned long long)(qe - qb));
+          __trap();
+        }
+#endif
         s.row_start[e] = rb;
         s.row_len[e] = (uint32_t)(re - rb);
         s.skip[e] = info <= -2 ? -2 - info : -1;
+        s.rmax[e] = ix.rowmax ? ix.rowmax[t] : 0.f;
         ++e;
       }
     }
@@ -478,11 +490,18 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   __syncwarp();
   const int E = s.ebeg[nr];
   const int nd = s.nd[0];
+#ifdef SL_DEBUG_CHECKS
+  if (lane == 0 && (nr > ra.R || nr == 0 || (uint32_t)E > ra.R * ra.qmax || (uint32_t)nd > ra.qmax)) {
+    printf("k_score_runs invariant: run %u nr %u R %u E %d qmax %u nd %d\n", run, nr, ra.R, E, ra.qmax, nd);
+    __trap();
+  }
+#endif
   // ---- per-lane entry state (registers)
   const bool ent = lane < E;
   const uint64_t rstart = ent ? s.row_start[lane] : 0ull;
   const uint32_t rlen = ent ? s.row_len[lane] : 0u;
   const int32_t sk = ent ? s.skip[lane] : -1;
+  const float rmx = ent ? s.rmax[lane] : 0.f;
   const uint32_t* tab = ix.skiptab + (uint64_t)(sk < 0 ? 0 : sk) * (ix.num_tiles + 1);
   uint32_t cursor = 0, nextdoc = 0xFFFFFFFFu;  // short rows
   uint32_t nsb = 0, ncnt = 0;                  // skip rows: slice of the NEXT tile (prefetched)
@@ -544,6 +563,26 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     }
     const uint32_t hmask = __ballot_sync(0xffffffffu, cnt != 0);
     const uint64_t rbase = rstart + sb;
+    // (1b) exact block-max pruning: UB(query, tile) = Σ dense-row tile maxima (ascending slot,
+    // the order of the real sum) + Σ gathered-row bounds of rows with postings here; a query
+    // whose UB cannot exceed its threshold score skips the tile (its later docs cannot win
+    // ties either: larger ids). 4e-6 relative margin covers the tree-order of the bound sum.
+    uint32_t live = (1u << nr) - 1u;
+    if (ra.prune) {
+      float ubd = 0.f;
+      for (int i = 0; i < nd; ++i) ubd += __ldg(ix.dmax + (uint64_t)s.dslot[i] * ix.num_tiles + tile);
+      const float bnd = cnt == 0 ? 0.f : (sk >= 0 ? __ldg(ix.smax + (uint64_t)sk * ix.num_tiles + tile) : rmx);
+      for (uint32_t r = 0; r < nr; ++r) {
+        const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
+        float v = (lane >= e0 && lane < e1) ? bnd : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const float ub = ubd + v;
+        const uint64_t tau = s.tau[r];
+        if (tau != 0 && ub + fabsf(ub) * 4e-6f <= tau_float(tau)) live &= ~(1u << r);
+      }
+      if (!live) continue;
+    }
     // (2) dense signature of the run, ascending slot order, all loads in flight
     if (!(ra.debug_skip & 4)) {
       float4 a[F4L];
@@ -569,6 +608,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
+      if (!((live >> r) & 1u)) continue;
       const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
       const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
@@ -981,6 +1021,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   }
   SL_CUDA_TRY(cudaEventRecord(sc->ev[0], st));
   const IndexView v = ix->view();
+  const bool have_bounds = v.rowmax && (!ix->dense_rows || v.dmax) && (!ix->skip_rows || v.smax);
   double* qconst;
   uint32_t* info;
   unsigned long long* bytes;
@@ -1036,6 +1077,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.warp_bytes = plan.warp_bytes;
   ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
   ra.kept_global = plan.kept_global;
+  ra.prune = have_bounds && env_int("SL_PRUNE", 0) ? 1u : 0u;  // opt-in
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;

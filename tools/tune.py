@@ -6,6 +6,8 @@ import json
 import os
 import sys
 
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
@@ -15,6 +17,7 @@ def main():
     ap.add_argument("--k", type=int, default=10)
     ap.add_argument("--sweep", default='[{}]')
     ap.add_argument("--dense-density", type=float, default=0.0)
+    ap.add_argument("--shard-of", type=int, default=1)
     a = ap.parse_args()
     import torch
     from paper_2407_03618_b200 import BM25Params, build_index, synth, _lib
@@ -22,9 +25,17 @@ def main():
     cfg = synth.config(a.config)
     cdf = synth.zipf_cdf(cfg)
     off = synth.doc_offsets(cfg)
+    if a.shard_of > 1:  # one shard of a document-sharded corpus (c5 on one GPU)
+        from paper_2407_03618_b200 import shard_ranges
+        d0, d1 = shard_ranges(off, a.shard_of)[0]
+        off = (off[d0:d1 + 1] - off[d0]).astype(np.uint64)
+        base = int(synth.doc_offsets(cfg, 0, d0)[-1]) if d0 else 0
+    else:
+        base = 0
     T = int(off[-1])
     tok = torch.empty(T, dtype=torch.uint32, device="cuda")
-    check(lib().sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, 0, T, SL_MEM_HOST, tok.data_ptr()))
+    check(lib().sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, base, T, SL_MEM_HOST,
+                                       tok.data_ptr()))
     idx = build_index(torch.from_numpy(off).cuda(), tok, cfg.vocab, BM25Params(), dense_min_density=a.dense_density)
     inf = idx.info()
     print(json.dumps({"build_ms": inf.build_ms, "dense_rows": inf.dense_rows, "skip_rows": inf.skip_rows,
