@@ -415,7 +415,7 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
 // One warp per (run, doc split): a run is <= R queries with the same dense signature.
 // Lane e owns gathered-row entry e of the run (the runs' queries' CSC tokens concatenated
 // in query order; at most 32). No CTA-level synchronisation: warps progress independently.
-template <int MODE>
+template <int MODE, bool PRUNE>
 __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
         s.row_start[e] = rb;
         s.row_len[e] = (uint32_t)(re - rb);
         s.skip[e] = info <= -2 ? -2 - info : -1;
-        s.rmax[e] = ix.rowmax ? ix.rowmax[t] : 0.f;
+        if (PRUNE) s.rmax[e] = ix.rowmax[t];
         ++e;
       }
     }
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   const uint64_t rstart = ent ? s.row_start[lane] : 0ull;
   const uint32_t rlen = ent ? s.row_len[lane] : 0u;
   const int32_t sk = ent ? s.skip[lane] : -1;
-  const float rmx = ent ? s.rmax[lane] : 0.f;
+  const float rmx = PRUNE && ent ? s.rmax[lane] : 0.f;
   const uint32_t* tab = ix.skiptab + (uint64_t)(sk < 0 ? 0 : sk) * (ix.num_tiles + 1);
   uint32_t cursor = 0, nextdoc = 0xFFFFFFFFu;  // short rows
   uint32_t nsb = 0, ncnt = 0;                  // skip rows: slice of the NEXT tile (prefetched)
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     // whose UB cannot exceed its threshold score skips the tile (its later docs cannot win
     // ties either: larger ids). 4e-6 relative margin covers the tree-order of the bound sum.
     uint32_t live = (1u << nr) - 1u;
-    if (ra.prune) {
+    if constexpr (PRUNE) {
       float ubd = 0.f;
       for (int i = 0; i < nd; ++i) ubd += __ldg(ix.dmax + (uint64_t)s.dslot[i] * ix.num_tiles + tile);
       const float bnd = cnt == 0 ? 0.f : (sk >= 0 ? __ldg(ix.smax + (uint64_t)sk * ix.num_tiles + tile) : rmx);
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
-      if (!((live >> r) & 1u)) continue;
+      if (PRUNE && !((live >> r) & 1u)) continue;
       const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
       const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
@@ -966,8 +966,8 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   p->smem = (size_t)p->wpc * p->warp_bytes;
   if (p->smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "top-k / query length too large for shared memory");
   int per_sm = 0;
-  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK>, NT, p->smem));
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
+  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, p->smem));
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
   uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
@@ -1085,7 +1085,13 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   const uint64_t grid = ((uint64_t)B * plan.n_splits + plan.wpc - 1) / plan.wpc;
   if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
   SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
-  k_score_runs<GM_TOPK><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+  if (ra.prune) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)plan.smem));
+    k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+  } else {
+    k_score_runs<GM_TOPK, false><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+  }
   SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
 
@@ -1198,8 +1204,8 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
   ra.warp_bytes = (uint32_t)warp_smem_bytes(ra.R, ra.C, ra.qmax);
   ra.dense_out = d_out;
   const size_t smem = (size_t)ra.wpc * ra.warp_bytes;
-  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_score_runs<GM_DENSE><<<(ra.n_splits + NW - 1) / NW, NT, smem, st>>>(v, ra);
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_score_runs<GM_DENSE, false><<<(ra.n_splits + NW - 1) / NW, NT, smem, st>>>(v, ra);
   SL_CUDA_TRY(cudaGetLastError());
   if (mem == SL_MEM_HOST)
     SL_CUDA_TRY(cudaMemcpyAsync(out, d_out, (uint64_t)ix->N * 4, cudaMemcpyDeviceToHost, st));

@@ -250,3 +250,20 @@ def test_top_k_random_vectors_ac3(cuda_ok):
         ri, rs = oracle.top_k(s.astype(np.float64), k)
         assert np.array_equal(gi.astype(np.int64), ri.astype(np.int64)), i
         assert np.array_equal(gs, rs.astype(np.float32)), i
+
+
+@pytest.mark.parametrize("p", [BM25Params(Variant.lucene), BM25Params(Variant.robertson),
+                               BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)], ids=lambda p: p.variant.name)
+@pytest.mark.parametrize("k", [10, 1000])
+def test_blockmax_pruning_is_exact(cuda_ok, c1, monkeypatch, p, k):
+    """Opt-in block-max pruning (SL_BLOCKMAX=1 build, SL_PRUNE=1 query) skips (query, tile)
+    pairs whose bound cannot beat the threshold: the top-k must be bit-identical."""
+    cfg, corp, qoff, qtok = c1
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as a:
+        ref = retrieve_batch(a, (qoff, qtok), k, as_arrays=True)
+    monkeypatch.setenv("SL_BLOCKMAX", "1")
+    monkeypatch.setenv("SL_PRUNE", "1")
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as b:
+        out = retrieve_batch(b, (qoff, qtok), k, as_arrays=True)
+    np.testing.assert_array_equal(out[0], ref[0])
+    np.testing.assert_array_equal(out[1], ref[1])
