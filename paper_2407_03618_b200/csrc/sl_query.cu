@@ -231,6 +231,7 @@ struct RunArgs {
   float* dense_out;           // GM_DENSE: [N]
   uint32_t debug_skip;        // timing experiments only (SL_DEBUG_SKIP): 1 gather, 2 filter, 4 dense
   uint32_t kept_global;       // large k: running candidates live in their cand slot (global/L2)
+  uint32_t split_major;       // work-item order (see k_score_runs)
   uint32_t prune;             // exact block-max pruning of (query, tile) pairs
 };
 
@@ -424,7 +425,11 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   const uint64_t item = (uint64_t)blockIdx.x * ra.wpc + warp;
   if (item >= (uint64_t)n_runs * ra.n_splits) return;
   const WSmem s = wcarve(smem_raw + (size_t)warp * ra.warp_bytes, ra.R, ra.kept_global ? 0u : ra.C, ra.qmax);
-  const uint32_t run = (uint32_t)(item / ra.n_splits), split = (uint32_t)(item % ra.n_splits);
+  // split-major order: concurrently resident warps sweep the same doc region, so each CSC
+  // slice / dense chunk is fetched from HBM once and served from L2 to every query using it
+  const bool smaj = ra.split_major != 0;
+  const uint32_t run = (uint32_t)(smaj ? item % n_runs : item / ra.n_splits);
+  const uint32_t split = (uint32_t)(smaj ? item / n_runs : item % ra.n_splits);
   const uint32_t pb = ra.run_begin[run];
   const uint32_t nr = ra.run_begin[run + 1] - pb;
   const uint32_t t0 = (uint32_t)((uint64_t)split * ix.num_tiles / ra.n_splits);
@@ -1077,6 +1082,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.warp_bytes = plan.warp_bytes;
   ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
   ra.kept_global = plan.kept_global;
+  ra.split_major = (uint32_t)env_int("SL_SPLIT_MAJOR", 1);
   ra.prune = have_bounds && env_int("SL_PRUNE", 0) ? 1u : 0u;  // opt-in
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
