@@ -46,7 +46,7 @@ struct Status {
 #endif
 constexpr int kTileDocs = SL_TILE_DOCS;  // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
 constexpr int kScoreThreads = 256;     // threads per scoring CTA
-constexpr int kQMax = 32;              // max query tokens (one lane per gathered row)
+constexpr int kQMax = 32;              // gathered rows per query in the warp kernel (one lane each); longer queries go to k_score_long
 constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path
 constexpr uint64_t kInvalidKey = 0ull; // never produced by a real (score, doc) key
 

@@ -654,18 +654,169 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
   }
 }
 
+// Queries with more than 32 gathered rows (one lane per row does not fit): one CTA per
+// (query, doc split). Same per-document summation order as k_score_runs — dense rows in
+// ascending slot order, then gathered rows in query order — so scores are bit-identical to
+// what the warp kernel would produce; the running top-k is the same warp-level filter.
+// Shared memory: acc[TILE] | tau, n_kept, hist | per-entry arrays [ne].
+template <int MODE>
+__global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uint32_t first, uint32_t n_long,
+                                                   uint32_t qcap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t li = blockIdx.x / ra.n_splits, split = blockIdx.x % ra.n_splits;
+  if (li >= n_long) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* acc = reinterpret_cast<float*>(smem_raw);
+  uint64_t* tau = reinterpret_cast<uint64_t*>(acc + TILE);
+  uint64_t* row_start = tau + 1;                                   // [qcap]
+  uint32_t* n_kept = reinterpret_cast<uint32_t*>(row_start + qcap);
+  uint32_t* hist = n_kept + 1;                                     // [16]
+  int32_t* counts = reinterpret_cast<int32_t*>(hist + 16);         // nd, ns
+  int32_t* dslot = counts + 2;                                     // [qcap]
+  uint32_t* row_len = reinterpret_cast<uint32_t*>(dslot + qcap);   // [qcap]
+  int32_t* skip = reinterpret_cast<int32_t*>(row_len + qcap);      // [qcap]
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(skip + qcap);     // [qcap]
+  uint32_t* nextdoc = cursor + qcap;                               // [qcap]
+  uint32_t* sbv = nextdoc + qcap;                                  // [qcap]
+  uint32_t* cntv = sbv + qcap;                                     // [qcap]
+  const uint32_t q = ra.perm[first + li];
+  const uint32_t t0 = (uint32_t)((uint64_t)split * ix.num_tiles / ra.n_splits);
+  const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * ix.num_tiles / ra.n_splits);
+  if (threadIdx.x == 0) {
+    int nd = 0, ns = 0;
+    for (uint64_t j = ra.q_off[q]; j < ra.q_off[q + 1]; ++j) {
+      const uint32_t t = ra.q_tok[j];
+      if (t >= ix.V || ix.df_global[t] == 0) continue;  // OOV drop (SPEC tokenizer decisions)
+      const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
+      if (rb == re) continue;
+      const int32_t info = ix.tokinfo[t];
+      if (info >= 0) {
+        int b = nd - 1;  // ascending slot order (canonical dense order)
+        while (b >= 0 && dslot[b] > info) {
+          dslot[b + 1] = dslot[b];
+          --b;
+        }
+        dslot[b + 1] = info;
+        ++nd;
+      } else {
+        row_start[ns] = rb;
+        row_len[ns] = (uint32_t)(re - rb);
+        skip[ns] = info <= -2 ? -2 - info : -1;
+        ++ns;
+      }
+    }
+    counts[0] = nd;
+    counts[1] = ns;
+    *tau = 0;
+    *n_kept = 0;
+  }
+  __syncthreads();
+  const int nd = counts[0], ns = counts[1];
+  for (int e = threadIdx.x; e < ns; e += NT) {
+    if (skip[e] < 0) {
+      const uint32_t* ids = ix.docids + row_start[e];
+      uint32_t lo = 0, hi = row_len[e];
+      const uint32_t dstart = t0 * TILE;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ids + mid) < dstart) lo = mid + 1; else hi = mid;
+      }
+      cursor[e] = lo;
+      nextdoc[e] = lo < row_len[e] ? __ldg(ids + lo) : 0xFFFFFFFFu;
+    }
+  }
+  __syncthreads();
+  WSmem ws{};
+  ws.tau = tau;
+  ws.n_kept = n_kept;
+  ws.hist = hist;
+  uint64_t* kept = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
+  const uint32_t rstride = ix.n_pad / 4;
+  for (uint32_t tile = t0; tile < t1; ++tile) {
+    const uint32_t d0 = tile * TILE, d1 = d0 + TILE;
+    const uint32_t nvalid = min((uint32_t)TILE, ix.N - d0);
+    // slices of the gathered rows in this tile (thread per entry)
+    for (int e = threadIdx.x; e < ns; e += NT) {
+      uint32_t sb, cnt = 0;
+      if (skip[e] >= 0) {
+        const uint32_t* tab = ix.skiptab + (uint64_t)skip[e] * (ix.num_tiles + 1) + tile;
+        sb = __ldg(tab);
+        cnt = __ldg(tab + 1) - sb;
+      } else {
+        sb = cursor[e];
+        if (nextdoc[e] < d1) {
+          const uint32_t* ids = ix.docids + row_start[e];
+          uint32_t cur = sb + 1, nxt = 0xFFFFFFFFu;
+          while (cur < row_len[e]) {
+            nxt = __ldg(ids + cur);
+            if (nxt >= d1) break;
+            ++cur;
+          }
+          if (cur >= row_len[e]) nxt = 0xFFFFFFFFu;
+          cnt = cur - sb;
+          cursor[e] = cur;
+          nextdoc[e] = nxt;
+        }
+      }
+      sbv[e] = sb;
+      cntv[e] = cnt;
+    }
+    // dense rows: thread-owned float4, ascending slot order (the warp kernel's order)
+    if (threadIdx.x < TILE / 4) {
+      const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + threadIdx.x;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < nd; ++i) {
+        const float4 v = __ldg(dbase + (uint64_t)dslot[i] * rstride);
+        a.x += v.x;
+        a.y += v.y;
+        a.z += v.z;
+        a.w += v.w;
+      }
+      reinterpret_cast<float4*>(acc)[threadIdx.x] = a;
+    }
+    __syncthreads();
+    // gathered rows one at a time in query order (unique docs within a row)
+    for (int e = 0; e < ns; ++e) {
+      const uint32_t cnt = cntv[e];
+      if (!cnt) continue;
+      const uint64_t base = row_start[e] + sbv[e];
+      for (uint32_t p = threadIdx.x; p < cnt; p += NT)
+        acc[__ldg(ix.docids + base + p) - d0] += __ldg(ix.values + base + p);
+      __syncthreads();
+    }
+    if constexpr (MODE == GM_DENSE) {
+      const double qc = ra.qconst[q];
+      for (uint32_t i = threadIdx.x; i < nvalid; i += NT) ra.dense_out[d0 + i] = __double2float_rn((double)acc[i] + qc);
+    } else {
+      if (warp == 0) filter_tile(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept);
+    }
+    __syncthreads();
+  }
+  if constexpr (MODE == GM_TOPK) {
+    if (warp == 0)
+      for (uint32_t i = *n_kept + lane; i < ra.C; i += 32) kept[i] = kInvalidKey;
+  }
+}
+
+__host__ inline size_t long_smem_bytes(uint32_t qcap) {
+  return (size_t)TILE * 4 + 8 + (size_t)qcap * 8 + 4 + 16 * 4 + 8 + (size_t)qcap * 4 * 7 + 16;
+}
+
 // Per query: sorted dense signature (slots of rows with a dense copy) and its hash.
 __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
                             IndexView ix, uint32_t qmax, int32_t* __restrict__ qdense, uint32_t* __restrict__ nden,
                             uint32_t* __restrict__ hkey, uint32_t* __restrict__ hval) {
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
     int32_t* d = qdense + (uint64_t)q * qmax;
-    uint32_t n = 0;
+    uint32_t n = 0, ng = 0;
     for (uint64_t j = q_off[q]; j < q_off[q + 1]; ++j) {
       const uint32_t t = q_tok[j];
       if (t >= ix.V || ix.df_global[t] == 0 || ix.indptr[t] == ix.indptr[t + 1]) continue;
       const int32_t info = ix.tokinfo[t];
-      if (info < 0) continue;
+      if (info < 0) {
+        ++ng;
+        continue;
+      }
       int b = (int)n - 1;
       while (b >= 0 && d[b] > info) {
         d[b + 1] = d[b];
@@ -677,7 +828,8 @@ __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* 
     uint32_t h = 2166136261u ^ n;  // FNV-1a over the sorted slots
     for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
     nden[q] = n;
-    hkey[q] = h;
+    // > 32 gathered rows: sorts after every short query (key 0xFFFFFFFF) -> k_score_long
+    hkey[q] = ng > 32 ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
     hval[q] = q;
   }
 }
@@ -877,6 +1029,7 @@ __global__ void k_query_prep(const uint64_t* __restrict__ q_off, const uint32_t*
     atomicMax(&info[1], (uint32_t)min(e - b, (uint64_t)0xFFFFFFFFu));
     double c = 0.0;
     unsigned long long pb = 0;
+    uint32_t ng = 0;
     for (uint64_t j = b; j < e; ++j) {
       const uint32_t t = q_tok[j];
       if (t >= ix.V) {
@@ -886,7 +1039,9 @@ __global__ void k_query_prep(const uint64_t* __restrict__ q_off, const uint32_t*
       if (ix.df_global[t] == 0) continue;
       c += (double)ix.theta[t];
       pb += 8ull * (ix.indptr[t + 1] - ix.indptr[t]);
+      if (ix.indptr[t + 1] != ix.indptr[t] && ix.tokinfo && ix.tokinfo[t] < 0) ++ng;
     }
+    if (ng > 32) atomicAdd(&info[2], 1u);
     qconst[q] = c;
     if (bytes && pb) atomicAdd(bytes, pb);
   }
@@ -1042,10 +1197,9 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_info[0] & 2u) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
-  if (h_info[1] > (uint32_t)kQMax)
-    SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: queries longer than 32 tokens are not supported yet");
-
   const uint32_t qmax = std::max(1u, h_info[1]);
+  const uint32_t n_long = h_info[2];   // queries with > 32 gathered rows -> k_score_long
+  const uint32_t B_short = B - n_long;  // they sort after every other query
   RunPlan plan;
   SL_TRY(plan_runs(ix, B, k, qmax, &plan));
   // group queries by dense signature: sort by signature hash, cut runs of <= R identical ones
@@ -1064,7 +1218,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv);
   const uint32_t *sk, *perm;
   SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
-  k_build_runs<<<1, 1024, 0, st>>>(perm, B, qdense, nden, qmax, plan.R, run_begin, n_runs);
+  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, qmax, plan.R, run_begin, n_runs);
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;
@@ -1088,7 +1242,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
   // upper bound on runs is B; warps past the real run count exit at once
-  const uint64_t grid = ((uint64_t)B * plan.n_splits + plan.wpc - 1) / plan.wpc;
+  const uint64_t grid = std::max<uint64_t>(1, ((uint64_t)B_short * plan.n_splits + plan.wpc - 1) / plan.wpc);
   if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
   SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
   if (ra.prune) {
@@ -1097,6 +1251,12 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
   } else {
     k_score_runs<GM_TOPK, false><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+  }
+  if (n_long) {
+    const size_t lsm = long_smem_bytes(qmax);
+    if (lsm > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: query too long for the device scorer");
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    k_score_long<GM_TOPK><<<n_long * plan.n_splits, NT, lsm, st>>>(v, ra, B_short, n_long, qmax);
   }
   SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
@@ -1153,14 +1313,13 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     stats->posting_bytes = hb;
     stats->scorevec_bytes = 4ull * ix->N * B;
     stats->unique_posting_bytes = 0;
-    stats->kernels_launched = dist ? (ix->comm->rank == 0 ? 4 : 3) : 3;
+    stats->kernels_launched = (dist ? (ix->comm->rank == 0 ? 4 : 3) : 3) + (n_long ? 1 : 0);
   }
   return SL_OK;
 }
 
 int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t q_len, int32_t mem, float* out) {
   if (!ix || !out) SL_FAIL(SL_EINVAL, "score_query: null argument");
-  if (q_len > (uint32_t)kQMax) SL_FAIL(SL_EUNSUPPORTED, "score_query: queries longer than 32 tokens are not supported yet");
   StreamCache* sc;
   SL_TRY(get_stream(ix->device, &sc));
   cudaStream_t st = sc->st;
@@ -1187,31 +1346,24 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
   SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
-  // one run holding the single query, one warp per tile
-  const uint32_t h_runs[3] = {0u, 1u, 1u};  // run_begin = {0, 1}; n_runs = 1
-  uint32_t *d_runs, *d_perm;
-  SL_TRY(scr.alloc(&d_runs, 3));
+  // the single query as a "long" query: one CTA per tile, same summation order as retrieval
+  uint32_t* d_perm;
   SL_TRY(scr.alloc(&d_perm, 1));
-  SL_CUDA_TRY(cudaMemcpyAsync(d_runs, h_runs, 12, cudaMemcpyHostToDevice, st));
   SL_CUDA_TRY(cudaMemsetAsync(d_perm, 0, 4, st));
   RunArgs ra{};
   ra.q_off = d_off;
   ra.q_tok = d_tok;
   ra.qconst = qconst;
   ra.perm = d_perm;
-  ra.run_begin = d_runs;
-  ra.n_runs = d_runs + 2;
   ra.k = 1;
   ra.C = kept_capacity(1);
-  ra.R = 1;
-  ra.qmax = std::max(1u, q_len);
   ra.n_splits = std::max(1u, ix->num_tiles);
-  ra.wpc = NW;
-  ra.warp_bytes = (uint32_t)warp_smem_bytes(ra.R, ra.C, ra.qmax);
   ra.dense_out = d_out;
-  const size_t smem = (size_t)ra.wpc * ra.warp_bytes;
-  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_DENSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_score_runs<GM_DENSE, false><<<(ra.n_splits + NW - 1) / NW, NT, smem, st>>>(v, ra);
+  const uint32_t qcap = std::max(1u, q_len);
+  const size_t smem = long_smem_bytes(qcap);
+  if (smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "score_query: query too long for the device scorer");
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_score_long<GM_DENSE><<<ra.n_splits, NT, smem, st>>>(v, ra, 0, 1, qcap);
   SL_CUDA_TRY(cudaGetLastError());
   if (mem == SL_MEM_HOST)
     SL_CUDA_TRY(cudaMemcpyAsync(out, d_out, (uint64_t)ix->N * 4, cudaMemcpyDeviceToHost, st));

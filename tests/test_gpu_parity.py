@@ -267,3 +267,32 @@ def test_blockmax_pruning_is_exact(cuda_ok, c1, monkeypatch, p, k):
         out = retrieve_batch(b, (qoff, qtok), k, as_arrays=True)
     np.testing.assert_array_equal(out[0], ref[0])
     np.testing.assert_array_equal(out[1], ref[1])
+
+
+@pytest.mark.parametrize("p", [BM25Params(Variant.lucene), BM25Params(Variant.bm25l, 1.5, 0.75, 0.5)],
+                         ids=lambda p: p.variant.name)
+def test_long_queries_mixed_batch(cuda_ok, c1, p):
+    """Queries with > 32 gathered rows (e.g. passage-length BEIR queries) run on the CTA kernel;
+    a batch mixing them with short queries must match the oracle query by query."""
+    cfg, corp, qoff, qtok = c1
+    rng = np.random.default_rng(9)
+    queries = []
+    for i in range(120):
+        if i % 3 == 0:  # long: 40..300 tokens, mostly distinct mid/low-frequency ids (+ some repeats)
+            n = int(rng.integers(40, 301))
+            q = list(rng.integers(30, cfg.vocab, n)) + list(rng.integers(0, 30, 5))
+        else:
+            q = list(qtok[int(qoff[i]):int(qoff[i + 1])])
+        queries.append(q)
+    qo, qt = csr(queries)
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    for k in (10, 100):
+        rid, rsc = ox.retrieve_batch(qo, qt, k, True, 8)
+        with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+            gid, gsc = retrieve_batch(gi, (qo, qt), k, as_arrays=True)
+            for b in range(0, 120, 7):
+                s = score_query(gi, queries[b])  # the CTA kernel: same bits as the top-k path
+                np.testing.assert_array_equal(s[gid[b, :k].astype(np.int64)], gsc[b, :k])
+        assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(queries[b]),
+                          lambda b: query_scale(exp, queries[b]), f"long {p.variant.name} k={k}")
