@@ -150,6 +150,7 @@ int32_t sl_index_load(const char* directory, int32_t device, float dense_min_den
  * documents by B(Q,D) = Σ S^Δ + Σ S^θ, score descending, ties -> smaller global doc id.
  * Outputs are [num_queries x k]; slots beyond min(k, N) hold id 0xFFFFFFFF, score -inf.
  * Query tokens with global df = 0 are dropped (SPEC OOV rule); ids >= |V| are an error.
+ * Any k >= 1 (k > 4096: full per-query ranking, single rank only); any query length.
  * `ordered` is accepted for API parity; results are always sorted (a valid order for
  * ordered == 0 as well). With a communicator, every rank passes the same queries and
  * the merged result is written on rank 0 only (other ranks may pass NULL outputs). */

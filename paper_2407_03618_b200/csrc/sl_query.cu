@@ -802,6 +802,28 @@ __host__ inline size_t long_smem_bytes(uint32_t qcap) {
   return (size_t)TILE * 4 + 8 + (size_t)qcap * 8 + 4 + 16 * 4 + 8 + (size_t)qcap * 4 * 7 + 16;
 }
 
+// Large k (> kMaxK): keys for a stable LSD radix sort that yields (score desc, doc asc).
+__global__ void k_rank_keys(const float* __restrict__ scores, uint32_t n, uint32_t id_base, uint32_t* __restrict__ key,
+                            uint32_t* __restrict__ val) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    key[i] = ~float_to_ord(scores[i]);  // ascending key == descending score
+    val[i] = id_base + i;                // ascending ids: stability gives smaller id first on ties
+  }
+}
+// first k of the sorted order -> outputs (score + query constant), padding beyond n
+__global__ void k_rank_emit(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val, uint32_t n, uint32_t k,
+                            double qc, uint32_t* __restrict__ ids, float* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+    if (i < n) {
+      ids[i] = val[i];
+      out[i] = __double2float_rn((double)ord_to_float(~key[i]) + qc);
+    } else {
+      ids[i] = 0xFFFFFFFFu;
+      out[i] = -INFINITY;
+    }
+  }
+}
+
 // Per query: sorted dense signature (slots of rows with a dense copy) and its hash.
 __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
                             IndexView ix, uint32_t qmax, int32_t* __restrict__ qdense, uint32_t* __restrict__ nden,
@@ -1147,6 +1169,32 @@ int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32
   return SL_OK;
 }
 
+// Full ranking of one score vector (device): the first k by (score desc, id asc).
+struct RankBufs {
+  uint32_t *k0, *v0, *k1, *v1, *k2, *v2;
+  int32_t alloc(Scratch& scr, uint32_t n) {
+    SL_TRY(scr.alloc(&k0, n));
+    SL_TRY(scr.alloc(&v0, n));
+    SL_TRY(scr.alloc(&k1, n));
+    SL_TRY(scr.alloc(&v1, n));
+    SL_TRY(scr.alloc(&k2, n));
+    SL_TRY(scr.alloc(&v2, n));
+    return SL_OK;
+  }
+};
+
+int32_t rank_full(const float* scores, uint32_t n, uint32_t k, uint32_t id_base, double qc, uint32_t* ids,
+                  float* out, cudaStream_t st, const RankBufs& rb) {
+  uint32_t *k0 = rb.k0, *v0 = rb.v0, *k1 = rb.k1, *v1 = rb.v1, *k2 = rb.k2, *v2 = rb.v2;
+  const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256 + 1, 148 * 32);
+  if (n) k_rank_keys<<<g, 256, 0, st>>>(scores, n, id_base, k0, v0);
+  const uint32_t *ks = k0, *vs = v0;
+  if (n) SL_TRY(radix_sort_pairs(k0, v0, n, 32, k1, k2, v1, v2, st, &ks, &vs, 0, nullptr));
+  k_rank_emit<<<(unsigned)std::min<uint64_t>((k + 255) / 256, 148 * 32), 256, 0, st>>>(ks, vs, n, k, qc, ids, out);
+  SL_CUDA_TRY(cudaGetLastError());
+  return SL_OK;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ entry points
@@ -1154,7 +1202,6 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
                       uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats) {
   if (!ix) SL_FAIL(SL_EINVAL, "retrieve_batch: null index");
   if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
-  if (k > kMaxK) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: k > 4096 is not supported by the fused top-k");
   if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "retrieve_batch: bad mem kind");
   const bool dist = ix->comm != nullptr;  // any communicator, 1 rank included
   const bool want_out = !dist || ix->comm->rank == 0;
@@ -1200,6 +1247,58 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   const uint32_t qmax = std::max(1u, h_info[1]);
   const uint32_t n_long = h_info[2];   // queries with > 32 gathered rows -> k_score_long
   const uint32_t B_short = B - n_long;  // they sort after every other query
+  if (k > kMaxK) {
+    // SPEC top_k for large k (up to |C|): dense score vector per query + full stable ranking
+    if (dist) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: k > 4096 is not supported across ranks");
+    uint32_t* ids_dev = out_ids;
+    float* sc_dev = out_scores;
+    if (mem == SL_MEM_HOST) {
+      SL_TRY(scr.alloc(&ids_dev, (uint64_t)B * k));
+      SL_TRY(scr.alloc(&sc_dev, (uint64_t)B * k));
+    }
+    float* vec;
+    double* zero;
+    uint32_t* iota;
+    SL_TRY(scr.alloc(&vec, std::max(1u, ix->N)));
+    SL_TRY(scr.alloc(&zero, B));
+    SL_TRY(scr.alloc(&iota, B));
+    SL_CUDA_TRY(cudaMemsetAsync(zero, 0, (uint64_t)B * 8, st));
+    std::vector<uint32_t> h_iota(B);
+    for (uint32_t i = 0; i < B; ++i) h_iota[i] = i;
+    SL_CUDA_TRY(cudaMemcpyAsync(iota, h_iota.data(), (uint64_t)B * 4, cudaMemcpyHostToDevice, st));
+    std::vector<double> h_qc(B);
+    SL_CUDA_TRY(cudaMemcpyAsync(h_qc.data(), qconst, (uint64_t)B * 8, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    RunArgs ra{};
+    ra.q_off = d_off;
+    ra.q_tok = d_tok;
+    ra.qconst = zero;  // rank by the accumulated score; the constant is added on output
+    ra.perm = iota;
+    ra.k = 1;
+    ra.C = kept_capacity(1);
+    ra.n_splits = std::max(1u, ix->num_tiles);
+    ra.dense_out = vec;
+    const size_t lsm = long_smem_bytes(qmax);
+    if (lsm > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: query too long for the device scorer");
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    RankBufs rbuf;
+    SL_TRY(rbuf.alloc(scr, std::max(1u, ix->N)));
+    SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
+    for (uint32_t b = 0; b < B; ++b) {
+      k_score_long<GM_DENSE><<<ra.n_splits, NT, lsm, st>>>(v, ra, b, 1, qmax);
+      SL_TRY(rank_full(vec, ix->N, k, ix->doc_base, h_qc[b], ids_dev + (uint64_t)b * k, sc_dev + (uint64_t)b * k, st,
+                       rbuf));
+    }
+    SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
+    SL_CUDA_TRY(cudaEventRecord(sc->ev[3], st));
+    if (mem == SL_MEM_HOST) {
+      SL_CUDA_TRY(cudaMemcpyAsync(out_ids, ids_dev, (uint64_t)B * k * 4, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaMemcpyAsync(out_scores, sc_dev, (uint64_t)B * k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return SL_OK;
+  }
   RunPlan plan;
   SL_TRY(plan_runs(ix, B, k, qmax, &plan));
   // group queries by dense signature: sort by signature hash, cut runs of <= R identical ones
@@ -1374,7 +1473,6 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
 int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int32_t device, uint32_t* out_ids,
                    float* out_scores) {
   if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
-  if (k > kMaxK) SL_FAIL(SL_EUNSUPPORTED, "top_k: k > 4096 is not supported");
   if (!out_ids || !out_scores || (!scores && n)) SL_FAIL(SL_EINVAL, "top_k: null argument");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -1395,6 +1493,17 @@ int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int
   if (mem == SL_MEM_HOST) {
     SL_TRY(scr.alloc(&ids_dev, k));
     SL_TRY(scr.alloc(&sc_dev, k));
+  }
+  if (k > kMaxK) {  // full stable ranking
+    RankBufs rbuf;
+    SL_TRY(rbuf.alloc(scr, std::max(1u, n)));
+    SL_TRY(rank_full(d_in, n, k, 0, 0.0, ids_dev, sc_dev, st, rbuf));
+    if (mem == SL_MEM_HOST) {
+      SL_CUDA_TRY(cudaMemcpyAsync(out_ids, ids_dev, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaMemcpyAsync(out_scores, sc_dev, (uint64_t)k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    return SL_OK;
   }
   const uint32_t C = std::max(512u, kept_capacity(k));
   const uint32_t n_tiles = std::max(1u, (n + TILE - 1) / TILE);

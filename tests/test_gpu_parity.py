@@ -296,3 +296,27 @@ def test_long_queries_mixed_batch(cuda_ok, c1, p):
                 np.testing.assert_array_equal(s[gid[b, :k].astype(np.int64)], gsc[b, :k])
         assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(queries[b]),
                           lambda b: query_scale(exp, queries[b]), f"long {p.variant.name} k={k}")
+
+
+def test_large_k_full_ranking(cuda_ok, c1):
+    """k > 4096 (SPEC top_k: up to |C|, 'k >= n returns all documents'): stable full ranking."""
+    cfg, corp, qoff, qtok = c1
+    p = BM25Params(Variant.robertson)
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    sel = [0, 5, 77, 500, 999]
+    qs = [qtok[int(qoff[b]):int(qoff[b + 1])] for b in sel]
+    qo, qt = csr(qs)
+    for k in (5000, cfg.num_docs, cfg.num_docs + 7):
+        rid, rsc = ox.retrieve_batch(qo, qt, k, True, 4)
+        with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+            gid, gsc = retrieve_batch(gi, (qo, qt), k, as_arrays=True)
+            small = retrieve_batch(gi, (qo, qt), 100, as_arrays=True)
+        np.testing.assert_array_equal(gid[:, :100], small[0])  # same ranking as the fused path
+        np.testing.assert_array_equal(gsc[:, :100], small[1])
+        assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(qs[b]),
+                          lambda b: query_scale(exp, qs[b]), f"large k={k}")
+    s = np.random.default_rng(1).integers(0, 50, 20000).astype(np.float32)
+    gi_, gs_ = top_k(s, 20000)
+    ri_, rs_ = oracle.top_k(s.astype(np.float64), 20000)
+    np.testing.assert_array_equal(gi_.astype(np.int64), ri_.astype(np.int64))
