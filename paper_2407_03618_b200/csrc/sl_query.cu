@@ -590,25 +590,31 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
     }
     // (2) dense signature of the run, ascending slot order, all loads in flight
     if (!(ra.debug_skip & 4)) {
-      float4 a[F4L];
+      // register passes of DCH float4 per lane (512 docs), so the tile size does not set the
+      // register footprint
+      constexpr int DCH = F4L < 4 ? F4L : 4;
+#pragma unroll 1
+      for (int c0 = 0; c0 < F4L; c0 += DCH) {
+        float4 a[DCH];
 #pragma unroll
-      for (int rr = 0; rr < F4L; ++rr) a[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane;
-      for (int i = 0; i < nd; ++i) {
-        const float4* row = dbase + (uint64_t)s.dslot[i] * rstride;
-        float4 v[F4L];
+        for (int rr = 0; rr < DCH; ++rr) a[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane + 32 * c0;
+        for (int i = 0; i < nd; ++i) {
+          const float4* row = dbase + (uint64_t)s.dslot[i] * rstride;
+          float4 v[DCH];
 #pragma unroll
-        for (int rr = 0; rr < F4L; ++rr) v[rr] = __ldg(row + 32 * rr);
+          for (int rr = 0; rr < DCH; ++rr) v[rr] = __ldg(row + 32 * rr);
 #pragma unroll
-        for (int rr = 0; rr < F4L; ++rr) {
-          a[rr].x += v[rr].x;
-          a[rr].y += v[rr].y;
-          a[rr].z += v[rr].z;
-          a[rr].w += v[rr].w;
+          for (int rr = 0; rr < DCH; ++rr) {
+            a[rr].x += v[rr].x;
+            a[rr].y += v[rr].y;
+            a[rr].z += v[rr].z;
+            a[rr].w += v[rr].w;
+          }
         }
-      }
 #pragma unroll
-      for (int rr = 0; rr < F4L; ++rr) dsum4[lane + 32 * rr] = a[rr];
+        for (int rr = 0; rr < DCH; ++rr) dsum4[lane + 32 * (c0 + rr)] = a[rr];
+      }
     }
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
