@@ -104,13 +104,13 @@ int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaSt
   if (total_host) SL_CUDA_TRY(cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, st));
   const uint64_t nb = (n + kScanTile - 1) / kScanTile;
   if (nb == 1) {
-    k_scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
+    k_scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr); ++t_launches;
   } else {
     uint32_t* sums = nullptr;
     SL_CUDA_TRY(cudaMallocAsync(&sums, nb * 4, st));
-    k_reduce_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
+    k_reduce_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums); ++t_launches;
     SL_TRY(exclusive_scan_u32(sums, sums, nb, st, nullptr));
-    k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+    k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums); ++t_launches;
     SL_CUDA_TRY(cudaFreeAsync(sums, st));
   }
   SL_CUDA_TRY(cudaGetLastError());
@@ -496,10 +496,10 @@ int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, i
     const int shift = p * width;
     k_radix_hist<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(ki, n, shift, mask, hist, (uint32_t)n_tiles,
                                                              v_check ? v_check : 0xFFFFFFFFu,
-                                                             p == 0 && v_check ? err : nullptr);
+                                                             p == 0 && v_check ? err : nullptr); ++t_launches;
     SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
     k_radix_scatter<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist,
-                                                                (uint32_t)n_tiles);
+                                                                (uint32_t)n_tiles); ++t_launches;
     ki = kb[p & 1];
     vi = vb[p & 1];
   }
@@ -591,13 +591,13 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
     dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
     k_dense_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok, ix->dense_rows, ix->n_pad,
-                                    ix->dense);
+                                    ix->dense); ++t_launches;
   }
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
     dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
     k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
-                                   ix->num_tiles, ix->skiptab);
+                                   ix->num_tiles, ix->skiptab); ++t_launches;
   }
   // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
   // DESIGN.md §8)
@@ -609,19 +609,19 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   SL_TRY(dalloc(ix, &ix->rowmax, V));
   SL_CUDA_TRY(cudaMemsetAsync(ix->rowmax, 0, (uint64_t)V * 4, st));
   if (ix->nnz)
-    k_row_max<<<grid_for(ix->nnz, 256), 256, 0, st>>>(ix->indptr, V, ix->values, ix->nnz, (uint32_t*)ix->rowmax);
+    k_row_max<<<grid_for(ix->nnz, 256), 256, 0, st>>>(ix->indptr, V, ix->values, ix->nnz, (uint32_t*)ix->rowmax); ++t_launches;
   if (ix->dense_rows) {
     SL_TRY(dalloc(ix, &ix->dmax, (uint64_t)ix->dense_rows * ix->num_tiles));
     const uint64_t warps = (uint64_t)ix->dense_rows * ix->num_tiles;
     k_dense_tile_max<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(ix->dense, ix->dense_rows, ix->num_tiles,
-                                                                         ix->n_pad, ix->dmax);
+                                                                         ix->n_pad, ix->dmax); ++t_launches;
   }
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->smax, (uint64_t)ix->skip_rows * ix->num_tiles));
     SL_CUDA_TRY(cudaMemsetAsync(ix->smax, 0, (uint64_t)ix->skip_rows * ix->num_tiles * 4, st));
     dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
     k_skip_tile_max<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok + dense_tok.size(),
-                                       ix->skip_rows, ix->num_tiles, (uint32_t*)ix->smax);
+                                       ix->skip_rows, ix->num_tiles, (uint32_t*)ix->smax); ++t_launches;
   }
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
@@ -672,7 +672,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   uint32_t *docs, *kb0, *kb1, *vb1;
   SL_TRY(tmp.alloc(&docs, T));
   SL_TRY(dalloc(ix, &ix->doclens, N));
-  k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err);
+  k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err); ++t_launches;
 
   // ---- K1: stable LSD radix sort of (token, doc) by token
   int bits = 0;
@@ -680,7 +680,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   const uint32_t* ksorted = tokens;
   const uint32_t* vsorted = docs;
   if (bits == 0) {
-    k_check_tokens<<<grid_for(T, 256), 256, 0, st>>>(tokens, T, V, err);
+    k_check_tokens<<<grid_for(T, 256), 256, 0, st>>>(tokens, T, V, err); ++t_launches;
   } else {
     SL_TRY(tmp.alloc(&kb0, T));
     SL_TRY(tmp.alloc(&kb1, T));
@@ -700,7 +700,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   uint32_t *flags, *pos;
   SL_TRY(tmp.alloc(&flags, T));
   SL_TRY(tmp.alloc(&pos, T));
-  k_rle_flags<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, T, flags);
+  k_rle_flags<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, T, flags); ++t_launches;
   uint32_t nnz32 = 0;
   SL_TRY(exclusive_scan_u32(flags, pos, T, st, &nnz32));
   const uint64_t nnz = nnz32;
@@ -711,7 +711,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(dalloc(ix, &ix->docids, nnz));
   SL_TRY(dalloc(ix, &ix->indptr, (uint64_t)V + 1));
   k_rle_emit<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, pos, T, nnz, V, ix->docids, rows,
-                                               runstart, ix->indptr);
+                                               runstart, ix->indptr); ++t_launches;
   uint32_t* tf;
   if (d->keep_tf) {
     SL_TRY(dalloc(ix, &ix->tf, nnz));
@@ -719,7 +719,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   } else {
     SL_TRY(tmp.alloc(&tf, nnz));
   }
-  k_tf<<<grid_for(nnz, 256), 256, 0, st>>>(runstart, nnz, tf);
+  k_tf<<<grid_for(nnz, 256), 256, 0, st>>>(runstart, nnz, tf); ++t_launches;
   tmp.release(runstart);
   tmp.release(pos);
   if (bits > 0) {
@@ -731,7 +731,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
 
   // ---- K2: df (global via NCCL), N, Σ|D|
   SL_TRY(dalloc(ix, &ix->df_global, V));
-  k_df_from_indptr<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, ix->df_global);
+  k_df_from_indptr<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, ix->df_global); ++t_launches;
   uint64_t stats[2] = {T, N};
   if (d->global_df) {
     // caller-supplied global statistics (virtual shards / external transport)
@@ -761,10 +761,10 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(tmp.alloc(&theta64, V));
   SL_TRY(dalloc(ix, &ix->theta, V));
   k_token_stats<<<grid_for(V, 256), 256, 0, st>>>(ix->df_global, V, ix->N_global, d->params, idf64, theta64,
-                                                 ix->theta);
+                                                 ix->theta); ++t_launches;
   SL_TRY(dalloc(ix, &ix->values, nnz));
   k_values<<<grid_for(nnz, 256), 256, 0, st>>>(rows, ix->docids, tf, ix->doclens, idf64, theta64, nnz,
-                                               d->params, ix->avg_len, ix->values);
+                                               d->params, ix->avg_len, ix->values); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
 
   SL_TRY(build_query_structures(ix, d->dense_min_density, st));
@@ -900,8 +900,8 @@ int32_t load_index_from_host(const HostIndex& h, int device, float dense_min_den
       SL_TRY(tmp.alloc(&err, 1));
       SL_CUDA_TRY(cudaMemsetAsync(start, 0, nnz, st));
       SL_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
-      k_row_starts<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, start);
-      k_check_rows<<<grid_for(nnz, 256), 256, 0, st>>>(ix->docids, start, nnz, N, err);
+      k_row_starts<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, V, start); ++t_launches;
+      k_check_rows<<<grid_for(nnz, 256), 256, 0, st>>>(ix->docids, start, nnz, N, err); ++t_launches;
       uint32_t herr = 0;
       SL_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
       SL_CUDA_TRY(cudaStreamSynchronize(st));

@@ -7,6 +7,7 @@
 #include "sl_synth.h"
 
 namespace sl {
+thread_local uint32_t t_launches = 0;
 namespace {
 thread_local std::string t_error;
 }
@@ -184,7 +185,7 @@ int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed,
   uint64_t blocks = (count + 255) / 256;
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   if (blocks == 0) blocks = 1;
-  k_synth_tokens<<<(unsigned)blocks, 256>>>(dcdf, vocab, seed, begin, count, token_ids_dev);
+  k_synth_tokens<<<(unsigned)blocks, 256>>>(dcdf, vocab, seed, begin, count, token_ids_dev); ++t_launches;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (tmp) cudaFree(tmp);

@@ -40,6 +40,9 @@ struct Status {
     return (code);             \
   } while (0)
 
+// kernels launched by this host thread (bench.py's gpu_launches evidence)
+extern thread_local uint32_t t_launches;
+
 // ---------------------------------------------------------------- constants
 #ifndef SL_TILE_DOCS
 #define SL_TILE_DOCS 512

@@ -1170,7 +1170,7 @@ int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32
   const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4;
   SL_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_merge<<<B, 256, smem, st>>>(cand, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores,
-                                keys);
+                                keys); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
@@ -1193,10 +1193,10 @@ int32_t rank_full(const float* scores, uint32_t n, uint32_t k, uint32_t id_base,
                   float* out, cudaStream_t st, const RankBufs& rb) {
   uint32_t *k0 = rb.k0, *v0 = rb.v0, *k1 = rb.k1, *v1 = rb.v1, *k2 = rb.k2, *v2 = rb.v2;
   const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256 + 1, 148 * 32);
-  if (n) k_rank_keys<<<g, 256, 0, st>>>(scores, n, id_base, k0, v0);
+  if (n) k_rank_keys<<<g, 256, 0, st>>>(scores, n, id_base, k0, v0); ++t_launches;
   const uint32_t *ks = k0, *vs = v0;
   if (n) SL_TRY(radix_sort_pairs(k0, v0, n, 32, k1, k2, v1, v2, st, &ks, &vs, 0, nullptr));
-  k_rank_emit<<<(unsigned)std::min<uint64_t>((k + 255) / 256, 148 * 32), 256, 0, st>>>(ks, vs, n, k, qc, ids, out);
+  k_rank_emit<<<(unsigned)std::min<uint64_t>((k + 255) / 256, 148 * 32), 256, 0, st>>>(ks, vs, n, k, qc, ids, out); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
@@ -1232,6 +1232,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     d_off = o;
     d_tok = t;
   }
+  const uint32_t launches0 = t_launches;
   SL_CUDA_TRY(cudaEventRecord(sc->ev[0], st));
   const IndexView v = ix->view();
   const bool have_bounds = v.rowmax && (!ix->dense_rows || v.dmax) && (!ix->skip_rows || v.smax);
@@ -1243,7 +1244,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_TRY(scr.alloc(&bytes, 1));
   SL_CUDA_TRY(cudaMemsetAsync(info, 0, 16, st));
   SL_CUDA_TRY(cudaMemsetAsync(bytes, 0, 8, st));
-  k_query_prep<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes);
+  k_query_prep<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   uint32_t h_info[4];
   SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
@@ -1291,7 +1292,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     SL_TRY(rbuf.alloc(scr, std::max(1u, ix->N)));
     SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
     for (uint32_t b = 0; b < B; ++b) {
-      k_score_long<GM_DENSE><<<ra.n_splits, NT, lsm, st>>>(v, ra, b, 1, qmax);
+      k_score_long<GM_DENSE><<<ra.n_splits, NT, lsm, st>>>(v, ra, b, 1, qmax); ++t_launches;
       SL_TRY(rank_full(vec, ix->N, k, ix->doc_base, h_qc[b], ids_dev + (uint64_t)b * k, sc_dev + (uint64_t)b * k, st,
                        rbuf));
     }
@@ -1320,10 +1321,10 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_TRY(scr.alloc(&v1, B));
   SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
   SL_TRY(scr.alloc(&n_runs, 1));
-  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv);
+  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv); ++t_launches;
   const uint32_t *sk, *perm;
   SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
-  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, qmax, plan.R, run_begin, n_runs);
+  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, qmax, plan.R, run_begin, n_runs); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;
@@ -1353,15 +1354,15 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   if (ra.prune) {
     SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)plan.smem));
-    k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+    k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra); ++t_launches;
   } else {
-    k_score_runs<GM_TOPK, false><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra);
+    k_score_runs<GM_TOPK, false><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra); ++t_launches;
   }
   if (n_long) {
     const size_t lsm = long_smem_bytes(qmax);
     if (lsm > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: query too long for the device scorer");
     SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_TOPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-    k_score_long<GM_TOPK><<<n_long * plan.n_splits, NT, lsm, st>>>(v, ra, B_short, n_long, qmax);
+    k_score_long<GM_TOPK><<<n_long * plan.n_splits, NT, lsm, st>>>(v, ra, B_short, n_long, qmax); ++t_launches;
   }
   SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
@@ -1418,7 +1419,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
     stats->posting_bytes = hb;
     stats->scorevec_bytes = 4ull * ix->N * B;
     stats->unique_posting_bytes = 0;
-    stats->kernels_launched = (dist ? (ix->comm->rank == 0 ? 4 : 3) : 3) + (n_long ? 1 : 0);
+    stats->kernels_launched = t_launches - launches0;  // every kernel of this call
   }
   return SL_OK;
 }
@@ -1446,7 +1447,7 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
   SL_TRY(scr.alloc(&qconst, 1));
   SL_TRY(scr.alloc(&info, 4));
   SL_CUDA_TRY(cudaMemsetAsync(info, 0, 16, st));
-  k_query_prep<<<1, 32, 0, st>>>(d_off, d_tok, 1, v, qconst, info, nullptr);
+  k_query_prep<<<1, 32, 0, st>>>(d_off, d_tok, 1, v, qconst, info, nullptr); ++t_launches;
   uint32_t h_info[4];
   SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1468,7 +1469,7 @@ int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t 
   const size_t smem = long_smem_bytes(qcap);
   if (smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "score_query: query too long for the device scorer");
   SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_score_long<GM_DENSE><<<ra.n_splits, NT, smem, st>>>(v, ra, 0, 1, qcap);
+  k_score_long<GM_DENSE><<<ra.n_splits, NT, smem, st>>>(v, ra, 0, 1, qcap); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   if (mem == SL_MEM_HOST)
     SL_CUDA_TRY(cudaMemcpyAsync(out, d_out, (uint64_t)ix->N * 4, cudaMemcpyDeviceToHost, st));
@@ -1519,7 +1520,7 @@ int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int
   if (n) {
     const size_t smem = (size_t)TILE * 4 + 2 * (size_t)C * 8 + 256 * 4 + 40 * 4;
     SL_CUDA_TRY(cudaFuncSetAttribute(k_topk_vector, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_topk_vector<<<n_splits, NT, smem, st>>>(d_in, n, k, C, n_splits, cand);
+    k_topk_vector<<<n_splits, NT, smem, st>>>(d_in, n, k, C, n_splits, cand); ++t_launches;
     SL_CUDA_TRY(cudaGetLastError());
   } else {
     SL_CUDA_TRY(cudaMemsetAsync(cand, 0, (uint64_t)C * 8, st));
