@@ -334,6 +334,10 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
 }
 
 // Running top-k of query r over one tile (warp-level) from buf[TILE].
+// tau is kept EXACT (the k-th best key so far, or 0 before k keys exist). Tiles are visited
+// in increasing doc order and a key carries ~doc, so a later doc whose score EQUALS tau's
+// score can never beat tau: the float pre-test is strict (x > tau_f), which rejects the
+// large tie classes (head-token-only / OOV queries) without building keys.
 __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
                                             uint32_t nvalid, const float* buf, uint64_t* kept) {
   const int lane = threadIdx.x & 31;
@@ -353,7 +357,7 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
         if (dl + c < nvalid) mx = fmaxf(mx, f4c(v, c));
     }
   }
-  if (!__any_sync(0xffffffffu, mx >= tf)) return;
+  if (!__any_sync(0xffffffffu, mx > tf || tau == 0)) return;
   auto tile_visit = [&](uint64_t thr, auto&& fn) {
 #pragma unroll
     for (int rr = 0; rr < F4L; ++rr) {
@@ -362,7 +366,7 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float x = f4c(v, c);
-        if (x >= tf && dl + c < nvalid) {
+        if ((x > tf || tau == 0) && dl + c < nvalid) {
           const uint64_t key = make_key(x, gdoc0 + dl + c);
           if (key >= thr) fn(key);
         }
@@ -405,9 +409,14 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
     uint64_t* dst = kept + out + inc2 - m2;
     tile_visit(nt, [&](uint64_t key) { *dst++ = key; });
     __syncwarp();
+    // exact k-th key = min of the k survivors
+    uint64_t mn = ~0ull;
+    for (uint32_t i = lane; i < out + tot2; i += 32) mn = min(mn, kept[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if (lane == 0) {
       s.n_kept[r] = out + tot2;
-      s.tau[r] = nt;
+      s.tau[r] = mn;
     }
   }
   __syncwarp();
