@@ -35,6 +35,9 @@ namespace sl {
 namespace {
 
 constexpr int NT = 256;
+#ifndef SL_MINB
+#define SL_MINB 4  // resident CTAs per SM the scoring kernel is register-budgeted for
+#endif
 constexpr int NW = NT / 32;
 constexpr int TILE = kTileDocs;      // 512
 constexpr int F4L = TILE / 4 / 32;   // float4 per lane when a warp scans one tile
@@ -257,6 +260,26 @@ struct WSmem {
   float* rmax;          // [E] row maximum max(0, S^Δ) (block-max bound of short rows)
 };
 
+// Static per-warp shared layout of k_score_runs: compile-time offsets, so every access is an
+// LDS/STS with an immediate offset (no generic-pointer rematerialisation). Bounds: <= 32
+// gathered rows and <= NDMAX dense rows per run (other queries take k_score_long).
+constexpr int WPC = 8;      // warps per CTA
+constexpr int NDMAX = 64;   // dense rows per query in the warp kernel
+struct __align__(16) WarpSmem {
+  float dsum[TILE];           // dense-signature sum of the current tile
+  float acc[TILE];            // working accumulator (runs with > 1 query)
+  uint64_t row_start[32];     // gathered-row entries (lane = entry)
+  uint64_t tau[RMAX];         // exact running threshold key per query
+  uint32_t row_len[32];
+  int32_t skip[32];
+  float rmax[32];             // row maxima (block-max pruning)
+  int32_t dslot[NDMAX];       // the run's dense signature, ascending slots
+  uint32_t hist[16];          // warp_select_kth histogram
+  uint32_t n_kept[RMAX];
+  int32_t ebeg[RMAX + 1];     // query r owns entries [ebeg[r], ebeg[r+1])
+  int32_t nd[1];
+};
+
 // C = candidates held in shared memory per query (0 when they live in global memory)
 __host__ __device__ inline size_t warp_smem_bytes(uint32_t R, uint32_t C, uint32_t qmax) {
   const size_t E = (size_t)R * qmax;
@@ -338,7 +361,9 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
 // in increasing doc order and a key carries ~doc, so a later doc whose score EQUALS tau's
 // score can never beat tau: the float pre-test is strict (x > tau_f), which rejects the
 // large tie classes (head-token-only / OOV queries) without building keys.
-__device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
+// FULL: all TILE docs of the tile exist (every tile but the last): no per-doc bound checks.
+template <bool FULL, class SM>
+__device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
                                             uint32_t nvalid, const float* buf, uint64_t* kept) {
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
@@ -349,7 +374,7 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
   for (int rr = 0; rr < F4L; ++rr) {
     const float4 v = b4[lane + 32 * rr];
     const uint32_t dl = 4 * (lane + 32 * rr);
-    if (dl + 3 < nvalid) {
+    if (FULL || dl + 3 < nvalid) {
       mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     } else {
 #pragma unroll
@@ -366,7 +391,7 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float x = f4c(v, c);
-        if ((x > tf || tau == 0) && dl + c < nvalid) {
+        if ((x > tf || tau == 0) && (FULL || dl + c < nvalid)) {
           const uint64_t key = make_key(x, gdoc0 + dl + c);
           if (key >= thr) fn(key);
         }
@@ -426,14 +451,13 @@ __device__ __forceinline__ void filter_tile(const WSmem& s, uint32_t r, uint32_t
 // Lane e owns gathered-row entry e of the run (the runs' queries' CSC tokens concatenated
 // in query order; at most 32). No CTA-level synchronisation: warps progress independently.
 template <int MODE, bool PRUNE>
-__global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArgs ra) {
+  __shared__ WarpSmem wsm[WPC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((uint32_t)warp >= ra.wpc) return;
   const uint32_t n_runs = *ra.n_runs;
-  const uint64_t item = (uint64_t)blockIdx.x * ra.wpc + warp;
+  const uint64_t item = (uint64_t)blockIdx.x * WPC + warp;
   if (item >= (uint64_t)n_runs * ra.n_splits) return;
-  const WSmem s = wcarve(smem_raw + (size_t)warp * ra.warp_bytes, ra.R, ra.kept_global ? 0u : ra.C, ra.qmax);
+  WarpSmem& s = wsm[warp];
   // split-major order: concurrently resident warps sweep the same doc region, so each CSC
   // slice / dense chunk is fetched from HBM once and served from L2 to every query using it
   const bool smaj = ra.split_major != 0;
@@ -467,7 +491,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
       if (rb == re) continue;                           // no local postings
       const int32_t info = ix.tokinfo[t];
       if (info >= 0) {
-        if (lane == 0) s.dslot[nd] = info;  // identical multiset for every query of the run
+        if (lane == 0 && nd < NDMAX) s.dslot[nd] = info;  // identical multiset for every query of the run
         ++nd;
       } else if (e < 32) {
 #ifdef SL_DEBUG_CHECKS
@@ -646,10 +670,13 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        uint64_t* kept = ra.kept_global
-                             ? ra.cand + ((uint64_t)ra.perm[pb + r] * ra.n_splits + split) * ra.C
-                             : s.kept + (size_t)r * ra.C;
-        if (!(ra.debug_skip & 2)) filter_tile(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
+        uint64_t* kept = ra.cand + ((uint64_t)ra.perm[pb + r] * ra.n_splits + split) * ra.C;
+        if (!(ra.debug_skip & 2)) {
+          if (nvalid == TILE)
+            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
+          else
+            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
+        }
       }
     }
     __syncwarp();
@@ -659,12 +686,7 @@ __global__ void __launch_bounds__(NT, 4) k_score_runs(IndexView ix, RunArgs ra) 
       const uint32_t q = ra.perm[pb + r];
       const uint32_t nk = s.n_kept[r];
       uint64_t* out = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
-      if (ra.kept_global) {  // candidates are already in place: pad the tail
-        for (uint32_t i = nk + lane; i < ra.C; i += 32) out[i] = kInvalidKey;
-      } else {
-        const uint64_t* kept = s.kept + (size_t)r * ra.C;
-        for (uint32_t i = lane; i < ra.C; i += 32) out[i] = i < nk ? kept[i] : kInvalidKey;
-      }
+      for (uint32_t i = nk + lane; i < ra.C; i += 32) out[i] = kInvalidKey;  // candidates are in place
     }
   }
 }
@@ -803,7 +825,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
       const double qc = ra.qconst[q];
       for (uint32_t i = threadIdx.x; i < nvalid; i += NT) ra.dense_out[d0 + i] = __double2float_rn((double)acc[i] + qc);
     } else {
-      if (warp == 0) filter_tile(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept);
+      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept);
     }
     __syncthreads();
   }
@@ -866,7 +888,7 @@ __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* 
     for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
     nden[q] = n;
     // > 32 gathered rows: sorts after every short query (key 0xFFFFFFFF) -> k_score_long
-    hkey[q] = ng > 32 ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
+    hkey[q] = (ng > 32 || n > (uint32_t)NDMAX) ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
     hval[q] = q;
   }
 }
@@ -1066,7 +1088,7 @@ __global__ void k_query_prep(const uint64_t* __restrict__ q_off, const uint32_t*
     atomicMax(&info[1], (uint32_t)min(e - b, (uint64_t)0xFFFFFFFFu));
     double c = 0.0;
     unsigned long long pb = 0;
-    uint32_t ng = 0;
+    uint32_t ng = 0, ndn = 0;
     for (uint64_t j = b; j < e; ++j) {
       const uint32_t t = q_tok[j];
       if (t >= ix.V) {
@@ -1076,9 +1098,9 @@ __global__ void k_query_prep(const uint64_t* __restrict__ q_off, const uint32_t*
       if (ix.df_global[t] == 0) continue;
       c += (double)ix.theta[t];
       pb += 8ull * (ix.indptr[t + 1] - ix.indptr[t]);
-      if (ix.indptr[t + 1] != ix.indptr[t] && ix.tokinfo && ix.tokinfo[t] < 0) ++ng;
+      if (ix.indptr[t + 1] != ix.indptr[t] && ix.tokinfo) ix.tokinfo[t] < 0 ? ++ng : ++ndn;
     }
-    if (ng > 32) atomicAdd(&info[2], 1u);
+    if (ng > 32 || ndn > NDMAX) atomicAdd(&info[2], 1u);
     qconst[q] = c;
     if (bytes && pb) atomicAdd(bytes, pb);
   }
@@ -1152,19 +1174,16 @@ struct RunPlan {
 // override the plan in tuning runs.
 int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
   p->C = kept_capacity(k);
-  p->kept_global = p->C > (uint32_t)env_int("SL_KEPT_SMEM_MAX", 0);  // large k: candidates in their global output slot (L2)
+  p->kept_global = 1;  // running candidates live in their global output slot (L2-resident)
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
   if (R == 0) R = RMAX;
   R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
-  p->R = std::max(1u, std::min<uint32_t>(R, 32));
-  p->warp_bytes = (uint32_t)warp_smem_bytes(p->R, p->kept_global ? 0u : p->C, qmax);
-  const size_t budget = (size_t)env_int("SL_SMEM_BUDGET", 72 * 1024);
-  p->wpc = (uint32_t)std::max<size_t>(1, std::min<size_t>(NW, budget / p->warp_bytes));
-  p->smem = (size_t)p->wpc * p->warp_bytes;
-  if (p->smem > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "top-k / query length too large for shared memory");
+  p->R = std::max(1u, std::min<uint32_t>(R, RMAX));
+  p->warp_bytes = (uint32_t)sizeof(WarpSmem);
+  p->wpc = WPC;
+  p->smem = 0;  // static layout (WarpSmem)
   int per_sm = 0;
-  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem));
-  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, p->smem));
+  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, 0));
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
   uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
@@ -1361,8 +1380,6 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
   SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
   if (ra.prune) {
-    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)plan.smem));
     k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra); ++t_launches;
   } else {
     k_score_runs<GM_TOPK, false><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra); ++t_launches;
