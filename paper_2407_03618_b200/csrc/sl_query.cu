@@ -223,6 +223,7 @@ struct RunArgs {
   const uint32_t* perm;       // sorted position -> original query id
   const uint32_t* run_begin;  // [n_runs+1] positions in perm
   const uint32_t* n_runs;     // device scalar
+  uint32_t* work;             // device scalar: next work item (zeroed by k_build_runs)
   uint32_t k;
   uint32_t C;                 // candidates kept per (query, split)
   uint32_t R;                 // max queries per run
@@ -450,14 +451,20 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
 // One warp per (run, doc split): a run is <= R queries with the same dense signature.
 // Lane e owns gathered-row entry e of the run (the runs' queries' CSC tokens concatenated
 // in query order; at most 32). No CTA-level synchronisation: warps progress independently.
+// Persistent: the grid fills the GPU once and every warp pulls (run, split) items from a
+// global counter in increasing order, so warps that finish short runs early stay busy.
 template <int MODE, bool PRUNE>
 __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArgs ra) {
   __shared__ WarpSmem wsm[WPC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n_runs = *ra.n_runs;
-  const uint64_t item = (uint64_t)blockIdx.x * WPC + warp;
-  if (item >= (uint64_t)n_runs * ra.n_splits) return;
+  const uint32_t total = n_runs * ra.n_splits;
   WarpSmem& s = wsm[warp];
+  for (;;) {
+  uint32_t it = 0;
+  if (lane == 0) it = atomicAdd(ra.work, 1u);
+  const uint32_t item = __shfl_sync(0xffffffffu, it, 0);
+  if (item >= total) break;
   // split-major order: concurrently resident warps sweep the same doc region, so each CSC
   // slice / dense chunk is fetched from HBM once and served from L2 to every query using it
   const bool smaj = ra.split_major != 0;
@@ -689,6 +696,8 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       for (uint32_t i = nk + lane; i < ra.C; i += 32) out[i] = kInvalidKey;  // candidates are in place
     }
   }
+  __syncwarp();
+  }  // work items
 }
 
 // Queries with more than 32 gathered rows (one lane per row does not fit): one CTA per
@@ -954,7 +963,8 @@ __global__ void __launch_bounds__(1024) k_build_runs(const uint32_t* __restrict_
   }
   if (threadIdx.x == 0) {
     run_begin[carry_count] = B;
-    *n_runs = carry_count;
+    n_runs[0] = carry_count;
+    n_runs[1] = 0;  // work-item counter of k_score_runs
   }
 }
 
@@ -1165,7 +1175,7 @@ int env_int(const char* name, int dflt) {
 }
 
 struct RunPlan {
-  uint32_t R, C, wpc, n_splits, warp_bytes, kept_global;
+  uint32_t R, C, wpc, n_splits, warp_bytes, kept_global, per_sm;
   size_t smem;
 };
 
@@ -1184,6 +1194,7 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   p->smem = 0;  // static layout (WarpSmem)
   int per_sm = 0;
   SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, 0));
+  p->per_sm = (uint32_t)std::max(1, per_sm);
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
   uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
@@ -1348,7 +1359,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_TRY(scr.alloc(&v0, B));
   SL_TRY(scr.alloc(&v1, B));
   SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
-  SL_TRY(scr.alloc(&n_runs, 1));
+  SL_TRY(scr.alloc(&n_runs, 2));
   k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv); ++t_launches;
   const uint32_t *sk, *perm;
   SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
@@ -1361,6 +1372,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.perm = perm;
   ra.run_begin = run_begin;
   ra.n_runs = n_runs;
+  ra.work = n_runs + 1;
   ra.k = k;
   ra.C = plan.C;
   ra.R = plan.R;
@@ -1375,9 +1387,11 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
-  // upper bound on runs is B; warps past the real run count exit at once
-  const uint64_t grid = std::max<uint64_t>(1, ((uint64_t)B_short * plan.n_splits + plan.wpc - 1) / plan.wpc);
-  if (grid > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
+  // persistent grid: resident CTAs only (never more warps than the upper bound of B items)
+  const uint64_t items_ub = (uint64_t)B_short * plan.n_splits;
+  if (items_ub > 0xFFFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
+  const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((items_ub + plan.wpc - 1) / plan.wpc,
+                                                                 (uint64_t)plan.per_sm * num_sms(ix->device)));
   SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
   if (ra.prune) {
     k_score_runs<GM_TOPK, true><<<(unsigned)grid, plan.wpc * 32, plan.smem, st>>>(v, ra); ++t_launches;

@@ -7,6 +7,6 @@ CASES=${AB_CASES:-"2:10 2:100 4:1000"}
 for L in "${@:-main}"; do
   if [ "$L" = main ]; then unset SPARSELEX_LIB; else export SPARSELEX_LIB=$PWD/paper_2407_03618_b200/csrc/build/$L/libsparselex_b200.so; fi
   for c in $CASES; do
-    echo "$L c${c%%:*} k${c##*:} $(python tools/tune.py --config ${c%%:*} --k ${c##*:} ${AB_ARGS:-} 2>&1 | tail -1)"
+    echo "$L c${c%%:*} k${c##*:} $(python tools/tune.py --config ${c%%:*} --k ${c##*:} ${AB_ARGS:-} 2>&1 | grep "\"env\"" | tr "\n" " ")"
   done
 done
