@@ -199,6 +199,53 @@ void sl_comm_destroy(sl_comm* comm);
 int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed, uint64_t begin,
                                uint64_t count, int32_t cdf_mem, uint32_t* token_ids_dev);
 
+/* ---- Text pipeline (SPEC.md [MODULE] tokenizer) ---------------
+ *   sl_tokenize(build=1)  <- tokenize_build(text, TokenizerConfig, Vocabulary&) per document
+ *                            proj/include/sparselex/tokenizer.hpp:36-39 (split -> lowercase ->
+ *                            stopword filter -> stem -> id; unseen tokens get the next ids in
+ *                            first-encounter order, vocabulary.hpp:26-33)
+ *   sl_tokenize(build=0)  <- tokenize_query(text, TokenizerConfig, const Vocabulary&)
+ *                            tokenizer.hpp:41-45 (out-of-vocabulary tokens dropped)
+ *   sl_stem_batch         <- stem_english(word) stemmer.hpp:16-18, one call per word
+ *   sl_vocab_*            <- Vocabulary (vocabulary.hpp:13-48): size, tokens in id order
+ * Documents are byte ranges [doc_offsets[d], doc_offsets[d+1]) of `text` (doc_offsets[0]
+ * must be 0), each tokenized on its own as the reference tokenizes one string. The output
+ * batch is device-resident: its offsets/ids feed sl_index_build / sl_retrieve_batch with
+ * mem = SL_MEM_DEVICE directly. Stopwords: newline-separated tokens, '#' lines ignored
+ * (stopwords.hpp:13-15), compared with the lowercased pre-stem token. */
+typedef enum { SL_STEMMER_NONE = 0, SL_STEMMER_SNOWBALL_ENGLISH = 1 } sl_stemmer;
+
+typedef struct {
+  int32_t lowercase;         /* TokenizerConfig.lowercase (tokenizer.hpp:17) */
+  int32_t stemmer;           /* sl_stemmer (stemmer.hpp:8-11) */
+  const char* stopwords;     /* NULL or newline-separated list (host memory) */
+  uint64_t stopwords_bytes;
+} sl_tokenizer_config;
+
+typedef struct sl_vocab sl_vocab;
+typedef struct sl_token_batch sl_token_batch;
+
+int32_t sl_vocab_create(int32_t device, sl_vocab** out);
+int32_t sl_vocab_destroy(sl_vocab* vocab);
+int32_t sl_vocab_size(const sl_vocab* vocab, uint32_t* size);
+/* tokens in id order: offsets[size+1] (NULL to skip), bytes (NULL to skip), total byte count */
+int32_t sl_vocab_export(const sl_vocab* vocab, uint64_t* offsets, char* bytes, uint64_t* total_bytes);
+/* fills an EMPTY vocabulary with n tokens in id order (load_index) */
+int32_t sl_vocab_import(sl_vocab* vocab, const uint64_t* offsets, const char* bytes, uint32_t n);
+
+int32_t sl_tokenize(sl_vocab* vocab, const sl_tokenizer_config* config, int32_t build, const char* text,
+                    const uint64_t* doc_offsets, uint32_t num_docs, int32_t mem, sl_token_batch** out);
+/* device pointers stay owned by the batch */
+int32_t sl_token_batch_info(const sl_token_batch* batch, uint32_t* num_docs, uint64_t* num_tokens,
+                            const uint64_t** d_offsets, const uint32_t** d_ids);
+int32_t sl_token_batch_copy(const sl_token_batch* batch, uint64_t* host_offsets, uint32_t* host_ids);
+int32_t sl_token_batch_destroy(sl_token_batch* batch);
+
+/* stem_english for n words (host buffers): out has the input's byte size, word i's stem is
+ * out[offsets[i] .. offsets[i] + out_len[i]) */
+int32_t sl_stem_batch(const char* words, const uint64_t* offsets, uint32_t n, int32_t device, char* out,
+                      uint32_t* out_len);
+
 #ifdef __cplusplus
 }
 #endif

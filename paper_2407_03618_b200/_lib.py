@@ -71,6 +71,11 @@ class RetrieveStats(C.Structure):
     ]
 
 
+class TokenizerConfig(C.Structure):
+    _fields_ = [("lowercase", C.c_int32), ("stemmer", C.c_int32), ("stopwords", C.c_char_p),
+                ("stopwords_bytes", C.c_uint64)]
+
+
 SIGNATURES = {
     "sl_abi_version": (_i32, []),
     "sl_last_error": (C.c_char_p, []),
@@ -91,6 +96,16 @@ SIGNATURES = {
     "sl_comm_init": (_i32, [_u8p, _i32, _i32, _i32, C.POINTER(C.c_void_p)]),
     "sl_comm_destroy": (None, [_vp]),
     "sl_synth_tokens_device": (_i32, [_vp, _u32, _u32, _u64, _u64, _i32, _vp]),
+    "sl_vocab_create": (_i32, [_i32, C.POINTER(C.c_void_p)]),
+    "sl_vocab_destroy": (_i32, [_vp]),
+    "sl_vocab_size": (_i32, [_vp, C.POINTER(_u32)]),
+    "sl_vocab_export": (_i32, [_vp, _vp, _vp, C.POINTER(_u64)]),
+    "sl_vocab_import": (_i32, [_vp, _vp, _vp, _u32]),
+    "sl_tokenize": (_i32, [_vp, C.POINTER(TokenizerConfig), _i32, _vp, _vp, _u32, _i32, C.POINTER(C.c_void_p)]),
+    "sl_token_batch_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp)]),
+    "sl_token_batch_copy": (_i32, [_vp, _vp, _vp]),
+    "sl_token_batch_destroy": (_i32, [_vp]),
+    "sl_stem_batch": (_i32, [_vp, _vp, _u32, _i32, _vp, _vp]),
 }
 
 _lib = None

@@ -1,0 +1,1392 @@
+// sl_text.cu — the text side of the path on the device:
+// UTF-8 split -> lowercase -> stopword filter -> Snowball English stem -> vocabulary ids.
+//
+// Reference semantics (paths relative to /root/reference):
+//   split_text / for_each_token   proj/src/tokenizer.cpp:52-113  maximal runs of >= 2 word
+//                                 codepoints; malformed UTF-8 byte -> U+FFFD (a separator)
+//                                 consuming one byte; a sequence never crosses its document
+//   word class / lowercase        proj/src/tokenizer.cpp:12-33  (tables: sl_unicode.inc)
+//   run_pipeline                  proj/src/tokenizer.cpp:115-129 stopwords compared on the
+//                                 lowercased, pre-stem token; stem; id
+//   stem_english                  proj/src/stemmer.cpp:29-411    (the reference's variant)
+//   Vocabulary                    proj/include/sparselex/vocabulary.hpp:13-48 ids in first-
+//                                 encounter order (document order, then position)
+//
+// Device design (byte-parallel, HBM-streaming):
+//   k_doc_marks     bitmap of document start bytes
+//   k_classify      one thread per byte: decode start / covering sequence (looks at <= 3
+//                   bytes either side), word class -> two bitmaps (word byte, word
+//                   codepoint start) written by warp ballots (1/4 of the text in bytes)
+//   k_tok_count/emit one thread per 32-byte bitmap word: token begins = word bytes whose
+//                   predecessor is not a word byte (or a document start); end and codepoint
+//                   count by bit scans; tokens of >= 2 codepoints kept, in byte order
+//   k_norm          one thread per token: lowercase, stopword probe, stem (on a one-byte-
+//                   per-codepoint shadow of the word: ASCII as itself, others as 0x80, so the
+//                   rules see exactly what the reference's codepoint loop sees), two 64-bit
+//                   hashes, vocabulary probe; normalised bytes to an arena (2x text)
+//   build mode      new tokens sorted by hash (the build's radix sort), grouped, groups
+//                   ordered by first occurrence -> ids appended to the vocabulary in the
+//                   reference's first-encounter order; open-addressing device hash table
+//   query mode      tokens absent from the frozen vocabulary are dropped (SPEC OOV rule)
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sl_index.cuh"
+
+#define SL_UNI_QUAL __device__
+namespace sl {
+namespace uni {
+#include "sl_unicode.inc"
+}
+}  // namespace sl
+
+struct sl_vocab {
+  int device = 0;
+  uint32_t V = 0;
+  uint32_t vcap = 0;         // capacity of offs (vcap + 1) / h2 / lens
+  uint64_t* offs = nullptr;  // [V+1] byte offsets into bytes
+  uint64_t* h2 = nullptr;    // [V] second hash (identity check)
+  uint8_t* bytes = nullptr;
+  uint64_t bcap = 0;
+  uint64_t bused = 0;
+  uint64_t* tkey = nullptr;  // [tcap] first hash (0 = empty)
+  uint32_t* tval = nullptr;  // [tcap] id
+  uint32_t tcap = 0;         // power of two
+};
+
+struct sl_token_batch {
+  int device = 0;
+  uint32_t N = 0;
+  uint64_t T = 0;
+  uint64_t* offs = nullptr;  // [N+1] token offsets per document
+  uint32_t* ids = nullptr;   // [T]
+};
+
+namespace sl {
+namespace {
+
+constexpr uint32_t kNew = 0xFFFFFFFFu;
+constexpr int kFastBytes = 64;  // tokens up to this many raw bytes normalise in registers/local memory
+
+// ------------------------------------------------------------------ unicode
+__device__ __forceinline__ bool is_word_cp(uint32_t c) {
+  if (c < 0x80) return (c >= '0' && c <= '9') || (c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z') || c == '_';
+  int lo = 0, hi = uni::kSlWordRangeCount;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (uni::kSlWordRanges[2 * mid] <= c) lo = mid + 1; else hi = mid;
+  }
+  return lo > 0 && c <= uni::kSlWordRanges[2 * (lo - 1) + 1];
+}
+
+__device__ __forceinline__ uint32_t lower_cp(uint32_t c) {
+  if (c < 0x80) return (c >= 'A' && c <= 'Z') ? c + 32 : c;
+  int lo = 0, hi = uni::kSlLowerCount;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (uni::kSlLowerFrom[mid] < c) lo = mid + 1; else hi = mid;
+  }
+  return (lo < uni::kSlLowerCount && uni::kSlLowerFrom[lo] == c) ? uni::kSlLowerTo[lo] : c;
+}
+
+__device__ __forceinline__ int put_utf8(uint8_t* o, uint32_t c) {
+  if (c < 0x80) {
+    o[0] = (uint8_t)c;
+    return 1;
+  }
+  if (c < 0x800) {
+    o[0] = (uint8_t)(0xC0 | (c >> 6));
+    o[1] = (uint8_t)(0x80 | (c & 0x3F));
+    return 2;
+  }
+  if (c < 0x10000) {
+    o[0] = (uint8_t)(0xE0 | (c >> 12));
+    o[1] = (uint8_t)(0x80 | ((c >> 6) & 0x3F));
+    o[2] = (uint8_t)(0x80 | (c & 0x3F));
+    return 3;
+  }
+  o[0] = (uint8_t)(0xF0 | (c >> 18));
+  o[1] = (uint8_t)(0x80 | ((c >> 12) & 0x3F));
+  o[2] = (uint8_t)(0x80 | ((c >> 6) & 0x3F));
+  o[3] = (uint8_t)(0x80 | (c & 0x3F));
+  return 4;
+}
+
+__device__ __forceinline__ int lead_len(uint32_t b) {
+  return (b >= 0xC0 && b <= 0xDF) ? 2 : (b >= 0xE0 && b <= 0xEF) ? 3 : (b >= 0xF0 && b <= 0xF7) ? 4 : 0;
+}
+
+// decode one codepoint of a known-good (or leniently accepted) sequence at p; returns length
+__device__ __forceinline__ int decode_at(const uint8_t* s, uint32_t* cp) {
+  const uint32_t b = s[0];
+  if (b < 0x80) {
+    *cp = b;
+    return 1;
+  }
+  const int L = lead_len(b);
+  uint32_t c = b & (L == 2 ? 0x1F : L == 3 ? 0x0F : 0x07);
+  for (int i = 1; i < L; ++i) c = (c << 6) | (s[i] & 0x3F);
+  *cp = c;
+  return L;
+}
+
+// ------------------------------------------------------------------ hashing
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+__host__ __device__ inline uint64_t fnv1a64(const uint8_t* s, uint32_t n) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (uint32_t i = 0; i < n; ++i) h = (h ^ s[i]) * 0x100000001b3ull;
+  return h;
+}
+struct H2 {
+  uint64_t a, b;
+};
+// two independent 64-bit hashes of one byte string; a is never 0 (0 = empty table slot)
+__device__ __forceinline__ H2 hash2(const uint8_t* s, uint32_t n) {
+  uint64_t a = 0xcbf29ce484222325ull, b = 0x9e3779b97f4a7c15ull ^ n;
+  for (uint32_t i = 0; i < n; ++i) {
+    a = (a ^ s[i]) * 0x100000001b3ull;
+    b = (b + s[i] + 1) * 0xd6e8feb86659fd93ull;
+    b ^= b >> 29;
+  }
+  a = fmix64(a ^ n);
+  b = fmix64(b);
+  return H2{a ? a : 1ull, b};
+}
+
+// ------------------------------------------------------------------ segmentation
+struct TextView {
+  const uint8_t* text;
+  uint64_t n;
+  const uint32_t* dstart;  // bitmap: document start bytes
+};
+
+__device__ __forceinline__ uint32_t byte_at(const TextView& t, int64_t p) {
+  return (p >= 0 && (uint64_t)p < t.n) ? (uint32_t)__ldg(t.text + p) : 0u;
+}
+__device__ __forceinline__ bool dstart_at(const TextView& t, uint64_t p) {
+  return p < t.n && ((__ldg(t.dstart + (p >> 5)) >> (p & 31)) & 1u);
+}
+
+// a valid UTF-8 sequence (tokenizer.cpp:52-94 rules) starts at q and stays in its document
+__device__ bool valid_at(const TextView& t, uint64_t q, uint32_t* cp, int* len) {
+  const uint32_t b = byte_at(t, (int64_t)q);
+  const int L = lead_len(b);
+  if (!L || q + L > t.n) return false;
+  uint32_t c = b & (L == 2 ? 0x1F : L == 3 ? 0x0F : 0x07);
+  for (int i = 1; i < L; ++i) {
+    if (dstart_at(t, q + i)) return false;
+    const uint32_t x = byte_at(t, (int64_t)(q + i));
+    if ((x & 0xC0) != 0x80) return false;
+    c = (c << 6) | (x & 0x3F);
+  }
+  const uint32_t lo = L == 2 ? 0x80u : L == 3 ? 0x800u : 0x10000u;
+  if (c < lo || c > 0x10FFFF || (c >= 0xD800 && c <= 0xDFFF)) return false;
+  *cp = c;
+  *len = L;
+  return true;
+}
+
+__global__ void k_doc_marks(const uint64_t* __restrict__ off, uint32_t N, uint64_t n, uint32_t* __restrict__ bits) {
+  for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d < N; d += gridDim.x * blockDim.x) {
+    const uint64_t b = off[d];
+    if (b < off[d + 1] && b < n) atomicOr(bits + (b >> 5), 1u << (b & 31));
+  }
+}
+
+// per byte: word-byte bit and word-codepoint-start bit
+__global__ void k_classify(TextView t, uint32_t* __restrict__ wbits, uint32_t* __restrict__ sbits) {
+  const uint64_t nw = (t.n + 31) >> 5;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t b = (w << 5) + (threadIdx.x & 31);
+    bool word = false, start = false;
+    if (b < t.n) {
+      const uint32_t x = byte_at(t, (int64_t)b);
+      uint32_t cp = 0;
+      int L = 0;
+      bool covered = false;
+      if ((x & 0xC0) == 0x80) {  // continuation byte: inside the nearest preceding valid sequence?
+        for (int back = 1; back <= 3 && (int64_t)b - back >= 0; ++back) {
+          const uint64_t q = b - back;
+          if (dstart_at(t, q + 1)) break;  // q is in an earlier document
+          const uint32_t y = byte_at(t, (int64_t)q);
+          if ((y & 0xC0) == 0x80) continue;
+          if (valid_at(t, q, &cp, &L) && q + L > b) covered = true;
+          break;
+        }
+      }
+      if (!covered) {
+        start = true;
+        if (x < 0x80) cp = x;
+        else if (!valid_at(t, b, &cp, &L)) cp = 0xFFFD;
+      }
+      word = is_word_cp(cp);
+    }
+    const uint32_t wm = __ballot_sync(0xffffffffu, word);
+    const uint32_t sm = __ballot_sync(0xffffffffu, word && start);
+    if ((threadIdx.x & 31) == 0) {
+      wbits[w] = wm;
+      sbits[w] = sm;
+    }
+  }
+}
+
+// token ending at the first non-word byte or document start after p; codepoint count
+__device__ __forceinline__ void token_extent(const uint32_t* wbits, const uint32_t* sbits, const uint32_t* dbits,
+                                             uint64_t nw, uint64_t p, uint64_t* end, uint32_t* ncp) {
+  uint64_t k = p >> 5;
+  const uint32_t j = (uint32_t)(p & 31);
+  uint32_t stop = (~wbits[k] | dbits[k]) & (j == 31 ? 0u : (0xFFFFFFFFu << (j + 1)));  // bits > j
+  uint32_t from = 0xFFFFFFFFu << j;                                                  // bits >= j
+  uint32_t cnt = 0;
+  while (!stop) {
+    cnt += __popc(sbits[k] & from);
+    from = 0xFFFFFFFFu;
+    if (++k >= nw) {
+      *end = nw << 5;
+      *ncp = cnt;
+      return;
+    }
+    stop = ~wbits[k] | dbits[k];
+  }
+  const uint32_t e = __ffs(stop) - 1;
+  cnt += __popc(sbits[k] & from & ((1u << e) - 1u));
+  *end = (k << 5) + e;
+  *ncp = cnt;
+}
+
+template <bool EMIT>
+__global__ void k_tokens(const uint32_t* __restrict__ wbits, const uint32_t* __restrict__ sbits,
+                         const uint32_t* __restrict__ dbits, uint64_t nw, uint32_t* __restrict__ cnt,
+                         const uint32_t* __restrict__ pos, uint64_t* __restrict__ tbeg, uint32_t* __restrict__ tlen) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t W = wbits[i], D = dbits[i];
+    const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
+    uint32_t B = W & (D | ~((W << 1) | prev));
+    uint32_t c = 0, o = EMIT ? pos[i] : 0;
+    while (B) {
+      const uint32_t j = __ffs(B) - 1;
+      B &= B - 1;
+      const uint64_t p = (i << 5) + j;
+      uint64_t e;
+      uint32_t ncp;
+      token_extent(wbits, sbits, dbits, nw, p, &e, &ncp);
+      if (ncp >= 2) {
+        if (EMIT) {
+          tbeg[o] = p;
+          tlen[o] = (uint32_t)(e - p);
+          ++o;
+        } else {
+          ++c;
+        }
+      }
+    }
+    if (!EMIT) cnt[i] = c;
+  }
+}
+
+// ------------------------------------------------------------------ stemmer (shadow form)
+// w: one byte per codepoint (ASCII as itself, anything else 0x80). Restates the
+// reference's stemmer.cpp:125-391 step by step; returns the new length.
+__device__ __forceinline__ bool sv(uint8_t c) { return c == 'a' || c == 'e' || c == 'i' || c == 'o' || c == 'u' || c == 'y'; }
+
+template <int M>
+__device__ __forceinline__ bool ends(const uint8_t* w, int n, const char (&s)[M]) {
+  constexpr int m = M - 1;
+  if (n < m) return false;
+#pragma unroll
+  for (int i = 0; i < m; ++i)
+    if (w[n - m + i] != (uint8_t)s[i]) return false;
+  return true;
+}
+template <int M>
+__device__ __forceinline__ bool same(const uint8_t* w, int n, const char (&s)[M]) {
+  return n == M - 1 && ends(w, n, s);
+}
+template <int M, int R>
+__device__ __forceinline__ int tail(uint8_t* w, int n, const char (&s)[M], const char (&r)[R]) {
+  n -= M - 1;
+#pragma unroll
+  for (int i = 0; i < R - 1; ++i) w[n + i] = (uint8_t)r[i];
+  return n + R - 1;
+}
+// "first listed suffix decides": matched -> replace when the suffix starts in the region
+#define SL_RULE(S, R, LIM)                                  \
+  if (ends(w, n, S)) {                                       \
+    if (n - (int)(sizeof(S) - 1) >= (LIM)) n = tail(w, n, S, R); \
+    goto done_##LIM##_rules;                                 \
+  }
+
+__device__ __forceinline__ bool vowel_before(const uint8_t* w, int end) {
+  for (int i = 0; i < end; ++i)
+    if (sv(w[i])) return true;
+  return false;
+}
+__device__ __forceinline__ bool short_syl(const uint8_t* w, int end) {
+  if (end >= 3) {
+    const uint8_t a = w[end - 3], b = w[end - 2], c = w[end - 1];
+    if (!sv(c) && c != 'w' && c != 'x' && c != 'Y' && sv(b) && !sv(a)) return true;
+  }
+  return end == 2 && sv(w[0]) && !sv(w[1]);
+}
+__device__ __forceinline__ bool is_dbl(uint8_t c) {
+  return c == 'b' || c == 'd' || c == 'f' || c == 'g' || c == 'm' || c == 'n' || c == 'p' || c == 'r' || c == 't';
+}
+__device__ __forceinline__ bool li_end(uint8_t c) {
+  return c == 'c' || c == 'd' || c == 'e' || c == 'g' || c == 'h' || c == 'k' || c == 'm' || c == 'n' || c == 'r' ||
+         c == 't';
+}
+
+// Stems the shadow in place. Returns the final length; *shift = leading apostrophe removed;
+// *ymark = some y was marked (postlude turns every 'Y' into 'y').
+__device__ int stem_shadow(uint8_t* w, int n, int* shift, bool* ymark) {
+  *shift = 0;
+  *ymark = false;
+  // irregular forms (stemmer.cpp:162-186), checked on the whole word before the prelude
+#define SL_IRR(F, T)          \
+  if (same(w, n, F)) {        \
+    return tail(w, n, F, T);  \
+  }
+  SL_IRR("skis", "ski") SL_IRR("skies", "sky") SL_IRR("dying", "die") SL_IRR("lying", "lie")
+  SL_IRR("tying", "tie") SL_IRR("idly", "idl") SL_IRR("gently", "gentl") SL_IRR("ugly", "ugli")
+  SL_IRR("early", "earli") SL_IRR("only", "onli") SL_IRR("singly", "singl")
+#undef SL_IRR
+  if (same(w, n, "sky") || same(w, n, "news") || same(w, n, "howe") || same(w, n, "atlas") ||
+      same(w, n, "cosmos") || same(w, n, "bias") || same(w, n, "andes"))
+    return n;
+  // prelude
+  if (n > 0 && w[0] == '\'') {
+    for (int i = 1; i < n; ++i) w[i - 1] = w[i];
+    --n;
+    *shift = 1;
+  }
+  bool ym = false;
+  if (n > 0 && w[0] == 'y') {
+    w[0] = 'Y';
+    ym = true;
+  }
+  for (int i = 1; i < n; ++i)
+    if (w[i] == 'y' && sv(w[i - 1])) {
+      w[i] = 'Y';
+      ym = true;
+    }
+  *ymark = ym;
+  // regions (stemmer.cpp:204-226; R1 starts AT the first non-vowel after a vowel)
+  int r1 = n, r2 = n;
+  {
+    int i = 0;
+    if (n >= 5 && w[0] == 'g' && w[1] == 'e' && w[2] == 'n' && w[3] == 'e' && w[4] == 'r') i = 5;
+    else if (n >= 6 && w[0] == 'c' && w[1] == 'o' && w[2] == 'm' && w[3] == 'm' && w[4] == 'u' && w[5] == 'n') i = 6;
+    else if (n >= 5 && w[0] == 'a' && w[1] == 'r' && w[2] == 's' && w[3] == 'e' && w[4] == 'n') i = 5;
+    bool done = false;
+    if (i == 0) {
+      while (i < n && !sv(w[i])) ++i;
+      while (i < n && sv(w[i])) ++i;
+      if (i == n) done = true;
+    }
+    if (!done) {
+      r1 = i;
+      while (i < n && !sv(w[i])) ++i;
+      while (i < n && sv(w[i])) ++i;
+      if (i != n) r2 = i;
+    }
+  }
+  // step 0
+  if (ends(w, n, "'s'")) n -= 3;
+  else if (ends(w, n, "'s")) n -= 2;
+  else if (ends(w, n, "'")) n -= 1;
+  // step 1a
+  if (ends(w, n, "sses")) {
+    n = tail(w, n, "sses", "ss");
+  } else if (ends(w, n, "ied") || ends(w, n, "ies")) {
+    if (n >= 5) n = tail(w, n, "ies", "i");
+    else n = tail(w, n, "ies", "ie");
+  } else if (ends(w, n, "us") || ends(w, n, "ss")) {
+  } else if (ends(w, n, "s")) {
+    if (n >= 3 && vowel_before(w, n - 2)) --n;
+  }
+  if (same(w, n, "inning") || same(w, n, "outing") || same(w, n, "canning") || same(w, n, "herring") ||
+      same(w, n, "earring") || same(w, n, "proceed") || same(w, n, "exceed") || same(w, n, "succeed"))
+    return n;
+  // step 1b
+  if (ends(w, n, "eedly") || ends(w, n, "eed")) {
+    const int m = ends(w, n, "eedly") ? 5 : 3;
+    if (n - m >= r1) {
+      n -= m;
+      w[n] = 'e';
+      w[n + 1] = 'e';
+      n += 2;
+    }
+  } else {
+    int m = 0;
+    if (ends(w, n, "ingly")) m = 5;
+    else if (ends(w, n, "edly")) m = 4;
+    else if (ends(w, n, "ing")) m = 3;
+    else if (ends(w, n, "ed")) m = 2;
+    if (m && vowel_before(w, n - m)) {
+      n -= m;
+      if (ends(w, n, "at") || ends(w, n, "bl") || ends(w, n, "iz")) {
+        w[n++] = 'e';
+      } else if (n >= 2 && w[n - 1] == w[n - 2] && is_dbl(w[n - 1])) {
+        --n;
+      } else if (n == r1 && short_syl(w, n)) {
+        w[n++] = 'e';
+      }
+    }
+  }
+  // step 1c
+  if (n >= 3 && (w[n - 1] == 'y' || w[n - 1] == 'Y') && !sv(w[n - 2])) w[n - 1] = 'i';
+  // step 2 (R1)
+  {
+    SL_RULE("ization", "ize", r1) SL_RULE("ational", "ate", r1) SL_RULE("fulness", "ful", r1)
+    SL_RULE("ousness", "ous", r1) SL_RULE("iveness", "ive", r1) SL_RULE("tional", "tion", r1)
+    SL_RULE("biliti", "ble", r1) SL_RULE("lessli", "less", r1) SL_RULE("entli", "ent", r1)
+    SL_RULE("fulli", "ful", r1) SL_RULE("ation", "ate", r1) SL_RULE("alism", "al", r1)
+    SL_RULE("aliti", "al", r1) SL_RULE("ousli", "ous", r1) SL_RULE("iviti", "ive", r1)
+    SL_RULE("enci", "ence", r1) SL_RULE("anci", "ance", r1) SL_RULE("abli", "able", r1)
+    SL_RULE("izer", "ize", r1) SL_RULE("ator", "ate", r1) SL_RULE("alli", "al", r1)
+    SL_RULE("bli", "ble", r1)
+    if (ends(w, n, "ogi")) {
+      const int s = n - 3;
+      if (s >= r1 && s >= 1 && w[s - 1] == 'l') n = tail(w, n, "ogi", "og");
+    } else if (ends(w, n, "li")) {
+      const int s = n - 2;
+      if (s >= r1 && s >= 1 && li_end(w[s - 1])) n = s;
+    }
+  }
+done_r1_rules:
+  // step 3
+  if (ends(w, n, "ative")) {
+    const int s = n - 5;
+    if (s >= r1 && s >= r2) n = s;
+  } else {
+#define SL_RULE3(S, R)                                    \
+  if (ends(w, n, S)) {                                     \
+    if (n - (int)(sizeof(S) - 1) >= r1) n = tail(w, n, S, R); \
+    goto done_step3;                                       \
+  }
+    SL_RULE3("ational", "ate") SL_RULE3("tional", "tion") SL_RULE3("alize", "al") SL_RULE3("icate", "ic")
+    SL_RULE3("iciti", "ic") SL_RULE3("ical", "ic") SL_RULE3("ness", "") SL_RULE3("ful", "")
+#undef SL_RULE3
+  }
+done_step3:
+  // step 4 (R2)
+  if (ends(w, n, "ement")) {
+    if (n - 5 >= r2) n -= 5;
+  } else if (ends(w, n, "ion")) {
+    const int s = n - 3;
+    if (s >= r2 && s >= 1 && (w[s - 1] == 's' || w[s - 1] == 't')) n = s;
+  } else {
+#define SL_DEL4(S)                                  \
+  if (ends(w, n, S)) {                               \
+    if (n - (int)(sizeof(S) - 1) >= r2) n -= sizeof(S) - 1; \
+    goto done_step4;                                 \
+  }
+    SL_DEL4("ement") SL_DEL4("ance") SL_DEL4("ence") SL_DEL4("able") SL_DEL4("ible") SL_DEL4("ment")
+    SL_DEL4("ant") SL_DEL4("ent") SL_DEL4("ism") SL_DEL4("ate") SL_DEL4("iti") SL_DEL4("ous")
+    SL_DEL4("ive") SL_DEL4("ize") SL_DEL4("al") SL_DEL4("er") SL_DEL4("ic")
+#undef SL_DEL4
+  }
+done_step4:
+  // step 5
+  if (n >= 1 && w[n - 1] == 'e') {
+    if (n - 1 >= r2 || (n - 1 >= r1 && !short_syl(w, n - 1))) --n;
+  } else if (n >= 2 && w[n - 1] == 'l' && w[n - 2] == 'l' && n - 1 >= r2) {
+    --n;
+  }
+  return n;
+}
+#undef SL_RULE
+
+// stem_english over UTF-8 bytes `in` (length len) into `out` (capacity >= len); `sh` is a
+// shadow buffer of >= len bytes. Lenient decode like stemmer.cpp:33-62 (malformed ->
+// unchanged). Returns the output length.
+__device__ uint32_t stem_utf8(const uint8_t* in, uint32_t len, uint8_t* sh, uint8_t* out) {
+  int n = 0;
+  bool ok = true;
+  for (uint32_t p = 0; p < len;) {
+    const uint32_t b = in[p];
+    if (b < 0x80) {
+      sh[n++] = (uint8_t)b;
+      ++p;
+      continue;
+    }
+    const int L = lead_len(b);
+    if (!L || p + L > len) {
+      ok = false;
+      break;
+    }
+    for (int i = 1; i < L; ++i)
+      if ((in[p + i] & 0xC0) != 0x80) ok = false;
+    if (!ok) break;
+    sh[n++] = 0x80;
+    p += L;
+  }
+  if (!ok || n <= 2) {
+    for (uint32_t i = 0; i < len; ++i) out[i] = in[i];
+    return len;
+  }
+  int shift;
+  bool ym;
+  const int m = stem_shadow(sh, n, &shift, &ym);
+  // rebuild: placeholders are the original codepoints at the same position (+ shift)
+  uint32_t o = 0, p = 0;
+  for (int i = 0; i < shift; ++i) p += (in[p] < 0x80) ? 1 : lead_len(in[p]);
+  for (int i = 0; i < m; ++i) {
+    const uint32_t L = in[p] < 0x80 ? 1u : (uint32_t)lead_len(in[p]);
+    if (sh[i] == 0x80) {
+      for (uint32_t k = 0; k < L; ++k) out[o++] = in[p + k];
+    } else {
+      out[o++] = (ym && sh[i] == 'Y') ? (uint8_t)'y' : sh[i];
+    }
+    p += L;  // positions past the original length only occur for ASCII replacements
+    if (p > len) p = len;
+  }
+  return o;
+}
+
+// ------------------------------------------------------------------ normalisation
+struct StopView {
+  const uint64_t* key;   // [cap] fnv1a64 of the word (0 = empty)
+  const uint32_t* off;   // [cap] byte offset into bytes
+  const uint32_t* len;   // [cap]
+  const uint8_t* bytes;
+  uint32_t cap;          // power of two (0 = no stopwords)
+};
+struct VocabView {
+  const uint64_t* tkey;
+  const uint32_t* tval;
+  uint32_t tcap;  // 0 = empty vocabulary
+  const uint64_t* offs;
+  const uint64_t* h2;
+  const uint8_t* bytes;
+};
+struct NormArgs {
+  TextView t;
+  const uint64_t* tbeg;
+  const uint32_t* tlen;
+  uint64_t n_tok;
+  int32_t lowercase, stem;
+  StopView stop;
+  VocabView voc;
+  uint8_t* arena;            // normalised bytes at 2 * tbeg (build mode), or nullptr
+  uint32_t* keep;            // 1 = not a stopword
+  uint32_t* id;              // vocabulary id or kNew
+  uint32_t* flen;            // normalised length
+  uint64_t* h1;
+  uint64_t* h2;
+  uint32_t* long_flag;       // token deferred to the global-scratch pass
+  uint32_t* err;             // bit 0: vocabulary hash collision
+};
+
+__device__ bool is_stopword(const StopView& s, const uint8_t* w, uint32_t n) {
+  if (!s.cap) return false;
+  const uint64_t k = fnv1a64(w, n) | 1ull;
+  for (uint32_t slot = (uint32_t)k & (s.cap - 1);; slot = (slot + 1) & (s.cap - 1)) {
+    const uint64_t e = s.key[slot];
+    if (!e) return false;
+    if (e == k && s.len[slot] == n) {
+      bool eq = true;
+      for (uint32_t i = 0; i < n && eq; ++i) eq = s.bytes[s.off[slot] + i] == w[i];
+      if (eq) return true;
+    }
+  }
+}
+
+__device__ uint32_t vocab_find(const VocabView& v, const uint8_t* w, uint32_t n, H2 h, uint32_t* err) {
+  if (!v.tcap) return kNew;
+  for (uint32_t slot = (uint32_t)h.a & (v.tcap - 1);; slot = (slot + 1) & (v.tcap - 1)) {
+    const uint64_t e = v.tkey[slot];
+    if (!e) return kNew;
+    if (e == h.a) {
+      const uint32_t id = v.tval[slot];
+      const uint64_t o = v.offs[id];
+      bool eq = v.h2[id] == h.b && v.offs[id + 1] - o == n;
+      for (uint32_t i = 0; i < n && eq; ++i) eq = v.bytes[o + i] == w[i];
+      if (eq) return id;
+      atomicOr(err, 1u);  // same first hash, different string: refuse rather than merge
+      return kNew;
+    }
+  }
+}
+
+// normalise token i with caller-provided buffers (nb: 2*len, sh: len+1, fb: 2*len)
+__device__ void norm_one(const NormArgs& a, uint64_t i, uint8_t* nb, uint8_t* sh, uint8_t* fb) {
+  const uint64_t b = a.tbeg[i];
+  const uint32_t len = a.tlen[i];
+  const uint8_t* src = a.t.text + b;
+  uint32_t nl = 0;
+  if (a.lowercase) {
+    for (uint32_t p = 0; p < len;) {
+      uint32_t cp;
+      p += decode_at(src + p, &cp);
+      nl += put_utf8(nb + nl, lower_cp(cp));
+    }
+  } else {
+    for (uint32_t p = 0; p < len; ++p) nb[p] = src[p];
+    nl = len;
+  }
+  if (is_stopword(a.stop, nb, nl)) {
+    a.keep[i] = 0;
+    a.id[i] = kNew;
+    a.flen[i] = 0;
+    return;
+  }
+  a.keep[i] = 1;
+  const uint8_t* fin = nb;
+  uint32_t fl = nl;
+  if (a.stem) {
+    fl = stem_utf8(nb, nl, sh, fb);
+    fin = fb;
+  }
+  const H2 h = hash2(fin, fl);
+  a.flen[i] = fl;
+  a.h1[i] = h.a;
+  a.h2[i] = h.b;
+  a.id[i] = vocab_find(a.voc, fin, fl, h, a.err);
+  if (a.arena)
+    for (uint32_t k = 0; k < fl; ++k) a.arena[2 * b + k] = fin[k];
+}
+
+__global__ void k_norm_fast(NormArgs a) {
+  uint8_t nb[2 * kFastBytes], sh[kFastBytes + 1], fb[2 * kFastBytes];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_tok;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (a.tlen[i] > kFastBytes) {
+      a.long_flag[i] = 1;
+      continue;
+    }
+    a.long_flag[i] = 0;
+    norm_one(a, i, nb, sh, fb);
+  }
+}
+
+// long tokens: scratch slot of 5 * len bytes each (nb 2len | sh len | fb 2len)
+__global__ void k_norm_long(NormArgs a, const uint32_t* __restrict__ list, uint32_t n_list,
+                            const uint64_t* __restrict__ soff, uint8_t* __restrict__ scratch) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_list; j += gridDim.x * blockDim.x) {
+    const uint64_t i = list[j];
+    uint8_t* base = scratch + soff[j];
+    const uint32_t len = a.tlen[i];
+    norm_one(a, i, base, base + 2 * (uint64_t)len, base + 3 * (uint64_t)len + 1);
+  }
+}
+
+// ------------------------------------------------------------------ small helpers
+__global__ void k_flag_to_u32(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint64_t n,
+                              uint32_t* __restrict__ out, int mode) {
+  // mode 0: out = a (copy); mode 1: out = a && b == kNew (new kept token); mode 2: a && b != kNew
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = mode == 0 ? a[i] : mode == 1 ? (a[i] && b[i] == kNew) : (a[i] && b[i] != kNew);
+}
+
+__global__ void k_compact_idx(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint64_t n,
+                              uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[pos[i]] = (uint32_t)i;
+}
+
+__global__ void k_gather_u64_lo_hi(const uint64_t* __restrict__ h, const uint32_t* __restrict__ idx, uint32_t n,
+                                   uint32_t* __restrict__ lo, uint32_t* __restrict__ hi) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint64_t x = h[idx[j]];
+    lo[j] = (uint32_t)x;
+    hi[j] = (uint32_t)(x >> 32);
+  }
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
+                             uint32_t* __restrict__ out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
+}
+
+// sorted new tokens (token index order preserved within equal hashes): group heads
+__global__ void k_group_heads(const uint32_t* __restrict__ tok, uint32_t n, const uint64_t* __restrict__ h1,
+                              const uint64_t* __restrict__ h2, const uint32_t* __restrict__ flen,
+                              uint32_t* __restrict__ head, uint32_t* __restrict__ err) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t t = tok[j];
+    bool h = j == 0;
+    if (!h) {
+      const uint32_t u = tok[j - 1];
+      h = h1[t] != h1[u];
+      if (!h && (h2[t] != h2[u] || flen[t] != flen[u])) atomicOr(err, 1u);
+    }
+    head[j] = h ? 1u : 0u;
+  }
+}
+
+// per group: first (smallest) token index, and group of every sorted element
+__global__ void k_group_first(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ head,
+                              const uint32_t* __restrict__ gpos, uint32_t n, uint32_t* __restrict__ gfirst) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    if (head[j]) gfirst[gpos[j]] = tok[j];
+}
+
+// groups sorted by first occurrence: rank -> id = V0 + rank
+__global__ void k_group_rank(const uint32_t* __restrict__ gsorted, uint32_t G, uint32_t* __restrict__ grank) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < G; r += gridDim.x * blockDim.x) grank[gsorted[r]] = r;
+}
+
+__global__ void k_assign_new(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ head,
+                             const uint32_t* __restrict__ gpos, uint32_t n, const uint32_t* __restrict__ grank,
+                             uint32_t V0, uint32_t* __restrict__ id) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t g = gpos[j] + head[j] - 1;  // inclusive group index
+    id[tok[j]] = V0 + grank[g];
+  }
+}
+
+// new vocabulary entries in id order: representative token, length
+__global__ void k_new_entries(const uint32_t* __restrict__ gsorted_first, uint32_t G, const uint32_t* __restrict__ flen,
+                              uint32_t* __restrict__ elen) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < G; r += gridDim.x * blockDim.x)
+    elen[r] = flen[gsorted_first[r]];
+}
+
+__global__ void k_copy_entries(const uint32_t* __restrict__ first, uint32_t G, const uint64_t* __restrict__ tbeg,
+                               const uint32_t* __restrict__ flen, const uint8_t* __restrict__ arena,
+                               const uint32_t* __restrict__ epos, uint64_t base, uint32_t V0,
+                               const uint64_t* __restrict__ h2tok, uint8_t* __restrict__ bytes,
+                               uint64_t* __restrict__ offs, uint64_t* __restrict__ h2v) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < G; r += gridDim.x * blockDim.x) {
+    const uint32_t t = first[r];
+    const uint64_t o = base + epos[r];
+    const uint32_t n = flen[t];
+    for (uint32_t k = 0; k < n; ++k) bytes[o + k] = arena[2 * tbeg[t] + k];
+    offs[V0 + r + 1] = o + n;
+    h2v[V0 + r] = h2tok[t];
+  }
+}
+
+__global__ void k_table_insert(const uint64_t* __restrict__ h1tok, const uint32_t* __restrict__ first, uint32_t G,
+                               uint32_t V0, uint64_t* __restrict__ tkey, uint32_t* __restrict__ tval, uint32_t tcap,
+                               uint32_t* __restrict__ err) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < G; r += gridDim.x * blockDim.x) {
+    const uint64_t k = h1tok[first[r]];
+    for (uint32_t slot = (uint32_t)k & (tcap - 1);; slot = (slot + 1) & (tcap - 1)) {
+      const unsigned long long prev = atomicCAS((unsigned long long*)tkey + slot, 0ull, (unsigned long long)k);
+      if (prev == 0ull) {
+        tval[slot] = V0 + r;
+        break;
+      }
+      if (prev == k) {  // cannot happen (groups have distinct first hashes)
+        atomicOr(err, 1u);
+        break;
+      }
+    }
+  }
+}
+
+// re-insert an existing vocabulary into a larger table: hash recomputed from the bytes
+__global__ void k_table_rehash(const uint64_t* __restrict__ offs, const uint8_t* __restrict__ bytes, uint32_t V,
+                               uint64_t* __restrict__ tkey, uint32_t* __restrict__ tval, uint32_t tcap,
+                               uint64_t* __restrict__ h2v) {
+  for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < V; id += gridDim.x * blockDim.x) {
+    const H2 h = hash2(bytes + offs[id], (uint32_t)(offs[id + 1] - offs[id]));
+    h2v[id] = h.b;
+    for (uint32_t slot = (uint32_t)h.a & (tcap - 1);; slot = (slot + 1) & (tcap - 1)) {
+      if (atomicCAS((unsigned long long*)tkey + slot, 0ull, (unsigned long long)h.a) == 0ull) {
+        tval[slot] = id;
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_out_ids(const uint32_t* __restrict__ kept_idx, uint64_t n, const uint32_t* __restrict__ id,
+                          const uint64_t* __restrict__ tbeg, uint32_t* __restrict__ out_ids,
+                          uint64_t* __restrict__ out_beg) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = kept_idx[j];
+    out_ids[j] = id[t];
+    out_beg[j] = tbeg[t];
+  }
+}
+
+// token offsets per document: lower_bound of the document's first byte among kept tokens
+__global__ void k_doc_token_offsets(const uint64_t* __restrict__ doc_off, uint32_t N,
+                                    const uint64_t* __restrict__ kbeg, uint64_t T, uint64_t* __restrict__ out) {
+  for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d <= N; d += gridDim.x * blockDim.x) {
+    if (d == N) {
+      out[d] = T;
+      continue;
+    }
+    const uint64_t x = doc_off[d];
+    uint64_t lo = 0, hi = T;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (kbeg[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    out[d] = lo;
+  }
+}
+
+__global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __restrict__ off, uint32_t n,
+                             uint8_t* __restrict__ scratch, uint8_t* __restrict__ out, uint32_t* __restrict__ olen) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t b = off[i];
+    const uint32_t len = (uint32_t)(off[i + 1] - b);
+    olen[i] = stem_utf8(in + b, len, scratch + b, out + b);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+inline unsigned grid_for(uint64_t n, int per = 256) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, 148ull * 64));
+}
+
+struct TScratch {
+  cudaStream_t st;
+  std::vector<void*> ps;
+  explicit TScratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  int32_t alloc(T** p, uint64_t n) {
+    if (n == 0) n = 1;
+    if (cudaMallocAsync((void**)p, n * sizeof(T), st) != cudaSuccess) {
+      *p = nullptr;
+      SL_FAIL(SL_ENOMEM, "tokenizer: device allocation of " + std::to_string(n * sizeof(T)) + " bytes failed");
+    }
+    ps.push_back(*p);
+    return SL_OK;
+  }
+  ~TScratch() {
+    for (void* p : ps) cudaFreeAsync(p, st);
+  }
+};
+
+struct TextStream {
+  int device = -1;
+  cudaStream_t st = nullptr;
+};
+thread_local TextStream t_text_stream[16];
+
+int32_t text_stream(int device, cudaStream_t* out) {
+  if (device < 0 || device >= 16) SL_FAIL(SL_EINVAL, "device ordinal out of range");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    SL_FAIL(SL_ECUDA, "tokenizer: no CUDA device available (there is no CPU fallback)");
+  SL_CUDA_TRY(cudaSetDevice(device));
+  TextStream& s = t_text_stream[device];
+  if (!s.st) {
+    SL_CUDA_TRY(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    s.device = device;
+  }
+  *out = s.st;
+  return SL_OK;
+}
+
+uint32_t pow2_at_least(uint64_t x) {
+  uint64_t c = 16;
+  while (c < x) c <<= 1;
+  return (uint32_t)std::min<uint64_t>(c, 1ull << 31);
+}
+
+// host-built stopword table
+struct StopTable {
+  std::vector<uint64_t> key;
+  std::vector<uint32_t> off, len;
+  std::vector<uint8_t> bytes;
+  uint32_t cap = 0;
+};
+
+std::vector<std::string> parse_stopwords(const char* s, uint64_t n) {
+  std::vector<std::string> out;
+  std::string cur;
+  auto flush = [&] {
+    // trim trailing '\r' and surrounding spaces; '#' lines are comments (stopwords.hpp:13-15)
+    while (!cur.empty() && (cur.back() == '\r' || cur.back() == ' ' || cur.back() == '\t')) cur.pop_back();
+    size_t a = 0;
+    while (a < cur.size() && (cur[a] == ' ' || cur[a] == '\t')) ++a;
+    cur = cur.substr(a);
+    if (!cur.empty() && cur[0] != '#') out.push_back(cur);
+    cur.clear();
+  };
+  for (uint64_t i = 0; i < n; ++i) {
+    if (s[i] == '\n') flush();
+    else cur += s[i];
+  }
+  flush();
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+
+StopTable make_stop_table(const std::vector<std::string>& words) {
+  StopTable t;
+  if (words.empty()) return t;
+  t.cap = pow2_at_least(words.size() * 2);
+  t.key.assign(t.cap, 0);
+  t.off.assign(t.cap, 0);
+  t.len.assign(t.cap, 0);
+  for (const auto& w : words) {
+    const uint64_t k = fnv1a64(reinterpret_cast<const uint8_t*>(w.data()), (uint32_t)w.size()) | 1ull;
+    uint32_t slot = (uint32_t)k & (t.cap - 1);
+    while (t.key[slot]) slot = (slot + 1) & (t.cap - 1);
+    t.key[slot] = k;
+    t.off[slot] = (uint32_t)t.bytes.size();
+    t.len[slot] = (uint32_t)w.size();
+    t.bytes.insert(t.bytes.end(), w.begin(), w.end());
+  }
+  return t;
+}
+
+// grow a device array (stream-ordered), keeping `keep` elements
+template <class T>
+int32_t grow(T** p, uint64_t keep, uint64_t newcap, cudaStream_t st) {
+  T* q = nullptr;
+  if (cudaMallocAsync((void**)&q, std::max<uint64_t>(newcap, 1) * sizeof(T), st) != cudaSuccess)
+    SL_FAIL(SL_ENOMEM, "vocabulary: device allocation failed");
+  if (*p && keep) SL_CUDA_TRY(cudaMemcpyAsync(q, *p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if (*p) cudaFreeAsync(*p, st);
+  *p = q;
+  return SL_OK;
+}
+
+int32_t vocab_reserve(sl_vocab* v, uint64_t n_entries, uint64_t n_bytes, cudaStream_t st) {
+  if (n_entries > v->vcap) {
+    const uint64_t cap = std::max<uint64_t>(n_entries, (uint64_t)v->vcap * 2);
+    if (cap > 0xFFFFFFF0ull) SL_FAIL(SL_EUNSUPPORTED, "vocabulary larger than 2^32 entries");
+    SL_TRY(grow(&v->offs, v->V + 1ull, cap + 1, st));
+    SL_TRY(grow(&v->h2, v->V, cap, st));
+    if (v->vcap == 0) SL_CUDA_TRY(cudaMemsetAsync(v->offs, 0, 8, st));
+    v->vcap = (uint32_t)cap;
+  }
+  if (n_bytes > v->bcap) {
+    const uint64_t cap = std::max<uint64_t>(n_bytes, v->bcap * 2);
+    SL_TRY(grow(&v->bytes, v->bused, cap, st));
+    v->bcap = cap;
+  }
+  const uint64_t want = pow2_at_least(n_entries * 2);
+  if (want > v->tcap) {  // rebuild the hash table
+    if (v->tkey) cudaFreeAsync(v->tkey, st);
+    if (v->tval) cudaFreeAsync(v->tval, st);
+    if (cudaMallocAsync((void**)&v->tkey, want * 8, st) != cudaSuccess ||
+        cudaMallocAsync((void**)&v->tval, want * 4, st) != cudaSuccess)
+      SL_FAIL(SL_ENOMEM, "vocabulary: hash table allocation failed");
+    SL_CUDA_TRY(cudaMemsetAsync(v->tkey, 0, want * 8, st));
+    v->tcap = (uint32_t)want;
+    if (v->V) {
+      k_table_rehash<<<grid_for(v->V), 256, 0, st>>>(v->offs, v->bytes, v->V, v->tkey, v->tval, v->tcap, v->h2);
+      ++t_launches;
+    }
+  }
+  SL_CUDA_TRY(cudaGetLastError());
+  return SL_OK;
+}
+
+int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build, const char* text_in,
+                      const uint64_t* doc_off_in, uint32_t N, int32_t mem, sl_token_batch** out) {
+  if (!v || !cfg || !out) SL_FAIL(SL_EINVAL, "tokenize: null argument");
+  if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "tokenize: bad mem kind");
+  if (cfg->stemmer != SL_STEMMER_NONE && cfg->stemmer != SL_STEMMER_SNOWBALL_ENGLISH)
+    SL_FAIL(SL_EINVAL, "unknown stemmer");
+  if (N && !doc_off_in) SL_FAIL(SL_EINVAL, "tokenize: null document offsets");
+  cudaStream_t st;
+  SL_TRY(text_stream(v->device, &st));
+  TScratch scr(st);
+  // ---- inputs on the device
+  uint64_t first = 0, last = 0;
+  const uint64_t* doc_off = doc_off_in;
+  if (N) {
+    if (mem == SL_MEM_HOST) {
+      first = doc_off_in[0];
+      last = doc_off_in[N];
+      for (uint32_t d = 0; d < N; ++d)
+        if (doc_off_in[d + 1] < doc_off_in[d]) SL_FAIL(SL_EINVAL, "tokenize: document offsets must be non-decreasing");
+    } else {
+      SL_CUDA_TRY(cudaMemcpyAsync(&first, doc_off_in, 8, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaMemcpyAsync(&last, doc_off_in + N, 8, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+      if (last < first) SL_FAIL(SL_EINVAL, "tokenize: document offsets must be non-decreasing");
+    }
+    if (first != 0) SL_FAIL(SL_EINVAL, "tokenize: doc_offsets[0] must be 0");
+  }
+  const uint64_t nb = last;
+  if (nb && !text_in) SL_FAIL(SL_EINVAL, "tokenize: null text");
+  const uint8_t* text = reinterpret_cast<const uint8_t*>(text_in);
+  if (mem == SL_MEM_HOST || N == 0) {
+    uint8_t* dt;
+    uint64_t* doff;
+    SL_TRY(scr.alloc(&dt, nb));
+    SL_TRY(scr.alloc(&doff, (uint64_t)N + 1));
+    if (nb) SL_CUDA_TRY(cudaMemcpyAsync(dt, text_in, nb, cudaMemcpyHostToDevice, st));
+    if (N) SL_CUDA_TRY(cudaMemcpyAsync(doff, doc_off_in, ((uint64_t)N + 1) * 8, cudaMemcpyHostToDevice, st));
+    else SL_CUDA_TRY(cudaMemsetAsync(doff, 0, 8, st));
+    text = dt;
+    doc_off = doff;
+  }
+  auto* tb = new sl_token_batch();
+  tb->device = v->device;
+  tb->N = N;
+  auto fail = [&](int32_t rc) {
+    if (tb->offs) cudaFreeAsync(tb->offs, st);
+    if (tb->ids) cudaFreeAsync(tb->ids, st);
+    cudaStreamSynchronize(st);
+    delete tb;
+    return rc;
+  };
+#define SL_TTRY(x)                      \
+  do {                                  \
+    const int32_t rc_ = (x);            \
+    if (rc_ != SL_OK) return fail(rc_); \
+  } while (0)
+  if (cudaMallocAsync((void**)&tb->offs, ((uint64_t)N + 1) * 8, st) != cudaSuccess)
+    return fail((set_error("tokenize: allocation failed"), SL_ENOMEM));
+  // ---- segmentation
+  const uint64_t nw = (nb + 31) / 32;
+  uint32_t *dbits, *wbits, *sbits, *cnt;
+  SL_TTRY(scr.alloc(&dbits, nw));
+  SL_TTRY(scr.alloc(&wbits, nw));
+  SL_TTRY(scr.alloc(&sbits, nw));
+  SL_TTRY(scr.alloc(&cnt, nw));
+  uint64_t n_tok = 0;
+  uint64_t *tbeg = nullptr;
+  uint32_t* tlen = nullptr;
+  if (nb) {
+    if (cudaMemsetAsync(dbits, 0, nw * 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
+    k_doc_marks<<<grid_for(N), 256, 0, st>>>(doc_off, N, nb, dbits); ++t_launches;
+    const TextView tv{text, nb, dbits};
+    k_classify<<<grid_for(nw * 32), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+    k_tokens<false><<<grid_for(nw), 256, 0, st>>>(wbits, sbits, dbits, nw, cnt, nullptr, nullptr, nullptr);
+    ++t_launches;
+    uint32_t tot = 0;
+    SL_TTRY(exclusive_scan_u32(cnt, cnt, nw, st, &tot));
+    n_tok = tot;
+    SL_TTRY(scr.alloc(&tbeg, n_tok));
+    SL_TTRY(scr.alloc(&tlen, n_tok));
+    k_tokens<true><<<grid_for(nw), 256, 0, st>>>(wbits, sbits, dbits, nw, nullptr, cnt, tbeg, tlen); ++t_launches;
+  }
+  // ---- normalisation + vocabulary probe
+  std::vector<std::string> sw;
+  if (cfg->stopwords && cfg->stopwords_bytes) sw = parse_stopwords(cfg->stopwords, cfg->stopwords_bytes);
+  const StopTable stab = make_stop_table(sw);
+  StopView sv{};
+  if (stab.cap) {
+    uint64_t* k;
+    uint32_t *o, *l;
+    uint8_t* by;
+    SL_TTRY(scr.alloc(&k, stab.cap));
+    SL_TTRY(scr.alloc(&o, stab.cap));
+    SL_TTRY(scr.alloc(&l, stab.cap));
+    SL_TTRY(scr.alloc(&by, stab.bytes.size()));
+    cudaMemcpyAsync(k, stab.key.data(), stab.cap * 8ull, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(o, stab.off.data(), stab.cap * 4ull, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(l, stab.len.data(), stab.cap * 4ull, cudaMemcpyHostToDevice, st);
+    if (!stab.bytes.empty()) cudaMemcpyAsync(by, stab.bytes.data(), stab.bytes.size(), cudaMemcpyHostToDevice, st);
+    sv = StopView{k, o, l, by, stab.cap};
+  }
+  NormArgs na{};
+  na.t = TextView{text, nb, dbits};
+  na.tbeg = tbeg;
+  na.tlen = tlen;
+  na.n_tok = n_tok;
+  na.lowercase = cfg->lowercase ? 1 : 0;
+  na.stem = cfg->stemmer == SL_STEMMER_SNOWBALL_ENGLISH ? 1 : 0;
+  na.stop = sv;
+  na.voc = VocabView{v->tkey, v->tval, v->V ? v->tcap : 0u, v->offs, v->h2, v->bytes};
+  uint32_t* err;
+  SL_TTRY(scr.alloc(&err, 1));
+  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
+  na.err = err;
+  SL_TTRY(scr.alloc(&na.keep, n_tok));
+  SL_TTRY(scr.alloc(&na.id, n_tok));
+  SL_TTRY(scr.alloc(&na.flen, n_tok));
+  SL_TTRY(scr.alloc(&na.h1, n_tok));
+  SL_TTRY(scr.alloc(&na.h2, n_tok));
+  SL_TTRY(scr.alloc(&na.long_flag, n_tok));
+  if (build) SL_TTRY(scr.alloc(&na.arena, 2 * nb));
+  if (n_tok) {
+    k_norm_fast<<<grid_for(n_tok, 128), 128, 0, st>>>(na); ++t_launches;
+    // deferred long tokens
+    uint32_t* lpos;
+    SL_TTRY(scr.alloc(&lpos, n_tok));
+    uint32_t n_long = 0;
+    SL_TTRY(exclusive_scan_u32(na.long_flag, lpos, n_tok, st, &n_long));
+    if (n_long) {
+      uint32_t* list;
+      SL_TTRY(scr.alloc(&list, n_long));
+      k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(na.long_flag, lpos, n_tok, list); ++t_launches;
+      // per long token scratch: 5 * len + 1 bytes
+      std::vector<uint64_t> so(n_long + 1, 0);
+      {
+        std::vector<uint32_t> lens(n_long);
+        uint32_t* dl;
+        SL_TTRY(scr.alloc(&dl, n_long));
+        k_gather_u32<<<grid_for(n_long), 256, 0, st>>>(tlen, list, n_long, dl); ++t_launches;
+        SL_CUDA_TRY(cudaMemcpyAsync(lens.data(), dl, n_long * 4ull, cudaMemcpyDeviceToHost, st));
+        SL_CUDA_TRY(cudaStreamSynchronize(st));
+        for (uint32_t j = 0; j < n_long; ++j) so[j + 1] = so[j] + 5ull * lens[j] + 1;
+      }
+      uint64_t* dso;
+      uint8_t* scratch;
+      SL_TTRY(scr.alloc(&dso, n_long + 1ull));
+      SL_TTRY(scr.alloc(&scratch, so[n_long]));
+      SL_CUDA_TRY(cudaMemcpyAsync(dso, so.data(), (n_long + 1ull) * 8, cudaMemcpyHostToDevice, st));
+      k_norm_long<<<grid_for(n_long, 64), 64, 0, st>>>(na, list, n_long, dso, scratch); ++t_launches;
+    }
+  }
+  // ---- kept tokens
+  uint32_t *kflag, *kpos, *kidx;
+  SL_TTRY(scr.alloc(&kflag, n_tok));
+  SL_TTRY(scr.alloc(&kpos, n_tok));
+  if (n_tok) {
+    k_flag_to_u32<<<grid_for(n_tok), 256, 0, st>>>(na.keep, na.id, n_tok, kflag, build ? 0 : 2); ++t_launches;
+  }
+  uint32_t T = 0;
+  SL_TTRY(exclusive_scan_u32(kflag, kpos, n_tok, st, &T));
+  SL_TTRY(scr.alloc(&kidx, T));
+  if (n_tok) {
+    k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(kflag, kpos, n_tok, kidx); ++t_launches;
+  }
+  // ---- new vocabulary entries (build mode)
+  if (build && T) {
+    uint32_t *nflag, *npos;
+    SL_TTRY(scr.alloc(&nflag, n_tok));
+    SL_TTRY(scr.alloc(&npos, n_tok));
+    k_flag_to_u32<<<grid_for(n_tok), 256, 0, st>>>(na.keep, na.id, n_tok, nflag, 1); ++t_launches;
+    uint32_t M = 0;
+    SL_TTRY(exclusive_scan_u32(nflag, npos, n_tok, st, &M));
+    if (M) {
+      uint32_t *ntok, *klo, *khi, *k0, *k1, *v0, *v1, *head, *gpos, *gfirst, *grank, *gs_k, *gs_v, *elen, *epos;
+      SL_TTRY(scr.alloc(&ntok, M));
+      SL_TTRY(scr.alloc(&klo, M));
+      SL_TTRY(scr.alloc(&khi, M));
+      SL_TTRY(scr.alloc(&k0, M));
+      SL_TTRY(scr.alloc(&k1, M));
+      SL_TTRY(scr.alloc(&v0, M));
+      SL_TTRY(scr.alloc(&v1, M));
+      SL_TTRY(scr.alloc(&head, M));
+      SL_TTRY(scr.alloc(&gpos, M));
+      k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(nflag, npos, n_tok, ntok); ++t_launches;
+      // stable LSD sort of token indices by h1: low word, then high word
+      k_gather_u64_lo_hi<<<grid_for(M), 256, 0, st>>>(na.h1, ntok, M, klo, khi); ++t_launches;
+      const uint32_t *ks, *vs;
+      SL_TTRY(radix_sort_pairs(klo, ntok, M, 32, k0, k1, v0, v1, st, &ks, &vs, 0, nullptr));
+      // vs = token indices ordered by low word; re-gather the high word in that order
+      uint32_t* perm1;
+      SL_TTRY(scr.alloc(&perm1, M));
+      SL_CUDA_TRY(cudaMemcpyAsync(perm1, vs, M * 4ull, cudaMemcpyDeviceToDevice, st));
+      k_gather_u64_lo_hi<<<grid_for(M), 256, 0, st>>>(na.h1, perm1, M, klo, khi); ++t_launches;
+      SL_TTRY(radix_sort_pairs(khi, perm1, M, 32, k0, k1, v0, v1, st, &ks, &vs, 0, nullptr));
+      uint32_t* sorted;
+      SL_TTRY(scr.alloc(&sorted, M));
+      SL_CUDA_TRY(cudaMemcpyAsync(sorted, vs, M * 4ull, cudaMemcpyDeviceToDevice, st));
+      k_group_heads<<<grid_for(M), 256, 0, st>>>(sorted, M, na.h1, na.h2, na.flen, head, err); ++t_launches;
+      uint32_t G = 0;
+      SL_TTRY(exclusive_scan_u32(head, gpos, M, st, &G));
+      SL_TTRY(scr.alloc(&gfirst, G));
+      SL_TTRY(scr.alloc(&grank, G));
+      SL_TTRY(scr.alloc(&gs_k, G));
+      SL_TTRY(scr.alloc(&gs_v, G));
+      SL_TTRY(scr.alloc(&elen, G));
+      SL_TTRY(scr.alloc(&epos, G));
+      k_group_first<<<grid_for(M), 256, 0, st>>>(sorted, head, gpos, M, gfirst); ++t_launches;
+      // order groups by first occurrence (token index = document/position order)
+      uint32_t* giota;
+      SL_TTRY(scr.alloc(&giota, G));
+      {
+        std::vector<uint32_t> io(G);
+        for (uint32_t g = 0; g < G; ++g) io[g] = g;
+        SL_CUDA_TRY(cudaMemcpyAsync(giota, io.data(), G * 4ull, cudaMemcpyHostToDevice, st));
+        SL_CUDA_TRY(cudaStreamSynchronize(st));
+      }
+      const uint32_t *fs, *gsv;
+      SL_TTRY(radix_sort_pairs(gfirst, giota, G, 32, k0, k1, v0, v1, st, &fs, &gsv, 0, nullptr));
+      SL_CUDA_TRY(cudaMemcpyAsync(gs_k, fs, G * 4ull, cudaMemcpyDeviceToDevice, st));  // first token per rank
+      SL_CUDA_TRY(cudaMemcpyAsync(gs_v, gsv, G * 4ull, cudaMemcpyDeviceToDevice, st)); // group per rank
+      k_group_rank<<<grid_for(G), 256, 0, st>>>(gs_v, G, grank); ++t_launches;
+      const uint32_t V0 = v->V;
+      k_assign_new<<<grid_for(M), 256, 0, st>>>(sorted, head, gpos, M, grank, V0, na.id); ++t_launches;
+      // append strings
+      k_new_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, na.flen, elen); ++t_launches;
+      uint32_t ebytes = 0;
+      SL_TTRY(exclusive_scan_u32(elen, epos, G, st, &ebytes));
+      uint32_t h_err = 0;
+      SL_CUDA_TRY(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+      if (h_err) {
+        set_error("tokenize: 128-bit token hash collision between distinct strings");
+        return fail(SL_EUNSUPPORTED);
+      }
+      SL_TTRY(vocab_reserve(v, (uint64_t)V0 + G, v->bused + ebytes, st));
+      k_copy_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, tbeg, na.flen, na.arena, epos, v->bused, V0, na.h2,
+                                                  v->bytes, v->offs, v->h2); ++t_launches;
+      k_table_insert<<<grid_for(G), 256, 0, st>>>(na.h1, gs_k, G, V0, v->tkey, v->tval, v->tcap, err); ++t_launches;
+      v->V = V0 + G;
+      v->bused += ebytes;
+    }
+  }
+  // ---- outputs
+  tb->T = T;
+  if (cudaMallocAsync((void**)&tb->ids, std::max<uint64_t>(T, 1) * 4, st) != cudaSuccess)
+    return fail((set_error("tokenize: allocation failed"), SL_ENOMEM));
+  uint64_t* kbeg;
+  SL_TTRY(scr.alloc(&kbeg, T));
+  if (T) {
+    k_out_ids<<<grid_for(T), 256, 0, st>>>(kidx, T, na.id, tbeg, tb->ids, kbeg); ++t_launches;
+  }
+  k_doc_token_offsets<<<grid_for((uint64_t)N + 1), 256, 0, st>>>(doc_off, N, kbeg, T, tb->offs); ++t_launches;
+  uint32_t h_err = 0;
+  SL_CUDA_TRY(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return fail((set_error(std::string("tokenize: CUDA failure: ") + cudaGetErrorString(cudaGetLastError())),
+                 SL_ECUDA));
+  if (h_err) {
+    set_error("tokenize: 128-bit token hash collision between distinct strings");
+    return fail(SL_EUNSUPPORTED);
+  }
+#undef SL_TTRY
+  *out = tb;
+  return SL_OK;
+}
+
+}  // namespace
+}  // namespace sl
+
+using namespace sl;
+
+extern "C" {
+
+int32_t sl_vocab_create(int32_t device, sl_vocab** out) {
+  if (!out) SL_FAIL(SL_EINVAL, "sl_vocab_create: null output");
+  cudaStream_t st;
+  SL_TRY(text_stream(device, &st));
+  auto* v = new sl_vocab();
+  v->device = device;
+  const int32_t rc = vocab_reserve(v, 16, 256, st);
+  cudaStreamSynchronize(st);
+  if (rc != SL_OK) {
+    delete v;
+    return rc;
+  }
+  *out = v;
+  return SL_OK;
+}
+
+int32_t sl_vocab_destroy(sl_vocab* v) {
+  if (!v) return SL_OK;
+  cudaSetDevice(v->device);
+  void* ps[] = {v->offs, v->h2, v->bytes, v->tkey, v->tval};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  delete v;
+  return SL_OK;
+}
+
+int32_t sl_vocab_size(const sl_vocab* v, uint32_t* size) {
+  if (!v || !size) SL_FAIL(SL_EINVAL, "sl_vocab_size: null argument");
+  *size = v->V;
+  return SL_OK;
+}
+
+int32_t sl_vocab_export(const sl_vocab* v, uint64_t* offsets, char* bytes, uint64_t* total_bytes) {
+  if (!v) SL_FAIL(SL_EINVAL, "sl_vocab_export: null vocabulary");
+  SL_CUDA_TRY(cudaSetDevice(v->device));
+  if (total_bytes) *total_bytes = v->bused;
+  if (offsets) SL_CUDA_TRY(cudaMemcpy(offsets, v->offs, (v->V + 1ull) * 8, cudaMemcpyDeviceToHost));
+  if (bytes && v->bused) SL_CUDA_TRY(cudaMemcpy(bytes, v->bytes, v->bused, cudaMemcpyDeviceToHost));
+  return SL_OK;
+}
+
+int32_t sl_vocab_import(sl_vocab* v, const uint64_t* offsets, const char* bytes, uint32_t n) {
+  if (!v || (n && (!offsets || !bytes))) SL_FAIL(SL_EINVAL, "sl_vocab_import: null argument");
+  if (v->V) SL_FAIL(SL_EINVAL, "sl_vocab_import: vocabulary is not empty");
+  if (n && offsets[0] != 0) SL_FAIL(SL_EINVAL, "sl_vocab_import: offsets[0] must be 0");
+  for (uint32_t i = 0; i < n; ++i)
+    if (offsets[i + 1] < offsets[i]) SL_FAIL(SL_EINVAL, "sl_vocab_import: offsets must be non-decreasing");
+  cudaStream_t st;
+  SL_TRY(text_stream(v->device, &st));
+  const uint64_t nbytes = n ? offsets[n] : 0;
+  // duplicates would make ids ambiguous (vocabulary.hpp: one id per token)
+  {
+    std::vector<std::string_view> s(n);
+    for (uint32_t i = 0; i < n; ++i) s[i] = std::string_view(bytes + offsets[i], offsets[i + 1] - offsets[i]);
+    std::sort(s.begin(), s.end());
+    for (uint32_t i = 1; i < n; ++i)
+      if (s[i] == s[i - 1]) SL_FAIL(SL_ECORRUPT, "sl_vocab_import: duplicate token '" + std::string(s[i]) + "'");
+  }
+  SL_TRY(vocab_reserve(v, std::max<uint64_t>(n, 16), std::max<uint64_t>(nbytes, 256), st));
+  if (n) {
+    SL_CUDA_TRY(cudaMemcpyAsync(v->offs, offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, st));
+    if (nbytes) SL_CUDA_TRY(cudaMemcpyAsync(v->bytes, bytes, nbytes, cudaMemcpyHostToDevice, st));
+    // h2 + table from the bytes (k_table_rehash writes the table; h2 via the same hash)
+    SL_CUDA_TRY(cudaMemsetAsync(v->tkey, 0, v->tcap * 8ull, st));
+    v->V = n;
+    v->bused = nbytes;
+    k_table_rehash<<<grid_for(n), 256, 0, st>>>(v->offs, v->bytes, n, v->tkey, v->tval, v->tcap, v->h2);
+    ++t_launches;
+  }
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  SL_CUDA_TRY(cudaGetLastError());
+  return SL_OK;
+}
+
+int32_t sl_tokenize(sl_vocab* vocab, const sl_tokenizer_config* cfg, int32_t build, const char* text,
+                    const uint64_t* doc_offsets, uint32_t num_docs, int32_t mem, sl_token_batch** out) {
+  return tokenize_impl(vocab, cfg, build, text, doc_offsets, num_docs, mem, out);
+}
+
+int32_t sl_token_batch_info(const sl_token_batch* b, uint32_t* num_docs, uint64_t* num_tokens,
+                            const uint64_t** d_offsets, const uint32_t** d_ids) {
+  if (!b) SL_FAIL(SL_EINVAL, "sl_token_batch_info: null batch");
+  if (num_docs) *num_docs = b->N;
+  if (num_tokens) *num_tokens = b->T;
+  if (d_offsets) *d_offsets = b->offs;
+  if (d_ids) *d_ids = b->ids;
+  return SL_OK;
+}
+
+int32_t sl_token_batch_copy(const sl_token_batch* b, uint64_t* offsets, uint32_t* ids) {
+  if (!b) SL_FAIL(SL_EINVAL, "sl_token_batch_copy: null batch");
+  SL_CUDA_TRY(cudaSetDevice(b->device));
+  if (offsets) SL_CUDA_TRY(cudaMemcpy(offsets, b->offs, (b->N + 1ull) * 8, cudaMemcpyDeviceToHost));
+  if (ids && b->T) SL_CUDA_TRY(cudaMemcpy(ids, b->ids, b->T * 4, cudaMemcpyDeviceToHost));
+  return SL_OK;
+}
+
+int32_t sl_token_batch_destroy(sl_token_batch* b) {
+  if (!b) return SL_OK;
+  cudaSetDevice(b->device);
+  if (b->offs) cudaFree(b->offs);
+  if (b->ids) cudaFree(b->ids);
+  delete b;
+  return SL_OK;
+}
+
+int32_t sl_stem_batch(const char* words, const uint64_t* offsets, uint32_t n, int32_t device, char* out,
+                      uint32_t* out_len) {
+  if (n && (!words || !offsets || !out || !out_len)) SL_FAIL(SL_EINVAL, "sl_stem_batch: null argument");
+  if (!n) return SL_OK;
+  cudaStream_t st;
+  SL_TRY(text_stream(device, &st));
+  TScratch scr(st);
+  const uint64_t nb = offsets[n];
+  uint8_t *din, *dout, *dsh;
+  uint64_t* doff;
+  uint32_t* dlen;
+  SL_TRY(scr.alloc(&din, nb));
+  SL_TRY(scr.alloc(&dout, nb));
+  SL_TRY(scr.alloc(&dsh, nb));
+  SL_TRY(scr.alloc(&doff, n + 1ull));
+  SL_TRY(scr.alloc(&dlen, n));
+  if (nb) SL_CUDA_TRY(cudaMemcpyAsync(din, words, nb, cudaMemcpyHostToDevice, st));
+  SL_CUDA_TRY(cudaMemcpyAsync(doff, offsets, (n + 1ull) * 8, cudaMemcpyHostToDevice, st));
+  k_stem_batch<<<grid_for(n, 128), 128, 0, st>>>(din, doff, n, dsh, dout, dlen); ++t_launches;
+  if (nb) SL_CUDA_TRY(cudaMemcpyAsync(out, dout, nb, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaMemcpyAsync(out_len, dlen, n * 4ull, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  SL_CUDA_TRY(cudaGetLastError());
+  return SL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,372 @@
+"""Text side of the SPEC API on the device (SPEC.md [MODULE] tokenizer).
+
+Mirrors the reference's tokenizer interface (proj/include/sparselex/tokenizer.hpp,
+stemmer.hpp, stopwords.hpp, vocabulary.hpp) over the C-ABI (sl_tokenize / sl_vocab_* /
+sl_stem_batch in include/sparselex_b200.h):
+
+  TokenizerConfig(lowercase, stopwords, stemmer), TokenizerConfig.english()
+  split_text(text, lowercase)            tokenizer.hpp:31-34
+  tokenize_build(texts, config, vocab)   tokenizer.hpp:36-39 (vocabulary grows, first-encounter ids)
+  tokenize_query(texts, config, vocab)   tokenizer.hpp:41-45 (frozen vocabulary, OOV dropped)
+  stem_english(word) / stem_batch(words) stemmer.hpp:16-18
+  english_stopwords(), load_stopwords(path), stopwords_hash(words)   stopwords.hpp:10-19
+  Vocabulary                             vocabulary.hpp:13-48
+  build_text_index(corpus, params, config) / retrieve_text(...)      SPEC build_index / retrieve
+
+All compute runs on the GPU; the only host work is argument marshalling.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import SL_MEM_DEVICE, SL_MEM_HOST, check, lib
+from .api import BM25Params, QueryResult, SearchIndex, load_index
+
+_DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+STOPWORDS_EN = os.path.join(_DATA, "stopwords_en.txt")
+
+
+class StemmerKind(enum.IntEnum):
+    """stemmer.hpp:8-11."""
+    none = 0
+    snowball_english = 1
+
+    @staticmethod
+    def from_string(name: str) -> "StemmerKind":  # stemmer.cpp:11-16
+        if name == "none":
+            return StemmerKind.none
+        if name in ("snowball-english", "snowball_english"):
+            return StemmerKind.snowball_english
+        raise ValueError(f"unknown stemmer: {name}")
+
+    def to_string(self) -> str:
+        return "none" if self == StemmerKind.none else "snowball-english"
+
+
+def load_stopwords(path: str) -> frozenset:
+    """stopwords.hpp:13-15: one lowercase token per line, UTF-8; blank and '#' lines ignored."""
+    out = set()
+    with open(path, encoding="utf-8") as f:
+        for line in f:
+            w = line.strip()
+            if w and not w.startswith("#"):
+                out.add(w)
+    return frozenset(out)
+
+
+def english_stopwords() -> frozenset:
+    """The bundled English list (env SPARSELEX_STOPWORDS overrides the path, SPEC cmd flags)."""
+    return load_stopwords(os.environ.get("SPARSELEX_STOPWORDS") or STOPWORDS_EN)
+
+
+def stopwords_hash(words) -> int:
+    """Order-independent hash of the set (stopwords.hpp:17-19): sum mod 2^64 of the FNV-1a-64
+    of each word's UTF-8 bytes."""
+    tot = 0
+    for w in words:
+        h = 0xCBF29CE484222325
+        for b in w.encode("utf-8"):
+            h = ((h ^ b) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+        tot = (tot + h) & 0xFFFFFFFFFFFFFFFF
+    return tot
+
+
+@dataclass
+class TokenizerConfig:
+    """tokenizer.hpp:16-23."""
+    lowercase: bool = True
+    stopwords: frozenset = field(default_factory=frozenset)
+    stemmer: StemmerKind = StemmerKind.none
+
+    @staticmethod
+    def english() -> "TokenizerConfig":
+        return TokenizerConfig(True, english_stopwords(), StemmerKind.snowball_english)
+
+    def to_c(self):
+        blob = "\n".join(sorted(self.stopwords)).encode("utf-8")
+        c = _lib.TokenizerConfig(int(bool(self.lowercase)), int(StemmerKind(self.stemmer)), blob or None, len(blob))
+        return c, blob
+
+    def to_json(self) -> dict:  # SPEC meta.json "tokenizer"
+        return {"lowercase": bool(self.lowercase), "stopwords_hash": stopwords_hash(self.stopwords),
+                "stemmer": StemmerKind(self.stemmer).to_string()}
+
+
+def _texts_to_csr(texts):
+    """list[str | bytes] -> (utf-8 bytes, u64 offsets[n+1])."""
+    if isinstance(texts, tuple) and len(texts) == 2:
+        return texts[0], np.ascontiguousarray(texts[1], np.uint64)
+    enc = [t.encode("utf-8") if isinstance(t, str) else bytes(t) for t in texts]
+    off = np.zeros(len(enc) + 1, np.uint64)
+    if enc:
+        off[1:] = np.cumsum([len(e) for e in enc])
+    return b"".join(enc), off
+
+
+class Vocabulary:
+    """Device-resident token <-> id map (vocabulary.hpp:13-48); ids in first-encounter order."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().sl_vocab_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self._cache = None
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise ValueError("Vocabulary is closed")
+        return self._h
+
+    def size(self) -> int:
+        n = C.c_uint32()
+        check(lib().sl_vocab_size(self.handle, C.byref(n)))
+        return n.value
+
+    __len__ = size
+
+    def tokens(self) -> list:
+        n = self.size()
+        if self._cache is not None and len(self._cache) == n:
+            return self._cache
+        off = np.empty(n + 1, np.uint64)
+        tot = C.c_uint64()
+        check(lib().sl_vocab_export(self.handle, None, None, C.byref(tot)))
+        buf = C.create_string_buffer(max(1, tot.value))
+        check(lib().sl_vocab_export(self.handle, off.ctypes.data, buf, C.byref(tot)))
+        raw = buf.raw
+        self._cache = [raw[off[i]:off[i + 1]].decode("utf-8") for i in range(n)]
+        return self._cache
+
+    def token(self, i: int) -> str:
+        return self.tokens()[i]
+
+    def lookup(self, token: str):
+        try:
+            return self.tokens().index(token)
+        except ValueError:
+            return None
+
+    @staticmethod
+    def from_tokens(tokens, device: int = 0) -> "Vocabulary":
+        v = Vocabulary(device)
+        enc = [t.encode("utf-8") for t in tokens]
+        off = np.zeros(len(enc) + 1, np.uint64)
+        if enc:
+            off[1:] = np.cumsum([len(e) for e in enc])
+        blob = b"".join(enc)
+        check(lib().sl_vocab_import(v.handle, off.ctypes.data, blob or b"\0", len(enc)))
+        return v
+
+    def close(self):
+        if self._h:
+            lib().sl_vocab_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TokenBatch:
+    """Tokenizer output on the device: document d's ids are ids[offsets[d]:offsets[d+1]]."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        n, t = C.c_uint32(), C.c_uint64()
+        po, pi = C.c_void_p(), C.c_void_p()
+        check(lib().sl_token_batch_info(self._h, C.byref(n), C.byref(t), C.byref(po), C.byref(pi)))
+        self.num_docs, self.num_tokens = n.value, t.value
+        self.d_offsets, self.d_ids = po.value, pi.value
+
+    def to_numpy(self):
+        off = np.empty(self.num_docs + 1, np.uint64)
+        ids = np.empty(max(1, self.num_tokens), np.uint32)
+        check(lib().sl_token_batch_copy(self._h, off.ctypes.data, ids.ctypes.data))
+        return off, ids[:self.num_tokens]
+
+    def lists(self):
+        off, ids = self.to_numpy()
+        return [ids[off[d]:off[d + 1]].tolist() for d in range(self.num_docs)]
+
+    def close(self):
+        if self._h:
+            lib().sl_token_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _tokenize(texts, config: TokenizerConfig, vocab: Vocabulary, build: bool, mem=None) -> TokenBatch:
+    text, off = _texts_to_csr(texts)
+    cfg, blob = config.to_c()
+    if mem == SL_MEM_DEVICE:  # (torch uint8 tensor, torch uint64 tensor) already on the device
+        tp, op = text.data_ptr(), off.data_ptr()
+        n = off.numel() - 1
+    else:
+        tb = np.frombuffer(text, np.uint8) if len(text) else np.zeros(1, np.uint8)
+        tp, op, n = tb.ctypes.data, off.ctypes.data, len(off) - 1
+        mem = SL_MEM_HOST
+    h = C.c_void_p()
+    check(lib().sl_tokenize(vocab.handle, C.byref(cfg), int(build), tp, op, n, mem, C.byref(h)))
+    return TokenBatch(h.value)
+
+
+def tokenize_build(texts, config: TokenizerConfig, vocab: Vocabulary, mem=None) -> TokenBatch:
+    """tokenize_build for every text in order (the vocabulary grows in first-encounter order)."""
+    return _tokenize(texts, config, vocab, True, mem)
+
+
+def tokenize_query(texts, config: TokenizerConfig, vocab: Vocabulary, mem=None) -> TokenBatch:
+    """tokenize_query for every text (frozen vocabulary; out-of-vocabulary tokens dropped)."""
+    return _tokenize(texts, config, vocab, False, mem)
+
+
+def split_text(text: str | bytes, lowercase: bool = True) -> list:
+    """split_text (tokenizer.hpp:31-34): maximal runs of >= 2 word codepoints, in order."""
+    v = Vocabulary()
+    b = tokenize_build([text], TokenizerConfig(lowercase), v)
+    toks = v.tokens()
+    out = [toks[i] for i in b.lists()[0]]
+    b.close()
+    v.close()
+    return out
+
+
+def stem_batch(words, device: int = 0) -> list:
+    """stem_english for each word (stemmer.hpp:16-18), on the device."""
+    enc = [w.encode("utf-8") if isinstance(w, str) else bytes(w) for w in words]
+    if not enc:
+        return []
+    off = np.zeros(len(enc) + 1, np.uint64)
+    off[1:] = np.cumsum([len(e) for e in enc])
+    blob = b"".join(enc) or b"\0"
+    out = C.create_string_buffer(max(1, len(blob)))
+    ln = np.empty(len(enc), np.uint32)
+    check(lib().sl_stem_batch(blob, off.ctypes.data, len(enc), device, out, ln.ctypes.data))
+    raw = out.raw
+    res = [raw[int(off[i]):int(off[i]) + int(ln[i])] for i in range(len(enc))]
+    return [r.decode("utf-8", errors="surrogateescape") if isinstance(w, str) else r for r, w in zip(res, words)]
+
+
+def stem_english(word: str) -> str:
+    return stem_batch([word])[0]
+
+
+# ---------------------------------------------------------------- text-level index (SPEC build_index)
+class TextIndex:
+    """SPEC SearchIndex with its vocabulary, tokenizer config and external document ids."""
+
+    def __init__(self, index: SearchIndex, vocab: Vocabulary, config: TokenizerConfig, doc_ids, params):
+        self.index, self.vocab, self.config, self.doc_ids, self.params = index, vocab, config, list(doc_ids), params
+
+    def save(self, directory: str) -> None:
+        """SPEC save_index (9 files): the device arrays via sl_index_save, then the text
+        metadata the token-id layout leaves generic (vocab.json tokens, docs.json ids,
+        meta.json tokenizer)."""
+        self.index.save(directory)
+        toks = self.vocab.tokens()
+        with open(os.path.join(directory, "vocab.json"), "w", encoding="utf-8") as f:
+            json.dump({t: i for i, t in enumerate(toks)}, f, ensure_ascii=False)
+        with open(os.path.join(directory, "docs.json"), "w", encoding="utf-8") as f:
+            json.dump(self.doc_ids, f, ensure_ascii=False)
+        mp = os.path.join(directory, "meta.json")
+        with open(mp, encoding="utf-8") as f:
+            meta = json.load(f)
+        meta["tokenizer"] = self.config.to_json()
+        meta["stopwords"] = sorted(self.config.stopwords)  # lets load_text_index restore the set
+        meta.pop("input", None)
+        with open(mp, "w", encoding="utf-8") as f:
+            json.dump(meta, f, indent=1)
+
+
+def build_text_index(corpus, params: BM25Params | None = None, config: TokenizerConfig | None = None, *,
+                     device: int = 0, dense_min_density: float = 0.0) -> TextIndex:
+    """SPEC build_index(corpus: sequence of (external_id, text), params, tokenizer_config).
+
+    Errors as the SPEC: empty corpus; every document tokenizing to nothing ("degenerate
+    corpus"); duplicate external ids."""
+    params = params or BM25Params()
+    config = config or TokenizerConfig.english()
+    corpus = list(corpus)
+    if not corpus:
+        raise ValueError("build_index: empty corpus")
+    ids = [c[0] for c in corpus]
+    if len(set(ids)) != len(ids):
+        raise ValueError("build_index: duplicate external ids")
+    vocab = Vocabulary(device)
+    batch = tokenize_build([c[1] for c in corpus], config, vocab)
+    if batch.num_tokens == 0:
+        raise ValueError("build_index: degenerate corpus (every document tokenizes to empty)")
+    d = _lib.BuildDesc()
+    d.doc_offsets, d.token_ids = batch.d_offsets, batch.d_ids
+    d.num_docs, d.vocab_size, d.doc_base, d.mem = batch.num_docs, vocab.size(), 0, SL_MEM_DEVICE
+    d.params = params.to_c()
+    d.device, d.keep_tf, d.dense_min_density = device, 0, float(dense_min_density)
+    h = C.c_void_p()
+    check(lib().sl_index_build(C.byref(d), C.byref(h)))
+    batch.close()
+    return TextIndex(SearchIndex(h.value, device), vocab, config, ids, params)
+
+
+def load_text_index(directory: str, *, device: int = 0) -> TextIndex:
+    """SPEC load_index for an index saved by TextIndex.save."""
+    index = load_index(directory, device=device)
+    with open(os.path.join(directory, "vocab.json"), encoding="utf-8") as f:
+        vj = json.load(f)
+    toks = [None] * len(vj)
+    for t, i in vj.items():
+        toks[i] = t
+    with open(os.path.join(directory, "docs.json"), encoding="utf-8") as f:
+        doc_ids = json.load(f)
+    with open(os.path.join(directory, "meta.json"), encoding="utf-8") as f:
+        meta = json.load(f)
+    tk = meta.get("tokenizer", {})
+    cfg = TokenizerConfig(bool(tk.get("lowercase", True)), frozenset(meta.get("stopwords", [])),
+                          StemmerKind.from_string(tk.get("stemmer", "none")))
+    if stopwords_hash(cfg.stopwords) != int(tk.get("stopwords_hash", stopwords_hash(cfg.stopwords))):
+        raise ValueError("load_index: stopword configuration does not match the index")
+    return TextIndex(index, Vocabulary.from_tokens(toks, device), cfg, doc_ids, None)
+
+
+def retrieve_text_batch(tindex: TextIndex, queries, k: int, ordered: bool = True, workers: int = 1):
+    """SPEC retrieve_batch over query texts: tokenize_query with the index's config and frozen
+    vocabulary (on the device), then score + top-k; doc_ids maps to external ids."""
+    if workers < 1:
+        raise ValueError("retrieve_batch: workers must be >= 1")
+    if k <= 0:
+        raise ValueError("top_k: k must be >= 1")
+    qb = tokenize_query(queries, tindex.config, tindex.vocab)
+    B = qb.num_docs
+    ids = np.empty((B, k), np.uint32)
+    sc = np.empty((B, k), np.float32)
+    # token ids are on the device; results come back to the host
+    import torch  # device output buffers (torch is the allocator, not the compute)
+    dids = torch.empty((B, k), dtype=torch.uint32, device=f"cuda:{tindex.index.device}")
+    dsc = torch.empty((B, k), dtype=torch.float32, device=f"cuda:{tindex.index.device}")
+    check(lib().sl_retrieve_batch(tindex.index.handle, qb.d_offsets, qb.d_ids or qb.d_offsets, B, k, int(ordered),
+                                  SL_MEM_DEVICE, dids.data_ptr(), dsc.data_ptr()))
+    ids[:] = dids.cpu().numpy()
+    sc[:] = dsc.cpu().numpy()
+    qb.close()
+    m = min(k, tindex.index.num_docs)
+    return [QueryResult(ids[b, :m].copy(), sc[b, :m].copy()) for b in range(B)]
+
+
+def retrieve_text(tindex: TextIndex, text: str, k: int, ordered: bool = True) -> QueryResult:
+    """SPEC retrieve(index, text, k, ordered)."""
+    return retrieve_text_batch(tindex, [text], k, ordered)[0]

@@ -13,7 +13,7 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the CUDA C-ABI)")
     config.addinivalue_line("markers", "slow: large-config parity (minutes)")
     # the CPU checker and the libraries are built by __graft_entry__.build(); build here only if absent
-    need = [os.path.join(ROOT, "oracle", "liboracle.so"),
+    need = [os.path.join(ROOT, "oracle", "liboracle.so"), os.path.join(ROOT, "oracle", "liboracle_text.so"),
             os.path.join(ROOT, "paper_2407_03618_b200", "libsparselex_b200.so"),
             os.path.join(ROOT, "paper_2407_03618_b200", "libsl_synth.so")]
     if not all(os.path.exists(p) for p in need):

@@ -1,0 +1,207 @@
+"""Device text pipeline (sl_tokenize / sl_stem_batch) against the
+reference's golden fixtures and the CPU oracle (oracle/text_oracle.cpp, itself pinned to the
+reference compiled in place). Token ids, per-document token offsets and the vocabulary (its
+strings in id order) must be identical."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.text import TextOracle, bundled_stopwords
+from paper_2407_03618_b200 import BM25Params, Variant
+from paper_2407_03618_b200 import text as T
+from paper_2407_03618_b200._lib import SparselexError
+from tests.helpers import assert_topk_match, query_scale
+from tests.text_words import make_corpus, make_words
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "text_golden.json")
+CONFIGS = [(True, False, False), (True, True, False), (True, False, True), (True, True, True), (False, False, True)]
+
+
+def cfg_of(lc, stop, stem):
+    return T.TokenizerConfig(bool(lc), frozenset(bundled_stopwords()) if stop else frozenset(),
+                             T.StemmerKind.snowball_english if stem else T.StemmerKind.none)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN, encoding="utf-8") as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def port():
+    return TextOracle("port")
+
+
+def gpu_tokenize(text, off, lc, stop, stem, vocab=None):
+    v = vocab if vocab is not None else T.Vocabulary()
+    b = T.tokenize_build((text, off), cfg_of(lc, stop, stem), v)
+    toff, ids = b.to_numpy()
+    b.close()
+    return toff, ids, v.tokens(), v
+
+
+def test_ac4_golden(cuda_ok, golden):
+    texts = [bytes.fromhex(r["text_hex"]) for r in golden["ac4"]]
+    for ci, (lc, stop, stem) in enumerate(golden["configs"]):
+        v = T.Vocabulary()
+        lists = T.tokenize_build(texts, cfg_of(lc, stop, stem), v).lists()
+        toks = v.tokens()
+        for row, ids in zip(golden["ac4"], lists):
+            assert [toks[i] for i in ids] == row["tokens"][ci], (bytes.fromhex(row["text_hex"]), lc, stop, stem)
+
+
+def test_stems_golden(cuda_ok, golden):
+    words = [w for w, _ in golden["stems"]]
+    assert T.stem_batch(words) == [s for _, s in golden["stems"]]
+
+
+def test_stems_vs_oracle(cuda_ok, port):
+    words = make_words(100000, seed=33, unicode_frac=0.1)
+    words = words + [w.upper() for w in words[:5000]] + ["'" + w for w in words[:5000]] + [w + "'s" for w in words[:5000]]
+    got = T.stem_batch(words)
+    want = [port.stem(w).decode("utf-8") for w in words]
+    bad = [(w, g, x) for w, g, x in zip(words, got, want) if g != x]
+    assert not bad, bad[:10]
+    # malformed input comes back unchanged (stemmer.cpp:393)
+    raw = [b"ab\xffcd", b"\xc3", b"runn\xe2\x82ing"]
+    assert T.stem_batch(raw) == [port.stem(r) for r in raw]
+
+
+@pytest.mark.parametrize("lc,stop,stem", CONFIGS)
+def test_corpus_vs_oracle(cuda_ok, port, lc, stop, stem):
+    words = make_words(6000, seed=12, unicode_frac=0.08)
+    text, off = make_corpus(4000, words, seed=8, malformed_frac=0.02, case_frac=0.3)
+    a = gpu_tokenize(text, off, lc, stop, stem)
+    b = port.tokenize_corpus(text, off, lc, stop, stem)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[1], b[1])
+    assert a[2] == b[2]
+
+
+def test_incremental_and_query(cuda_ok, port):
+    """Two build calls share one vocabulary (ids continue in first-encounter order); query
+    mode drops out-of-vocabulary tokens."""
+    words = make_words(3000, seed=41)
+    t1, o1 = make_corpus(700, words[:2000], seed=1)
+    t2, o2 = make_corpus(500, words, seed=2)
+    v = T.Vocabulary()
+    g1 = gpu_tokenize(t1, o1, 1, 1, 1, v)
+    g2 = gpu_tokenize(t2, o2, 1, 1, 1, v)
+    ov = port.vocab_new()
+    want1 = [port.tokenize(ov, t1[o1[d]:o1[d + 1]], True, 1, 1, 1) for d in range(len(o1) - 1)]
+    want2 = [port.tokenize(ov, t2[o2[d]:o2[d + 1]], True, 1, 1, 1) for d in range(len(o2) - 1)]
+    assert [g1[1][g1[0][d]:g1[0][d + 1]].tolist() for d in range(len(o1) - 1)] == want1
+    assert [g2[1][g2[0][d]:g2[0][d + 1]].tolist() for d in range(len(o2) - 1)] == want2
+    assert v.tokens() == port.vocab_tokens(ov)
+    # query mode against the frozen vocabulary
+    words_q = words + make_words(500, seed=99)  # some unseen words
+    tq, oq = make_corpus(300, words_q, seed=5, mean_words=6)
+    qb = T.tokenize_query((tq, oq), cfg_of(1, 1, 1), v)
+    lists = qb.lists()
+    assert len(v.tokens()) == len(port.vocab_tokens(ov))  # frozen
+    for d in range(len(oq) - 1):
+        assert lists[d] == port.tokenize(ov, tq[oq[d]:oq[d + 1]], False, 1, 1, 1)
+    port.vocab_free(ov)
+
+
+def test_edges(cuda_ok, port):
+    long_word = "Internationalizations" * 5  # > 64 bytes: the global-scratch path
+    docs = [b"", b"a", b"  ..  ", b"ab", long_word.encode(), ("Ü" * 40 + "ing").encode(), b"caf\xc3",
+            b"\xa9abc d\xc3\xa9f", b"the and of", b"x" * 200, "Ǆ" * 70, b"\xf0\x9f", b"\x98\x80 ok"]
+    docs = [d.encode() if isinstance(d, str) else d for d in docs]
+    off = np.zeros(len(docs) + 1, np.uint64)
+    off[1:] = np.cumsum([len(d) for d in docs])
+    text = b"".join(docs)
+    for lc, stop, stem in CONFIGS:
+        a = gpu_tokenize(text, off, lc, stop, stem)
+        b = port.tokenize_corpus(text, off, lc, stop, stem)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2], (lc, stop, stem)
+    # no documents / no tokens at all
+    v = T.Vocabulary()
+    b = T.tokenize_build([], cfg_of(1, 0, 0), v)
+    assert b.num_docs == 0 and b.num_tokens == 0
+    b = T.tokenize_build(["", "!", "a b"], cfg_of(1, 0, 0), v)
+    assert b.lists() == [[], [], []] and v.size() == 0
+
+
+def test_split_and_spec_examples(cuda_ok):
+    assert T.split_text("Hello, World! a_b x") == ["hello", "world", "a_b"]
+    assert T.split_text("Hello World", lowercase=False) == ["Hello", "World"]
+    # SPEC.md:65-67
+    cfg = T.TokenizerConfig(True, frozenset({"the", "is"}), T.StemmerKind.snowball_english)
+    v = T.Vocabulary()
+    ids = T.tokenize_build(["the cat is running"], cfg, v).lists()[0]
+    assert [v.token(i) for i in ids] == ["cat", "run"]
+    ids = T.tokenize_build(["cat cat"], T.TokenizerConfig(), v).lists()[0]
+    assert ids[0] == ids[1]
+    assert T.tokenize_query(["zebra"], T.TokenizerConfig(), v).lists() == [[]]
+    assert T.StemmerKind.from_string("snowball-english") == T.StemmerKind.snowball_english
+    with pytest.raises(ValueError, match="unknown stemmer"):
+        T.StemmerKind.from_string("porter")
+
+
+def test_text_index_retrieval_vs_oracle(cuda_ok, port, tmp_path):
+    """SPEC build_index(corpus texts) + retrieve(text): GPU tokenization + index + top-k
+    against the oracle tokenizer feeding the oracle index."""
+    words = make_words(5000, seed=77)
+    text, off = make_corpus(3000, words, seed=6, mean_words=40)
+    corpus = [(f"d{d}", text[off[d]:off[d + 1]].decode("utf-8")) for d in range(len(off) - 1)]
+    cfg = T.TokenizerConfig.english()
+    p = BM25Params.for_variant(Variant.bm25plus)
+    ti = T.build_text_index(corpus, p, cfg)
+    toff, tids, toks = port.tokenize_corpus(text, off, 1, 1, 1)
+    assert ti.vocab.tokens() == toks
+    oi = oracle.OracleIndex(toff, tids, len(toks), int(p.variant), p.k1, p.b, p.delta)
+    exp = oi.export()
+    g = ti.index.export()
+    for key in ("indptr", "docids", "df", "doclens"):
+        assert np.array_equal(g[key], exp[key]), key
+    qtext, qoff = make_corpus(200, words + ["unseenword"], seed=9, mean_words=5)
+    queries = [qtext[qoff[q]:qoff[q + 1]].decode("utf-8") for q in range(len(qoff) - 1)]
+    res = T.retrieve_text_batch(ti, queries, 10)
+    ov = port.vocab_new()
+    port.tokenize_corpus(text, off, 1, 1, 1, vocab=ov)
+    qlists = [port.tokenize(ov, q, False, 1, 1, 1) for q in queries]
+    port.vocab_free(ov)
+    qo = np.zeros(len(qlists) + 1, np.uint64)
+    qo[1:] = np.cumsum([len(q) for q in qlists])
+    qt = np.array([t for q in qlists for t in q] or [0], np.uint32)
+    rid, rsc = oi.retrieve_batch(qo, qt, 10)
+    gid = np.stack([r.doc_indices for r in res])
+    gsc = np.stack([r.scores for r in res])
+    assert_topk_match(gid, gsc, rid, rsc, 10, len(corpus), lambda b: oi.score_query(qlists[b]),
+                      lambda b: query_scale(exp, qlists[b]), "text")
+    # save / load roundtrip answers identically
+    ti.save(str(tmp_path / "ix"))
+    with open(tmp_path / "ix" / "vocab.json", encoding="utf-8") as f:
+        assert json.load(f) == {t: i for i, t in enumerate(toks)}
+    tl = T.load_text_index(str(tmp_path / "ix"))
+    assert tl.doc_ids == [c[0] for c in corpus] and tl.vocab.tokens() == toks
+    res2 = T.retrieve_text_batch(tl, queries, 10)
+    for a, b in zip(res, res2):
+        assert np.array_equal(a.doc_indices, b.doc_indices) and np.array_equal(a.scores, b.scores)
+
+
+def test_text_index_errors(cuda_ok):
+    with pytest.raises(ValueError, match="empty corpus"):
+        T.build_text_index([])
+    with pytest.raises(ValueError, match="duplicate external ids"):
+        T.build_text_index([("a", "x y"), ("a", "z w")])
+    with pytest.raises(ValueError, match="degenerate corpus"):
+        T.build_text_index([("a", "the"), ("b", "! ?")])
+    import ctypes as C
+    from paper_2407_03618_b200 import _lib
+    v = T.Vocabulary()
+    bad = _lib.TokenizerConfig(1, 7, None, 0)
+    h = C.c_void_p()
+    off = np.array([0, 2], np.uint64)
+    with pytest.raises(SparselexError, match="unknown stemmer"):
+        _lib.check(_lib.lib().sl_tokenize(v.handle, C.byref(bad), 1, b"ab", off.ctypes.data, 1, 0, C.byref(h)))
+    off = np.array([1, 2], np.uint64)
+    with pytest.raises(ValueError, match="doc_offsets"):
+        T.tokenize_build((b"ab", off), T.TokenizerConfig(), v)
