@@ -29,6 +29,7 @@
 #define SL_STREAM_QLEN 3u
 #define SL_STREAM_QTOK 4u
 #define SL_STREAM_QHEAD 5u
+#define SL_STREAM_TEXT 6u
 
 SL_HD void sl_mulhilo32(uint32_t a, uint32_t b, uint32_t* hi, uint32_t* lo) {
   uint64_t p = (uint64_t)a * (uint64_t)b;

@@ -30,6 +30,7 @@
 //   query mode      tokens absent from the frozen vocabulary are dropped (SPEC OOV rule)
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -296,35 +297,50 @@ __global__ void k_tokens(const uint32_t* __restrict__ wbits, const uint32_t* __r
 
 // ------------------------------------------------------------------ stemmer (shadow form)
 // w: one byte per codepoint (ASCII as itself, anything else 0x80). Restates the
-// reference's stemmer.cpp:125-391 step by step; returns the new length.
+// reference's stemmer.cpp:125-391 step by step; returns the new length. Suffix tests run on
+// a register copy of the last 8 symbols (byte k = w[n-1-k]) against compile-time packed
+// constants, so each test is one AND + one compare.
 __device__ __forceinline__ bool sv(uint8_t c) { return c == 'a' || c == 'e' || c == 'i' || c == 'o' || c == 'u' || c == 'y'; }
 
 template <int M>
-__device__ __forceinline__ bool ends(const uint8_t* w, int n, const char (&s)[M]) {
-  constexpr int m = M - 1;
-  if (n < m) return false;
-#pragma unroll
-  for (int i = 0; i < m; ++i)
-    if (w[n - m + i] != (uint8_t)s[i]) return false;
-  return true;
+__host__ __device__ constexpr uint64_t pk(const char (&s)[M]) {
+  uint64_t v = 0;
+  for (int k = 0; k < M - 1; ++k) v |= (uint64_t)(uint8_t)s[M - 2 - k] << (8 * k);
+  return v;
 }
-template <int M>
-__device__ __forceinline__ bool same(const uint8_t* w, int n, const char (&s)[M]) {
-  return n == M - 1 && ends(w, n, s);
+__host__ __device__ constexpr uint64_t lenmask(int m) { return m >= 8 ? ~0ull : ((1ull << (8 * m)) - 1ull); }
+
+__device__ __forceinline__ uint64_t tail8(const uint8_t* w, int n) {
+  uint64_t t = 0;
+  const int m = n < 8 ? n : 8;
+  for (int k = 0; k < m; ++k) t |= (uint64_t)w[n - 1 - k] << (8 * k);
+  return t;
 }
-template <int M, int R>
-__device__ __forceinline__ int tail(uint8_t* w, int n, const char (&s)[M], const char (&r)[R]) {
-  n -= M - 1;
-#pragma unroll
-  for (int i = 0; i < R - 1; ++i) w[n + i] = (uint8_t)r[i];
-  return n + R - 1;
-}
-// "first listed suffix decides": matched -> replace when the suffix starts in the region
-#define SL_RULE(S, R, LIM)                                  \
-  if (ends(w, n, S)) {                                       \
-    if (n - (int)(sizeof(S) - 1) >= (LIM)) n = tail(w, n, S, R); \
-    goto done_##LIM##_rules;                                 \
-  }
+
+// compile-time constants for a literal suffix
+#define SL_PK(S) (std::integral_constant<uint64_t, pk(S)>::value)
+#define SL_MK(S) (std::integral_constant<uint64_t, lenmask((int)sizeof(S) - 1)>::value)
+#define ENDS(S) (n >= (int)sizeof(S) - 1 && (t & SL_MK(S)) == SL_PK(S))
+#define SAME(S) (n == (int)sizeof(S) - 1 && (t & SL_MK(S)) == SL_PK(S))
+#define SYNC() (t = tail8(w, n))
+#define REPL(S, R)                                                    \
+  do {                                                                \
+    n -= (int)sizeof(S) - 1;                                          \
+    for (int i_ = 0; i_ < (int)sizeof(R) - 1; ++i_) w[n + i_] = (uint8_t)(R)[i_]; \
+    n += (int)sizeof(R) - 1;                                          \
+    SYNC();                                                           \
+  } while (0)
+#define CUT(M)  \
+  do {          \
+    n -= (M);   \
+    SYNC();     \
+  } while (0)
+#define PUSH(C)                        \
+  do {                                 \
+    w[n++] = (uint8_t)(C);             \
+    t = (t << 8) | (uint64_t)(uint8_t)(C); \
+  } while (0)
+#define LAST(K) ((uint8_t)(t >> (8 * (K))))
 
 __device__ __forceinline__ bool vowel_before(const uint8_t* w, int end) {
   for (int i = 0; i < end; ++i)
@@ -351,17 +367,20 @@ __device__ __forceinline__ bool li_end(uint8_t c) {
 __device__ int stem_shadow(uint8_t* w, int n, int* shift, bool* ymark) {
   *shift = 0;
   *ymark = false;
+  uint64_t t;
+  SYNC();
   // irregular forms (stemmer.cpp:162-186), checked on the whole word before the prelude
-#define SL_IRR(F, T)          \
-  if (same(w, n, F)) {        \
-    return tail(w, n, F, T);  \
+#define SL_IRR(F, T)                                                        \
+  if (SAME(F)) {                                                            \
+    for (int i_ = 0; i_ < (int)sizeof(T) - 1; ++i_) w[i_] = (uint8_t)(T)[i_]; \
+    return (int)sizeof(T) - 1;                                              \
   }
   SL_IRR("skis", "ski") SL_IRR("skies", "sky") SL_IRR("dying", "die") SL_IRR("lying", "lie")
   SL_IRR("tying", "tie") SL_IRR("idly", "idl") SL_IRR("gently", "gentl") SL_IRR("ugly", "ugli")
   SL_IRR("early", "earli") SL_IRR("only", "onli") SL_IRR("singly", "singl")
 #undef SL_IRR
-  if (same(w, n, "sky") || same(w, n, "news") || same(w, n, "howe") || same(w, n, "atlas") ||
-      same(w, n, "cosmos") || same(w, n, "bias") || same(w, n, "andes"))
+  if (SAME("sky") || SAME("news") || SAME("howe") || SAME("atlas") || SAME("cosmos") || SAME("bias") ||
+      SAME("andes"))
     return n;
   // prelude
   if (n > 0 && w[0] == '\'') {
@@ -380,6 +399,7 @@ __device__ int stem_shadow(uint8_t* w, int n, int* shift, bool* ymark) {
       ym = true;
     }
   *ymark = ym;
+  SYNC();
   // regions (stemmer.cpp:204-226; R1 starts AT the first non-vowel after a vowel)
   int r1 = n, r2 = n;
   {
@@ -401,111 +421,119 @@ __device__ int stem_shadow(uint8_t* w, int n, int* shift, bool* ymark) {
     }
   }
   // step 0
-  if (ends(w, n, "'s'")) n -= 3;
-  else if (ends(w, n, "'s")) n -= 2;
-  else if (ends(w, n, "'")) n -= 1;
+  if (ENDS("'s'")) CUT(3);
+  else if (ENDS("'s")) CUT(2);
+  else if (ENDS("'")) CUT(1);
   // step 1a
-  if (ends(w, n, "sses")) {
-    n = tail(w, n, "sses", "ss");
-  } else if (ends(w, n, "ied") || ends(w, n, "ies")) {
-    if (n >= 5) n = tail(w, n, "ies", "i");
-    else n = tail(w, n, "ies", "ie");
-  } else if (ends(w, n, "us") || ends(w, n, "ss")) {
-  } else if (ends(w, n, "s")) {
-    if (n >= 3 && vowel_before(w, n - 2)) --n;
+  if (ENDS("sses")) {
+    REPL("sses", "ss");
+  } else if (ENDS("ied") || ENDS("ies")) {
+    if (n >= 5) REPL("ies", "i");
+    else REPL("ies", "ie");
+  } else if (ENDS("us") || ENDS("ss")) {
+  } else if (ENDS("s")) {
+    if (n >= 3 && vowel_before(w, n - 2)) CUT(1);
   }
-  if (same(w, n, "inning") || same(w, n, "outing") || same(w, n, "canning") || same(w, n, "herring") ||
-      same(w, n, "earring") || same(w, n, "proceed") || same(w, n, "exceed") || same(w, n, "succeed"))
+  if (SAME("inning") || SAME("outing") || SAME("canning") || SAME("herring") || SAME("earring") ||
+      SAME("proceed") || SAME("exceed") || SAME("succeed"))
     return n;
   // step 1b
-  if (ends(w, n, "eedly") || ends(w, n, "eed")) {
-    const int m = ends(w, n, "eedly") ? 5 : 3;
+  if (ENDS("eedly") || ENDS("eed")) {
+    const int m = ENDS("eedly") ? 5 : 3;
     if (n - m >= r1) {
-      n -= m;
-      w[n] = 'e';
-      w[n + 1] = 'e';
-      n += 2;
+      CUT(m);
+      PUSH('e');
+      PUSH('e');
     }
   } else {
     int m = 0;
-    if (ends(w, n, "ingly")) m = 5;
-    else if (ends(w, n, "edly")) m = 4;
-    else if (ends(w, n, "ing")) m = 3;
-    else if (ends(w, n, "ed")) m = 2;
+    if (ENDS("ingly")) m = 5;
+    else if (ENDS("edly")) m = 4;
+    else if (ENDS("ing")) m = 3;
+    else if (ENDS("ed")) m = 2;
     if (m && vowel_before(w, n - m)) {
-      n -= m;
-      if (ends(w, n, "at") || ends(w, n, "bl") || ends(w, n, "iz")) {
-        w[n++] = 'e';
-      } else if (n >= 2 && w[n - 1] == w[n - 2] && is_dbl(w[n - 1])) {
-        --n;
+      CUT(m);
+      if (ENDS("at") || ENDS("bl") || ENDS("iz")) {
+        PUSH('e');
+      } else if (n >= 2 && LAST(0) == LAST(1) && is_dbl(LAST(0))) {
+        CUT(1);
       } else if (n == r1 && short_syl(w, n)) {
-        w[n++] = 'e';
+        PUSH('e');
       }
     }
   }
   // step 1c
-  if (n >= 3 && (w[n - 1] == 'y' || w[n - 1] == 'Y') && !sv(w[n - 2])) w[n - 1] = 'i';
-  // step 2 (R1)
-  {
-    SL_RULE("ization", "ize", r1) SL_RULE("ational", "ate", r1) SL_RULE("fulness", "ful", r1)
-    SL_RULE("ousness", "ous", r1) SL_RULE("iveness", "ive", r1) SL_RULE("tional", "tion", r1)
-    SL_RULE("biliti", "ble", r1) SL_RULE("lessli", "less", r1) SL_RULE("entli", "ent", r1)
-    SL_RULE("fulli", "ful", r1) SL_RULE("ation", "ate", r1) SL_RULE("alism", "al", r1)
-    SL_RULE("aliti", "al", r1) SL_RULE("ousli", "ous", r1) SL_RULE("iviti", "ive", r1)
-    SL_RULE("enci", "ence", r1) SL_RULE("anci", "ance", r1) SL_RULE("abli", "able", r1)
-    SL_RULE("izer", "ize", r1) SL_RULE("ator", "ate", r1) SL_RULE("alli", "al", r1)
-    SL_RULE("bli", "ble", r1)
-    if (ends(w, n, "ogi")) {
-      const int s = n - 3;
-      if (s >= r1 && s >= 1 && w[s - 1] == 'l') n = tail(w, n, "ogi", "og");
-    } else if (ends(w, n, "li")) {
-      const int s = n - 2;
-      if (s >= r1 && s >= 1 && li_end(w[s - 1])) n = s;
-    }
+  if (n >= 3 && (LAST(0) == 'y' || LAST(0) == 'Y') && !sv(LAST(1))) {
+    w[n - 1] = 'i';
+    t = (t & ~0xFFull) | 'i';
   }
-done_r1_rules:
+  // steps 2 and 3 (R1): the first listed suffix that matches decides
+#define SL_RULE(S, R, DONE)                        \
+  if (ENDS(S)) {                                   \
+    if (n - (int)(sizeof(S) - 1) >= r1) REPL(S, R); \
+    goto DONE;                                     \
+  }
+  SL_RULE("ization", "ize", done_step2) SL_RULE("ational", "ate", done_step2)
+  SL_RULE("fulness", "ful", done_step2) SL_RULE("ousness", "ous", done_step2)
+  SL_RULE("iveness", "ive", done_step2) SL_RULE("tional", "tion", done_step2)
+  SL_RULE("biliti", "ble", done_step2) SL_RULE("lessli", "less", done_step2)
+  SL_RULE("entli", "ent", done_step2) SL_RULE("fulli", "ful", done_step2) SL_RULE("ation", "ate", done_step2)
+  SL_RULE("alism", "al", done_step2) SL_RULE("aliti", "al", done_step2) SL_RULE("ousli", "ous", done_step2)
+  SL_RULE("iviti", "ive", done_step2) SL_RULE("enci", "ence", done_step2) SL_RULE("anci", "ance", done_step2)
+  SL_RULE("abli", "able", done_step2) SL_RULE("izer", "ize", done_step2) SL_RULE("ator", "ate", done_step2)
+  SL_RULE("alli", "al", done_step2) SL_RULE("bli", "ble", done_step2)
+  if (ENDS("ogi")) {
+    const int s = n - 3;
+    if (s >= r1 && s >= 1 && LAST(3) == 'l') REPL("ogi", "og");
+  } else if (ENDS("li")) {
+    const int s = n - 2;
+    if (s >= r1 && s >= 1 && li_end(LAST(2))) CUT(2);
+  }
+done_step2:
   // step 3
-  if (ends(w, n, "ative")) {
+  if (ENDS("ative")) {
     const int s = n - 5;
-    if (s >= r1 && s >= r2) n = s;
+    if (s >= r1 && s >= r2) CUT(5);
   } else {
-#define SL_RULE3(S, R)                                    \
-  if (ends(w, n, S)) {                                     \
-    if (n - (int)(sizeof(S) - 1) >= r1) n = tail(w, n, S, R); \
-    goto done_step3;                                       \
+    SL_RULE("ational", "ate", done_step3) SL_RULE("tional", "tion", done_step3)
+    SL_RULE("alize", "al", done_step3) SL_RULE("icate", "ic", done_step3) SL_RULE("iciti", "ic", done_step3)
+    SL_RULE("ical", "ic", done_step3) SL_RULE("ness", "", done_step3) SL_RULE("ful", "", done_step3)
   }
-    SL_RULE3("ational", "ate") SL_RULE3("tional", "tion") SL_RULE3("alize", "al") SL_RULE3("icate", "ic")
-    SL_RULE3("iciti", "ic") SL_RULE3("ical", "ic") SL_RULE3("ness", "") SL_RULE3("ful", "")
-#undef SL_RULE3
-  }
+#undef SL_RULE
 done_step3:
   // step 4 (R2)
-  if (ends(w, n, "ement")) {
-    if (n - 5 >= r2) n -= 5;
-  } else if (ends(w, n, "ion")) {
+  if (ENDS("ement")) {
+    if (n - 5 >= r2) CUT(5);
+  } else if (ENDS("ion")) {
     const int s = n - 3;
-    if (s >= r2 && s >= 1 && (w[s - 1] == 's' || w[s - 1] == 't')) n = s;
+    if (s >= r2 && s >= 1 && (LAST(3) == 's' || LAST(3) == 't')) CUT(3);
   } else {
-#define SL_DEL4(S)                                  \
-  if (ends(w, n, S)) {                               \
-    if (n - (int)(sizeof(S) - 1) >= r2) n -= sizeof(S) - 1; \
-    goto done_step4;                                 \
+#define SL_DEL4(S)                                        \
+  if (ENDS(S)) {                                          \
+    if (n - (int)(sizeof(S) - 1) >= r2) CUT((int)sizeof(S) - 1); \
+    goto done_step4;                                      \
   }
-    SL_DEL4("ement") SL_DEL4("ance") SL_DEL4("ence") SL_DEL4("able") SL_DEL4("ible") SL_DEL4("ment")
-    SL_DEL4("ant") SL_DEL4("ent") SL_DEL4("ism") SL_DEL4("ate") SL_DEL4("iti") SL_DEL4("ous")
-    SL_DEL4("ive") SL_DEL4("ize") SL_DEL4("al") SL_DEL4("er") SL_DEL4("ic")
+    SL_DEL4("ance") SL_DEL4("ence") SL_DEL4("able") SL_DEL4("ible") SL_DEL4("ment") SL_DEL4("ant")
+    SL_DEL4("ent") SL_DEL4("ism") SL_DEL4("ate") SL_DEL4("iti") SL_DEL4("ous") SL_DEL4("ive") SL_DEL4("ize")
+    SL_DEL4("al") SL_DEL4("er") SL_DEL4("ic")
 #undef SL_DEL4
   }
 done_step4:
   // step 5
-  if (n >= 1 && w[n - 1] == 'e') {
+  if (n >= 1 && LAST(0) == 'e') {
     if (n - 1 >= r2 || (n - 1 >= r1 && !short_syl(w, n - 1))) --n;
-  } else if (n >= 2 && w[n - 1] == 'l' && w[n - 2] == 'l' && n - 1 >= r2) {
+  } else if (n >= 2 && LAST(0) == 'l' && LAST(1) == 'l' && n - 1 >= r2) {
     --n;
   }
   return n;
 }
-#undef SL_RULE
+#undef ENDS
+#undef SAME
+#undef SYNC
+#undef REPL
+#undef CUT
+#undef PUSH
+#undef LAST
 
 // stem_english over UTF-8 bytes `in` (length len) into `out` (capacity >= len); `sh` is a
 // shadow buffer of >= len bytes. Lenient decode like stemmer.cpp:33-62 (malformed ->
@@ -561,6 +589,7 @@ struct StopView {
   const uint32_t* len;   // [cap]
   const uint8_t* bytes;
   uint32_t cap;          // power of two (0 = no stopwords)
+  uint32_t max_len;      // longest stopword (bytes): longer tokens skip the probe
 };
 struct VocabView {
   const uint64_t* tkey;
@@ -589,7 +618,7 @@ struct NormArgs {
 };
 
 __device__ bool is_stopword(const StopView& s, const uint8_t* w, uint32_t n) {
-  if (!s.cap) return false;
+  if (!s.cap || n > s.max_len) return false;
   const uint64_t k = fnv1a64(w, n) | 1ull;
   for (uint32_t slot = (uint32_t)k & (s.cap - 1);; slot = (slot + 1) & (s.cap - 1)) {
     const uint64_t e = s.key[slot];
@@ -627,6 +656,12 @@ __device__ void norm_one(const NormArgs& a, uint64_t i, uint8_t* nb, uint8_t* sh
   uint32_t nl = 0;
   if (a.lowercase) {
     for (uint32_t p = 0; p < len;) {
+      const uint32_t c0 = src[p];
+      if (c0 < 0x80) {  // ASCII fast path
+        nb[nl++] = (uint8_t)((c0 >= 'A' && c0 <= 'Z') ? c0 + 32 : c0);
+        ++p;
+        continue;
+      }
       uint32_t cp;
       p += decode_at(src + p, &cp);
       nl += put_utf8(nb + nl, lower_cp(cp));
@@ -695,55 +730,79 @@ __global__ void k_compact_idx(const uint32_t* __restrict__ flag, const uint32_t*
     if (flag[i]) out[pos[i]] = (uint32_t)i;
 }
 
-__global__ void k_gather_u64_lo_hi(const uint64_t* __restrict__ h, const uint32_t* __restrict__ idx, uint32_t n,
-                                   uint32_t* __restrict__ lo, uint32_t* __restrict__ hi) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint64_t x = h[idx[j]];
-    lo[j] = (uint32_t)x;
-    hi[j] = (uint32_t)(x >> 32);
-  }
-}
-
 __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
                              uint32_t* __restrict__ out) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
 }
 
-// sorted new tokens (token index order preserved within equal hashes): group heads
-__global__ void k_group_heads(const uint32_t* __restrict__ tok, uint32_t n, const uint64_t* __restrict__ h1,
-                              const uint64_t* __restrict__ h2, const uint32_t* __restrict__ flen,
-                              uint32_t* __restrict__ head, uint32_t* __restrict__ err) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t t = tok[j];
-    bool h = j == 0;
-    if (!h) {
-      const uint32_t u = tok[j - 1];
-      h = h1[t] != h1[u];
-      if (!h && (h2[t] != h2[u] || flen[t] != flen[u])) atomicOr(err, 1u);
+// batch-local distinct-string table: key = first hash, first = smallest token index
+__global__ void k_dedup_insert(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ h1,
+                               uint64_t* __restrict__ key, uint32_t* __restrict__ first, uint32_t cap,
+                               uint32_t* __restrict__ cnt /*[0] inserted [1] overflow*/) {
+  // whole warps iterate together (the match below needs every lane)
+  for (uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; j0 < M; j0 += gridDim.x * blockDim.x) {
+    const uint32_t j = j0 + (threadIdx.x & 31);
+    const bool act = j < M;
+    const uint32_t i = act ? ntok[j] : 0xFFFFFFFFu;
+    const uint64_t k = act ? h1[i] : 0ull;
+    // Zipf head tokens repeat within a warp: one lane per distinct hash (the lowest lane =
+    // the smallest token index, ntok is ascending) touches the table
+    const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)k);
+    if (!act || (__ffs(grp) - 1) != (int)(threadIdx.x & 31)) continue;
+    uint32_t slot = (uint32_t)k & (cap - 1);
+    for (uint32_t probes = 0;; ++probes) {
+      if (probes == cap) {
+        atomicOr(cnt + 1, 1u);
+        break;
+      }
+      unsigned long long cur = key[slot];
+      if (cur == 0ull) cur = atomicCAS((unsigned long long*)key + slot, 0ull, (unsigned long long)k);
+      if (cur == 0ull || cur == k) {
+        if (cur == 0ull) atomicAdd(cnt, 1u);
+        if (*(volatile uint32_t*)(first + slot) > i) atomicMin(first + slot, i);
+        break;
+      }
+      slot = (slot + 1) & (cap - 1);
     }
-    head[j] = h ? 1u : 0u;
   }
 }
 
-// per group: first (smallest) token index, and group of every sorted element
-__global__ void k_group_first(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ head,
-                              const uint32_t* __restrict__ gpos, uint32_t n, uint32_t* __restrict__ gfirst) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    if (head[j]) gfirst[gpos[j]] = tok[j];
+__global__ void k_slot_flags(const uint64_t* __restrict__ key, uint32_t cap, uint32_t* __restrict__ flag) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+    flag[s] = key[s] != 0ull;
+}
+
+__global__ void k_slot_list(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                            const uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ slots,
+                            uint32_t* __restrict__ fk) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x)
+    if (flag[s]) {
+      slots[pos[s]] = s;
+      fk[pos[s]] = first[s];
+    }
+}
+
+// id of every new token; the second hash and length must agree with the group's first
+// occurrence (otherwise two distinct strings share the first hash: refuse)
+__global__ void k_dedup_assign(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ h1,
+                               const uint64_t* __restrict__ h2, const uint32_t* __restrict__ flen,
+                               const uint64_t* __restrict__ key, const uint32_t* __restrict__ first,
+                               const uint32_t* __restrict__ rank, uint32_t cap, uint32_t V0, uint32_t* __restrict__ id,
+                               uint32_t* __restrict__ err) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+    const uint32_t i = ntok[j];
+    const uint64_t k = h1[i];
+    uint32_t slot = (uint32_t)k & (cap - 1);
+    while (key[slot] != k) slot = (slot + 1) & (cap - 1);
+    const uint32_t f = first[slot];
+    if (h2[f] != h2[i] || flen[f] != flen[i]) atomicOr(err, 1u);
+    id[i] = V0 + rank[slot];
+  }
 }
 
 // groups sorted by first occurrence: rank -> id = V0 + rank
 __global__ void k_group_rank(const uint32_t* __restrict__ gsorted, uint32_t G, uint32_t* __restrict__ grank) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < G; r += gridDim.x * blockDim.x) grank[gsorted[r]] = r;
-}
-
-__global__ void k_assign_new(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ head,
-                             const uint32_t* __restrict__ gpos, uint32_t n, const uint32_t* __restrict__ grank,
-                             uint32_t V0, uint32_t* __restrict__ id) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t g = gpos[j] + head[j] - 1;  // inclusive group index
-    id[tok[j]] = V0 + grank[g];
-  }
 }
 
 // new vocabulary entries in id order: representative token, length
@@ -880,6 +939,11 @@ int32_t text_stream(int device, cudaStream_t* out) {
   if (!s.st) {
     SL_CUDA_TRY(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
     s.device = device;
+    cudaMemPool_t pool;  // keep freed scratch mapped between calls (no page re-mapping per batch)
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
   }
   *out = s.st;
   return SL_OK;
@@ -897,6 +961,7 @@ struct StopTable {
   std::vector<uint32_t> off, len;
   std::vector<uint8_t> bytes;
   uint32_t cap = 0;
+  uint32_t max_len = 0;
 };
 
 std::vector<std::string> parse_stopwords(const char* s, uint64_t n) {
@@ -935,6 +1000,7 @@ StopTable make_stop_table(const std::vector<std::string>& words) {
     t.key[slot] = k;
     t.off[slot] = (uint32_t)t.bytes.size();
     t.len[slot] = (uint32_t)w.size();
+    t.max_len = std::max<uint32_t>(t.max_len, (uint32_t)w.size());
     t.bytes.insert(t.bytes.end(), w.begin(), w.end());
   }
   return t;
@@ -1083,7 +1149,7 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     cudaMemcpyAsync(o, stab.off.data(), stab.cap * 4ull, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(l, stab.len.data(), stab.cap * 4ull, cudaMemcpyHostToDevice, st);
     if (!stab.bytes.empty()) cudaMemcpyAsync(by, stab.bytes.data(), stab.bytes.size(), cudaMemcpyHostToDevice, st);
-    sv = StopView{k, o, l, by, stab.cap};
+    sv = StopView{k, o, l, by, stab.cap, stab.max_len};
   }
   NormArgs na{};
   na.t = TextView{text, nb, dbits};
@@ -1157,56 +1223,57 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     uint32_t M = 0;
     SL_TTRY(exclusive_scan_u32(nflag, npos, n_tok, st, &M));
     if (M) {
-      uint32_t *ntok, *klo, *khi, *k0, *k1, *v0, *v1, *head, *gpos, *gfirst, *grank, *gs_k, *gs_v, *elen, *epos;
+      uint32_t *ntok, *slots, *fk, *k0, *k1, *v0, *v1, *elen, *epos, *cnt2;
       SL_TTRY(scr.alloc(&ntok, M));
-      SL_TTRY(scr.alloc(&klo, M));
-      SL_TTRY(scr.alloc(&khi, M));
-      SL_TTRY(scr.alloc(&k0, M));
-      SL_TTRY(scr.alloc(&k1, M));
-      SL_TTRY(scr.alloc(&v0, M));
-      SL_TTRY(scr.alloc(&v1, M));
-      SL_TTRY(scr.alloc(&head, M));
-      SL_TTRY(scr.alloc(&gpos, M));
       k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(nflag, npos, n_tok, ntok); ++t_launches;
-      // stable LSD sort of token indices by h1: low word, then high word
-      k_gather_u64_lo_hi<<<grid_for(M), 256, 0, st>>>(na.h1, ntok, M, klo, khi); ++t_launches;
-      const uint32_t *ks, *vs;
-      SL_TTRY(radix_sort_pairs(klo, ntok, M, 32, k0, k1, v0, v1, st, &ks, &vs, 0, nullptr));
-      // vs = token indices ordered by low word; re-gather the high word in that order
-      uint32_t* perm1;
-      SL_TTRY(scr.alloc(&perm1, M));
-      SL_CUDA_TRY(cudaMemcpyAsync(perm1, vs, M * 4ull, cudaMemcpyDeviceToDevice, st));
-      k_gather_u64_lo_hi<<<grid_for(M), 256, 0, st>>>(na.h1, perm1, M, klo, khi); ++t_launches;
-      SL_TTRY(radix_sort_pairs(khi, perm1, M, 32, k0, k1, v0, v1, st, &ks, &vs, 0, nullptr));
-      uint32_t* sorted;
-      SL_TTRY(scr.alloc(&sorted, M));
-      SL_CUDA_TRY(cudaMemcpyAsync(sorted, vs, M * 4ull, cudaMemcpyDeviceToDevice, st));
-      k_group_heads<<<grid_for(M), 256, 0, st>>>(sorted, M, na.h1, na.h2, na.flen, head, err); ++t_launches;
+      // distinct new strings: batch-local hash table keyed by the first hash, value = the
+      // smallest token index (first occurrence); grows and retries on overflow
+      uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(M, 1ull << 22));
+      uint64_t* key = nullptr;
+      uint32_t *first = nullptr, *rank = nullptr, *sflag = nullptr, *spos = nullptr;
+      SL_TTRY(scr.alloc(&cnt2, 2));
+      for (;;) {
+        SL_TTRY(scr.alloc(&key, cap));
+        SL_TTRY(scr.alloc(&first, cap));
+        if (cudaMemsetAsync(key, 0, cap * 8, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
+            cudaMemsetAsync(cnt2, 0, 8, st) != cudaSuccess)
+          return fail((set_error("memset"), SL_ECUDA));
+        k_dedup_insert<<<grid_for(M), 256, 0, st>>>(ntok, M, na.h1, key, first, (uint32_t)cap, cnt2); ++t_launches;
+        uint32_t h[2];
+        SL_CUDA_TRY(cudaMemcpyAsync(h, cnt2, 8, cudaMemcpyDeviceToHost, st));
+        SL_CUDA_TRY(cudaStreamSynchronize(st));
+        if (!h[1] && (uint64_t)h[0] * 2 <= cap) break;
+        if (cap >= (1ull << 31)) return fail((set_error("tokenize: too many distinct tokens in one batch"), SL_EUNSUPPORTED));
+        cap = std::min<uint64_t>(cap * 4, 1ull << 31);
+      }
+      SL_TTRY(scr.alloc(&sflag, cap));
+      SL_TTRY(scr.alloc(&spos, cap));
+      SL_TTRY(scr.alloc(&rank, cap));
+      k_slot_flags<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
       uint32_t G = 0;
-      SL_TTRY(exclusive_scan_u32(head, gpos, M, st, &G));
-      SL_TTRY(scr.alloc(&gfirst, G));
-      SL_TTRY(scr.alloc(&grank, G));
-      SL_TTRY(scr.alloc(&gs_k, G));
-      SL_TTRY(scr.alloc(&gs_v, G));
+      SL_TTRY(exclusive_scan_u32(sflag, spos, cap, st, &G));
+      SL_TTRY(scr.alloc(&slots, G));
+      SL_TTRY(scr.alloc(&fk, G));
+      SL_TTRY(scr.alloc(&k0, G));
+      SL_TTRY(scr.alloc(&k1, G));
+      SL_TTRY(scr.alloc(&v0, G));
+      SL_TTRY(scr.alloc(&v1, G));
       SL_TTRY(scr.alloc(&elen, G));
       SL_TTRY(scr.alloc(&epos, G));
-      k_group_first<<<grid_for(M), 256, 0, st>>>(sorted, head, gpos, M, gfirst); ++t_launches;
-      // order groups by first occurrence (token index = document/position order)
-      uint32_t* giota;
-      SL_TTRY(scr.alloc(&giota, G));
-      {
-        std::vector<uint32_t> io(G);
-        for (uint32_t g = 0; g < G; ++g) io[g] = g;
-        SL_CUDA_TRY(cudaMemcpyAsync(giota, io.data(), G * 4ull, cudaMemcpyHostToDevice, st));
-        SL_CUDA_TRY(cudaStreamSynchronize(st));
-      }
-      const uint32_t *fs, *gsv;
-      SL_TTRY(radix_sort_pairs(gfirst, giota, G, 32, k0, k1, v0, v1, st, &fs, &gsv, 0, nullptr));
-      SL_CUDA_TRY(cudaMemcpyAsync(gs_k, fs, G * 4ull, cudaMemcpyDeviceToDevice, st));  // first token per rank
-      SL_CUDA_TRY(cudaMemcpyAsync(gs_v, gsv, G * 4ull, cudaMemcpyDeviceToDevice, st)); // group per rank
-      k_group_rank<<<grid_for(G), 256, 0, st>>>(gs_v, G, grank); ++t_launches;
+      k_slot_list<<<grid_for(cap), 256, 0, st>>>(sflag, spos, first, (uint32_t)cap, slots, fk); ++t_launches;
+      // groups in first-occurrence order (document order, then position)
+      const uint32_t *fs, *ss;
+      SL_TTRY(radix_sort_pairs(fk, slots, G, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
+      uint32_t *gs_k, *gs_slot;
+      SL_TTRY(scr.alloc(&gs_k, G));
+      SL_TTRY(scr.alloc(&gs_slot, G));
+      SL_CUDA_TRY(cudaMemcpyAsync(gs_k, fs, G * 4ull, cudaMemcpyDeviceToDevice, st));     // first token per rank
+      SL_CUDA_TRY(cudaMemcpyAsync(gs_slot, ss, G * 4ull, cudaMemcpyDeviceToDevice, st));  // slot per rank
+      k_group_rank<<<grid_for(G), 256, 0, st>>>(gs_slot, G, rank); ++t_launches;
       const uint32_t V0 = v->V;
-      k_assign_new<<<grid_for(M), 256, 0, st>>>(sorted, head, gpos, M, grank, V0, na.id); ++t_launches;
+      k_dedup_assign<<<grid_for(M), 256, 0, st>>>(ntok, M, na.h1, na.h2, na.flen, key, first, rank, (uint32_t)cap, V0,
+                                                  na.id, err);
+      ++t_launches;
       // append strings
       k_new_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, na.flen, elen); ++t_launches;
       uint32_t ebytes = 0;

@@ -168,4 +168,76 @@ int sl_synth_queries(const sl_synth_config* c, const double* cdf, uint32_t q_beg
   return 0;
 }
 
+// Renders token-id documents as text (the text-pipeline workload): token t -> words[t]
+// (word_off[n_words+1] into `words`), each followed by a separator drawn with Philox
+// (seed, SL_STREAM_TEXT, global token position); 10% of words start with a capital.
+// out == NULL: only out_doc_off[N+1] (byte offsets) is filled; call again with a buffer of
+// out_doc_off[N] bytes.
+static const char* kSeps[] = {" ", ", ", ". ", "\n", "; ", " (", ") ", " - ", "! "};
+static const double kSepCdf[] = {0.80, 0.86, 0.90, 0.93, 0.95, 0.97, 0.98, 0.99, 1.01};
+
+static inline int pick_sep(double u) {
+  int k = 0;
+  while (u >= kSepCdf[k]) ++k;
+  return k;
+}
+
+int sl_synth_render_text(const uint32_t* tokens, const uint64_t* doc_off, uint32_t N, const char* words,
+                         const uint64_t* word_off, uint32_t n_words, uint32_t seed, char* out,
+                         uint64_t* out_doc_off, int threads) {
+  if (!tokens || !doc_off || !words || !word_off || !out_doc_off) return 1;
+  if (threads < 1) threads = 1;
+  std::vector<uint64_t> sz(N, 0);
+  auto run = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    const uint32_t chunk = (N + (uint32_t)threads - 1) / (uint32_t)threads;
+    for (int t = 0; t < threads; ++t) {
+      const uint32_t lo = (uint32_t)t * chunk, hi = lo + chunk < N ? lo + chunk : N;
+      if (lo >= hi) break;
+      pool.emplace_back([=, &body] {
+        for (uint32_t d = lo; d < hi; ++d) body(d);
+      });
+    }
+    for (auto& th : pool) th.join();
+  };
+  if (!out) {
+    int bad = 0;
+    run([&](uint32_t d) {
+      uint64_t n = 0;
+      for (uint64_t i = doc_off[d]; i < doc_off[d + 1]; ++i) {
+        const uint32_t t = tokens[i];
+        if (t >= n_words) {
+          bad = 1;
+          continue;
+        }
+        double u0, u1;
+        sl_uniform2(seed, SL_STREAM_TEXT, i, &u0, &u1);
+        n += (word_off[t + 1] - word_off[t]) + std::strlen(kSeps[pick_sep(u0)]);
+      }
+      sz[d] = n;
+    });
+    out_doc_off[0] = 0;
+    for (uint32_t d = 0; d < N; ++d) out_doc_off[d + 1] = out_doc_off[d] + sz[d];
+    return bad;
+  }
+  run([&](uint32_t d) {
+    char* o = out + out_doc_off[d];
+    for (uint64_t i = doc_off[d]; i < doc_off[d + 1]; ++i) {
+      const uint32_t t = tokens[i];
+      if (t >= n_words) continue;
+      double u0, u1;
+      sl_uniform2(seed, SL_STREAM_TEXT, i, &u0, &u1);
+      const uint64_t wl = word_off[t + 1] - word_off[t];
+      std::memcpy(o, words + word_off[t], wl);
+      if (u1 < 0.1 && o[0] >= 'a' && o[0] <= 'z') o[0] = (char)(o[0] - 32);
+      o += wl;
+      const char* s = kSeps[pick_sep(u0)];
+      const size_t sl = std::strlen(s);
+      std::memcpy(o, s, sl);
+      o += sl;
+    }
+  });
+  return 0;
+}
+
 }  // extern "C"

@@ -111,3 +111,65 @@ def corpus_host(cfg: SynthConfig, threads: int = 8) -> Corpus:
     off = doc_offsets(cfg)
     tok = tokens_host(cfg, cdf, 0, int(off[-1]), threads)
     return Corpus(cfg, cdf, off, tok)
+
+
+# ---------------------------------------------------------------- text workload (t<i>)
+_ON = ["", "b", "c", "d", "f", "g", "h", "j", "k", "l", "m", "n", "p", "r", "s", "t", "v", "w", "z", "bl", "br",
+       "ch", "cl", "cr", "dr", "fl", "fr", "gl", "gr", "pl", "pr", "sc", "sh", "sk", "sl", "sp", "st", "str", "th",
+       "tr", "wh", "qu"]
+_NU = ["a", "e", "i", "o", "u", "y", "ai", "ea", "ee", "ie", "oa", "oo", "ou", "ay", "oy"]
+_CO = ["", "b", "d", "g", "l", "m", "n", "p", "r", "s", "t", "x", "ck", "ll", "ng", "nt", "rd", "rt", "ss", "st"]
+_SUF = ["", "", "", "", "", "s", "es", "ing", "ed", "ly", "er", "ation", "ness", "ment", "ful", "ity", "ize",
+        "able", "ous", "ive", "al", "ism", "ist", "ence", "ance"]
+
+
+def word_list(n: int, seed: int = 17) -> list:
+    """n distinct lowercase ASCII pseudo-words (syllables + suffixes), rank order = Zipf
+    rank order; none is a bundled stopword or shorter than 2 letters."""
+    rng = np.random.default_rng(seed)
+    stop = set()
+    try:
+        import os
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "stopwords_en.txt")) as f:
+            stop = {w.strip() for w in f if w.strip() and not w.startswith("#")}
+    except OSError:
+        pass
+    out, seen = [], set()
+    while len(out) < n:
+        m = max(1024, (n - len(out)) * 2)
+        ns = rng.integers(1, 4, m)
+        o = rng.integers(len(_ON), size=(m, 3))
+        u = rng.integers(len(_NU), size=(m, 3))
+        c = rng.integers(len(_CO), size=(m, 3))
+        sfx = rng.integers(len(_SUF), size=m)
+        for i in range(m):
+            w = "".join(_ON[o[i, j]] + _NU[u[i, j]] + _CO[c[i, j]] for j in range(ns[i])) + _SUF[sfx[i]]
+            if len(w) >= 2 and w not in seen and w not in stop:
+                seen.add(w)
+                out.append(w)
+                if len(out) == n:
+                    break
+    return out
+
+
+def render_text(tokens: np.ndarray, doc_off: np.ndarray, words: list, seed: int, threads: int = 16):
+    """Token-id documents -> UTF-8 text: token t -> words[t] + a Philox-drawn separator, 10%
+    capitalised (libsl_synth sl_synth_render_text). Returns (bytes ndarray u8, u64 offsets)."""
+    enc = [w.encode("utf-8") for w in words]
+    wo = np.zeros(len(enc) + 1, np.uint64)
+    wo[1:] = np.cumsum([len(e) for e in enc])
+    wb = np.frombuffer(b"".join(enc), np.uint8)
+    tok = np.ascontiguousarray(tokens, np.uint32)
+    off = np.ascontiguousarray(doc_off, np.uint64)
+    N = len(off) - 1
+    L = _lib.synth_lib()
+    L.sl_synth_render_text.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
+                                       C.c_uint32, C.c_void_p, C.c_void_p, C.c_int]
+    toff = np.empty(N + 1, np.uint64)
+    if L.sl_synth_render_text(_ptr(tok), _ptr(off), N, _ptr(wb), _ptr(wo), len(enc), seed, None, _ptr(toff),
+                              threads) != 0:
+        raise ValueError("render_text: token id outside the word list")
+    text = np.empty(max(1, int(toff[-1])), np.uint8)
+    L.sl_synth_render_text(_ptr(tok), _ptr(off), N, _ptr(wb), _ptr(wo), len(enc), seed, _ptr(text), _ptr(toff),
+                           threads)
+    return text[:int(toff[-1])], toff

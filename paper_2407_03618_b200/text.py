@@ -212,7 +212,7 @@ class TokenBatch:
 
 
 def _tokenize(texts, config: TokenizerConfig, vocab: Vocabulary, build: bool, mem=None) -> TokenBatch:
-    text, off = _texts_to_csr(texts)
+    text, off = texts if mem == SL_MEM_DEVICE else _texts_to_csr(texts)
     cfg, blob = config.to_c()
     if mem == SL_MEM_DEVICE:  # (torch uint8 tensor, torch uint64 tensor) already on the device
         tp, op = text.data_ptr(), off.data_ptr()
