@@ -37,6 +37,9 @@
 #include "sl_index.cuh"
 
 #define SL_UNI_QUAL __device__
+#ifndef SL_TAIL_INLINE
+#define SL_TAIL_INLINE __noinline__
+#endif
 namespace sl {
 namespace uni {
 #include "sl_unicode.inc"
@@ -300,7 +303,10 @@ __global__ void k_tokens(const uint32_t* __restrict__ wbits, const uint32_t* __r
 // reference's stemmer.cpp:125-391 step by step; returns the new length. Suffix tests run on
 // a register copy of the last 8 symbols (byte k = w[n-1-k]) against compile-time packed
 // constants, so each test is one AND + one compare.
-__device__ __forceinline__ bool sv(uint8_t c) { return c == 'a' || c == 'e' || c == 'i' || c == 'o' || c == 'u' || c == 'y'; }
+__device__ __forceinline__ bool sv(uint32_t c) {  // a e i o u y
+  const uint32_t d = c - 'a';
+  return d < 26u && ((0x1104111u >> d) & 1u);
+}
 
 template <int M>
 __host__ __device__ constexpr uint64_t pk(const char (&s)[M]) {
@@ -310,7 +316,7 @@ __host__ __device__ constexpr uint64_t pk(const char (&s)[M]) {
 }
 __host__ __device__ constexpr uint64_t lenmask(int m) { return m >= 8 ? ~0ull : ((1ull << (8 * m)) - 1ull); }
 
-__device__ __forceinline__ uint64_t tail8(const uint8_t* w, int n) {
+__device__ SL_TAIL_INLINE uint64_t tail8(const uint8_t* w, int n) {
   uint64_t t = 0;
   const int m = n < 8 ? n : 8;
   for (int k = 0; k < m; ++k) t |= (uint64_t)w[n - 1 - k] << (8 * k);
@@ -354,12 +360,13 @@ __device__ __forceinline__ bool short_syl(const uint8_t* w, int end) {
   }
   return end == 2 && sv(w[0]) && !sv(w[1]);
 }
-__device__ __forceinline__ bool is_dbl(uint8_t c) {
-  return c == 'b' || c == 'd' || c == 'f' || c == 'g' || c == 'm' || c == 'n' || c == 'p' || c == 'r' || c == 't';
+__device__ __forceinline__ bool is_dbl(uint32_t c) {  // b d f g m n p r t
+  const uint32_t d = c - 'a';
+  return d < 26u && ((0xAB06Au >> d) & 1u);
 }
-__device__ __forceinline__ bool li_end(uint8_t c) {
-  return c == 'c' || c == 'd' || c == 'e' || c == 'g' || c == 'h' || c == 'k' || c == 'm' || c == 'n' || c == 'r' ||
-         c == 't';
+__device__ __forceinline__ bool li_end(uint32_t c) {  // c d e g h k m n r t
+  const uint32_t d = c - 'a';
+  return d < 26u && ((0xA34DCu >> d) & 1u);
 }
 
 // Stems the shadow in place. Returns the final length; *shift = leading apostrophe removed;
