@@ -156,6 +156,78 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU leg
+def text_pipeline_block(cfg_i, hbm, reps=3, cpu_docs=20000):
+    """the text side (sl_tokenize, english config: lowercase + bundled
+    stopwords + Snowball English) on config c<i>'s corpus rendered as text (synth.render_text).
+    Device-resident text timed with CUDA events around the call; e2e from pinned host memory;
+    the reference's own tokenizer (oracle/_ref, else the oracle port) on a CPU sample."""
+    import torch
+
+    from paper_2407_03618_b200 import synth, text as T
+    from paper_2407_03618_b200._lib import SL_MEM_DEVICE, SL_MEM_HOST
+    cfg = synth.config(cfg_i)
+    corp = synth.corpus_host(cfg, threads=os.cpu_count() or 8)
+    words = synth.word_list(cfg.vocab)
+    text, off = synth.render_text(corp.tokens, corp.offsets, words, cfg.corpus_seed)
+    nb, N = len(text), len(off) - 1
+    tc = T.TokenizerConfig.english()
+    dtext = torch.from_numpy(text).cuda()
+    doff = torch.from_numpy(off.view(np.int64)).cuda()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dev_ms, T_out, V = [], 0, 0
+    for r in range(reps + 1):
+        v = T.Vocabulary()
+        torch.cuda.synchronize()
+        ev0.record()
+        b = T.tokenize_build((dtext, doff), tc, v, mem=SL_MEM_DEVICE)  # the call synchronises its stream
+        ev1.record()
+        torch.cuda.synchronize()
+        if r:
+            dev_ms.append(ev0.elapsed_time(ev1))
+        T_out, V = b.num_tokens, v.size()
+        b.close()
+        v.close()
+    htext = torch.from_numpy(text).pin_memory()
+    hoff = torch.from_numpy(off.view(np.int64)).pin_memory()
+    e2e_ms = []
+    for r in range(reps + 1):
+        v = T.Vocabulary()
+        t0 = time.perf_counter()
+        b = T._tokenize_raw(htext.data_ptr(), hoff.data_ptr(), N, tc, v, True, SL_MEM_HOST)
+        out_off, out_ids = b.to_numpy()  # D2H of the result inside the region
+        if r:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        b.close()
+        v.close()
+    ms = min(dev_ms)
+    alg = nb + 8 * (N + 1) + 4 * T_out + 8 * (N + 1)  # read text + offsets, write ids + token offsets
+    ach = alg / (ms / 1e3) / 1e9
+    blk = {"workload": f"t{cfg_i}: c{cfg_i} corpus rendered as UTF-8 text (synth.render_text)",
+           "tokenizer": "english (lowercase, bundled stopwords, Snowball English)", "docs": N, "bytes": nb,
+           "tokens": T_out, "vocab": V, "ms": ms, "bytes_per_s": nb / (ms / 1e3), "tokens_per_s": T_out / (ms / 1e3),
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "algorithmic_bytes": alg,
+                        "note": "issue-bound per-token string work (k_norm_fast), far from the HBM roofline"},
+           "e2e": {"ms": min(e2e_ms), "bytes_per_s": nb / (min(e2e_ms) / 1e3), "h2d_bytes": nb + 8 * (N + 1),
+                   "d2h_bytes": 4 * T_out + 8 * (N + 1)}}
+    try:
+        from oracle.text import TextOracle, ref_available
+        kind = "ref" if ref_available() else "port"
+        o = TextOracle(kind)
+        n = min(N, cpu_docs)
+        sample = bytes(text[:int(off[n])])
+        t0 = time.perf_counter()
+        _, ids, _ = o.tokenize_corpus(sample, off[:n + 1], 1, 1, 1)
+        cs = time.perf_counter() - t0
+        blk["cpu_baseline"] = {"value": len(sample) / cs, "unit": "bytes/s", "cores": 1,
+                               "kind": "reference" if kind == "ref" else "port",
+                               "sample": f"first {n} documents ({len(sample)} bytes), tokenize_build, 1 thread",
+                               "tokens_per_s": len(ids) / cs}
+    except Exception as e:  # noqa: BLE001
+        blk["cpu_baseline"] = {"unavailable": str(e)}
+    return blk
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -329,6 +401,8 @@ def run_ours(args):
                                               f"{r['tokens'] / r['build_s']:.3g} tokens/s"}
             agree = float(np.mean(res_ids[: args.cpu_sample] == r["ids"]))
             line["parity_sample"] = {"queries": args.cpu_sample, "top_k_id_agreement": agree}
+        if world == 1 and not args.no_text:
+            line["text_pipeline"] = text_pipeline_block(args.config, hbm)
         print(json.dumps(line), flush=True)
     idx.close()
     if comm:
@@ -348,6 +422,7 @@ def main():
     ap.add_argument("--k", type=int, default=10)
     ap.add_argument("--dense-density", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-text", action="store_true", help="skip the text-pipeline block")
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--ref-sample", type=int, default=128)
     ap.add_argument("--shard-of", type=int, default=1, help="build one shard of an N-way doc sharding (1 GPU)")

@@ -211,6 +211,15 @@ class TokenBatch:
             pass
 
 
+def _tokenize_raw(text_ptr: int, off_ptr: int, n_docs: int, config: TokenizerConfig, vocab: Vocabulary, build: bool,
+                  mem: int) -> TokenBatch:
+    """sl_tokenize on raw pointers (host or device per mem): bench / zero-copy callers."""
+    cfg, blob = config.to_c()
+    h = C.c_void_p()
+    check(lib().sl_tokenize(vocab.handle, C.byref(cfg), int(build), text_ptr, off_ptr, n_docs, mem, C.byref(h)))
+    return TokenBatch(h.value)
+
+
 def _tokenize(texts, config: TokenizerConfig, vocab: Vocabulary, build: bool, mem=None) -> TokenBatch:
     text, off = texts if mem == SL_MEM_DEVICE else _texts_to_csr(texts)
     cfg, blob = config.to_c()
