@@ -218,4 +218,151 @@ inline QueryResult retrieve(const SearchIndex& index, std::span<const uint32_t> 
   return std::move(retrieve_batch(index, {std::vector<uint32_t>(query.begin(), query.end())}, k, ordered)[0]);
 }
 
+// ---------------------------------------------------------------- text (SPEC [MODULE] tokenizer)
+// stemmer.hpp:8-11
+enum class StemmerKind : int32_t { none = SL_STEMMER_NONE, snowball_english = SL_STEMMER_SNOWBALL_ENGLISH };
+
+// tokenizer.hpp:16-23; stopwords compared with the lowercased pre-stem token
+struct TokenizerConfig {
+  bool lowercase = true;
+  std::vector<std::string> stopwords;
+  StemmerKind stemmer = StemmerKind::none;
+};
+
+// vocabulary.hpp:13-48 on the device (ids in first-encounter order)
+class Vocabulary {
+ public:
+  explicit Vocabulary(int device = 0) { check(sl_vocab_create(device, &h_)); }
+  Vocabulary(Vocabulary&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Vocabulary& operator=(Vocabulary&& o) noexcept {
+    if (this != &o) {
+      if (h_) sl_vocab_destroy(h_);
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  Vocabulary(const Vocabulary&) = delete;
+  Vocabulary& operator=(const Vocabulary&) = delete;
+  ~Vocabulary() {
+    if (h_) sl_vocab_destroy(h_);
+  }
+  sl_vocab* handle() const { return h_; }
+  uint32_t size() const {
+    uint32_t n = 0;
+    check(sl_vocab_size(h_, &n));
+    return n;
+  }
+  std::vector<std::string> tokens() const {
+    const uint32_t n = size();
+    std::vector<uint64_t> off(n + 1ull);
+    uint64_t total = 0;
+    check(sl_vocab_export(h_, nullptr, nullptr, &total));
+    std::string bytes(total, '\0');
+    check(sl_vocab_export(h_, off.data(), bytes.data(), &total));
+    std::vector<std::string> out(n);
+    for (uint32_t i = 0; i < n; ++i) out[i] = bytes.substr(off[i], off[i + 1] - off[i]);
+    return out;
+  }
+
+ private:
+  sl_vocab* h_ = nullptr;
+};
+
+// Token ids per document (host copy of a device sl_token_batch)
+struct TokenizedCorpus {
+  std::vector<uint64_t> doc_offsets;
+  std::vector<uint32_t> token_ids;
+  std::vector<uint32_t> doc(size_t d) const {
+    return {token_ids.begin() + doc_offsets[d], token_ids.begin() + doc_offsets[d + 1]};
+  }
+};
+
+namespace detail {
+struct CfgC {
+  std::string blob;
+  sl_tokenizer_config c{};
+  explicit CfgC(const TokenizerConfig& t) {
+    for (const auto& w : t.stopwords) blob += w + "\n";
+    c.lowercase = t.lowercase ? 1 : 0;
+    c.stemmer = static_cast<int32_t>(t.stemmer);
+    c.stopwords = blob.empty() ? nullptr : blob.data();
+    c.stopwords_bytes = blob.size();
+  }
+};
+inline TokenizedCorpus tokenize(const std::vector<std::string>& texts, const TokenizerConfig& cfg, Vocabulary& v,
+                                bool build) {
+  std::string all;
+  std::vector<uint64_t> off{0};
+  for (const auto& t : texts) {
+    all += t;
+    off.push_back(all.size());
+  }
+  if (all.empty()) all.push_back('\0');
+  CfgC c(cfg);
+  sl_token_batch* b = nullptr;
+  check(sl_tokenize(v.handle(), &c.c, build ? 1 : 0, all.data(), off.data(), static_cast<uint32_t>(texts.size()),
+                    SL_MEM_HOST, &b));
+  uint32_t n = 0;
+  uint64_t T = 0;
+  sl_token_batch_info(b, &n, &T, nullptr, nullptr);
+  TokenizedCorpus out;
+  out.doc_offsets.resize(n + 1ull);
+  out.token_ids.resize(T);
+  const int32_t rc = sl_token_batch_copy(b, out.doc_offsets.data(), out.token_ids.data());
+  sl_token_batch_destroy(b);
+  check(rc);
+  return out;
+}
+}  // namespace detail
+
+// tokenize_build / tokenize_query (tokenizer.hpp:36-45), every text a separate document
+inline TokenizedCorpus tokenize_build(const std::vector<std::string>& texts, const TokenizerConfig& cfg,
+                                      Vocabulary& vocab) {
+  return detail::tokenize(texts, cfg, vocab, true);
+}
+inline TokenizedCorpus tokenize_query(const std::vector<std::string>& texts, const TokenizerConfig& cfg,
+                                      Vocabulary& vocab) {
+  return detail::tokenize(texts, cfg, vocab, false);
+}
+
+// stem_english (stemmer.hpp:16-18), on the device
+inline std::vector<std::string> stem_english(const std::vector<std::string>& words, int device = 0) {
+  std::string all;
+  std::vector<uint64_t> off{0};
+  for (const auto& w : words) {
+    all += w;
+    off.push_back(all.size());
+  }
+  std::string out(all.size() + 1, '\0');
+  std::vector<uint32_t> len(words.size());
+  if (!words.empty())
+    check(sl_stem_batch(all.data(), off.data(), static_cast<uint32_t>(words.size()), device, out.data(), len.data()));
+  std::vector<std::string> r(words.size());
+  for (size_t i = 0; i < words.size(); ++i) r[i] = out.substr(off[i], len[i]);
+  return r;
+}
+
+// SPEC build_index(corpus texts, params, tokenizer_config) -> index + vocabulary
+struct TextIndex {
+  SearchIndex index;
+  Vocabulary vocab;
+  TokenizerConfig config;
+};
+inline TextIndex build_text_index(const std::vector<std::string>& docs, const BM25Params& params,
+                                  const TokenizerConfig& cfg, int device = 0) {
+  if (docs.empty()) throw std::invalid_argument("build_index: empty corpus");
+  Vocabulary v(device);
+  TokenizedCorpus tc = tokenize_build(docs, cfg, v);
+  if (tc.token_ids.empty()) throw std::invalid_argument("build_index: degenerate corpus");
+  BuildOptions o;
+  o.device = device;
+  SearchIndex ix = build_index({tc.doc_offsets, tc.token_ids, v.size()}, params, o);
+  return TextIndex{std::move(ix), std::move(v), cfg};
+}
+// SPEC retrieve(index, text, k, ordered): frozen vocabulary, OOV tokens dropped
+inline QueryResult retrieve(TextIndex& t, const std::string& text, uint32_t k, bool ordered = true) {
+  TokenizedCorpus q = tokenize_query({text}, t.config, t.vocab);
+  return retrieve(t.index, q.doc(0), k, ordered);
+}
+
 }  // namespace sparselex::b200

@@ -60,6 +60,22 @@ int main() {
   SearchIndex ixp = build_index(corpus, bp);
   auto ap = ixp.export_arrays();
   EXPECT(ap.theta[0] == 0.693147181f && ap.values[0] == 0.740767956f);
+  // text side: SPEC.md:65-67 and the SPEC toy corpus built from text
+  {
+    TokenizerConfig tc{true, {"the", "is"}, StemmerKind::snowball_english};
+    Vocabulary v;
+    auto tk = tokenize_build({"the cat is running", "cat cat"}, tc, v);
+    auto toks = v.tokens();
+    EXPECT(toks == (std::vector<std::string>{"cat", "run"}));
+    EXPECT(tk.doc(0) == (std::vector<uint32_t>{0, 1}) && tk.doc(1) == (std::vector<uint32_t>{0, 0}));
+    EXPECT(tokenize_query({"zebra running"}, tc, v).doc(0) == (std::vector<uint32_t>{1}));
+    EXPECT(stem_english({"running", "skies", "generously"}) ==
+           (std::vector<std::string>{"run", "sky", "generous"}));
+    TextIndex ti = build_text_index({"cat sat", "dog ran", "cat cat cat"}, BM25Params{}, TokenizerConfig{});
+    EXPECT(ti.vocab.tokens() == (std::vector<std::string>{"cat", "sat", "dog", "ran"}));
+    auto rt = retrieve(ti, "Cat!", 2);
+    EXPECT(rt.doc_indices == (std::vector<uint32_t>{2, 0}) && rt.scores[0] == 0.292446703f);
+  }
   std::printf("cpp api ok\n");
   return 0;
 }
