@@ -224,6 +224,7 @@ struct RunArgs {
   const uint32_t* run_begin;  // [n_runs+1] positions in perm
   const uint32_t* n_runs;     // device scalar
   uint32_t* work;             // device scalar: next work item (zeroed by k_build_runs)
+  uint64_t* gtau;             // [B] shared threshold per query across doc splits (nullptr: off)
   uint32_t k;
   uint32_t C;                 // candidates kept per (query, split)
   uint32_t R;                 // max queries per run
@@ -363,13 +364,18 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
 // score can never beat tau: the float pre-test is strict (x > tau_f), which rejects the
 // large tie classes (head-token-only / OOV queries) without building keys.
 // FULL: all TILE docs of the tile exist (every tile but the last): no per-doc bound checks.
+// gpub: the query's threshold shared by its doc splits (atomicMax after every select). A
+// split's exact k-th key bounds the global k-th key from below, so keys under it cannot be
+// in the result. It is published one score ordinal lower with the largest doc part, so the
+// strict float pre-test stays exact for equal scores in any split. Read only once the local
+// pre-test passes (tiles without candidates stay load-free).
 template <bool FULL, class SM>
 __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
-                                            uint32_t nvalid, const float* buf, uint64_t* kept) {
+                                            uint32_t nvalid, const float* buf, uint64_t* kept, uint64_t* gpub) {
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
-  const uint64_t tau = s.tau[r];
-  const float tf = tau_float(tau);
+  uint64_t tau = s.tau[r];
+  float tf = tau_float(tau);
   float mx = -INFINITY;
 #pragma unroll
   for (int rr = 0; rr < F4L; ++rr) {
@@ -384,6 +390,14 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
     }
   }
   if (!__any_sync(0xffffffffu, mx > tf || tau == 0)) return;
+  if (gpub) {
+    const uint64_t g = *(volatile const uint64_t*)gpub;
+    if (g > tau) {
+      tau = g;
+      tf = tau_float(g);
+      if (!__any_sync(0xffffffffu, mx > tf)) return;
+    }
+  }
   auto tile_visit = [&](uint64_t thr, auto&& fn) {
 #pragma unroll
     for (int rr = 0; rr < F4L; ++rr) {
@@ -428,12 +442,13 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
       out += __popc(bal);
       __syncwarp();
     }
+    const uint64_t nt2 = nt > tau ? nt : tau;  // survivors among this tile's candidates (keys >= tau)
     uint32_t m2 = 0;
-    tile_visit(nt, [&](uint64_t) { ++m2; });
+    tile_visit(nt2, [&](uint64_t) { ++m2; });
     const uint32_t inc2 = warp_incl_scan(m2);
     const uint32_t tot2 = __shfl_sync(0xffffffffu, inc2, 31);
     uint64_t* dst = kept + out + inc2 - m2;
-    tile_visit(nt, [&](uint64_t key) { *dst++ = key; });
+    tile_visit(nt2, [&](uint64_t key) { *dst++ = key; });
     __syncwarp();
     // exact k-th key = min of the k survivors
     uint64_t mn = ~0ull;
@@ -443,6 +458,8 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
     if (lane == 0) {
       s.n_kept[r] = out + tot2;
       s.tau[r] = mn;
+      const uint64_t hi = mn >> 32;
+      if (gpub && hi > 1) atomicMax((unsigned long long*)gpub, (unsigned long long)(((hi - 1) << 32) | 0xFFFFFFFFull));
     }
   }
   __syncwarp();
@@ -677,12 +694,14 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        uint64_t* kept = ra.cand + ((uint64_t)ra.perm[pb + r] * ra.n_splits + split) * ra.C;
+        const uint32_t q = ra.perm[pb + r];
+        uint64_t* kept = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
+        uint64_t* gp = ra.gtau ? ra.gtau + q : nullptr;
         if (!(ra.debug_skip & 2)) {
           if (nvalid == TILE)
-            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
+            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp);
           else
-            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept);
+            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp);
         }
       }
     }
@@ -834,7 +853,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
       const double qc = ra.qconst[q];
       for (uint32_t i = threadIdx.x; i < nvalid; i += NT) ra.dense_out[d0 + i] = __double2float_rn((double)acc[i] + qc);
     } else {
-      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept);
+      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept, nullptr);
     }
     __syncthreads();
   }
@@ -1387,6 +1406,10 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
+  if (plan.n_splits > 1 && env_int("SL_GTAU", 1)) {
+    SL_TRY(scr.alloc(&ra.gtau, B));
+    SL_CUDA_TRY(cudaMemsetAsync(ra.gtau, 0, (uint64_t)B * 8, st));
+  }
   // persistent grid: resident CTAs only (never more warps than the upper bound of B items)
   const uint64_t items_ub = (uint64_t)B_short * plan.n_splits;
   if (items_ub > 0xFFFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "query batch too large");
