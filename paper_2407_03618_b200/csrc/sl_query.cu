@@ -1217,7 +1217,11 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
   uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
-  if (ns == 0) ns = (uint32_t)std::max<uint64_t>(1, (4 * warps + items - 1) / items);
+  // doc splits: enough (run, split) items to keep every warp busy several times over; the
+  // splits of a query share its threshold, so small k affords more of them (merge cost
+  // grows with splits x k). Measured: c2 top-10 best at 12 items/warp, top-100 / c4 top-1000 at 8.
+  const uint64_t f = k <= 16 ? 12 : 8;
+  if (ns == 0) ns = (uint32_t)std::max<uint64_t>(1, (f * warps + items - 1) / items);
   p->n_splits = std::max(1u, std::min(ns, std::max(1u, ix->num_tiles)));
   return SL_OK;
 }
