@@ -320,8 +320,9 @@ __device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_
 // together and the rounds are applied in order with __syncwarp between them, so every
 // document receives its terms in token order without atomics.
 // cnt/rbase are this lane's entry slice (length, absolute start).
-__device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask, uint32_t cnt, uint64_t rbase,
-                                             float* buf, uint32_t d0) {
+__device__ __forceinline__ float apply_slices(const IndexView& ix, uint32_t emask, uint32_t cnt, uint64_t rbase,
+                                              float* buf, uint32_t d0) {
+  float gm = -INFINITY;  // max of the values this lane wrote (feeds the filter's pre-test)
   const int lane = threadIdx.x & 31;
   uint32_t m = __ballot_sync(0xffffffffu, cnt != 0) & emask;  // entries with postings here
   int tk = m ? __ffs(m) - 1 : 32;
@@ -352,10 +353,15 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
     }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      if (doc[u] != 0xFFFFFFFFu) buf[doc[u] - d0] += val[u];
+      if (doc[u] != 0xFFFFFFFFu) {
+        const float nv = buf[doc[u] - d0] + val[u];
+        buf[doc[u] - d0] = nv;
+        gm = fmaxf(gm, nv);
+      }
       __syncwarp();
     }
   }
+  return gm;
 }
 
 // Running top-k of query r over one tile (warp-level) from buf[TILE].
@@ -369,14 +375,19 @@ __device__ __forceinline__ void apply_slices(const IndexView& ix, uint32_t emask
 // in the result. It is published one score ordinal lower with the largest doc part, so the
 // strict float pre-test stays exact for equal scores in any split. Read only once the local
 // pre-test passes (tiles without candidates stay load-free).
+// pmax: when not NaN, an upper bound (per lane, warp-wide max >= every value of the tile)
+// supplied by the caller, which skips the max pass over buf.
 template <bool FULL, class SM>
 __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
-                                            uint32_t nvalid, const float* buf, uint64_t* kept, uint64_t* gpub) {
+                                            uint32_t nvalid, const float* buf, uint64_t* kept, uint64_t* gpub,
+                                            float pmax) {
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   uint64_t tau = s.tau[r];
   float tf = tau_float(tau);
-  float mx = -INFINITY;
+  float mx = pmax;
+  if (isnan(pmax)) {
+  mx = -INFINITY;
 #pragma unroll
   for (int rr = 0; rr < F4L; ++rr) {
     const float4 v = b4[lane + 32 * rr];
@@ -388,6 +399,7 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
       for (int c = 0; c < 4; ++c)
         if (dl + c < nvalid) mx = fmaxf(mx, f4c(v, c));
     }
+  }
   }
   if (!__any_sync(0xffffffffu, mx > tf || tau == 0)) return;
   if (gpub) {
@@ -646,7 +658,9 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       if (!live) continue;
     }
     // (2) dense signature of the run, ascending slot order, all loads in flight
+    float dm = INFINITY;  // lane max of its dense sums (padding docs included: an upper bound)
     if (!(ra.debug_skip & 4)) {
+      dm = -INFINITY;
       // register passes of DCH float4 per lane (512 docs), so the tile size does not set the
       // register footprint
       constexpr int DCH = F4L < 4 ? F4L : 4;
@@ -670,7 +684,10 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           }
         }
 #pragma unroll
-        for (int rr = 0; rr < DCH; ++rr) dsum4[lane + 32 * (c0 + rr)] = a[rr];
+        for (int rr = 0; rr < DCH; ++rr) {
+          dsum4[lane + 32 * (c0 + rr)] = a[rr];
+          dm = fmaxf(dm, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
+        }
       }
     }
     __syncwarp();
@@ -680,6 +697,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
       const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
+      float lmax = dm;
       if ((hmask & emask) && !(ra.debug_skip & 1)) {
         if (nr > 1) {  // keep the shared dense sum intact for the run's other queries
 #pragma unroll
@@ -687,7 +705,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           __syncwarp();
           buf = s.acc;
         }
-        apply_slices(ix, emask, cnt, rbase, buf, d0);
+        lmax = fmaxf(lmax, apply_slices(ix, emask, cnt, rbase, buf, d0));
       }
       if constexpr (MODE == GM_DENSE) {
         const double qc = ra.qconst[ra.perm[pb + r]];
@@ -699,9 +717,9 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         uint64_t* gp = ra.gtau ? ra.gtau + q : nullptr;
         if (!(ra.debug_skip & 2)) {
           if (nvalid == TILE)
-            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp);
+            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax);
           else
-            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp);
+            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax);
         }
       }
     }
@@ -853,7 +871,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
       const double qc = ra.qconst[q];
       for (uint32_t i = threadIdx.x; i < nvalid; i += NT) ra.dense_out[d0 + i] = __double2float_rn((double)acc[i] + qc);
     } else {
-      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept, nullptr);
+      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept, nullptr, NAN);
     }
     __syncthreads();
   }
