@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       float* buf = s.dsum;
       float lmax = dm;
       if ((hmask & emask) && !(ra.debug_skip & 1)) {
-        if (nr > 1) {  // keep the shared dense sum intact for the run's other queries
+        if (r + 1 < nr) {  // keep the shared dense sum intact for the run's later queries
 #pragma unroll
           for (int rr = 0; rr < F4L; ++rr) acc4[lane + 32 * rr] = dsum4[lane + 32 * rr];
           __syncwarp();
