@@ -278,6 +278,7 @@ struct __align__(16) WarpSmem {
   int32_t dslot[NDMAX];       // the run's dense signature, ascending slots
   uint32_t hist[16];          // warp_select_kth histogram
   uint32_t n_kept[RMAX];
+  uint32_t qid[RMAX];         // original query index of run member r
   int32_t ebeg[RMAX + 1];     // query r owns entries [ebeg[r], ebeg[r+1])
   int32_t nd[1];
 };
@@ -380,7 +381,7 @@ __device__ __forceinline__ float apply_slices(const IndexView& ix, uint32_t emas
 template <bool FULL, class SM>
 __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint32_t C, uint32_t gdoc0,
                                             uint32_t nvalid, const float* buf, uint64_t* kept, uint64_t* gpub,
-                                            float pmax) {
+                                            float pmax, uint64_t g) {
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   uint64_t tau = s.tau[r];
@@ -403,7 +404,6 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
   }
   if (!__any_sync(0xffffffffu, mx > tf || tau == 0)) return;
   if (gpub) {
-    const uint64_t g = *(volatile const uint64_t*)gpub;
     if (g > tau) {
       tau = g;
       tf = tau_float(g);
@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   {
     const bool act = (uint32_t)lane < nr;
     const uint32_t q = act ? ra.perm[pb + lane] : 0u;
+    if (act) s.qid[lane] = q;
     const uint64_t qb = act ? ra.q_off[q] : 0, qe = act ? ra.q_off[q + 1] : 0;
     uint32_t ns = 0, nd = 0;
     for (uint64_t j = qb; j < qe; ++j) {
@@ -698,6 +699,9 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
       float* buf = s.dsum;
       float lmax = dm;
+      const uint32_t q = s.qid[r];
+      uint64_t* gp = ra.gtau ? ra.gtau + q : nullptr;
+      const uint64_t gv = gp ? *(volatile const uint64_t*)gp : 0ull;  // in flight during the gather
       if ((hmask & emask) && !(ra.debug_skip & 1)) {
         if (r + 1 < nr) {  // keep the shared dense sum intact for the run's later queries
 #pragma unroll
@@ -712,14 +716,12 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        const uint32_t q = ra.perm[pb + r];
         uint64_t* kept = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
-        uint64_t* gp = ra.gtau ? ra.gtau + q : nullptr;
         if (!(ra.debug_skip & 2)) {
           if (nvalid == TILE)
-            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax);
+            filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
           else
-            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax);
+            filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
         }
       }
     }
@@ -727,7 +729,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   }
   if constexpr (MODE == GM_TOPK) {
     for (uint32_t r = 0; r < nr; ++r) {
-      const uint32_t q = ra.perm[pb + r];
+      const uint32_t q = s.qid[r];
       const uint32_t nk = s.n_kept[r];
       uint64_t* out = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
       for (uint32_t i = nk + lane; i < ra.C; i += 32) out[i] = kInvalidKey;  // candidates are in place
@@ -871,7 +873,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
       const double qc = ra.qconst[q];
       for (uint32_t i = threadIdx.x; i < nvalid; i += NT) ra.dense_out[d0 + i] = __double2float_rn((double)acc[i] + qc);
     } else {
-      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept, nullptr, NAN);
+      if (warp == 0) filter_tile<false>(ws, 0, ra.k, ra.C, ix.doc_base + d0, nvalid, acc, kept, nullptr, NAN, 0ull);
     }
     __syncthreads();
   }
