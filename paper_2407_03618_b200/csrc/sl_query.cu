@@ -579,11 +579,11 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   const float rmx = PRUNE && ent ? s.rmax[lane] : 0.f;
   const uint32_t* tab = ix.skiptab + (uint64_t)(sk < 0 ? 0 : sk) * (ix.num_tiles + 1);
   uint32_t cursor = 0, nextdoc = 0xFFFFFFFFu;  // short rows
-  uint32_t nsb = 0, ncnt = 0;                  // skip rows: slice of the NEXT tile (prefetched)
+  uint32_t nsb = 0, nse = 0;                   // skip rows: slice [nsb, nse) of the current tile
   if (ent) {
     if (sk >= 0) {
       nsb = __ldg(tab + t0);
-      ncnt = __ldg(tab + t0 + 1) - nsb;
+      nse = __ldg(tab + t0 + 1);
     } else {
       const uint32_t* ids = ix.docids + rstart;
       const uint32_t dstart = t0 * TILE;
@@ -608,11 +608,9 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     if (ent) {
       if (sk >= 0) {
         sb = nsb;
-        cnt = ncnt;
-        if (tile + 1 < t1) {  // prefetch the next tile's slice; consumed one iteration later
-          nsb = __ldg(tab + tile + 1);
-          ncnt = __ldg(tab + tile + 2) - nsb;
-        }
+        cnt = nse - nsb;
+        nsb = nse;  // the next tile's slice starts where this one ends
+        if (tile + 1 < t1) nse = __ldg(tab + tile + 2);  // consumed one iteration later
       } else if (nextdoc < d1) {
         const uint32_t* ids = ix.docids + rstart;
         sb = cursor;
