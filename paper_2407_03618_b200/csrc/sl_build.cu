@@ -166,7 +166,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-// per-tile digit histogram (warp-aggregated with match.any), digit-major output
+// Lanes holding the same digit (among valid lanes): bit-sliced ballots, one per digit bit.
+// (__match_any_sync runs at 1/64 of a shuffle's rate on this GPU: tools/micro/match_bench.cu)
+__device__ __forceinline__ uint32_t digit_peers(uint32_t dg, int bits, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+  for (int b = 0; b < bits; ++b) {
+    const bool on = (dg >> b) & 1u;
+    const uint32_t bb = __ballot_sync(0xffffffffu, on);
+    m &= on ? bb : ~bb;
+  }
+  return m;
+}
+
+// per-tile digit histogram (warp-aggregated by digit peers), digit-major output
 __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __restrict__ keys,
                                                              uint64_t n, int shift, uint32_t mask,
                                                              uint32_t* __restrict__ hist,
@@ -176,6 +188,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
   for (int i = threadIdx.x; i < 256; i += kSortThreads) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const int bits = 32 - __clz(mask);
   const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
   bool bad = false;
 #pragma unroll 4
@@ -184,8 +197,8 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
     const bool valid = i < n;
     uint32_t k = valid ? keys[i] : 0u;
     bad |= valid && k >= V;
-    const uint32_t dg = valid ? ((k >> shift) & mask) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t dg = valid ? ((k >> shift) & mask) : 0u;
+    const uint32_t peers = digit_peers(dg, bits, valid);
     if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[dg], (uint32_t)__popc(peers));
   }
   if (err && bad) atomicOr(err, kErrToken);
@@ -193,7 +206,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
   for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) hist[(uint64_t)dg * n_tiles + blockIdx.x] = sh[dg];
 }
 
-// stable scatter: warp w owns a contiguous 32*IPT sub-tile; ranks via match.any
+// stable scatter: warp w owns a contiguous 32*IPT sub-tile; ranks from digit peers
 __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
@@ -205,6 +218,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)blockIdx.x * kSortTile + (uint64_t)w * 32 * kSortIPT;
   const uint32_t lt = lanemask_lt();
+  const int bits = 32 - __clz(mask);
   uint32_t kk[kSortIPT], vv[kSortIPT], rr[kSortIPT];
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
@@ -217,8 +231,8 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
   for (int j = 0; j < kSortIPT; ++j) {
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     const bool valid = i < n;
-    const uint32_t dg = valid ? ((kk[j] >> shift) & mask) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    const uint32_t dg = valid ? ((kk[j] >> shift) & mask) : 0u;
+    const uint32_t peers = digit_peers(dg, bits, valid);
     const uint32_t before = valid ? wc[w][dg] : 0u;
     rr[j] = before + __popc(peers & lt);
     __syncwarp();
