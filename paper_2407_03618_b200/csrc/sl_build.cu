@@ -206,19 +206,28 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
   for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) hist[(uint64_t)dg * n_tiles + blockIdx.x] = sh[dg];
 }
 
-// stable scatter: warp w owns a contiguous 32*IPT sub-tile; ranks from digit peers
-__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
+// Stable scatter of one tile (kSortTile elements): (1) rank every element within its warp and
+// digit with a per-warp shared counter (one atomicAdd per digit group, the leader's old value
+// shuffled to its peers; no per-element warp barriers), (2) block-wide digit offsets, (3) stage
+// the tile in shared memory in digit order, (4) write each digit's run to its global position
+// with consecutive threads on consecutive addresses (coalesced).
+__global__ void __launch_bounds__(kSortThreads, 3) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
     uint32_t n_tiles) {
   constexpr int NW = kSortThreads / 32;
-  __shared__ uint32_t wc[NW][256];
+  __shared__ uint32_t wc[NW][256];    // per-warp digit counts, then per-warp digit bases
+  __shared__ uint32_t lstart[256];    // block-local start of each digit
+  __shared__ uint32_t gstart[256];    // global start of each digit's run for this tile
+  __shared__ uint32_t skey[kSortTile], sval[kSortTile];
   for (int i = threadIdx.x; i < NW * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t base = (uint64_t)blockIdx.x * kSortTile + (uint64_t)w * 32 * kSortIPT;
+  const uint64_t tile0 = (uint64_t)blockIdx.x * kSortTile;
+  const uint64_t base = tile0 + (uint64_t)w * 32 * kSortIPT;
   const uint32_t lt = lanemask_lt();
   const int bits = 32 - __clz(mask);
+  const uint32_t nd = mask + 1;
   uint32_t kk[kSortIPT], vv[kSortIPT], rr[kSortIPT];
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
@@ -231,22 +240,42 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
   for (int j = 0; j < kSortIPT; ++j) {
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     const bool valid = i < n;
-    const uint32_t dg = valid ? ((kk[j] >> shift) & mask) : 0u;
+    const uint32_t dg = (kk[j] >> shift) & mask;
     const uint32_t peers = digit_peers(dg, bits, valid);
-    const uint32_t before = valid ? wc[w][dg] : 0u;
-    rr[j] = before + __popc(peers & lt);
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wc[w][dg] = before + __popc(peers);
-    __syncwarp();
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) old = atomicAdd(&wc[w][dg], (uint32_t)__popc(peers));
+    rr[j] = __popc(peers & lt);
+    const uint32_t o = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
+    rr[j] += o;
   }
   __syncthreads();
-  for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) {
-    uint32_t run = offs[(uint64_t)dg * n_tiles + blockIdx.x];
+  // per digit: exclusive scan over warps (bases) and the digit's tile total
+  for (uint32_t dg = threadIdx.x; dg < nd; dg += kSortThreads) {
+    uint32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < NW; ++ww) {
       const uint32_t c = wc[ww][dg];
       wc[ww][dg] = run;
       run += c;
+    }
+    lstart[dg] = run;  // total for now
+    gstart[dg] = offs[(uint64_t)dg * n_tiles + blockIdx.x];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the digit totals (<= 256) by one warp
+    uint32_t carry = 0;
+    for (uint32_t d0 = 0; d0 < nd; d0 += 32) {
+      const uint32_t dg = d0 + lane;
+      const uint32_t t = dg < nd ? lstart[dg] : 0u;
+      uint32_t x = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (dg < nd) lstart[dg] = carry + x - t;
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
   }
   __syncthreads();
@@ -255,10 +284,19 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
     const uint64_t i = base + (uint64_t)j * 32 + lane;
     if (i < n) {
       const uint32_t dg = (kk[j] >> shift) & mask;
-      const uint32_t pos = wc[w][dg] + rr[j];
-      kout[pos] = kk[j];
-      vout[pos] = vv[j];
+      const uint32_t lp = lstart[dg] + wc[w][dg] + rr[j];
+      skey[lp] = kk[j];
+      sval[lp] = vv[j];
     }
+  }
+  __syncthreads();
+  const uint32_t cnt = (uint32_t)min((uint64_t)kSortTile, n - tile0);
+  for (uint32_t i = threadIdx.x; i < cnt; i += kSortThreads) {
+    const uint32_t k = skey[i];
+    const uint32_t dg = (k >> shift) & mask;
+    const uint32_t pos = gstart[dg] + (i - lstart[dg]);
+    kout[pos] = k;
+    vout[pos] = sval[i];
   }
 }
 
