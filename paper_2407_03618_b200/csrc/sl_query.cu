@@ -410,23 +410,31 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
       if (!__any_sync(0xffffffffu, mx > tf)) return;
     }
   }
-  auto tile_visit = [&](uint64_t thr, auto&& fn) {
+  // one test pass: bit (4*rr + c) of pm = element passes (key >= tau); later passes walk pm
+  static_assert(F4L * 4 <= 32, "tile elements per lane must fit a 32-bit mask");
+  uint32_t pm = 0;
 #pragma unroll
-    for (int rr = 0; rr < F4L; ++rr) {
-      const float4 v = b4[lane + 32 * rr];
-      const uint32_t dl = 4 * (lane + 32 * rr);
+  for (int rr = 0; rr < F4L; ++rr) {
+    const float4 v = b4[lane + 32 * rr];
+    const uint32_t dl = 4 * (lane + 32 * rr);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float x = f4c(v, c);
-        if ((x > tf || tau == 0) && (FULL || dl + c < nvalid)) {
-          const uint64_t key = make_key(x, gdoc0 + dl + c);
-          if (key >= thr) fn(key);
-        }
+    for (int c = 0; c < 4; ++c) {
+      const float x = f4c(v, c);
+      if ((x > tf || tau == 0) && (FULL || dl + c < nvalid)) {
+        if (make_key(x, gdoc0 + dl + c) >= tau) pm |= 1u << (4 * rr + c);
       }
     }
+  }
+  const float* bf = buf;
+  auto tile_visit = [&](uint64_t thr, auto&& fn) {  // keys >= max(thr, tau) of this lane
+    for (uint32_t m = pm; m; m &= m - 1) {
+      const int bit = __ffs(m) - 1;
+      const uint32_t dl = 4 * (lane + 32 * (bit >> 2)) + (bit & 3);
+      const uint64_t key = make_key(bf[dl], gdoc0 + dl);
+      if (key >= thr) fn(key);
+    }
   };
-  uint32_t mine = 0;
-  tile_visit(tau, [&](uint64_t) { ++mine; });
+  const uint32_t mine = __popc(pm);
   const uint32_t incl = warp_incl_scan(mine);
   const uint32_t P = __shfl_sync(0xffffffffu, incl, 31);
   const uint32_t nk = s.n_kept[r];
