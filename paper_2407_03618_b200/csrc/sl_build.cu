@@ -12,6 +12,7 @@
 // per-tile skip offsets) that sl_query.cu consumes.
 // Everything is HBM-streaming integer work; no tensor cores are involved.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -613,7 +614,32 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.25;
   const double dense_thr = density * (double)ix->N_global;
-  const uint64_t skip_thr = 4ull * ix->num_tiles;  // >= 4 postings per tile expected
+  // Per-tile skip tables for rows with >= SL_SKIP_PER_TILE postings per tile on average: a
+  // prefetched table entry beats probing the row's doc ids from one posting per few tiles on
+  // (c2 top-10: 4 -> 0.25 postings/tile +4.5%). Tables cost (tiles+1) x 4 B per row, so they
+  // are held to half the CSC's bytes: beyond that budget only the longest rows get one.
+#ifndef SL_SKIP_PER_TILE
+#define SL_SKIP_PER_TILE 0.25
+#endif
+  uint64_t skip_thr = std::max<uint64_t>(1, (uint64_t)(SL_SKIP_PER_TILE * ix->num_tiles));
+  {
+    const uint64_t row_bytes = ((uint64_t)ix->num_tiles + 1) * 4;
+    const uint64_t budget = std::max<uint64_t>(4 * ix->nnz, 64ull << 20);
+    std::vector<uint64_t> cand;
+    for (uint32_t t = 0; t < V; ++t) {
+      const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
+      if (dl >= skip_thr && h_df[t] && (double)h_df[t] < dense_thr) cand.push_back(dl);
+    }
+    const uint64_t max_rows = budget / row_bytes;
+    if (cand.size() > max_rows) {
+      if (max_rows == 0) {
+        skip_thr = UINT64_MAX;
+      } else {
+        std::nth_element(cand.begin(), cand.begin() + (max_rows - 1), cand.end(), std::greater<uint64_t>());
+        skip_thr = cand[max_rows - 1] + 1;  // strictly above: ties beyond the budget are dropped
+      }
+    }
+  }
   std::vector<int32_t> info(V, -1);
   std::vector<uint32_t> dense_tok, skip_tok;
   for (uint32_t t = 0; t < V; ++t) {
