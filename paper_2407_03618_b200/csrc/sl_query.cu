@@ -214,7 +214,10 @@ __device__ __forceinline__ float f4c(const float4& v, int c) {
 enum GroupMode { GM_TOPK = 0, GM_DENSE = 1 };
 
 constexpr int RMAX = 2;      // queries per run (same dense signature) handled by one warp
-constexpr int UNROLL = 4;    // gather rounds whose loads are issued together
+#ifndef SL_UNROLL
+#define SL_UNROLL 4
+#endif
+constexpr int UNROLL = SL_UNROLL;  // gather rounds whose loads are issued together
 
 struct RunArgs {
   const uint64_t* q_off;      // [B+1]
