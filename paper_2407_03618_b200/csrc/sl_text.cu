@@ -906,6 +906,75 @@ __global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __r
   }
 }
 
+// ------------------------------------------------------------------ raw-string dedup
+// Normalisation (lowercase, stopwords, stemming) is a function of the token's raw bytes, and a
+// Zipf corpus repeats a few hundred thousand surface forms tens of millions of times: the raw
+// strings are deduplicated first (two 64-bit hashes per token, an L2-resident table) and only
+// the distinct ones are normalised.
+__global__ void k_raw_hash(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
+                           const uint32_t* __restrict__ tlen, uint64_t n, uint64_t* __restrict__ h1,
+                           uint64_t* __restrict__ h2) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const H2 h = hash2(text + tbeg[i], tlen[i]);
+    h1[i] = h.a;
+    h2[i] = h.b;
+  }
+}
+
+// table of distinct raw strings: key = first hash, first = smallest token index
+__global__ void k_raw_insert(const uint64_t* __restrict__ h1, uint64_t n, uint64_t* __restrict__ key,
+                             uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = h1[i];
+    uint32_t slot = (uint32_t)k & (cap - 1);
+    for (uint32_t probes = 0;; ++probes) {
+      if (probes == cap) {
+        atomicOr(cnt + 1, 1u);
+        break;
+      }
+      unsigned long long cur = key[slot];  // plain read first: repeated strings skip the atomics
+      if (cur == 0ull) cur = atomicCAS((unsigned long long*)key + slot, 0ull, (unsigned long long)k);
+      if (cur == 0ull || cur == k) {
+        if (cur == 0ull) atomicAdd(cnt, 1u);
+        if (*(volatile uint32_t*)(first + slot) > (uint32_t)i) atomicMin(first + slot, (uint32_t)i);
+        break;
+      }
+      slot = (slot + 1) & (cap - 1);
+    }
+  }
+}
+
+// raw entry of every token; identity checked against the entry's first token (2nd hash, length)
+__global__ void k_raw_assign(const uint64_t* __restrict__ h1, const uint64_t* __restrict__ h2,
+                             const uint32_t* __restrict__ tlen, uint64_t n, const uint64_t* __restrict__ key,
+                             const uint32_t* __restrict__ first, const uint32_t* __restrict__ rank, uint32_t cap,
+                             uint32_t* __restrict__ tr, uint32_t* __restrict__ err) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = h1[i];
+    uint32_t slot = (uint32_t)k & (cap - 1);
+    while (key[slot] != k) slot = (slot + 1) & (cap - 1);
+    const uint32_t f = first[slot];
+    if (h2[f] != h2[i] || tlen[f] != tlen[i]) atomicOr(err, 1u);
+    tr[i] = rank[slot];
+  }
+}
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
+                             uint64_t* __restrict__ out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
+}
+
+// per token: keep flag and id of its raw entry
+__global__ void k_raw_expand(const uint32_t* __restrict__ tr, uint64_t n, const uint32_t* __restrict__ rkeep,
+                             const uint32_t* __restrict__ rid, uint32_t* __restrict__ keep,
+                             uint32_t* __restrict__ id) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = tr[i];
+    keep[i] = rkeep[r];
+    id[i] = rid[r];
+  }
+}
+
 // ------------------------------------------------------------------ host side
 inline unsigned grid_for(uint64_t n, int per = 256) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, 148ull * 64));
@@ -1158,37 +1227,94 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     if (!stab.bytes.empty()) cudaMemcpyAsync(by, stab.bytes.data(), stab.bytes.size(), cudaMemcpyHostToDevice, st);
     sv = StopView{k, o, l, by, stab.cap, stab.max_len};
   }
+  uint32_t* err;
+  SL_TTRY(scr.alloc(&err, 1));
+  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
+  // ---- distinct raw strings: entry r in first-occurrence order, tr[i] = entry of token i
+  uint32_t R = 0;
+  uint32_t* tr = nullptr;
+  uint64_t* rbeg = nullptr;
+  uint32_t* rlen = nullptr;
+  SL_TTRY(scr.alloc(&tr, n_tok));
+  if (n_tok) {
+    uint64_t *rh1, *rh2;
+    SL_TTRY(scr.alloc(&rh1, n_tok));
+    SL_TTRY(scr.alloc(&rh2, n_tok));
+    k_raw_hash<<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, rh1, rh2); ++t_launches;
+    uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 22));
+    uint64_t* key = nullptr;
+    uint32_t *first = nullptr, *cntr = nullptr;
+    SL_TTRY(scr.alloc(&cntr, 2));
+    for (;;) {
+      SL_TTRY(scr.alloc(&key, cap));
+      SL_TTRY(scr.alloc(&first, cap));
+      if (cudaMemsetAsync(key, 0, cap * 8, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
+          cudaMemsetAsync(cntr, 0, 8, st) != cudaSuccess)
+        return fail((set_error("memset"), SL_ECUDA));
+      k_raw_insert<<<grid_for(n_tok), 256, 0, st>>>(rh1, n_tok, key, first, (uint32_t)cap, cntr); ++t_launches;
+      uint32_t h[2];
+      SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 8, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+      if (!h[1] && (uint64_t)h[0] * 2 <= cap) break;
+      if (cap >= (1ull << 31)) return fail((set_error("tokenize: too many distinct tokens in one batch"), SL_EUNSUPPORTED));
+      cap = std::min<uint64_t>(cap * 4, 1ull << 31);
+    }
+    uint32_t *sflag, *spos, *slots, *fk, *k0, *k1, *v0, *v1, *rank, *repf;
+    SL_TTRY(scr.alloc(&sflag, cap));
+    SL_TTRY(scr.alloc(&spos, cap));
+    SL_TTRY(scr.alloc(&rank, cap));
+    k_slot_flags<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
+    SL_TTRY(exclusive_scan_u32(sflag, spos, cap, st, &R));
+    SL_TTRY(scr.alloc(&slots, R));
+    SL_TTRY(scr.alloc(&fk, R));
+    SL_TTRY(scr.alloc(&k0, R));
+    SL_TTRY(scr.alloc(&k1, R));
+    SL_TTRY(scr.alloc(&v0, R));
+    SL_TTRY(scr.alloc(&v1, R));
+    SL_TTRY(scr.alloc(&repf, R));
+    k_slot_list<<<grid_for(cap), 256, 0, st>>>(sflag, spos, first, (uint32_t)cap, slots, fk); ++t_launches;
+    const uint32_t *fs, *ss;
+    SL_TTRY(radix_sort_pairs(fk, slots, R, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
+    SL_CUDA_TRY(cudaMemcpyAsync(repf, fs, R * 4ull, cudaMemcpyDeviceToDevice, st));  // first token of entry r
+    k_group_rank<<<grid_for(R), 256, 0, st>>>(ss, R, rank); ++t_launches;            // slot -> r
+    k_raw_assign<<<grid_for(n_tok), 256, 0, st>>>(rh1, rh2, tlen, n_tok, key, first, rank, (uint32_t)cap, tr, err);
+    ++t_launches;
+    SL_TTRY(scr.alloc(&rbeg, R));
+    SL_TTRY(scr.alloc(&rlen, R));
+    k_gather_u64<<<grid_for(R), 256, 0, st>>>(tbeg, repf, R, rbeg); ++t_launches;
+    k_gather_u32<<<grid_for(R), 256, 0, st>>>(tlen, repf, R, rlen); ++t_launches;
+  }
+  // normalisation works on the R distinct raw strings ("tokens" below are raw entries)
+  const uint64_t n_all = n_tok;
   NormArgs na{};
   na.t = TextView{text, nb, dbits};
-  na.tbeg = tbeg;
-  na.tlen = tlen;
-  na.n_tok = n_tok;
+  na.tbeg = rbeg;
+  na.tlen = rlen;
+  na.n_tok = R;
   na.lowercase = cfg->lowercase ? 1 : 0;
   na.stem = cfg->stemmer == SL_STEMMER_SNOWBALL_ENGLISH ? 1 : 0;
   na.stop = sv;
   na.voc = VocabView{v->tkey, v->tval, v->V ? v->tcap : 0u, v->offs, v->h2, v->bytes};
-  uint32_t* err;
-  SL_TTRY(scr.alloc(&err, 1));
-  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
   na.err = err;
-  SL_TTRY(scr.alloc(&na.keep, n_tok));
-  SL_TTRY(scr.alloc(&na.id, n_tok));
-  SL_TTRY(scr.alloc(&na.flen, n_tok));
-  SL_TTRY(scr.alloc(&na.h1, n_tok));
-  SL_TTRY(scr.alloc(&na.h2, n_tok));
-  SL_TTRY(scr.alloc(&na.long_flag, n_tok));
+  const uint64_t nR = R;
+  SL_TTRY(scr.alloc(&na.keep, nR));
+  SL_TTRY(scr.alloc(&na.id, nR));
+  SL_TTRY(scr.alloc(&na.flen, nR));
+  SL_TTRY(scr.alloc(&na.h1, nR));
+  SL_TTRY(scr.alloc(&na.h2, nR));
+  SL_TTRY(scr.alloc(&na.long_flag, nR));
   if (build) SL_TTRY(scr.alloc(&na.arena, 2 * nb));
-  if (n_tok) {
-    k_norm_fast<<<grid_for(n_tok, 128), 128, 0, st>>>(na); ++t_launches;
+  if (nR) {
+    k_norm_fast<<<grid_for(nR, 128), 128, 0, st>>>(na); ++t_launches;
     // deferred long tokens
     uint32_t* lpos;
-    SL_TTRY(scr.alloc(&lpos, n_tok));
+    SL_TTRY(scr.alloc(&lpos, nR));
     uint32_t n_long = 0;
-    SL_TTRY(exclusive_scan_u32(na.long_flag, lpos, n_tok, st, &n_long));
+    SL_TTRY(exclusive_scan_u32(na.long_flag, lpos, nR, st, &n_long));
     if (n_long) {
       uint32_t* list;
       SL_TTRY(scr.alloc(&list, n_long));
-      k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(na.long_flag, lpos, n_tok, list); ++t_launches;
+      k_compact_idx<<<grid_for(nR), 256, 0, st>>>(na.long_flag, lpos, nR, list); ++t_launches;
       // per long token scratch: 5 * len + 1 bytes
       std::vector<uint64_t> so(n_long + 1, 0);
       {
@@ -1208,31 +1334,18 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
       k_norm_long<<<grid_for(n_long, 64), 64, 0, st>>>(na, list, n_long, dso, scratch); ++t_launches;
     }
   }
-  // ---- kept tokens
-  uint32_t *kflag, *kpos, *kidx;
-  SL_TTRY(scr.alloc(&kflag, n_tok));
-  SL_TTRY(scr.alloc(&kpos, n_tok));
-  if (n_tok) {
-    k_flag_to_u32<<<grid_for(n_tok), 256, 0, st>>>(na.keep, na.id, n_tok, kflag, build ? 0 : 2); ++t_launches;
-  }
-  uint32_t T = 0;
-  SL_TTRY(exclusive_scan_u32(kflag, kpos, n_tok, st, &T));
-  SL_TTRY(scr.alloc(&kidx, T));
-  if (n_tok) {
-    k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(kflag, kpos, n_tok, kidx); ++t_launches;
-  }
   // ---- new vocabulary entries (build mode)
-  if (build && T) {
+  if (build && R) {
     uint32_t *nflag, *npos;
-    SL_TTRY(scr.alloc(&nflag, n_tok));
-    SL_TTRY(scr.alloc(&npos, n_tok));
-    k_flag_to_u32<<<grid_for(n_tok), 256, 0, st>>>(na.keep, na.id, n_tok, nflag, 1); ++t_launches;
+    SL_TTRY(scr.alloc(&nflag, nR));
+    SL_TTRY(scr.alloc(&npos, nR));
+    k_flag_to_u32<<<grid_for(nR), 256, 0, st>>>(na.keep, na.id, nR, nflag, 1); ++t_launches;
     uint32_t M = 0;
-    SL_TTRY(exclusive_scan_u32(nflag, npos, n_tok, st, &M));
+    SL_TTRY(exclusive_scan_u32(nflag, npos, nR, st, &M));
     if (M) {
       uint32_t *ntok, *slots, *fk, *k0, *k1, *v0, *v1, *elen, *epos, *cnt2;
       SL_TTRY(scr.alloc(&ntok, M));
-      k_compact_idx<<<grid_for(n_tok), 256, 0, st>>>(nflag, npos, n_tok, ntok); ++t_launches;
+      k_compact_idx<<<grid_for(nR), 256, 0, st>>>(nflag, npos, nR, ntok); ++t_launches;
       // distinct new strings: batch-local hash table keyed by the first hash, value = the
       // smallest token index (first occurrence); grows and retries on overflow
       uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(M, 1ull << 22));
@@ -1293,12 +1406,32 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
         return fail(SL_EUNSUPPORTED);
       }
       SL_TTRY(vocab_reserve(v, (uint64_t)V0 + G, v->bused + ebytes, st));
-      k_copy_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, tbeg, na.flen, na.arena, epos, v->bused, V0, na.h2,
+      k_copy_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, na.tbeg, na.flen, na.arena, epos, v->bused, V0, na.h2,
                                                   v->bytes, v->offs, v->h2); ++t_launches;
       k_table_insert<<<grid_for(G), 256, 0, st>>>(na.h1, gs_k, G, V0, v->tkey, v->tval, v->tcap, err); ++t_launches;
       v->V = V0 + G;
       v->bused += ebytes;
     }
+  }
+  // ---- every token takes its raw entry's keep flag and id
+  uint32_t *tkeep, *tid;
+  SL_TTRY(scr.alloc(&tkeep, n_all));
+  SL_TTRY(scr.alloc(&tid, n_all));
+  if (n_all) {
+    k_raw_expand<<<grid_for(n_all), 256, 0, st>>>(tr, n_all, na.keep, na.id, tkeep, tid); ++t_launches;
+  }
+  // ---- kept tokens
+  uint32_t *kflag, *kpos, *kidx;
+  SL_TTRY(scr.alloc(&kflag, n_all));
+  SL_TTRY(scr.alloc(&kpos, n_all));
+  if (n_all) {
+    k_flag_to_u32<<<grid_for(n_all), 256, 0, st>>>(tkeep, tid, n_all, kflag, build ? 0 : 2); ++t_launches;
+  }
+  uint32_t T = 0;
+  SL_TTRY(exclusive_scan_u32(kflag, kpos, n_all, st, &T));
+  SL_TTRY(scr.alloc(&kidx, T));
+  if (n_all) {
+    k_compact_idx<<<grid_for(n_all), 256, 0, st>>>(kflag, kpos, n_all, kidx); ++t_launches;
   }
   // ---- outputs
   tb->T = T;
@@ -1307,7 +1440,7 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   uint64_t* kbeg;
   SL_TTRY(scr.alloc(&kbeg, T));
   if (T) {
-    k_out_ids<<<grid_for(T), 256, 0, st>>>(kidx, T, na.id, tbeg, tb->ids, kbeg); ++t_launches;
+    k_out_ids<<<grid_for(T), 256, 0, st>>>(kidx, T, tid, tbeg, tb->ids, kbeg); ++t_launches;
   }
   k_doc_token_offsets<<<grid_for((uint64_t)N + 1), 256, 0, st>>>(doc_off, N, kbeg, T, tb->offs); ++t_launches;
   uint32_t h_err = 0;
