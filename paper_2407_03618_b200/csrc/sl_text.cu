@@ -911,21 +911,22 @@ __global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __r
 // Zipf corpus repeats a few hundred thousand surface forms tens of millions of times: the raw
 // strings are deduplicated first (two 64-bit hashes per token, an L2-resident table) and only
 // the distinct ones are normalised.
-__global__ void k_raw_hash(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
-                           const uint32_t* __restrict__ tlen, uint64_t n, uint64_t* __restrict__ h1,
-                           uint64_t* __restrict__ h2) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const H2 h = hash2(text + tbeg[i], tlen[i]);
-    h1[i] = h.a;
-    h2[i] = h.b;
-  }
-}
-
-// table of distinct raw strings: key = first hash, first = smallest token index
-__global__ void k_raw_insert(const uint64_t* __restrict__ h1, uint64_t n, uint64_t* __restrict__ key,
+// table of distinct raw strings: key = first hash, first = smallest token index. HASH: the
+// hashes are computed here (first attempt) instead of read back (retry after a table overflow).
+template <bool HASH>
+__global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
+                             const uint32_t* __restrict__ tlen, uint64_t* __restrict__ h1,
+                             uint64_t* __restrict__ h2, uint64_t n, uint64_t* __restrict__ key,
                              uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = h1[i];
+    uint64_t k;
+    if (HASH) {
+      const H2 h = hash2(text + tbeg[i], tlen[i]);
+      h1[i] = k = h.a;
+      h2[i] = h.b;
+    } else {
+      k = h1[i];
+    }
     uint32_t slot = (uint32_t)k & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
@@ -944,35 +945,30 @@ __global__ void k_raw_insert(const uint64_t* __restrict__ h1, uint64_t n, uint64
   }
 }
 
-// raw entry of every token; identity checked against the entry's first token (2nd hash, length)
+// per token: its raw entry (identity checked against the entry's first token: second hash,
+// length), then the entry's id and the kept flag (build: not a stopword; query: also in the
+// vocabulary)
 __global__ void k_raw_assign(const uint64_t* __restrict__ h1, const uint64_t* __restrict__ h2,
                              const uint32_t* __restrict__ tlen, uint64_t n, const uint64_t* __restrict__ key,
                              const uint32_t* __restrict__ first, const uint32_t* __restrict__ rank, uint32_t cap,
-                             uint32_t* __restrict__ tr, uint32_t* __restrict__ err) {
+                             const uint32_t* __restrict__ rkeep, const uint32_t* __restrict__ rid, int build,
+                             uint32_t* __restrict__ id, uint32_t* __restrict__ kflag, uint32_t* __restrict__ err) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = h1[i];
     uint32_t slot = (uint32_t)k & (cap - 1);
     while (key[slot] != k) slot = (slot + 1) & (cap - 1);
     const uint32_t f = first[slot];
     if (h2[f] != h2[i] || tlen[f] != tlen[i]) atomicOr(err, 1u);
-    tr[i] = rank[slot];
+    const uint32_t r = rank[slot];
+    const uint32_t t = rid[r];
+    id[i] = t;
+    kflag[i] = rkeep[r] && (build || t != kNew);
   }
 }
 
 __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t n,
                              uint64_t* __restrict__ out) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
-}
-
-// per token: keep flag and id of its raw entry
-__global__ void k_raw_expand(const uint32_t* __restrict__ tr, uint64_t n, const uint32_t* __restrict__ rkeep,
-                             const uint32_t* __restrict__ rid, uint32_t* __restrict__ keep,
-                             uint32_t* __restrict__ id) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = tr[i];
-    keep[i] = rkeep[r];
-    id[i] = rid[r];
-  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -1232,26 +1228,32 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
   // ---- distinct raw strings: entry r in first-occurrence order, tr[i] = entry of token i
   uint32_t R = 0;
-  uint32_t* tr = nullptr;
   uint64_t* rbeg = nullptr;
   uint32_t* rlen = nullptr;
-  SL_TTRY(scr.alloc(&tr, n_tok));
+  uint64_t *r_h1 = nullptr, *r_h2 = nullptr, *r_key = nullptr;
+  uint32_t *r_first = nullptr, *r_rank = nullptr;
+  uint64_t r_cap = 0;
   if (n_tok) {
     uint64_t *rh1, *rh2;
     SL_TTRY(scr.alloc(&rh1, n_tok));
     SL_TTRY(scr.alloc(&rh2, n_tok));
-    k_raw_hash<<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, rh1, rh2); ++t_launches;
     uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 22));
     uint64_t* key = nullptr;
     uint32_t *first = nullptr, *cntr = nullptr;
     SL_TTRY(scr.alloc(&cntr, 2));
-    for (;;) {
+    for (bool hashed = false;; hashed = true) {
       SL_TTRY(scr.alloc(&key, cap));
       SL_TTRY(scr.alloc(&first, cap));
       if (cudaMemsetAsync(key, 0, cap * 8, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
           cudaMemsetAsync(cntr, 0, 8, st) != cudaSuccess)
         return fail((set_error("memset"), SL_ECUDA));
-      k_raw_insert<<<grid_for(n_tok), 256, 0, st>>>(rh1, n_tok, key, first, (uint32_t)cap, cntr); ++t_launches;
+      if (!hashed)
+        k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, rh1, rh2, n_tok, key, first,
+                                                            (uint32_t)cap, cntr);
+      else
+        k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, rh1, rh2, n_tok, key, first,
+                                                             (uint32_t)cap, cntr);
+      ++t_launches;
       uint32_t h[2];
       SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 8, cudaMemcpyDeviceToHost, st));
       SL_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1277,8 +1279,12 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     SL_TTRY(radix_sort_pairs(fk, slots, R, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
     SL_CUDA_TRY(cudaMemcpyAsync(repf, fs, R * 4ull, cudaMemcpyDeviceToDevice, st));  // first token of entry r
     k_group_rank<<<grid_for(R), 256, 0, st>>>(ss, R, rank); ++t_launches;            // slot -> r
-    k_raw_assign<<<grid_for(n_tok), 256, 0, st>>>(rh1, rh2, tlen, n_tok, key, first, rank, (uint32_t)cap, tr, err);
-    ++t_launches;
+    r_h1 = rh1;
+    r_h2 = rh2;
+    r_key = key;
+    r_first = first;
+    r_rank = rank;
+    r_cap = cap;
     SL_TTRY(scr.alloc(&rbeg, R));
     SL_TTRY(scr.alloc(&rlen, R));
     k_gather_u64<<<grid_for(R), 256, 0, st>>>(tbeg, repf, R, rbeg); ++t_launches;
@@ -1413,19 +1419,15 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
       v->bused += ebytes;
     }
   }
-  // ---- every token takes its raw entry's keep flag and id
-  uint32_t *tkeep, *tid;
-  SL_TTRY(scr.alloc(&tkeep, n_all));
+  // ---- every token takes its raw entry's id; kept flags
+  uint32_t *tid, *kflag, *kpos, *kidx;
   SL_TTRY(scr.alloc(&tid, n_all));
-  if (n_all) {
-    k_raw_expand<<<grid_for(n_all), 256, 0, st>>>(tr, n_all, na.keep, na.id, tkeep, tid); ++t_launches;
-  }
-  // ---- kept tokens
-  uint32_t *kflag, *kpos, *kidx;
   SL_TTRY(scr.alloc(&kflag, n_all));
   SL_TTRY(scr.alloc(&kpos, n_all));
   if (n_all) {
-    k_flag_to_u32<<<grid_for(n_all), 256, 0, st>>>(tkeep, tid, n_all, kflag, build ? 0 : 2); ++t_launches;
+    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_h1, r_h2, tlen, n_all, r_key, r_first, r_rank, (uint32_t)r_cap,
+                                                  na.keep, na.id, build ? 1 : 0, tid, kflag, err);
+    ++t_launches;
   }
   uint32_t T = 0;
   SL_TTRY(exclusive_scan_u32(kflag, kpos, n_all, st, &T));
