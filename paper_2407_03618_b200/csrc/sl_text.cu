@@ -244,6 +244,80 @@ __global__ void k_classify(TextView t, uint32_t* __restrict__ wbits, uint32_t* _
   }
 }
 
+// byte b's (word, codepoint-start) flags, the general path of k_classify
+__device__ __forceinline__ void classify_byte(const TextView& t, uint64_t b, bool& word, bool& start) {
+  const uint32_t x = byte_at(t, (int64_t)b);
+  uint32_t cp = 0;
+  int L = 0;
+  bool covered = false;
+  if ((x & 0xC0) == 0x80) {  // continuation byte: inside the nearest preceding valid sequence?
+    for (int back = 1; back <= 3 && (int64_t)b - back >= 0; ++back) {
+      const uint64_t q = b - back;
+      if (dstart_at(t, q + 1)) break;  // q is in an earlier document
+      const uint32_t y = byte_at(t, (int64_t)q);
+      if ((y & 0xC0) == 0x80) continue;
+      if (valid_at(t, q, &cp, &L) && q + L > b) covered = true;
+      break;
+    }
+  }
+  start = !covered;
+  if (!covered) {
+    if (x < 0x80) cp = x;
+    else if (!valid_at(t, b, &cp, &L)) cp = 0xFFFD;
+  }
+  word = is_word_cp(cp);
+}
+
+// Four bytes per thread from one aligned 32-bit load: an all-ASCII group (the common case)
+// classifies in registers; any other group takes classify_byte. Eight lanes' nibbles OR
+// into one bitmap word. Requires a 4-byte-aligned text pointer.
+__global__ void k_classify4(TextView t, uint32_t* __restrict__ wbits, uint32_t* __restrict__ sbits) {
+  const uint64_t nq = (t.n + 3) >> 2;                 // 4-byte groups
+  const uint64_t nq_pad = ((nq + 31) >> 5) << 5;      // whole warps iterate together
+  const int lane = threadIdx.x & 31;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nq_pad; g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t wn = 0, sn = 0;  // nibbles
+    const uint64_t b0 = g << 2;
+    if (b0 + 4 <= t.n) {
+      const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(t.text) + g);
+      if (!(v & 0x80808080u)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t c = (v >> (8 * j)) & 0xFFu;
+          const bool w = (c - '0' < 10u) || ((c | 0x20u) - 'a' < 26u) || c == '_';
+          wn |= (uint32_t)w << j;
+        }
+        sn = wn;  // ASCII bytes are codepoint starts
+      } else {
+        for (int j = 0; j < 4; ++j) {
+          bool w, st;
+          classify_byte(t, b0 + j, w, st);
+          wn |= (uint32_t)w << j;
+          sn |= (uint32_t)(w && st) << j;
+        }
+      }
+    } else if (b0 < t.n) {
+      for (int j = 0; j < 4 && b0 + j < t.n; ++j) {
+        bool w, st;
+        classify_byte(t, b0 + j, w, st);
+        wn |= (uint32_t)w << j;
+        sn |= (uint32_t)(w && st) << j;
+      }
+    }
+    uint32_t wv = wn << (4 * (lane & 7)), sv = sn << (4 * (lane & 7));
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      wv |= __shfl_xor_sync(0xffffffffu, wv, o);
+      sv |= __shfl_xor_sync(0xffffffffu, sv, o);
+    }
+    const uint64_t word_idx = g >> 3;
+    if ((lane & 7) == 0 && (word_idx << 5) < t.n) {
+      wbits[word_idx] = wv;
+      sbits[word_idx] = sv;
+    }
+  }
+}
+
 // token ending at the first non-word byte or document start after p; codepoint count
 __device__ __forceinline__ void token_extent(const uint32_t* wbits, const uint32_t* sbits, const uint32_t* dbits,
                                              uint64_t nw, uint64_t p, uint64_t* end, uint32_t* ncp) {
@@ -1194,7 +1268,11 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     if (cudaMemsetAsync(dbits, 0, nw * 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
     k_doc_marks<<<grid_for(N), 256, 0, st>>>(doc_off, N, nb, dbits); ++t_launches;
     const TextView tv{text, nb, dbits};
-    k_classify<<<grid_for(nw * 32), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+    if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0) {
+      k_classify4<<<grid_for((nb + 3) / 4), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+    } else {
+      k_classify<<<grid_for(nw * 32), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+    }
     k_tokens<false><<<grid_for(nw), 256, 0, st>>>(wbits, sbits, dbits, nw, cnt, nullptr, nullptr, nullptr);
     ++t_launches;
     uint32_t tot = 0;

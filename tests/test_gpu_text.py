@@ -205,3 +205,21 @@ def test_text_index_errors(cuda_ok):
     off = np.array([1, 2], np.uint64)
     with pytest.raises(ValueError, match="doc_offsets"):
         T.tokenize_build((b"ab", off), T.TokenizerConfig(), v)
+
+
+def test_device_input_unaligned(cuda_ok, port):
+    """Device-resident text (zero-copy) at an odd address takes the byte-wise classifier."""
+    import torch
+    from paper_2407_03618_b200._lib import SL_MEM_DEVICE
+    words = make_words(2000, seed=61, unicode_frac=0.1)
+    text, off = make_corpus(500, words, seed=3, malformed_frac=0.02)
+    want = port.tokenize_corpus(text, off, 1, 1, 1)
+    for shift in (0, 1, 3):
+        buf = torch.zeros(len(text) + 8, dtype=torch.uint8, device="cuda")
+        buf[shift:shift + len(text)] = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+        doff = torch.from_numpy(off.view(np.int64)).cuda()
+        v = T.Vocabulary()
+        b = T._tokenize_raw(buf.data_ptr() + shift, doff.data_ptr(), len(off) - 1, cfg_of(1, 1, 1), v, True,
+                            SL_MEM_DEVICE)
+        got_off, got_ids = b.to_numpy()
+        assert np.array_equal(got_off, want[0]) and np.array_equal(got_ids, want[1]) and v.tokens() == want[2], shift
