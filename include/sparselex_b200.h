@@ -89,7 +89,7 @@ typedef struct {
   int32_t device;              /* CUDA device ordinal */
   int32_t keep_tf;             /* keep per-nonzero tf for sl_index_export (debug/parity) */
   float dense_min_density;     /* rows with global df >= density * N_global get a dense
-                                  query-side copy; <= 0 selects the default (0.25) */
+                                  query-side copy; <= 0 selects the default (0.125) */
   sl_comm* comm;               /* NULL = single shard */
   /* Optional precomputed GLOBAL statistics (host memory). When global_df != NULL the
    * build uses them instead of its own counts / the NCCL all-reduce: df[V] summed over all
