@@ -247,6 +247,9 @@ def run_ours(args):
     offsets = synth.doc_offsets(cfg)
     if args.shard_of > 1:  # one GPU builds shard `shard_index` of a shard_of-way sharding (c5 memory plan)
         d0, d1 = shard_ranges(offsets, args.shard_of)[args.shard_index]
+        # the library caps dense copies by the GLOBAL doc count (12 GB / 4N rows); a shard built
+        # with shard-local statistics would not see the full corpus's cap, so pass it explicitly
+        os.environ.setdefault("SL_DENSE_MAX_ROWS", str((12 << 30) // (4 * cfg.num_docs)))
     else:
         d0, d1 = shard_ranges(offsets, world)[rank]
     o0, o1 = int(offsets[d0]), int(offsets[d1])

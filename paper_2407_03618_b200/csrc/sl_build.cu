@@ -612,8 +612,29 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   SL_CUDA_TRY(cudaMemcpyAsync(h_df.data(), ix->df_global, (uint64_t)V * 4, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaMemcpyAsync(h_ptr.data(), ix->indptr, ((uint64_t)V + 1) * 8, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
-  const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.125;  // c2 top-10: 0.25 -> 0.125 +2.4%, 1/16 worse
-  const double dense_thr = density * (double)ix->N_global;
+  // Dense copies: rows with global df >= N/8 (c2 top-10: N/4 -> N/8 +2.4%, N/16 worse). By
+  // default their global footprint is capped at 12 GB (at most 12 GB / (4 N) rows, highest df
+  // first): c5's 50M docs would otherwise take 141 rows, whose chunks crowd L2 (c5 shard
+  // top-100 -8% against the 59 rows of N/4). The cap uses only global quantities, so every
+  // shard of any sharding classifies the same rows (identical per-document summation order).
+  const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.125;
+  double dense_thr = density * (double)ix->N_global;
+  if (!(dense_min_density > 0.f) && ix->N_global) {
+    uint64_t max_rows = (12ull << 30) / (4ull * ix->N_global);
+    if (const char* e = std::getenv("SL_DENSE_MAX_ROWS"))  // bench: a one-GPU stand-in for one shard
+      if (*e) max_rows = std::strtoull(e, nullptr, 10);     // of a larger corpus uses the corpus's cap
+    std::vector<uint32_t> cand;
+    for (uint32_t t = 0; t < V; ++t)
+      if (h_df[t] && (double)h_df[t] >= dense_thr) cand.push_back(h_df[t]);
+    if (cand.size() > max_rows) {
+      if (max_rows == 0) {
+        dense_thr = INFINITY;
+      } else {
+        std::nth_element(cand.begin(), cand.begin() + (max_rows - 1), cand.end(), std::greater<uint32_t>());
+        dense_thr = (double)cand[max_rows - 1] + 1.0;  // strictly above: ties past the cap stay sparse
+      }
+    }
+  }
   // Per-tile skip tables for rows with >= SL_SKIP_PER_TILE postings per tile on average: a
   // prefetched table entry beats probing the row's doc ids from one posting per few tiles on
   // (c2 top-10: 4 -> 0.25 postings/tile +4.5%). Tables cost (tiles+1) x 4 B per row, so they

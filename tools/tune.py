@@ -28,6 +28,7 @@ def main():
     if a.shard_of > 1:  # one shard of a document-sharded corpus (c5 on one GPU)
         from paper_2407_03618_b200 import shard_ranges
         d0, d1 = shard_ranges(off, a.shard_of)[0]
+        os.environ.setdefault("SL_DENSE_MAX_ROWS", str((12 << 30) // (4 * cfg.num_docs)))  # the full corpus's cap
         off = (off[d0:d1 + 1] - off[d0]).astype(np.uint64)
         base = int(synth.doc_offsets(cfg, 0, d0)[-1]) if d0 else 0
     else:
