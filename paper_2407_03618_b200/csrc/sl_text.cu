@@ -1019,24 +1019,44 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
   }
 }
 
+// per occupied slot of the raw table: what a token needs to verify and resolve its entry
+// (second hash and length of the entry's first token, its entry's id and kept flag), packed
+// in one 16-byte record so a token's lookup touches two sectors (key, record)
+struct RawSlot {
+  uint64_t h2;
+  uint32_t len;
+  uint32_t ik;  // entry id (31 bits: ids < 2^31 or kNew) | kept << 31
+};
+
+__global__ void k_raw_slots(const uint64_t* __restrict__ key, const uint32_t* __restrict__ first,
+                            const uint32_t* __restrict__ rank, uint32_t cap, const uint64_t* __restrict__ h2,
+                            const uint32_t* __restrict__ tlen, const uint32_t* __restrict__ rkeep,
+                            const uint32_t* __restrict__ rid, int build, RawSlot* __restrict__ rs) {
+  for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < cap; sl += gridDim.x * blockDim.x) {
+    if (!key[sl]) continue;
+    const uint32_t f = first[sl], r = rank[sl];
+    const uint32_t t = rid[r];
+    const bool kept = rkeep[r] && (build || t != kNew);
+    rs[sl] = RawSlot{h2[f], tlen[f], (t & 0x7FFFFFFFu) | (kept ? 0x80000000u : 0u)};
+  }
+}
+
 // per token: its raw entry (identity checked against the entry's first token: second hash,
 // length), then the entry's id and the kept flag (build: not a stopword; query: also in the
 // vocabulary)
 __global__ void k_raw_assign(const uint64_t* __restrict__ h1, const uint64_t* __restrict__ h2,
                              const uint32_t* __restrict__ tlen, uint64_t n, const uint64_t* __restrict__ key,
-                             const uint32_t* __restrict__ first, const uint32_t* __restrict__ rank, uint32_t cap,
-                             const uint32_t* __restrict__ rkeep, const uint32_t* __restrict__ rid, int build,
-                             uint32_t* __restrict__ id, uint32_t* __restrict__ kflag, uint32_t* __restrict__ err) {
+                             const RawSlot* __restrict__ rs, uint32_t cap, uint32_t* __restrict__ id,
+                             uint32_t* __restrict__ kflag, uint32_t* __restrict__ err) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = h1[i];
     uint32_t slot = (uint32_t)k & (cap - 1);
     while (key[slot] != k) slot = (slot + 1) & (cap - 1);
-    const uint32_t f = first[slot];
-    if (h2[f] != h2[i] || tlen[f] != tlen[i]) atomicOr(err, 1u);
-    const uint32_t r = rank[slot];
-    const uint32_t t = rid[r];
-    id[i] = t;
-    kflag[i] = rkeep[r] && (build || t != kNew);
+    const RawSlot r = rs[slot];
+    if (r.h2 != h2[i] || r.len != tlen[i]) atomicOr(err, 1u);
+    const uint32_t t = r.ik & 0x7FFFFFFFu;
+    id[i] = t == 0x7FFFFFFFu ? kNew : t;
+    kflag[i] = r.ik >> 31;
   }
 }
 
@@ -1167,7 +1187,7 @@ int32_t grow(T** p, uint64_t keep, uint64_t newcap, cudaStream_t st) {
 int32_t vocab_reserve(sl_vocab* v, uint64_t n_entries, uint64_t n_bytes, cudaStream_t st) {
   if (n_entries > v->vcap) {
     const uint64_t cap = std::max<uint64_t>(n_entries, (uint64_t)v->vcap * 2);
-    if (cap > 0xFFFFFFF0ull) SL_FAIL(SL_EUNSUPPORTED, "vocabulary larger than 2^32 entries");
+    if (n_entries > 0x7FFFFFF0ull) SL_FAIL(SL_EUNSUPPORTED, "vocabulary larger than 2^31 entries");
     SL_TRY(grow(&v->offs, v->V + 1ull, cap + 1, st));
     SL_TRY(grow(&v->h2, v->V, cap, st));
     if (v->vcap == 0) SL_CUDA_TRY(cudaMemsetAsync(v->offs, 0, 8, st));
@@ -1315,7 +1335,8 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     uint64_t *rh1, *rh2;
     SL_TTRY(scr.alloc(&rh1, n_tok));
     SL_TTRY(scr.alloc(&rh2, n_tok));
-    uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 22));
+    // sized for a Zipf vocabulary (grows 4x and retries when more than half full)
+    uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 19));
     uint64_t* key = nullptr;
     uint32_t *first = nullptr, *cntr = nullptr;
     SL_TTRY(scr.alloc(&cntr, 2));
@@ -1503,9 +1524,12 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   SL_TTRY(scr.alloc(&kflag, n_all));
   SL_TTRY(scr.alloc(&kpos, n_all));
   if (n_all) {
-    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_h1, r_h2, tlen, n_all, r_key, r_first, r_rank, (uint32_t)r_cap,
-                                                  na.keep, na.id, build ? 1 : 0, tid, kflag, err);
-    ++t_launches;
+    RawSlot* rslot;
+    SL_TTRY(scr.alloc(&rslot, r_cap));
+    k_raw_slots<<<grid_for(r_cap), 256, 0, st>>>(r_key, r_first, r_rank, (uint32_t)r_cap, r_h2, tlen, na.keep, na.id,
+                                                build ? 1 : 0, rslot); ++t_launches;
+    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_h1, r_h2, tlen, n_all, r_key, rslot, (uint32_t)r_cap, tid, kflag,
+                                                  err); ++t_launches;
   }
   uint32_t T = 0;
   SL_TTRY(exclusive_scan_u32(kflag, kpos, n_all, st, &T));

@@ -223,3 +223,28 @@ def test_device_input_unaligned(cuda_ok, port):
                             SL_MEM_DEVICE)
         got_off, got_ids = b.to_numpy()
         assert np.array_equal(got_off, want[0]) and np.array_equal(got_ids, want[1]) and v.tokens() == want[2], shift
+
+
+def test_many_distinct_strings_table_growth(cuda_ok):
+    """More distinct raw strings than the raw table's first size (grows and retries); ids in
+    first-encounter order against a plain dict reference (lowercase ASCII, no stop/stem)."""
+    rng = np.random.default_rng(17)
+    n = 1_500_000
+    letters = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", np.uint8)
+    lens = rng.integers(3, 9, n)
+    chars = letters[rng.integers(0, 26, int(lens.sum()))]
+    words, p = [], 0
+    for L in lens:
+        words.append(chars[p:p + L].tobytes())
+        p += L
+    words += words[: n // 3]  # repeats
+    text = b" ".join(words)
+    ref_ids, seen = [], {}
+    for w in words:
+        ref_ids.append(seen.setdefault(w, len(seen)))
+    v = T.Vocabulary()
+    off = np.array([0, len(text)], np.uint64)
+    b = T.tokenize_build((text, off), T.TokenizerConfig(), v)
+    _, ids = b.to_numpy()
+    assert len(seen) > 1_000_000 and v.size() == len(seen)
+    assert np.array_equal(ids, np.array(ref_ids, np.uint32))
