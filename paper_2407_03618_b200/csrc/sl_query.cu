@@ -234,11 +234,9 @@ struct RunArgs {
   uint32_t qmax;
   uint32_t n_splits;
   uint32_t wpc;               // warps per CTA in use
-  uint32_t warp_bytes;        // shared memory per warp
   uint64_t* cand;             // [B][n_splits][C] (original query order)
   float* dense_out;           // GM_DENSE: [N]
   uint32_t debug_skip;        // timing experiments only (SL_DEBUG_SKIP): 1 gather, 2 filter, 4 dense
-  uint32_t kept_global;       // large k: running candidates live in their cand slot (global/L2)
   uint32_t split_major;       // work-item order (see k_score_runs)
   uint32_t prune;             // exact block-max pruning of (query, tile) pairs
 };
@@ -1223,21 +1221,19 @@ int env_int(const char* name, int dflt) {
 }
 
 struct RunPlan {
-  uint32_t R, C, wpc, n_splits, warp_bytes, kept_global, per_sm;
+  uint32_t R, C, wpc, n_splits, per_sm;
   size_t smem;
 };
 
-// Warps per CTA under a shared-memory budget (3 CTAs/SM); splits so that the expected
-// number of warp work items covers several waves. SL_SMEM_BUDGET / SL_SPLITS / SL_RUN
+// Launch plan of k_score_runs: candidate capacity per (query, split), queries per run, the
+// resident CTAs of the persistent grid and the number of doc splits. SL_SPLITS / SL_RUN
 // override the plan in tuning runs.
 int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
   p->C = kept_capacity(k);
-  p->kept_global = 1;  // running candidates live in their global output slot (L2-resident)
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
   if (R == 0) R = RMAX;
   R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
   p->R = std::max(1u, std::min<uint32_t>(R, RMAX));
-  p->warp_bytes = (uint32_t)sizeof(WarpSmem);
   p->wpc = WPC;
   p->smem = 0;  // static layout (WarpSmem)
   int per_sm = 0;
@@ -1431,9 +1427,7 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   ra.qmax = qmax;
   ra.n_splits = plan.n_splits;
   ra.wpc = plan.wpc;
-  ra.warp_bytes = plan.warp_bytes;
   ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
-  ra.kept_global = plan.kept_global;
   ra.split_major = (uint32_t)env_int("SL_SPLIT_MAJOR", 1);
   ra.prune = have_bounds && env_int("SL_PRUNE", 0) ? 1u : 0u;  // opt-in
   uint64_t* cand;

@@ -1,5 +1,5 @@
 """Tuning sweep: build config c<i> once, time retrieve_batch under plan overrides
-(SL_RUN / SL_SPLITS / SL_SMEM_BUDGET env vars read by the library at each call)."""
+(SL_RUN / SL_SPLITS / SL_GTAU / SL_DEBUG_SKIP env vars read by the library at each call)."""
 import argparse
 import ctypes as C
 import json
@@ -50,7 +50,7 @@ def main():
     sc = torch.empty((B, a.k), dtype=torch.float32, device="cuda")
     st = _lib.RetrieveStats()
     for env in json.loads(a.sweep):
-        for key in ("SL_RUN", "SL_SPLITS", "SL_SMEM_BUDGET"):
+        for key in ("SL_RUN", "SL_SPLITS", "SL_GTAU", "SL_DEBUG_SKIP"):
             os.environ.pop(key, None)
         os.environ.update({k: str(v) for k, v in env.items()})
         ts = []
