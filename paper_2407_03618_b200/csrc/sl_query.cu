@@ -280,6 +280,8 @@ struct __align__(16) WarpSmem {
   uint32_t hist[16];          // warp_select_kth histogram
   uint32_t n_kept[RMAX];
   uint32_t qid[RMAX];         // original query index of run member r
+  uint32_t emask[RMAX];       // its gathered-row entries as a lane mask
+  uint64_t* keptp[RMAX];      // its candidate slot for this split
   int32_t ebeg[RMAX + 1];     // query r owns entries [ebeg[r], ebeg[r+1])
   int32_t nd[1];
 };
@@ -572,6 +574,12 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     }
   }
   __syncwarp();
+  if ((uint32_t)lane < nr) {
+    const int e0 = s.ebeg[lane], e1 = s.ebeg[lane + 1];
+    s.emask[lane] = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
+    s.keptp[lane] = ra.cand + ((uint64_t)s.qid[lane] * ra.n_splits + split) * ra.C;
+  }
+  __syncwarp();
   const int E = s.ebeg[nr];
   const int nd = s.nd[0];
 #ifdef SL_DEBUG_CHECKS
@@ -702,8 +710,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
       if (PRUNE && !((live >> r) & 1u)) continue;
-      const int e0 = s.ebeg[r], e1 = s.ebeg[r + 1];
-      const uint32_t emask = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
+      const uint32_t emask = s.emask[r];
       float* buf = s.dsum;
       float lmax = dm;
       const uint32_t q = s.qid[r];
@@ -723,7 +730,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
-        uint64_t* kept = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
+        uint64_t* kept = s.keptp[r];
         if (!(ra.debug_skip & 2)) {
           if (nvalid == TILE)
             filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
