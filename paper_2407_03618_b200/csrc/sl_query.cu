@@ -241,26 +241,12 @@ struct RunArgs {
   uint32_t prune;             // exact block-max pruning of (query, tile) pairs
 };
 
-// per-warp shared memory; E = R * qmax gathered-row entries (the run's queries' CSC
-// tokens concatenated, query r owning entries [ebeg[r], ebeg[r+1]))
+// top-k state of the CTA-per-query kernel (k_score_long), in its dynamic shared memory;
+// filter_tile takes this or the warp kernel's WarpSmem
 struct WSmem {
-  float* dsum;          // [TILE] dense-signature sum of the current tile
-  float* acc;           // [TILE] working accumulator (runs with > 1 query)
-  uint64_t* kept;       // [R][C]
-  uint64_t* tau;        // [R]
-  uint64_t* row_start;  // [E]
-  uint32_t* hist;       // [16]
-  uint32_t* n_kept;     // [R]
-  int32_t* ebeg;        // [R+1]
-  int32_t* nd;          // [1]
-  int32_t* dslot;       // [qmax]
-  uint32_t* row_len;    // [E]
-  int32_t* skip;        // [E]
-  uint32_t* cursor;     // [E] short rows: first posting not consumed yet
-  uint32_t* nextdoc;    // [E] short rows: doc id at the cursor (UINT32_MAX at the end)
-  uint32_t* sb;         // [E] slice of the current tile (row-relative start)
-  uint32_t* cnt;        // [E] and length
-  float* rmax;          // [E] row maximum max(0, S^Δ) (block-max bound of short rows)
+  uint64_t* tau;     // [1]
+  uint32_t* n_kept;  // [1]
+  uint32_t* hist;    // [16] warp_select_kth histogram
 };
 
 // Static per-warp shared layout of k_score_runs: compile-time offsets, so every access is an
@@ -286,36 +272,6 @@ struct __align__(16) WarpSmem {
   int32_t nd[1];
 };
 
-// C = candidates held in shared memory per query (0 when they live in global memory)
-__host__ __device__ inline size_t warp_smem_bytes(uint32_t R, uint32_t C, uint32_t qmax) {
-  const size_t E = (size_t)R * qmax;
-  size_t b = (size_t)TILE * 8 + (size_t)R * C * 8 + (size_t)R * 8 + E * 8 + 16 * 4 + (size_t)R * 4 + (R + 1) * 4 + 4 +
-             (size_t)qmax * 4 + E * 4 * 7;
-  return (b + 15) & ~(size_t)15;
-}
-
-__device__ inline WSmem wcarve(unsigned char* p, uint32_t R, uint32_t C, uint32_t qmax) {
-  const size_t E = (size_t)R * qmax;
-  WSmem s;
-  s.dsum = (float*)p; p += (size_t)TILE * 4;
-  s.acc = (float*)p; p += (size_t)TILE * 4;
-  s.kept = (uint64_t*)p; p += (size_t)R * C * 8;
-  s.tau = (uint64_t*)p; p += (size_t)R * 8;
-  s.row_start = (uint64_t*)p; p += E * 8;
-  s.hist = (uint32_t*)p; p += 16 * 4;
-  s.n_kept = (uint32_t*)p; p += (size_t)R * 4;
-  s.ebeg = (int32_t*)p; p += (size_t)(R + 1) * 4;
-  s.nd = (int32_t*)p; p += 4;
-  s.dslot = (int32_t*)p; p += (size_t)qmax * 4;
-  s.row_len = (uint32_t*)p; p += E * 4;
-  s.skip = (int32_t*)p; p += E * 4;
-  s.cursor = (uint32_t*)p; p += E * 4;
-  s.nextdoc = (uint32_t*)p; p += E * 4;
-  s.sb = (uint32_t*)p; p += E * 4;
-  s.cnt = (uint32_t*)p; p += E * 4;
-  s.rmax = (float*)p;
-  return s;
-}
 
 // Add the tile slices of the query owning lanes [e0, e1) (lane = gathered-row entry, in
 // query order) to buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are
