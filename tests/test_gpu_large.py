@@ -1,4 +1,5 @@
-"""BASELINE.json configs c2 / c3 at full size (1M docs, V=200k, ~8.3e7 tokens) against the oracle.
+"""BASELINE.json configs c2 / c3 at full size (1M docs, V=200k, ~8.3e7 tokens), c4 at full size and a
+c5-distribution shard against the oracle.
 
 c2: full CSC structure bit-exact (indptr, docids, df, doclens, tf); values within 1e-5 (and
     counted for bit-identity); top-10 and top-100 parity on a 400-query sample of the 10k.
@@ -89,3 +90,21 @@ def test_c4_csc_and_top1000(cuda_ok):
     corp = synth.corpus_host(cfg, threads=32)
     qoff, qtok = synth.queries(cfg, corp.cdf, 0, 8192)
     _run(cfg, corp, qoff, qtok, BM25Params(Variant.lucene, 1.5, 0.75), (1000,), 128, 4)
+
+
+def test_c5_shard_csc_and_top100(cuda_ok):
+    """c5's distribution (50M long docs, V=4M, Zipf(1.0), queries of 2-32 tokens with a 5% head
+    tail) on one shard: shard 0 of a 64-way token-balanced sharding (~780k docs, ~2.6e8 tokens)
+    built with shard-local statistics, full CSC vs the oracle and top-100 parity on 96 queries of
+    the first batch (head-heavy queries included) — SURVEY.md §8d c5 parity plan, shard-sized."""
+    cfg = synth.config(5)
+    cdf = synth.zipf_cdf(cfg)
+    off = synth.doc_offsets(cfg, 0, 781_250)  # the first 1/64 of the documents
+    tok = synth.tokens_host(cfg, cdf, 0, int(off[-1]), threads=32)
+    corp = synth.Corpus(cfg, cdf, off, tok)
+    qoff, qtok = synth.queries(cfg, cdf, 0, 4096)
+    n_head = sum(1 for q in range(len(qoff) - 1) if int(qoff[q + 1] - qoff[q]) and
+                 int(qtok[int(qoff[q]):int(qoff[q + 1])].max()) < cfg.head_ranks)
+    assert n_head > 100  # the 5% head tail is present in the batch
+    sub = synth.config(5, num_docs=781_250)
+    _run(sub, corp, qoff, qtok, BM25Params(Variant.lucene, 1.5, 0.75), (100,), 96, 5)
