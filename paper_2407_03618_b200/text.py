@@ -119,6 +119,7 @@ class Vocabulary:
         self._h = h
         self.device = device
         self._cache = None
+        self._index = None
 
     @property
     def handle(self):
@@ -150,10 +151,11 @@ class Vocabulary:
         return self.tokens()[i]
 
     def lookup(self, token: str):
-        try:
-            return self.tokens().index(token)
-        except ValueError:
-            return None
+        """vocabulary.hpp:20-24: the id of a (normalised) token, or None."""
+        toks = self.tokens()
+        if getattr(self, "_index", None) is None or len(self._index) != len(toks):
+            self._index = {t: i for i, t in enumerate(toks)}
+        return self._index.get(token)
 
     @staticmethod
     def from_tokens(tokens, device: int = 0) -> "Vocabulary":
