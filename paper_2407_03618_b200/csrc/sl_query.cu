@@ -1041,10 +1041,13 @@ __global__ void __launch_bounds__(NT) k_topk_vector(const float* __restrict__ ve
 }
 
 // Per query: top-k over n_splits x per_split candidate keys (invalid = 0), sorted, decoded.
+// gtau (nullable): the query's threshold shared by its doc splits, a lower bound of its k-th
+// key — candidates below it cannot be selected and are skipped.
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand, uint32_t n_splits,
                                                uint32_t per_split, uint64_t split_stride, uint64_t query_stride,
                                                uint32_t k, const double* __restrict__ qconst, uint32_t* out_ids,
-                                               float* out_scores, uint64_t* out_keys) {
+                                               float* out_scores, uint64_t* out_keys,
+                                               const uint64_t* __restrict__ gtau) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* buf = (uint64_t*)smem_raw;  // [p2]
   const uint32_t p2 = next_pow2(max(k, 2u));
@@ -1052,33 +1055,42 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
   uint32_t* sw = hist + 256;
   const uint32_t q = blockIdx.x;
   const uint64_t* base = cand + (uint64_t)q * query_stride;
+  const uint64_t g = gtau ? gtau[q] : 0ull;
+  // every valid candidate (>= g); power-of-two split sizes (the single-rank case) index with
+  // shifts, others walk split by split
+  const bool pow2 = (per_split & (per_split - 1)) == 0;
+  const int lg = pow2 ? __ffs(per_split) - 1 : 0;
   const uint64_t total = (uint64_t)n_splits * per_split;
-  auto at = [&](uint64_t i) { return base[(i / per_split) * split_stride + (i % per_split)]; };
-
+  auto visit = [&](auto&& f) {
+    if (pow2) {
+      for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) {
+        const uint64_t x = base[(i >> lg) * split_stride + (i & (per_split - 1))];
+        if (x != kInvalidKey && x >= g) f(x);
+      }
+    } else {
+      for (uint32_t sp = 0; sp < n_splits; ++sp) {
+        const uint64_t* p = base + (uint64_t)sp * split_stride;
+        for (uint32_t j = threadIdx.x; j < per_split; j += blockDim.x) {
+          const uint64_t x = p[j];
+          if (x != kInvalidKey && x >= g) f(x);
+        }
+      }
+    }
+  };
   uint32_t mine = 0;
-  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) mine += at(i) != kInvalidKey;
+  visit([&](uint64_t) { ++mine; });
   uint32_t nvalid;
   block_excl_scan(mine, sw, &nvalid);
   uint64_t tau = 1;
-  if (nvalid > k) {
-    tau = block_select_kth(
-        [&](auto&& f) {
-          for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) {
-            const uint64_t x = at(i);
-            if (x != kInvalidKey) f(x);
-          }
-        },
-        k, hist, sw + 36);
-  }
+  if (nvalid > k) tau = block_select_kth(visit, k, hist, sw + 36);
   uint32_t m2 = 0;
-  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) m2 += at(i) >= tau;
+  visit([&](uint64_t x) { m2 += x >= tau; });
   uint32_t m;
   const uint32_t o = block_excl_scan(m2, sw, &m);
   uint64_t* dst = buf + o;
-  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) {
-    const uint64_t x = at(i);
+  visit([&](uint64_t x) {
     if (x >= tau) *dst++ = x;
-  }
+  });
   for (uint32_t i = m + threadIdx.x; i < p2; i += blockDim.x) buf[i] = kInvalidKey;
   __syncthreads();
   block_bitonic_desc(buf, p2);
@@ -1216,11 +1228,11 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
 
 int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32_t per_split, uint64_t split_stride,
                      uint64_t query_stride, uint32_t k, const double* qconst, uint32_t* ids, float* scores,
-                     uint64_t* keys, cudaStream_t st) {
+                     uint64_t* keys, cudaStream_t st, const uint64_t* gtau = nullptr) {
   const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4;
   SL_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_merge<<<B, 256, smem, st>>>(cand, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores,
-                                keys); ++t_launches;
+  k_merge<<<B, 256, smem, st>>>(cand, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores, keys,
+                                gtau); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
@@ -1433,13 +1445,15 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   }
   const uint64_t qstride = (uint64_t)plan.n_splits * plan.C;
   if (!dist) {
-    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids_dev, sc_dev, nullptr, st));
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids_dev, sc_dev, nullptr, st,
+                        ra.gtau));
   } else {
     // local merge -> keys, gather the G x k candidates on rank 0 (NCCL), merge there
     const sl_comm* cm = ix->comm;
     uint64_t* local;
     SL_TRY(scr.alloc(&local, (uint64_t)B * k));
-    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, local, st));
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, local, st,
+                        ra.gtau));
     uint64_t* gathered = nullptr;
     if (cm->rank == 0) SL_TRY(scr.alloc(&gathered, (uint64_t)cm->nranks * B * k));
     const size_t cnt = (size_t)B * k;
