@@ -45,9 +45,9 @@ extern thread_local uint32_t t_launches;
 
 // ---------------------------------------------------------------- constants
 #ifndef SL_TILE_DOCS
-#define SL_TILE_DOCS 512
+#define SL_TILE_DOCS 1024
 #endif
-constexpr int kTileDocs = SL_TILE_DOCS;  // docs per scoring tile (f32 accumulator = 2 KB smem per warp)
+constexpr int kTileDocs = SL_TILE_DOCS;  // docs per scoring tile (f32 accumulator = 4 KB smem per warp)
 constexpr int kScoreThreads = 256;     // threads per scoring CTA
 constexpr int kQMax = 32;              // gathered rows per query in the warp kernel (one lane each); longer queries go to k_score_long
 constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path

@@ -35,6 +35,9 @@ namespace sl {
 namespace {
 
 constexpr int NT = 256;
+#ifndef SL_DYN_WSMEM
+#define SL_DYN_WSMEM (SL_TILE_DOCS > 512)  // per-warp layouts above 48 KB per CTA need dynamic smem
+#endif
 #ifndef SL_MINB
 #define SL_MINB 4  // resident CTAs per SM the scoring kernel is register-budgeted for
 #endif
@@ -451,7 +454,12 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
 // global counter in increasing order, so warps that finish short runs early stay busy.
 template <int MODE, bool PRUNE>
 __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArgs ra) {
+#if SL_DYN_WSMEM
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  WarpSmem* wsm = reinterpret_cast<WarpSmem*>(wsm_raw);
+#else
   __shared__ WarpSmem wsm[WPC];
+#endif
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n_runs = *ra.n_runs;
   const uint32_t total = n_runs * ra.n_splits;
@@ -1210,9 +1218,15 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
   p->R = std::max(1u, std::min<uint32_t>(R, RMAX));
   p->wpc = WPC;
-  p->smem = 0;  // static layout (WarpSmem)
+  p->smem = SL_DYN_WSMEM ? sizeof(WarpSmem) * WPC : 0;  // static layout unless it exceeds 48 KB
   int per_sm = 0;
-  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, 0));
+  if (p->smem) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)p->smem));
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_runs<GM_TOPK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)p->smem));
+  }
+  SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, p->smem));
   p->per_sm = (uint32_t)std::max(1, per_sm);
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
