@@ -1234,8 +1234,17 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   // doc splits: enough (run, split) items to keep every warp busy several times over; the
   // splits of a query share its threshold, so small k affords more of them (merge cost
   // grows with splits x k). Measured: c2 top-10 best at 12 items/warp, top-100 / c4 top-1000 at 8.
+  // They also bound the doc region the resident warps sweep together (split-major order): it
+  // must stay small enough for its dense-row chunks and posting slices to be served from L2 —
+  // at most 128k docs per split (k <= 256; larger candidate sets trade region size for merge
+  // cost: 128k x C/512). c5 shard (6.25M docs): 2 -> 48 splits, 38.8k -> 71k QPS.
   const uint64_t f = k <= 16 ? 12 : 8;
-  if (ns == 0) ns = (uint32_t)std::max<uint64_t>(1, (f * warps + items - 1) / items);
+  if (ns == 0) {
+    const uint64_t by_work = (f * warps + items - 1) / items;
+    const uint64_t region = 131072ull * std::max(1u, p->C / 512);
+    const uint64_t by_l2 = ((uint64_t)ix->N + region - 1) / region;
+    ns = (uint32_t)std::max<uint64_t>(1, std::max(by_work, by_l2));
+  }
   p->n_splits = std::max(1u, std::min(ns, std::max(1u, ix->num_tiles)));
   return SL_OK;
 }
