@@ -216,8 +216,9 @@ __device__ __forceinline__ float f4c(const float4& v, int c) {
 
 enum GroupMode { GM_TOPK = 0, GM_DENSE = 1 };
 
+constexpr int ULOG = 8;  // undo-log capacity in gather slots
 #ifndef SL_RMAX_CT
-#define SL_RMAX_CT 1  // one query per warp item: without the second accumulator 32 warps fit per SM (+4..6% over 2)
+#define SL_RMAX_CT 2  // two queries of one dense signature per warp item, the second via the undo log
 #endif
 constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) handled by one warp
 #ifndef SL_UNROLL
@@ -263,7 +264,10 @@ constexpr int NDMAX = 64;   // dense rows per query in the warp kernel
 struct __align__(16) WarpSmem {
   float dsum[TILE];           // dense-signature sum of the current tile
 #if SL_RMAX_CT > 1
-  float acc[TILE];            // working accumulator (runs with > 1 query)
+  // undo log of a non-last run member's gather into the shared dense sum: (doc, old value)
+  // per applied posting, replayed backwards after its filter (<= ULOG slots of 32 postings)
+  uint16_t ulog_doc[ULOG * 32];
+  float ulog_old[ULOG * 32];
 #endif
   uint64_t row_start[32];     // gathered-row entries (lane = entry)
   uint64_t tau[RMAX];         // exact running threshold key per query
@@ -288,8 +292,11 @@ struct __align__(16) WarpSmem {
 // together and the rounds are applied in order with __syncwarp between them, so every
 // document receives its terms in token order without atomics.
 // cnt/rbase are this lane's entry slice (length, absolute start).
+template <bool LOG = false>
 __device__ __forceinline__ float apply_slices(const IndexView& ix, uint32_t emask, uint32_t cnt, uint64_t rbase,
-                                              float* buf, uint32_t d0) {
+                                              float* buf, uint32_t d0, uint16_t* ldoc = nullptr,
+                                              float* lold = nullptr, uint32_t* nslots = nullptr) {
+  uint32_t slot = 0;
   float gm = -INFINITY;  // max of the values this lane wrote (feeds the filter's pre-test)
   const int lane = threadIdx.x & 31;
   uint32_t m = __ballot_sync(0xffffffffu, cnt != 0) & emask;  // entries with postings here
@@ -322,13 +329,22 @@ __device__ __forceinline__ float apply_slices(const IndexView& ix, uint32_t emas
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       if (doc[u] != 0xFFFFFFFFu) {
-        const float nv = buf[doc[u] - d0] + val[u];
+        const float old = buf[doc[u] - d0];
+        const float nv = old + val[u];
         buf[doc[u] - d0] = nv;
         gm = fmaxf(gm, nv);
+        if (LOG) {
+          ldoc[slot * 32 + lane] = (uint16_t)(doc[u] - d0);
+          lold[slot * 32 + lane] = old;
+        }
+      } else if (LOG) {
+        ldoc[slot * 32 + lane] = 0xFFFFu;
       }
+      if (LOG) ++slot;
       __syncwarp();
     }
   }
+  if (LOG) *nslots = slot;
   return gm;
 }
 
@@ -584,9 +600,6 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   }
   const uint32_t rstride = ix.n_pad / 4;
   float4* dsum4 = reinterpret_cast<float4*>(s.dsum);
-#if SL_RMAX_CT > 1
-  float4* acc4 = reinterpret_cast<float4*>(s.acc);
-#endif
 
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint32_t d0 = tile * TILE, d1 = d0 + TILE;
@@ -645,11 +658,10 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       if (!live) continue;
     }
     // (2) dense signature of the run, ascending slot order, all loads in flight
-    float dm = INFINITY;  // lane max of its dense sums (padding docs included: an upper bound)
-    if (!(ra.debug_skip & 4)) {
-      dm = -INFINITY;
-      // register passes of DCH float4 per lane (512 docs), so the tile size does not set the
-      // register footprint
+    // register passes of DCH float4 per lane, so the tile size does not set the register
+    // footprint; returns the lane max of its sums (padding docs included: an upper bound)
+    auto dense_pass = [&]() -> float {
+      float m = -INFINITY;
       constexpr int DCH = F4L < 4 ? F4L : 4;
 #pragma unroll 1
       for (int c0 = 0; c0 < F4L; c0 += DCH) {
@@ -673,10 +685,12 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
 #pragma unroll
         for (int rr = 0; rr < DCH; ++rr) {
           dsum4[lane + 32 * (c0 + rr)] = a[rr];
-          dm = fmaxf(dm, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
+          m = fmaxf(m, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
         }
       }
-    }
+      return m;
+    };
+    const float dm = (ra.debug_skip & 4) ? INFINITY : dense_pass();
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
@@ -687,18 +701,23 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       const uint32_t q = s.qid[r];
       uint64_t* gp = ra.gtau ? ra.gtau + q : nullptr;
       const uint64_t gv = gp ? *(volatile const uint64_t*)gp : 0ull;  // in flight during the gather
+      // a non-last run member gathers into the shared dense sum and undoes its postings after
+      // its filter (log replayed backwards: each doc gets its first old value back); too many
+      // rounds for the log -> the dense sum is recomputed instead
+      int undo = 0;  // 0 none, 1 replay the log, 2 recompute the dense sum
+      uint32_t nslots = 0;
       if ((hmask & emask) && !(ra.debug_skip & 1)) {
-        if (r + 1 < nr) {  // keep the shared dense sum intact for the run's later queries
-#pragma unroll
 #if SL_RMAX_CT > 1
-          for (int rr = 0; rr < F4L; ++rr) acc4[lane + 32 * rr] = dsum4[lane + 32 * rr];
-#endif
-          __syncwarp();
-#if SL_RMAX_CT > 1
-          buf = s.acc;
-#endif
+        if (r + 1 < nr) {
+          const uint32_t mine = ((emask >> lane) & 1u) ? (cnt + 31) / 32 : 0u;
+          const uint32_t rounds = __reduce_add_sync(0xffffffffu, mine);
+          undo = rounds + UNROLL - 1 <= (uint32_t)ULOG ? 1 : 2;
         }
-        lmax = fmaxf(lmax, apply_slices(ix, emask, cnt, rbase, buf, d0));
+        if (undo == 1)
+          lmax = fmaxf(lmax, apply_slices<true>(ix, emask, cnt, rbase, buf, d0, s.ulog_doc, s.ulog_old, &nslots));
+        else
+#endif
+          lmax = fmaxf(lmax, apply_slices(ix, emask, cnt, rbase, buf, d0));
       }
       if constexpr (MODE == GM_DENSE) {
         const double qc = ra.qconst[ra.perm[pb + r]];
@@ -713,6 +732,20 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
             filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
         }
       }
+#if SL_RMAX_CT > 1
+      if (undo == 1) {
+        __syncwarp();
+        for (int sl = (int)nslots - 1; sl >= 0; --sl) {
+          const uint32_t d = s.ulog_doc[sl * 32 + lane];
+          if (d != 0xFFFFu) buf[d] = s.ulog_old[sl * 32 + lane];
+          __syncwarp();
+        }
+      } else if (undo == 2) {
+        __syncwarp();
+        dense_pass();
+        __syncwarp();
+      }
+#endif
     }
     __syncwarp();
   }
