@@ -4,7 +4,7 @@
 // passes (pass 1: count_terms + DF + lengths, tokenizer.cpp:162-168 /
 // vocabulary.hpp:38; pass 2: S^Δ per nonzero, scoring.cpp:116-145) become:
 //   K1  doc expansion + stable LSD radix sort of (token, doc) by token   -> (t,d) order
-//   K1' run-length encoding of equal (t,d) runs -> tf, doc ids, indptr (row starts)
+//   K1' run-length encoding of equal (t,d) runs -> doc ids, run starts (tf), indptr
 //   K2  df = row lengths (+ NCCL all-reduce of df, Σ|D|, N across shards)
 //   K3  idf(t), S^θ(t) in f64 (scoring.cpp:60-79, 125-145)
 //   K4  values[p] = f32(idf * tf_component - S^θ)  (scoring.cpp:81-123)
@@ -160,187 +160,236 @@ __global__ void k_check_tokens(const uint32_t* __restrict__ keys, uint64_t n, ui
 constexpr int kSortThreads = 256;
 constexpr int kSortIPT = 16;
 constexpr int kSortTile = kSortThreads * kSortIPT;
+constexpr int kSortMaxBits = 7;  // digit width cap: rank counters take 2^(bits+1) x 256 B of shared memory
 
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// Lanes holding the same digit (among valid lanes): bit-sliced ballots, one per digit bit.
-// (__match_any_sync runs at 1/64 of a shuffle's rate on this GPU: tools/micro/match_bench.cu)
-__device__ __forceinline__ uint32_t digit_peers(uint32_t dg, int bits, bool valid) {
-  uint32_t m = __ballot_sync(0xffffffffu, valid);
-  for (int b = 0; b < bits; ++b) {
-    const bool on = (dg >> b) & 1u;
-    const uint32_t bb = __ballot_sync(0xffffffffu, on);
-    m &= on ? bb : ~bb;
-  }
-  return m;
-}
-
-// per-tile digit histogram (warp-aggregated by digit peers), digit-major output
+// per-tile digit histogram, digit-major output (hist[digit * n_tiles + tile]). One shared
+// atomic per element into per-warp copies (a hot Zipf digit contends within one warp only).
 __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __restrict__ keys,
                                                              uint64_t n, int shift, uint32_t mask,
                                                              uint32_t* __restrict__ hist,
                                                              uint32_t n_tiles, uint32_t V,
                                                              uint32_t* err) {
-  __shared__ uint32_t sh[256];
-  for (int i = threadIdx.x; i < 256; i += kSortThreads) sh[i] = 0;
+  constexpr int NW = kSortThreads / 32;
+  __shared__ uint32_t sh[NW][1 << kSortMaxBits];
+  const int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NW * (1 << kSortMaxBits); i += kSortThreads) (&sh[0][0])[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int bits = 32 - __clz(mask);
-  const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
-  bool bad = false;
-#pragma unroll 4
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile + threadIdx.x;
+  uint32_t kk[kSortIPT];
+#pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
-    const uint64_t i = base + (uint64_t)j * kSortThreads + threadIdx.x;
-    const bool valid = i < n;
-    uint32_t k = valid ? keys[i] : 0u;
-    bad |= valid && k >= V;
-    const uint32_t dg = valid ? ((k >> shift) & mask) : 0u;
-    const uint32_t peers = digit_peers(dg, bits, valid);
-    if (valid && lane == __ffs(peers) - 1) atomicAdd(&sh[dg], (uint32_t)__popc(peers));
+    const uint64_t i = base + (uint64_t)j * kSortThreads;
+    kk[j] = i < n ? keys[i] : 0xFFFFFFFFu;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const bool valid = base + (uint64_t)j * kSortThreads < n;
+    bad |= valid && kk[j] >= V;
+    if (valid) atomicAdd(&sh[w][(kk[j] >> shift) & mask], 1u);
   }
   if (err && bad) atomicOr(err, kErrToken);
   __syncthreads();
-  for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) hist[(uint64_t)dg * n_tiles + blockIdx.x] = sh[dg];
+  for (uint32_t dg = threadIdx.x; dg <= mask; dg += kSortThreads) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) c += sh[ww][dg];
+    hist[(uint64_t)dg * n_tiles + blockIdx.x] = c;
+  }
 }
 
-// Stable scatter of one tile (kSortTile elements): (1) rank every element within its warp and
-// digit with a per-warp shared counter (one atomicAdd per digit group, the leader's old value
-// shuffled to its peers; no per-element warp barriers), (2) block-wide digit offsets, (3) stage
-// the tile in shared memory in digit order, (4) write each digit's run to its global position
-// with consecutive threads on consecutive addresses (coalesced).
+// Stable scatter of one tile (kSortTile elements, 16 consecutive per thread) by digit
+// ranking with per-thread counters (the counting scheme of Merrill & Grimshaw's GPU radix
+// sort): every thread counts its own elements per digit in private 16-bit shared counters
+// (two digits per word: digits [0, ND/2) in the low halves, [ND/2, ND) in the high halves),
+// one raking scan over the counters in (digit, thread) order turns them into exclusive
+// ranks, and an element's rank = its counter's scanned value + the earlier elements of the
+// same digit in its own thread. The tile is then staged in shared memory in rank order and
+// every digit's run written to its global offset (coalesced). No warp votes per element.
+template <int LOGD>
 __global__ void __launch_bounds__(kSortThreads, 3) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
     uint32_t n_tiles) {
-  constexpr int NW = kSortThreads / 32;
-  __shared__ uint32_t wc[NW][256];    // per-warp digit counts, then per-warp digit bases
-  __shared__ uint32_t lstart[256];    // block-local start of each digit
-  __shared__ uint32_t gstart[256];    // global start of each digit's run for this tile
-  __shared__ uint32_t skey[kSortTile], sval[kSortTile];
-  for (int i = threadIdx.x; i < NW * 256; i += kSortThreads) (&wc[0][0])[i] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int ND = 1 << LOGD, LANES = ND / 2;
+  constexpr int R = LANES;                        // counter words per thread in the raking scan
+  constexpr int NWORDS = LANES * kSortThreads;
+  constexpr int NPAD = NWORDS + NWORDS / 32;      // one pad word per 32 (conflict-free raking)
+  static_assert(NPAD >= 2 * kSortTile, "staging aliases the counters");
+  extern __shared__ uint32_t smem[];
+  uint32_t* cw = smem;                            // packed counters, then the staged tile
+  __shared__ uint32_t dstart[ND], gstart[ND], sw[33];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NPAD; i += kSortThreads) cw[i] = 0;
   const uint64_t tile0 = (uint64_t)blockIdx.x * kSortTile;
-  const uint64_t base = tile0 + (uint64_t)w * 32 * kSortIPT;
-  const uint32_t lt = lanemask_lt();
-  const int bits = 32 - __clz(mask);
-  const uint32_t nd = mask + 1;
-  uint32_t kk[kSortIPT], vv[kSortIPT], rr[kSortIPT];
-#pragma unroll
-  for (int j = 0; j < kSortIPT; ++j) {
-    const uint64_t i = base + (uint64_t)j * 32 + lane;
-    const bool valid = i < n;
-    kk[j] = valid ? kin[i] : 0u;
-    vv[j] = valid ? vin[i] : 0u;
-  }
-#pragma unroll
-  for (int j = 0; j < kSortIPT; ++j) {
-    const uint64_t i = base + (uint64_t)j * 32 + lane;
-    const bool valid = i < n;
-    const uint32_t dg = (kk[j] >> shift) & mask;
-    const uint32_t peers = digit_peers(dg, bits, valid);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (valid && lane == leader) old = atomicAdd(&wc[w][dg], (uint32_t)__popc(peers));
-    rr[j] = __popc(peers & lt);
-    const uint32_t o = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
-    rr[j] += o;
-  }
-  __syncthreads();
-  // per digit: exclusive scan over warps (bases) and the digit's tile total
-  for (uint32_t dg = threadIdx.x; dg < nd; dg += kSortThreads) {
-    uint32_t run = 0;
-#pragma unroll
-    for (int ww = 0; ww < NW; ++ww) {
-      const uint32_t c = wc[ww][dg];
-      wc[ww][dg] = run;
-      run += c;
-    }
-    lstart[dg] = run;  // total for now
-    gstart[dg] = offs[(uint64_t)dg * n_tiles + blockIdx.x];
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive scan of the digit totals (<= 256) by one warp
-    uint32_t carry = 0;
-    for (uint32_t d0 = 0; d0 < nd; d0 += 32) {
-      const uint32_t dg = d0 + lane;
-      const uint32_t t = dg < nd ? lstart[dg] : 0u;
-      uint32_t x = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (dg < nd) lstart[dg] = carry + x - t;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kSortIPT; ++j) {
-    const uint64_t i = base + (uint64_t)j * 32 + lane;
-    if (i < n) {
-      const uint32_t dg = (kk[j] >> shift) & mask;
-      const uint32_t lp = lstart[dg] + wc[w][dg] + rr[j];
-      skey[lp] = kk[j];
-      sval[lp] = vv[j];
-    }
-  }
-  __syncthreads();
+  const uint64_t b = tile0 + (uint64_t)tid * kSortIPT;
   const uint32_t cnt = (uint32_t)min((uint64_t)kSortTile, n - tile0);
-  for (uint32_t i = threadIdx.x; i < cnt; i += kSortThreads) {
+  uint32_t kk[kSortIPT], vv[kSortIPT];
+  const bool full = cnt == kSortTile && ((((uintptr_t)(kin + b)) | ((uintptr_t)(vin + b))) & 15) == 0;
+  if (full) {
+#pragma unroll
+    for (int j = 0; j < kSortIPT; j += 4) {
+      const uint4 a = *reinterpret_cast<const uint4*>(kin + b + j);
+      const uint4 c = *reinterpret_cast<const uint4*>(vin + b + j);
+      kk[j] = a.x; kk[j + 1] = a.y; kk[j + 2] = a.z; kk[j + 3] = a.w;
+      vv[j] = c.x; vv[j + 1] = c.y; vv[j + 2] = c.z; vv[j + 3] = c.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kSortIPT; ++j) {
+      const bool valid = b + j < n;
+      kk[j] = valid ? kin[b + j] : 0u;
+      vv[j] = valid ? vin[b + j] : 0u;
+    }
+  }
+  __syncthreads();
+  auto cptr = [&](uint32_t dg) {  // this thread's 16-bit counter of digit dg
+    const uint32_t w = (dg & (LANES - 1)) * kSortThreads + tid;
+    return reinterpret_cast<uint16_t*>(cw + w + (w >> 5)) + (dg >> (LOGD - 1));
+  };
+  uint32_t pre[kSortIPT];
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    if (b + j < n) {
+      uint16_t* c = cptr((kk[j] >> shift) & mask);
+      pre[j] = *c;
+      *c = (uint16_t)(pre[j] + 1);
+    }
+  }
+  __syncthreads();
+  // raking exclusive scan of the packed counters in (digit lane, thread) order
+  uint32_t* seg = cw + tid * R + ((tid * R) >> 5);
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) s += seg[i + (i >> 5)];
+  uint32_t tot;
+  uint32_t run = block_excl_scan(s, sw, &tot);
+  run += (tot & 0xFFFFu) << 16;  // high-half digits follow every low-half digit
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint32_t c = seg[i + (i >> 5)];
+    seg[i + (i >> 5)] = run;
+    run += c;
+  }
+  __syncthreads();
+  for (uint32_t dg = tid; dg < ND; dg += kSortThreads) {
+    const uint32_t w = (dg & (LANES - 1)) * kSortThreads;  // thread 0's counter
+    dstart[dg] = reinterpret_cast<const uint16_t*>(cw + w + (w >> 5))[dg >> (LOGD - 1)];
+    gstart[dg] = dg <= mask ? offs[(uint64_t)dg * n_tiles + blockIdx.x] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j)
+    if (b + j < n) pre[j] += *cptr((kk[j] >> shift) & mask);
+  __syncthreads();
+  uint32_t* skey = cw;
+  uint32_t* sval = cw + kSortTile;
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j)
+    if (b + j < n) {
+      skey[pre[j]] = kk[j];
+      sval[pre[j]] = vv[j];
+    }
+  __syncthreads();
+  for (uint32_t i = tid; i < cnt; i += kSortThreads) {
     const uint32_t k = skey[i];
     const uint32_t dg = (k >> shift) & mask;
-    const uint32_t pos = gstart[dg] + (i - lstart[dg]);
+    const uint32_t pos = gstart[dg] + (i - dstart[dg]);
     kout[pos] = k;
     vout[pos] = sval[i];
   }
 }
 
-__device__ __forceinline__ bool run_head(const uint32_t* k, const uint32_t* v, uint64_t i) {
-  return i == 0 || k[i] != k[i - 1] || v[i] != v[i - 1];
+template <int LOGD>
+constexpr size_t scatter_smem() {
+  return ((size_t)(1 << (LOGD - 1)) * kSortThreads * 33 / 32) * 4;
 }
 
-__global__ void k_rle_flags(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v, uint64_t n,
-                            uint32_t* __restrict__ flags) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    flags[i] = run_head(k, v, i) ? 1u : 0u;
-}
+// Run-length encoding of the sorted (token, doc) stream in two passes over 4096-element
+// tiles (16 consecutive elements per thread): k_rle_count counts run heads per tile, an
+// exclusive scan of the tile counts gives every tile's first nonzero, k_rle_emit writes each
+// run's doc id, row and start (tf = distance to the next run's start) and the row starts
+// into indptr.
+constexpr int kRleThreads = 256, kRleIPT = 16, kRleTile = kRleThreads * kRleIPT;
 
-// one nonzero per (t,d) run: doc id, row id, run start; row starts fill indptr
-__global__ void k_rle_emit(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v,
-                           const uint32_t* __restrict__ pos, uint64_t n, uint64_t nnz, uint32_t V,
-                           uint32_t* __restrict__ docids, uint32_t* __restrict__ rows,
-                           uint32_t* __restrict__ runstart, uint64_t* __restrict__ indptr) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = k[i];
-    if (run_head(k, v, i)) {
-      const uint32_t p = pos[i];
-      docids[p] = v[i];
-      rows[p] = t;
-      runstart[p] = (uint32_t)i;
-      if (i == 0 || k[i - 1] != t) {
-        const int64_t prev = i == 0 ? -1 : (int64_t)k[i - 1];
-        for (int64_t x = prev + 1; x <= (int64_t)t; ++x) indptr[x] = p;
-      }
+struct RleItems {
+  uint32_t k[kRleIPT], v[kRleIPT];
+  uint32_t pk, pv;  // element before the thread's first (pk = 0xFFFFFFFF at i = 0)
+  uint32_t heads;   // bit j: element j starts a run
+};
+
+__device__ __forceinline__ void rle_load(const uint32_t* __restrict__ k, const uint32_t* __restrict__ v,
+                                         uint64_t n, RleItems& it) {
+  const uint64_t b = (uint64_t)blockIdx.x * kRleTile + (uint64_t)threadIdx.x * kRleIPT;
+  if (b + kRleIPT <= n && ((((uintptr_t)(k + b)) | ((uintptr_t)(v + b))) & 15) == 0) {
+#pragma unroll
+    for (int j = 0; j < kRleIPT; j += 4) {
+      const uint4 a = *reinterpret_cast<const uint4*>(k + b + j);
+      const uint4 c = *reinterpret_cast<const uint4*>(v + b + j);
+      it.k[j] = a.x; it.k[j + 1] = a.y; it.k[j + 2] = a.z; it.k[j + 3] = a.w;
+      it.v[j] = c.x; it.v[j + 1] = c.y; it.v[j + 2] = c.z; it.v[j + 3] = c.w;
     }
-    if (i == n - 1) {
-      for (uint64_t x = (uint64_t)t + 1; x <= V; ++x) indptr[x] = nnz;
-      runstart[nnz] = (uint32_t)n;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kRleIPT; ++j) {
+      const bool valid = b + j < n;
+      it.k[j] = valid ? k[b + j] : 0xFFFFFFFFu;
+      it.v[j] = valid ? v[b + j] : 0xFFFFFFFFu;
     }
   }
+  it.pk = b == 0 || b > n ? 0xFFFFFFFFu : k[b - 1];
+  it.pv = b == 0 || b > n ? 0xFFFFFFFFu : v[b - 1];
+  uint32_t h = 0, pk = it.pk, pv = it.pv;
+#pragma unroll
+  for (int j = 0; j < kRleIPT; ++j) {
+    if (b + j < n && (b + j == 0 || it.k[j] != pk || it.v[j] != pv)) h |= 1u << j;
+    pk = it.k[j];
+    pv = it.v[j];
+  }
+  it.heads = h;
 }
 
-__global__ void k_tf(const uint32_t* __restrict__ runstart, uint64_t nnz, uint32_t* __restrict__ tf) {
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
-       p += (uint64_t)gridDim.x * blockDim.x)
-    tf[p] = runstart[p + 1] - runstart[p];
+__global__ void __launch_bounds__(kRleThreads) k_rle_count(const uint32_t* __restrict__ k,
+                                                           const uint32_t* __restrict__ v, uint64_t n,
+                                                           uint32_t* __restrict__ tile_counts) {
+  __shared__ uint32_t sw[33];
+  RleItems it;
+  rle_load(k, v, n, it);
+  uint32_t tot;
+  block_excl_scan(__popc(it.heads), sw, &tot);
+  if (threadIdx.x == 0) tile_counts[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kRleThreads) k_rle_emit(const uint32_t* __restrict__ k,
+                                                          const uint32_t* __restrict__ v, uint64_t n,
+                                                          const uint32_t* __restrict__ tile_offs, uint64_t nnz,
+                                                          uint32_t V, uint32_t* __restrict__ docids,
+                                                          uint32_t* __restrict__ rows, uint32_t* __restrict__ runstart,
+                                                          uint64_t* __restrict__ indptr) {
+  __shared__ uint32_t sw[33];
+  RleItems it;
+  rle_load(k, v, n, it);
+  uint32_t p = block_excl_scan(__popc(it.heads), sw, nullptr) + tile_offs[blockIdx.x];
+  const uint64_t b = (uint64_t)blockIdx.x * kRleTile + (uint64_t)threadIdx.x * kRleIPT;
+  uint32_t pk = it.pk;
+#pragma unroll
+  for (int j = 0; j < kRleIPT; ++j) {
+    if ((it.heads >> j) & 1u) {
+      const uint32_t t = it.k[j];
+      docids[p] = it.v[j];
+      rows[p] = t;
+      runstart[p] = (uint32_t)(b + j);
+      if (b + j == 0 || pk != t) {  // row start: rows (previous row, t] begin here
+        const int64_t prev = b + j == 0 ? -1 : (int64_t)pk;
+        for (int64_t x = prev + 1; x <= (int64_t)t; ++x) indptr[x] = p;
+      }
+      ++p;
+    }
+    if (b + j == n - 1) {
+      for (uint64_t x = (uint64_t)it.k[j] + 1; x <= V; ++x) indptr[x] = nnz;
+      runstart[nnz] = (uint32_t)n;
+    }
+    pk = it.k[j];
+  }
 }
 
 __global__ void k_df_from_indptr(const uint64_t* __restrict__ indptr, uint32_t V, uint32_t* __restrict__ df) {
@@ -365,15 +414,19 @@ __global__ void k_token_stats(const uint32_t* __restrict__ df, uint32_t V, uint3
   }
 }
 
-// K4: S^Δ = idf * tf_component - S^θ in f64, narrowed to f32 (SPEC index pass 2)
+// K4: S^Δ = idf * tf_component - S^θ in f64, narrowed to f32 (SPEC index pass 2); tf is the
+// run length of the (t, d) run (kept for export when tf_out != nullptr)
 __global__ void k_values(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ docids,
-                         const uint32_t* __restrict__ tf, const uint32_t* __restrict__ doclens,
+                         const uint32_t* __restrict__ runstart, const uint32_t* __restrict__ doclens,
                          const double* __restrict__ idf64, const double* __restrict__ theta64,
-                         uint64_t nnz, sl_params p, double avg, float* __restrict__ values) {
+                         uint64_t nnz, sl_params p, double avg, float* __restrict__ values,
+                         uint32_t* __restrict__ tf_out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t t = rows[i];
-    const double tfc = d_tf_component(p.variant, (double)tf[i], (double)doclens[docids[i]], avg, p.k1,
+    const uint32_t tf = runstart[i + 1] - runstart[i];
+    if (tf_out) tf_out[i] = tf;
+    const double tfc = d_tf_component(p.variant, (double)tf, (double)doclens[docids[i]], avg, p.k1,
                                       p.b, p.delta);
     const double s = __dmul_rn(idf64[t], tfc);
     values[i] = __double2float_rn(__dsub_rn(s, theta64[t]));
@@ -524,7 +577,7 @@ struct Temps {
 
 }  // namespace
 
-// Stable LSD radix sort of u32 (key, value) pairs by the low `bits` key bits (8-bit
+// Stable LSD radix sort of u32 (key, value) pairs by the low `bits` key bits (<= 7-bit
 // digits, widths balanced over the passes). Pass p reads the previous output and writes
 // k{p&1}/v{p&1}; kin/vin are only read by the first pass, so v1 may alias vin. When
 // v_check != 0, keys >= v_check set err bit 2 during the first histogram pass.
@@ -534,11 +587,20 @@ int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, i
   *kout = kin;
   *vout = vin;
   if (bits <= 0 || n == 0) return SL_OK;
-  const int passes = (bits + 7) / 8;
+  const int passes = (bits + kSortMaxBits - 1) / kSortMaxBits;
   const int width = (bits + passes - 1) / passes;
   const uint32_t mask = (1u << width) - 1u;
+  const int logd = width <= 6 ? 6 : 7;  // counter layout: at least 64 digits
   const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
   if (n_tiles > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "radix sort: too many tiles");
+  static bool attr_set = false;
+  if (!attr_set) {
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter_smem<6>()));
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter_smem<7>()));
+    attr_set = true;
+  }
   uint32_t* hist;
   SL_CUDA_TRY(cudaMallocAsync(&hist, n_tiles * (uint64_t)(mask + 1) * 4, st));
   uint32_t* kb[2] = {k0, k1};
@@ -551,8 +613,13 @@ int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, i
                                                              v_check ? v_check : 0xFFFFFFFFu,
                                                              p == 0 && v_check ? err : nullptr); ++t_launches;
     SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
-    k_radix_scatter<<<(unsigned)n_tiles, kSortThreads, 0, st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist,
-                                                                (uint32_t)n_tiles); ++t_launches;
+    if (logd == 6)
+      k_radix_scatter<6><<<(unsigned)n_tiles, kSortThreads, scatter_smem<6>(), st>>>(
+          ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist, (uint32_t)n_tiles);
+    else
+      k_radix_scatter<7><<<(unsigned)n_tiles, kSortThreads, scatter_smem<7>(), st>>>(
+          ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist, (uint32_t)n_tiles);
+    ++t_launches;
     ki = kb[p & 1];
     vi = vb[p & 1];
   }
@@ -796,31 +863,22 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   if (herr & kErrDocLen) SL_FAIL(SL_EUNSUPPORTED, "build_index: document longer than 2^32-1 tokens");
 
   // ---- K1': run-length encode (t,d) runs
-  uint32_t *flags, *pos;
-  SL_TRY(tmp.alloc(&flags, T));
-  SL_TRY(tmp.alloc(&pos, T));
-  k_rle_flags<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, T, flags); ++t_launches;
+  const uint64_t rle_tiles = (T + kRleTile - 1) / kRleTile;
+  uint32_t* tile_offs;
+  SL_TRY(tmp.alloc(&tile_offs, rle_tiles));
+  k_rle_count<<<(unsigned)rle_tiles, kRleThreads, 0, st>>>(ksorted, vsorted, T, tile_offs); ++t_launches;
   uint32_t nnz32 = 0;
-  SL_TRY(exclusive_scan_u32(flags, pos, T, st, &nnz32));
+  SL_TRY(exclusive_scan_u32(tile_offs, tile_offs, rle_tiles, st, &nnz32));
   const uint64_t nnz = nnz32;
   ix->nnz = nnz;
-  uint32_t* rows = flags;  // flags are recomputed by the emit kernel; reuse the buffer
-  uint32_t* runstart;
+  uint32_t *rows, *runstart;
+  SL_TRY(tmp.alloc(&rows, nnz));
   SL_TRY(tmp.alloc(&runstart, nnz + 1));
   SL_TRY(dalloc(ix, &ix->docids, nnz));
   SL_TRY(dalloc(ix, &ix->indptr, (uint64_t)V + 1));
-  k_rle_emit<<<grid_for(T, 256), 256, 0, st>>>(ksorted, vsorted, pos, T, nnz, V, ix->docids, rows,
-                                               runstart, ix->indptr); ++t_launches;
-  uint32_t* tf;
-  if (d->keep_tf) {
-    SL_TRY(dalloc(ix, &ix->tf, nnz));
-    tf = ix->tf;
-  } else {
-    SL_TRY(tmp.alloc(&tf, nnz));
-  }
-  k_tf<<<grid_for(nnz, 256), 256, 0, st>>>(runstart, nnz, tf); ++t_launches;
-  tmp.release(runstart);
-  tmp.release(pos);
+  k_rle_emit<<<(unsigned)rle_tiles, kRleThreads, 0, st>>>(ksorted, vsorted, T, tile_offs, nnz, V, ix->docids, rows,
+                                                          runstart, ix->indptr); ++t_launches;
+  if (d->keep_tf) SL_TRY(dalloc(ix, &ix->tf, nnz));
   if (bits > 0) {
     tmp.release(kb0);
     tmp.release(kb1);
@@ -862,8 +920,8 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   k_token_stats<<<grid_for(V, 256), 256, 0, st>>>(ix->df_global, V, ix->N_global, d->params, idf64, theta64,
                                                  ix->theta); ++t_launches;
   SL_TRY(dalloc(ix, &ix->values, nnz));
-  k_values<<<grid_for(nnz, 256), 256, 0, st>>>(rows, ix->docids, tf, ix->doclens, idf64, theta64, nnz,
-                                               d->params, ix->avg_len, ix->values); ++t_launches;
+  k_values<<<grid_for(nnz, 256), 256, 0, st>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64, nnz,
+                                               d->params, ix->avg_len, ix->values, ix->tf); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
 
   SL_TRY(build_query_structures(ix, d->dense_min_density, st));
