@@ -157,7 +157,13 @@ __global__ void k_check_tokens(const uint32_t* __restrict__ keys, uint64_t n, ui
     if (keys[i] >= V) atomicOr(err, kErrToken);
 }
 
-constexpr int kSortThreads = 256;
+#ifndef SL_SORT_THREADS
+#define SL_SORT_THREADS 128
+#endif
+#ifndef SL_SORT_MINB
+#define SL_SORT_MINB 6
+#endif
+constexpr int kSortThreads = SL_SORT_THREADS;
 constexpr int kSortIPT = 16;
 constexpr int kSortTile = kSortThreads * kSortIPT;
 constexpr int kSortMaxBits = 7;  // digit width cap: rank counters take 2^(bits+1) x 256 B of shared memory
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
 // same digit in its own thread. The tile is then staged in shared memory in rank order and
 // every digit's run written to its global offset (coalesced). No warp votes per element.
 template <int LOGD>
-__global__ void __launch_bounds__(kSortThreads, 3) k_radix_scatter(
+__global__ void __launch_bounds__(kSortThreads, SL_SORT_MINB) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
     uint32_t n_tiles) {
@@ -365,30 +371,41 @@ __global__ void __launch_bounds__(kRleThreads) k_rle_emit(const uint32_t* __rest
                                                           uint32_t V, uint32_t* __restrict__ docids,
                                                           uint32_t* __restrict__ rows, uint32_t* __restrict__ runstart,
                                                           uint64_t* __restrict__ indptr) {
+  // the tile's runs are staged in shared memory and written as one contiguous range
   __shared__ uint32_t sw[33];
+  extern __shared__ uint32_t s_runs[];  // 3 x kRleTile
+  uint32_t *s_doc = s_runs, *s_row = s_runs + kRleTile, *s_start = s_runs + 2 * kRleTile;
   RleItems it;
   rle_load(k, v, n, it);
-  uint32_t p = block_excl_scan(__popc(it.heads), sw, nullptr) + tile_offs[blockIdx.x];
+  uint32_t tile_runs;
+  uint32_t q = block_excl_scan(__popc(it.heads), sw, &tile_runs);
+  const uint32_t p0 = tile_offs[blockIdx.x];
   const uint64_t b = (uint64_t)blockIdx.x * kRleTile + (uint64_t)threadIdx.x * kRleIPT;
   uint32_t pk = it.pk;
 #pragma unroll
   for (int j = 0; j < kRleIPT; ++j) {
     if ((it.heads >> j) & 1u) {
       const uint32_t t = it.k[j];
-      docids[p] = it.v[j];
-      rows[p] = t;
-      runstart[p] = (uint32_t)(b + j);
+      s_doc[q] = it.v[j];
+      s_row[q] = t;
+      s_start[q] = (uint32_t)(b + j);
       if (b + j == 0 || pk != t) {  // row start: rows (previous row, t] begin here
         const int64_t prev = b + j == 0 ? -1 : (int64_t)pk;
-        for (int64_t x = prev + 1; x <= (int64_t)t; ++x) indptr[x] = p;
+        for (int64_t x = prev + 1; x <= (int64_t)t; ++x) indptr[x] = p0 + q;
       }
-      ++p;
+      ++q;
     }
     if (b + j == n - 1) {
       for (uint64_t x = (uint64_t)it.k[j] + 1; x <= V; ++x) indptr[x] = nnz;
       runstart[nnz] = (uint32_t)n;
     }
     pk = it.k[j];
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tile_runs; i += kRleThreads) {
+    docids[p0 + i] = s_doc[i];
+    rows[p0 + i] = s_row[i];
+    runstart[p0 + i] = s_start[i];
   }
 }
 
@@ -415,21 +432,41 @@ __global__ void k_token_stats(const uint32_t* __restrict__ df, uint32_t V, uint3
 }
 
 // K4: S^Δ = idf * tf_component - S^θ in f64, narrowed to f32 (SPEC index pass 2); tf is the
-// run length of the (t, d) run (kept for export when tf_out != nullptr)
+// run length of the (t, d) run (kept for export when tf_out != nullptr). Four consecutive
+// nonzeros per thread (vector loads: more bytes in flight per thread).
+__device__ __forceinline__ float value_of(const sl_params& p, double avg, uint32_t t, uint32_t tf, uint32_t dl,
+                                          const double* __restrict__ idf64, const double* __restrict__ theta64) {
+  const double tfc = d_tf_component(p.variant, (double)tf, (double)dl, avg, p.k1, p.b, p.delta);
+  const double s = __dmul_rn(idf64[t], tfc);
+  return __double2float_rn(__dsub_rn(s, theta64[t]));
+}
+
 __global__ void k_values(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ docids,
                          const uint32_t* __restrict__ runstart, const uint32_t* __restrict__ doclens,
                          const double* __restrict__ idf64, const double* __restrict__ theta64,
                          uint64_t nnz, sl_params p, double avg, float* __restrict__ values,
                          uint32_t* __restrict__ tf_out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+  const uint64_t n4 = nnz / 4;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 t = reinterpret_cast<const uint4*>(rows)[q];
+    const uint4 d = reinterpret_cast<const uint4*>(docids)[q];
+    const uint4 r = reinterpret_cast<const uint4*>(runstart)[q];
+    const uint32_t r4 = runstart[4 * q + 4];
+    const uint4 tf = make_uint4(r.y - r.x, r.z - r.y, r.w - r.z, r4 - r.w);
+    const uint32_t l0 = doclens[d.x], l1 = doclens[d.y], l2 = doclens[d.z], l3 = doclens[d.w];
+    if (tf_out) reinterpret_cast<uint4*>(tf_out)[q] = tf;
+    float4 o;
+    o.x = value_of(p, avg, t.x, tf.x, l0, idf64, theta64);
+    o.y = value_of(p, avg, t.y, tf.y, l1, idf64, theta64);
+    o.z = value_of(p, avg, t.z, tf.z, l2, idf64, theta64);
+    o.w = value_of(p, avg, t.w, tf.w, l3, idf64, theta64);
+    reinterpret_cast<float4*>(values)[q] = o;
+  }
+  for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = rows[i];
     const uint32_t tf = runstart[i + 1] - runstart[i];
     if (tf_out) tf_out[i] = tf;
-    const double tfc = d_tf_component(p.variant, (double)tf, (double)doclens[docids[i]], avg, p.k1,
-                                      p.b, p.delta);
-    const double s = __dmul_rn(idf64[t], tfc);
-    values[i] = __double2float_rn(__dsub_rn(s, theta64[t]));
+    values[i] = value_of(p, avg, rows[i], tf, doclens[docids[i]], idf64, theta64);
   }
 }
 
@@ -446,23 +483,70 @@ __global__ void k_dense_fill(const uint64_t* __restrict__ indptr, const uint32_t
   }
 }
 
-// skip[s][tile] = first row-relative posting with doc >= tile * kTileDocs
-__global__ void k_skip_fill(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ docids,
-                            const uint32_t* __restrict__ slot_tok, uint32_t n_slots, uint32_t n_tiles,
-                            uint32_t* __restrict__ skip) {
-  for (uint32_t s = blockIdx.y; s < n_slots; s += gridDim.y) {
+// skip[s][tile] = first row-relative posting with doc >= tile * kTileDocs; one CTA per row
+// (grid-stride over rows), four postings per thread per step
+__global__ void __launch_bounds__(256) k_skip_fill(const uint64_t* __restrict__ indptr,
+                                                   const uint32_t* __restrict__ docids,
+                                                   const uint32_t* __restrict__ slot_tok, uint32_t n_slots,
+                                                   uint32_t n_tiles, uint32_t* __restrict__ skip) {
+  for (uint32_t s = blockIdx.x; s < n_slots; s += gridDim.x) {
     const uint32_t t = slot_tok[s];
     const uint64_t b = indptr[t];
     const uint32_t len = (uint32_t)(indptr[t + 1] - b);
+    const uint32_t* row = docids + b;
     uint32_t* tab = skip + (uint64_t)s * (n_tiles + 1);
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < len; j += gridDim.x * blockDim.x) {
-      const int64_t tile = docids[b + j] / kTileDocs;
-      const int64_t prev = j == 0 ? -1 : (int64_t)(docids[b + j - 1] / kTileDocs);
-      for (int64_t x = prev + 1; x <= tile; ++x) tab[x] = j;
-      if (j == len - 1)
-        for (int64_t x = tile + 1; x <= (int64_t)n_tiles; ++x) tab[x] = len;
+    for (uint32_t j0 = threadIdx.x * 4; j0 < len; j0 += 256 * 4) {
+      uint32_t tl[5];
+      tl[0] = j0 == 0 ? 0xFFFFFFFFu : row[j0 - 1] / kTileDocs;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) tl[u + 1] = j0 + u < len ? row[j0 + u] / kTileDocs : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u;
+        if (j < len) {
+          const int64_t prev = j == 0 ? -1 : (int64_t)tl[u];
+          for (int64_t x = prev + 1; x <= (int64_t)tl[u + 1]; ++x) tab[x] = j;
+          if (j == len - 1)
+            for (int64_t x = (int64_t)tl[u + 1] + 1; x <= (int64_t)n_tiles; ++x) tab[x] = len;
+        }
+      }
     }
   }
+}
+
+// planning candidates: rows with df >= dthr or row length >= sthr ({t, df, len} triples,
+// appended in any order; out == nullptr only counts)
+__global__ void k_plan_count(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ df, uint32_t V,
+                             uint32_t dthr, uint32_t sthr, uint32_t* __restrict__ cnt, uint32_t* __restrict__ out) {
+  for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < V; t0 += gridDim.x * blockDim.x) {
+    const uint32_t t = t0 + threadIdx.x;
+    bool c = false;
+    uint32_t f = 0, dl = 0;
+    if (t < V) {
+      dl = (uint32_t)(indptr[t + 1] - indptr[t]);
+      f = df[t];
+      c = dl && f && (f >= dthr || dl >= sthr);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, c);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (c && out) {
+      const uint32_t i = base + __popc(m & ((1u << lane) - 1u));
+      out[3 * i] = t;
+      out[3 * i + 1] = f;
+      out[3 * i + 2] = dl;
+    }
+  }
+}
+
+// tokinfo[t] = dense slot (>= 0) or -2 - skip slot
+__global__ void k_set_tokinfo(const uint32_t* __restrict__ slot_tok, uint32_t n_dense, uint32_t n_skip,
+                              int32_t* __restrict__ info) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_dense + n_skip; s += gridDim.x * blockDim.x)
+    info[slot_tok[s]] = s < n_dense ? (int32_t)s : -2 - (int32_t)(s - n_dense);
 }
 
 // max(0, v) as order-preserving bits (non-negative floats order like their bit patterns)
@@ -674,77 +758,94 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   const uint32_t N = ix->N, V = ix->V;
   ix->num_tiles = (N + kTileDocs - 1) / kTileDocs;
   ix->n_pad = ix->num_tiles * kTileDocs;
-  std::vector<uint32_t> h_df(V);
-  std::vector<uint64_t> h_ptr((size_t)V + 1);
-  SL_CUDA_TRY(cudaMemcpyAsync(h_df.data(), ix->df_global, (uint64_t)V * 4, cudaMemcpyDeviceToHost, st));
-  SL_CUDA_TRY(cudaMemcpyAsync(h_ptr.data(), ix->indptr, ((uint64_t)V + 1) * 8, cudaMemcpyDeviceToHost, st));
-  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.125;
+  double dense_thr = density > 1.0 ? INFINITY : density * (double)ix->N_global;
+#ifndef SL_SKIP_PER_TILE
+#define SL_SKIP_PER_TILE 0.25
+#endif
+  uint64_t skip_thr = std::max<uint64_t>(1, (uint64_t)(SL_SKIP_PER_TILE * ix->num_tiles));
+  // Candidates (rows that can get a dense copy or a skip table under the thresholds before
+  // the caps below, which only raise them) are compacted on the device; only they travel to
+  // the host, sorted there so slot order is token order.
+  std::vector<uint32_t> cand;  // {t, df, row length} triples
+  {
+    uint32_t* d_cand;
+    uint32_t* d_cnt;
+    SL_TRY(tmp.alloc(&d_cnt, 1));
+    SL_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
+    const uint32_t dthr = dense_thr >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)std::ceil(dense_thr);
+    const uint32_t sthr = skip_thr >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)skip_thr;
+    k_plan_count<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, ix->df_global, V, dthr, sthr, d_cnt, nullptr); ++t_launches;
+    uint32_t nc = 0;
+    SL_CUDA_TRY(cudaMemcpyAsync(&nc, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    if (nc) {
+      SL_TRY(tmp.alloc(&d_cand, 3ull * nc));
+      SL_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
+      k_plan_count<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, ix->df_global, V, dthr, sthr, d_cnt, d_cand); ++t_launches;
+      cand.resize(3ull * nc);
+      SL_CUDA_TRY(cudaMemcpyAsync(cand.data(), d_cand, 12ull * nc, cudaMemcpyDeviceToHost, st));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
+  const size_t nc = cand.size() / 3;
+  std::vector<uint32_t> order(nc);
+  for (size_t i = 0; i < nc; ++i) order[i] = (uint32_t)i;
+  std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cand[3 * x] < cand[3 * y]; });
+  auto c_t = [&](size_t i) { return cand[3 * order[i]]; };
+  auto c_df = [&](size_t i) { return cand[3 * order[i] + 1]; };
+  auto c_dl = [&](size_t i) { return (uint64_t)cand[3 * order[i] + 2]; };
   // Dense copies: rows with global df >= N/8 (c2 top-10: N/4 -> N/8 +2.4%, N/16 worse). By
   // default their global footprint is capped at 12 GB (at most 12 GB / (4 N) rows, highest df
   // first): c5's 50M docs would otherwise take 141 rows, whose chunks crowd L2 (c5 shard
   // top-100 -8% against the 59 rows of N/4). The cap uses only global quantities, so every
   // shard of any sharding classifies the same rows (identical per-document summation order).
-  const double density = dense_min_density > 0.f ? (double)dense_min_density : 0.125;
-  double dense_thr = density * (double)ix->N_global;
   if (!(dense_min_density > 0.f) && ix->N_global) {
     uint64_t max_rows = (12ull << 30) / (4ull * ix->N_global);
     if (const char* e = std::getenv("SL_DENSE_MAX_ROWS"))  // bench: a one-GPU stand-in for one shard
       if (*e) max_rows = std::strtoull(e, nullptr, 10);     // of a larger corpus uses the corpus's cap
-    std::vector<uint32_t> cand;
-    for (uint32_t t = 0; t < V; ++t)
-      if (h_df[t] && (double)h_df[t] >= dense_thr) cand.push_back(h_df[t]);
-    if (cand.size() > max_rows) {
+    std::vector<uint32_t> dc;
+    for (size_t i = 0; i < nc; ++i)
+      if ((double)c_df(i) >= dense_thr) dc.push_back(c_df(i));
+    if (dc.size() > max_rows) {
       if (max_rows == 0) {
         dense_thr = INFINITY;
       } else {
-        std::nth_element(cand.begin(), cand.begin() + (max_rows - 1), cand.end(), std::greater<uint32_t>());
-        dense_thr = (double)cand[max_rows - 1] + 1.0;  // strictly above: ties past the cap stay sparse
+        std::nth_element(dc.begin(), dc.begin() + (max_rows - 1), dc.end(), std::greater<uint32_t>());
+        dense_thr = (double)dc[max_rows - 1] + 1.0;  // strictly above: ties past the cap stay sparse
       }
     }
   }
   // Per-tile skip tables for rows with >= SL_SKIP_PER_TILE postings per tile on average: a
   // prefetched table entry beats probing the row's doc ids from one posting per few tiles on
   // (c2 top-10: 4 -> 0.25 postings/tile +4.5%). Tables cost (tiles+1) x 4 B per row, so they
-  // are held to half the CSC's bytes: beyond that budget only the longest rows get one.
-#ifndef SL_SKIP_PER_TILE
-#define SL_SKIP_PER_TILE 0.25
-#endif
-  uint64_t skip_thr = std::max<uint64_t>(1, (uint64_t)(SL_SKIP_PER_TILE * ix->num_tiles));
+  // are held to 4 B per nonzero (at least 64 MB): beyond that budget only the longest rows
+  // get one.
   {
     const uint64_t row_bytes = ((uint64_t)ix->num_tiles + 1) * 4;
     const uint64_t budget = std::max<uint64_t>(4 * ix->nnz, 64ull << 20);
-    std::vector<uint64_t> cand;
-    for (uint32_t t = 0; t < V; ++t) {
-      const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
-      if (dl >= skip_thr && h_df[t] && (double)h_df[t] < dense_thr) cand.push_back(dl);
-    }
+    std::vector<uint64_t> sc;
+    for (size_t i = 0; i < nc; ++i)
+      if (c_dl(i) >= skip_thr && (double)c_df(i) < dense_thr) sc.push_back(c_dl(i));
     const uint64_t max_rows = budget / row_bytes;
-    if (cand.size() > max_rows) {
+    if (sc.size() > max_rows) {
       if (max_rows == 0) {
         skip_thr = UINT64_MAX;
       } else {
-        std::nth_element(cand.begin(), cand.begin() + (max_rows - 1), cand.end(), std::greater<uint64_t>());
-        skip_thr = cand[max_rows - 1] + 1;  // strictly above: ties beyond the budget are dropped
+        std::nth_element(sc.begin(), sc.begin() + (max_rows - 1), sc.end(), std::greater<uint64_t>());
+        skip_thr = sc[max_rows - 1] + 1;  // strictly above: ties beyond the budget are dropped
       }
     }
   }
-  std::vector<int32_t> info(V, -1);
   std::vector<uint32_t> dense_tok, skip_tok;
-  for (uint32_t t = 0; t < V; ++t) {
-    const uint64_t dl = h_ptr[t + 1] - h_ptr[t];
-    if (dl == 0 || h_df[t] == 0) continue;
-    if ((double)h_df[t] >= dense_thr && density <= 1.0) {
-      info[t] = (int32_t)dense_tok.size();
-      dense_tok.push_back(t);
-    } else if (dl >= skip_thr) {
-      info[t] = -2 - (int32_t)skip_tok.size();
-      skip_tok.push_back(t);
-    }
+  for (size_t i = 0; i < nc; ++i) {
+    if ((double)c_df(i) >= dense_thr) dense_tok.push_back(c_t(i));
+    else if (c_dl(i) >= skip_thr) skip_tok.push_back(c_t(i));
   }
   ix->dense_rows = (uint32_t)dense_tok.size();
   ix->skip_rows = (uint32_t)skip_tok.size();
   SL_TRY(dalloc(ix, &ix->tokinfo, V));
-  SL_CUDA_TRY(cudaMemcpyAsync(ix->tokinfo, info.data(), (uint64_t)V * 4, cudaMemcpyHostToDevice, st));
+  SL_CUDA_TRY(cudaMemsetAsync(ix->tokinfo, 0xFF, (uint64_t)V * 4, st));  // -1: short row
   uint32_t* slot_tok;
   SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
   if (!dense_tok.empty())
@@ -752,6 +853,10 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   if (!skip_tok.empty())
     SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
                                 cudaMemcpyHostToDevice, st));
+  if (ix->dense_rows + ix->skip_rows) {
+    k_set_tokinfo<<<grid_for(ix->dense_rows + ix->skip_rows, 256), 256, 0, st>>>(slot_tok, ix->dense_rows,
+                                                                                ix->skip_rows, ix->tokinfo); ++t_launches;
+  }
   if (ix->dense_rows) {
     SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
     SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
@@ -761,9 +866,8 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   }
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
-    dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
-    k_skip_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows,
-                                   ix->num_tiles, ix->skiptab); ++t_launches;
+    k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 148 * 8), 256, 0, st>>>(
+        ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
   }
   // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
   // DESIGN.md §8)
@@ -876,7 +980,8 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(tmp.alloc(&runstart, nnz + 1));
   SL_TRY(dalloc(ix, &ix->docids, nnz));
   SL_TRY(dalloc(ix, &ix->indptr, (uint64_t)V + 1));
-  k_rle_emit<<<(unsigned)rle_tiles, kRleThreads, 0, st>>>(ksorted, vsorted, T, tile_offs, nnz, V, ix->docids, rows,
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_rle_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kRleTile * 4));
+  k_rle_emit<<<(unsigned)rle_tiles, kRleThreads, 3 * kRleTile * 4, st>>>(ksorted, vsorted, T, tile_offs, nnz, V, ix->docids, rows,
                                                           runstart, ix->indptr); ++t_launches;
   if (d->keep_tf) SL_TRY(dalloc(ix, &ix->tf, nnz));
   if (bits > 0) {
@@ -920,7 +1025,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   k_token_stats<<<grid_for(V, 256), 256, 0, st>>>(ix->df_global, V, ix->N_global, d->params, idf64, theta64,
                                                  ix->theta); ++t_launches;
   SL_TRY(dalloc(ix, &ix->values, nnz));
-  k_values<<<grid_for(nnz, 256), 256, 0, st>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64, nnz,
+  k_values<<<grid_for(nnz / 4 + 1, 256), 256, 0, st>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64, nnz,
                                                d->params, ix->avg_len, ix->values, ix->tf); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
 
