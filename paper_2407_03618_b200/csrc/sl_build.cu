@@ -15,6 +15,7 @@
 #include <functional>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -542,6 +543,34 @@ __global__ void k_plan_count(const uint64_t* __restrict__ indptr, const uint32_t
   }
 }
 
+// planning fast path: per-token class flags (dense copy / skip table) under the thresholds
+__global__ void k_plan_flags(const uint64_t* __restrict__ indptr, const uint32_t* __restrict__ df, uint32_t V,
+                             uint32_t dthr, uint32_t sthr, uint32_t* __restrict__ fd, uint32_t* __restrict__ fs) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x) {
+    const uint32_t dl = (uint32_t)(indptr[t + 1] - indptr[t]), f = df[t];
+    const bool dn = dl && f && f >= dthr;
+    fd[t] = dn;
+    fs[t] = dl && f && !dn && dl >= sthr;
+  }
+}
+
+// slots in token order from the scanned flags; tokinfo for every token
+__global__ void k_plan_assign(const uint32_t* __restrict__ fd, const uint32_t* __restrict__ pd,
+                              const uint32_t* __restrict__ fs, const uint32_t* __restrict__ ps, uint32_t V,
+                              uint32_t n_dense, uint32_t* __restrict__ slot_tok, int32_t* __restrict__ info) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < V; t += gridDim.x * blockDim.x) {
+    int32_t v = -1;
+    if (fd[t]) {
+      v = (int32_t)pd[t];
+      slot_tok[pd[t]] = t;
+    } else if (fs[t]) {
+      v = -2 - (int32_t)ps[t];
+      slot_tok[n_dense + ps[t]] = t;
+    }
+    info[t] = v;
+  }
+}
+
 // tokinfo[t] = dense slot (>= 0) or -2 - skip slot
 __global__ void k_set_tokinfo(const uint32_t* __restrict__ slot_tok, uint32_t n_dense, uint32_t n_skip,
                               int32_t* __restrict__ info) {
@@ -764,17 +793,64 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
 #define SL_SKIP_PER_TILE 0.25
 #endif
   uint64_t skip_thr = std::max<uint64_t>(1, (uint64_t)(SL_SKIP_PER_TILE * ix->num_tiles));
-  // Candidates (rows that can get a dense copy or a skip table under the thresholds before
-  // the caps below, which only raise them) are compacted on the device; only they travel to
-  // the host, sorted there so slot order is token order.
-  std::vector<uint32_t> cand;  // {t, df, row length} triples
+  const uint32_t dthr = dense_thr >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)std::ceil(dense_thr);
+  const uint32_t sthr = skip_thr >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)skip_thr;
+  // Dense copies: rows with global df >= N/8 (c2 top-10: N/4 -> N/8 +2.4%, N/16 worse). By
+  // default their global footprint is capped at 12 GB (at most 12 GB / (4 N) rows, highest df
+  // first): c5's 50M docs would otherwise take 141 rows, whose chunks crowd L2 (c5 shard
+  // top-100 -8% against the 59 rows of N/4). The cap uses only global quantities, so every
+  // shard of any sharding classifies the same rows (identical per-document summation order).
+  uint64_t dense_cap = UINT64_MAX;
+  if (!(dense_min_density > 0.f) && ix->N_global) {
+    dense_cap = (12ull << 30) / (4ull * ix->N_global);
+    if (const char* e = std::getenv("SL_DENSE_MAX_ROWS"))  // bench: a one-GPU stand-in for one shard
+      if (*e) dense_cap = std::strtoull(e, nullptr, 10);    // of a larger corpus uses the corpus's cap
+  }
+  // Per-tile skip tables for rows with >= SL_SKIP_PER_TILE postings per tile on average: a
+  // prefetched table entry beats probing the row's doc ids from one posting per few tiles on
+  // (c2 top-10: 4 -> 0.25 postings/tile +4.5%). Tables cost (tiles+1) x 4 B per row, so they
+  // are held to 4 B per nonzero (at least 64 MB): beyond that budget only the longest rows
+  // get one.
+  const uint64_t skip_row_bytes = ((uint64_t)ix->num_tiles + 1) * 4;
+  const uint64_t skip_cap = std::max<uint64_t>(4 * ix->nnz, 64ull << 20) / skip_row_bytes;
+  std::vector<uint32_t> dense_tok, skip_tok;
+  uint32_t* slot_tok = nullptr;
+  bool planned = false;
   {
+    // fast path (no cap binds): class flags, ordered slots and tokinfo on the device; only
+    // the two counts travel to the host
+    uint32_t *f, *pf;
+    SL_TRY(tmp.alloc(&f, 2ull * V));
+    SL_TRY(tmp.alloc(&pf, 2ull * V));
+    k_plan_flags<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, ix->df_global, V, dthr, sthr, f, f + V); ++t_launches;
+    SL_TRY(exclusive_scan_u32(f, pf, V, st, nullptr));
+    SL_TRY(exclusive_scan_u32(f + V, pf + V, V, st, nullptr));
+    uint32_t h[4];
+    SL_CUDA_TRY(cudaMemcpyAsync(h, f + V - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(h + 1, pf + V - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(h + 2, f + 2ull * V - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(h + 3, pf + 2ull * V - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaStreamSynchronize(st));
+    const uint32_t nd = h[0] + h[1], ns = h[2] + h[3];
+    if (nd <= dense_cap && ns <= skip_cap) {
+      ix->dense_rows = nd;
+      ix->skip_rows = ns;
+      SL_TRY(dalloc(ix, &ix->tokinfo, V));
+      SL_TRY(tmp.alloc(&slot_tok, (uint64_t)nd + ns));
+      k_plan_assign<<<grid_for(V, 256), 256, 0, st>>>(f, pf, f + V, pf + V, V, nd, slot_tok, ix->tokinfo);
+      ++t_launches;
+      planned = true;
+    }
+  }
+  // Capped path: candidates (rows that can get a dense copy or a skip table under the
+  // thresholds before the caps, which only raise them) are compacted on the device; only they
+  // travel to the host, sorted there so slot order is token order.
+  std::vector<uint32_t> cand;  // {t, df, row length} triples
+  if (!planned) {
     uint32_t* d_cand;
     uint32_t* d_cnt;
     SL_TRY(tmp.alloc(&d_cnt, 1));
     SL_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
-    const uint32_t dthr = dense_thr >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)std::ceil(dense_thr);
-    const uint32_t sthr = skip_thr >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)skip_thr;
     k_plan_count<<<grid_for(V, 256), 256, 0, st>>>(ix->indptr, ix->df_global, V, dthr, sthr, d_cnt, nullptr); ++t_launches;
     uint32_t nc = 0;
     SL_CUDA_TRY(cudaMemcpyAsync(&nc, d_cnt, 4, cudaMemcpyDeviceToHost, st));
@@ -788,74 +864,59 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
       SL_CUDA_TRY(cudaStreamSynchronize(st));
     }
   }
-  const size_t nc = cand.size() / 3;
-  std::vector<uint32_t> order(nc);
-  for (size_t i = 0; i < nc; ++i) order[i] = (uint32_t)i;
-  std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cand[3 * x] < cand[3 * y]; });
-  auto c_t = [&](size_t i) { return cand[3 * order[i]]; };
-  auto c_df = [&](size_t i) { return cand[3 * order[i] + 1]; };
-  auto c_dl = [&](size_t i) { return (uint64_t)cand[3 * order[i] + 2]; };
-  // Dense copies: rows with global df >= N/8 (c2 top-10: N/4 -> N/8 +2.4%, N/16 worse). By
-  // default their global footprint is capped at 12 GB (at most 12 GB / (4 N) rows, highest df
-  // first): c5's 50M docs would otherwise take 141 rows, whose chunks crowd L2 (c5 shard
-  // top-100 -8% against the 59 rows of N/4). The cap uses only global quantities, so every
-  // shard of any sharding classifies the same rows (identical per-document summation order).
-  if (!(dense_min_density > 0.f) && ix->N_global) {
-    uint64_t max_rows = (12ull << 30) / (4ull * ix->N_global);
-    if (const char* e = std::getenv("SL_DENSE_MAX_ROWS"))  // bench: a one-GPU stand-in for one shard
-      if (*e) max_rows = std::strtoull(e, nullptr, 10);     // of a larger corpus uses the corpus's cap
-    std::vector<uint32_t> dc;
-    for (size_t i = 0; i < nc; ++i)
-      if ((double)c_df(i) >= dense_thr) dc.push_back(c_df(i));
-    if (dc.size() > max_rows) {
-      if (max_rows == 0) {
-        dense_thr = INFINITY;
-      } else {
-        std::nth_element(dc.begin(), dc.begin() + (max_rows - 1), dc.end(), std::greater<uint32_t>());
-        dense_thr = (double)dc[max_rows - 1] + 1.0;  // strictly above: ties past the cap stay sparse
+  if (!planned) {
+    const size_t nc = cand.size() / 3;
+    std::vector<uint32_t> order(nc);
+    for (size_t i = 0; i < nc; ++i) order[i] = (uint32_t)i;
+    std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return cand[3 * x] < cand[3 * y]; });
+    auto c_t = [&](size_t i) { return cand[3 * order[i]]; };
+    auto c_df = [&](size_t i) { return cand[3 * order[i] + 1]; };
+    auto c_dl = [&](size_t i) { return (uint64_t)cand[3 * order[i] + 2]; };
+    if (dense_cap != UINT64_MAX) {  // highest df first within the cap
+      std::vector<uint32_t> dc;
+      for (size_t i = 0; i < nc; ++i)
+        if ((double)c_df(i) >= dense_thr) dc.push_back(c_df(i));
+      if (dc.size() > dense_cap) {
+        if (dense_cap == 0) {
+          dense_thr = INFINITY;
+        } else {
+          std::nth_element(dc.begin(), dc.begin() + (dense_cap - 1), dc.end(), std::greater<uint32_t>());
+          dense_thr = (double)dc[dense_cap - 1] + 1.0;  // strictly above: ties past the cap stay sparse
+        }
       }
     }
-  }
-  // Per-tile skip tables for rows with >= SL_SKIP_PER_TILE postings per tile on average: a
-  // prefetched table entry beats probing the row's doc ids from one posting per few tiles on
-  // (c2 top-10: 4 -> 0.25 postings/tile +4.5%). Tables cost (tiles+1) x 4 B per row, so they
-  // are held to 4 B per nonzero (at least 64 MB): beyond that budget only the longest rows
-  // get one.
-  {
-    const uint64_t row_bytes = ((uint64_t)ix->num_tiles + 1) * 4;
-    const uint64_t budget = std::max<uint64_t>(4 * ix->nnz, 64ull << 20);
-    std::vector<uint64_t> sc;
-    for (size_t i = 0; i < nc; ++i)
-      if (c_dl(i) >= skip_thr && (double)c_df(i) < dense_thr) sc.push_back(c_dl(i));
-    const uint64_t max_rows = budget / row_bytes;
-    if (sc.size() > max_rows) {
-      if (max_rows == 0) {
-        skip_thr = UINT64_MAX;
-      } else {
-        std::nth_element(sc.begin(), sc.begin() + (max_rows - 1), sc.end(), std::greater<uint64_t>());
-        skip_thr = sc[max_rows - 1] + 1;  // strictly above: ties beyond the budget are dropped
+    {  // longest rows first within the skip-table budget
+      std::vector<uint64_t> sc;
+      for (size_t i = 0; i < nc; ++i)
+        if (c_dl(i) >= skip_thr && (double)c_df(i) < dense_thr) sc.push_back(c_dl(i));
+      if (sc.size() > skip_cap) {
+        if (skip_cap == 0) {
+          skip_thr = UINT64_MAX;
+        } else {
+          std::nth_element(sc.begin(), sc.begin() + (skip_cap - 1), sc.end(), std::greater<uint64_t>());
+          skip_thr = sc[skip_cap - 1] + 1;  // strictly above: ties beyond the budget are dropped
+        }
       }
     }
-  }
-  std::vector<uint32_t> dense_tok, skip_tok;
-  for (size_t i = 0; i < nc; ++i) {
-    if ((double)c_df(i) >= dense_thr) dense_tok.push_back(c_t(i));
-    else if (c_dl(i) >= skip_thr) skip_tok.push_back(c_t(i));
-  }
-  ix->dense_rows = (uint32_t)dense_tok.size();
-  ix->skip_rows = (uint32_t)skip_tok.size();
-  SL_TRY(dalloc(ix, &ix->tokinfo, V));
-  SL_CUDA_TRY(cudaMemsetAsync(ix->tokinfo, 0xFF, (uint64_t)V * 4, st));  // -1: short row
-  uint32_t* slot_tok;
-  SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
-  if (!dense_tok.empty())
-    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok, dense_tok.data(), dense_tok.size() * 4, cudaMemcpyHostToDevice, st));
-  if (!skip_tok.empty())
-    SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
-                                cudaMemcpyHostToDevice, st));
-  if (ix->dense_rows + ix->skip_rows) {
-    k_set_tokinfo<<<grid_for(ix->dense_rows + ix->skip_rows, 256), 256, 0, st>>>(slot_tok, ix->dense_rows,
-                                                                                ix->skip_rows, ix->tokinfo); ++t_launches;
+    for (size_t i = 0; i < nc; ++i) {
+      if ((double)c_df(i) >= dense_thr) dense_tok.push_back(c_t(i));
+      else if (c_dl(i) >= skip_thr) skip_tok.push_back(c_t(i));
+    }
+    ix->dense_rows = (uint32_t)dense_tok.size();
+    ix->skip_rows = (uint32_t)skip_tok.size();
+    SL_TRY(dalloc(ix, &ix->tokinfo, V));
+    SL_CUDA_TRY(cudaMemsetAsync(ix->tokinfo, 0xFF, (uint64_t)V * 4, st));  // -1: short row
+    SL_TRY(tmp.alloc(&slot_tok, dense_tok.size() + skip_tok.size()));
+    if (!dense_tok.empty())
+      SL_CUDA_TRY(cudaMemcpyAsync(slot_tok, dense_tok.data(), dense_tok.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!skip_tok.empty())
+      SL_CUDA_TRY(cudaMemcpyAsync(slot_tok + dense_tok.size(), skip_tok.data(), skip_tok.size() * 4,
+                                  cudaMemcpyHostToDevice, st));
+    if (ix->dense_rows + ix->skip_rows) {
+      k_set_tokinfo<<<grid_for(ix->dense_rows + ix->skip_rows, 256), 256, 0, st>>>(slot_tok, ix->dense_rows,
+                                                                                  ix->skip_rows, ix->tokinfo);
+      ++t_launches;
+    }
   }
   if (ix->dense_rows) {
     SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
@@ -867,7 +928,7 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
     k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 148 * 8), 256, 0, st>>>(
-        ix->indptr, ix->docids, slot_tok + dense_tok.size(), ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
+        ix->indptr, ix->docids, slot_tok + ix->dense_rows, ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
   }
   // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
   // DESIGN.md §8)
@@ -890,14 +951,43 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     SL_TRY(dalloc(ix, &ix->smax, (uint64_t)ix->skip_rows * ix->num_tiles));
     SL_CUDA_TRY(cudaMemsetAsync(ix->smax, 0, (uint64_t)ix->skip_rows * ix->num_tiles * 4, st));
     dim3 g(8, std::min<uint32_t>(ix->skip_rows, 65535));
-    k_skip_tile_max<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok + dense_tok.size(),
+    k_skip_tile_max<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok + ix->dense_rows,
                                        ix->skip_rows, ix->num_tiles, (uint32_t*)ix->smax); ++t_launches;
   }
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
 
+// SL_BUILD_TRACE=1: device time between build phases (events on the build stream), stderr
+struct PhaseTrace {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  explicit PhaseTrace(cudaStream_t s) : st(s) {
+    const char* e = std::getenv("SL_BUILD_TRACE");
+    on = e && std::atoi(e);
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(name, e);
+  }
+  ~PhaseTrace() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "[build] %-14s %8.3f ms\n", ev[i].first, ms);
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+  }
+};
+
 int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
+  PhaseTrace tr(st);
   const uint32_t N = d->num_docs, V = d->vocab_size;
   // ---- inputs on the device
   uint64_t o0 = 0, oN = 0;
@@ -933,6 +1023,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_CUDA_TRY(cudaEventCreate(&ev0));
   SL_CUDA_TRY(cudaEventCreate(&ev1));
   SL_CUDA_TRY(cudaEventRecord(ev0, st));
+  tr.mark("start");
 
   uint32_t* err;
   SL_TRY(tmp.alloc(&err, 1));
@@ -943,6 +1034,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(tmp.alloc(&docs, T));
   SL_TRY(dalloc(ix, &ix->doclens, N));
   k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err); ++t_launches;
+  tr.mark("doc_expand");
 
   // ---- K1: stable LSD radix sort of (token, doc) by token
   int bits = 0;
@@ -959,12 +1051,14 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
     SL_TRY(radix_sort_pairs(tokens, docs, T, bits, kb0, kb1, vb1, docs, st, &ksorted, &vsorted, V, err));
   }
   SL_CUDA_TRY(cudaGetLastError());
+  tr.mark("sort");
   uint32_t herr = 0;
   SL_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (herr & kErrOffsets) SL_FAIL(SL_EINVAL, "build_index: doc offsets must be non-decreasing");
   if (herr & kErrToken) SL_FAIL(SL_EINVAL, "build_index: token id >= vocab size");
   if (herr & kErrDocLen) SL_FAIL(SL_EUNSUPPORTED, "build_index: document longer than 2^32-1 tokens");
+  tr.mark("err_sync");
 
   // ---- K1': run-length encode (t,d) runs
   const uint64_t rle_tiles = (T + kRleTile - 1) / kRleTile;
@@ -975,6 +1069,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(exclusive_scan_u32(tile_offs, tile_offs, rle_tiles, st, &nnz32));
   const uint64_t nnz = nnz32;
   ix->nnz = nnz;
+  tr.mark("rle_count+sync");
   uint32_t *rows, *runstart;
   SL_TRY(tmp.alloc(&rows, nnz));
   SL_TRY(tmp.alloc(&runstart, nnz + 1));
@@ -983,6 +1078,7 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_CUDA_TRY(cudaFuncSetAttribute(k_rle_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kRleTile * 4));
   k_rle_emit<<<(unsigned)rle_tiles, kRleThreads, 3 * kRleTile * 4, st>>>(ksorted, vsorted, T, tile_offs, nnz, V, ix->docids, rows,
                                                           runstart, ix->indptr); ++t_launches;
+  tr.mark("rle_emit");
   if (d->keep_tf) SL_TRY(dalloc(ix, &ix->tf, nnz));
   if (bits > 0) {
     tmp.release(kb0);
@@ -1028,8 +1124,10 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   k_values<<<grid_for(nnz / 4 + 1, 256), 256, 0, st>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64, nnz,
                                                d->params, ix->avg_len, ix->values, ix->tf); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
+  tr.mark("df+stats+values");
 
   SL_TRY(build_query_structures(ix, d->dense_min_density, st));
+  tr.mark("structures");
   SL_CUDA_TRY(cudaEventRecord(ev1, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   SL_CUDA_TRY(cudaEventElapsedTime(&ix->build_ms, ev0, ev1));

@@ -320,3 +320,24 @@ def test_large_k_full_ranking(cuda_ok, c1):
     gi_, gs_ = top_k(s, 20000)
     ri_, rs_ = oracle.top_k(s.astype(np.float64), 20000)
     np.testing.assert_array_equal(gi_.astype(np.int64), ri_.astype(np.int64))
+
+
+@pytest.mark.parametrize("cap", ["0", "3"])
+def test_dense_cap_planning_path(cuda_ok, c1, monkeypatch, cap):
+    """SL_DENSE_MAX_ROWS binds the dense-copy cap: the build plans its access structures on the
+    host (capped path) instead of the device fast path; the highest-df rows stay dense and the
+    top-k still matches the oracle."""
+    cfg, corp, qoff, qtok = c1
+    p = BM25Params(Variant.lucene)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        assert gi.info().dense_rows > 3
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    rid, rsc = ox.retrieve_batch(qoff, qtok, 20, True, 8)
+    monkeypatch.setenv("SL_DENSE_MAX_ROWS", cap)
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        assert gi.info().dense_rows <= int(cap)  # ties at the cap boundary stay sparse
+        gid, gsc = retrieve_batch(gi, (qoff, qtok), 20, as_arrays=True)
+    q = lambda i: qtok[int(qoff[i]):int(qoff[i + 1])]  # noqa: E731
+    assert_topk_match(gid, gsc, rid, rsc, 20, cfg.num_docs, lambda i: ox.score_query(q(i)),
+                      lambda i: query_scale(exp, q(i)), f"dense cap {cap}")
