@@ -985,33 +985,67 @@ __global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __r
 // Zipf corpus repeats a few hundred thousand surface forms tens of millions of times: the raw
 // strings are deduplicated first (two 64-bit hashes per token, an L2-resident table) and only
 // the distinct ones are normalised.
-// table of distinct raw strings: key = first hash, first = smallest token index. HASH: the
-// hashes are computed here (first attempt) instead of read back (retry after a table overflow).
-template <bool HASH>
+// table of distinct raw strings: key = a 128-bit hash of the bytes (two 64-bit lanes, the
+// second mixed with the length), inserted with one 128-bit CAS, so strings that share one lane
+// simply occupy different slots; first = smallest token index; tslot[i] = token i's slot.
+__device__ __forceinline__ ulonglong2 raw_key(const uint8_t* __restrict__ s, uint32_t n) {
+  // 8 bytes per mixing round on two independent lanes (batch-local: never compared with
+  // hashes from elsewhere)
+  uint64_t a = 0x243f6a8885a308d3ull ^ n, b = 0x13198a2e03707344ull + 0x9e3779b97f4a7c15ull * n;
+  uint32_t i = 0;
+  while (i < n) {
+    uint64_t w = 0;
+    const uint32_t m = min(8u, n - i);
+    for (uint32_t j = 0; j < m; ++j) w |= (uint64_t)__ldg(s + i + j) << (8 * j);
+    a = (a ^ w) * 0x100000001b3ull;
+    a ^= a >> 29;
+    b = (b + w) * 0xd6e8feb86659fd93ull;
+    b ^= b >> 32;
+    i += m;
+  }
+  ulonglong2 k;
+  k.x = fmix64(a);
+  k.y = fmix64(b ^ (a >> 7));
+  if ((k.x | k.y) == 0ull) k.y = 1ull;  // (0, 0) marks an empty slot
+  return k;
+}
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\tmov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+      : "memory");
+  return old;
+}
+
 __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
-                             const uint32_t* __restrict__ tlen, uint64_t* __restrict__ h1,
-                             uint64_t* __restrict__ h2, uint64_t n, uint64_t* __restrict__ key,
-                             uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt) {
+                             const uint32_t* __restrict__ tlen, uint64_t n, ulonglong2* __restrict__ key,
+                             uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ tslot) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t k;
-    if (HASH) {
-      const H2 h = hash2(text + tbeg[i], tlen[i]);
-      h1[i] = k = h.a;
-      h2[i] = h.b;
-    } else {
-      k = h1[i];
-    }
-    uint32_t slot = (uint32_t)k & (cap - 1);
+    const ulonglong2 k = raw_key(text + tbeg[i], tlen[i]);
+    uint32_t slot = (uint32_t)k.x & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
         atomicOr(cnt + 1, 1u);
         break;
       }
-      unsigned long long cur = key[slot];  // plain read first: repeated strings skip the atomics
-      if (cur == 0ull) cur = atomicCAS((unsigned long long*)key + slot, 0ull, (unsigned long long)k);
-      if (cur == 0ull || cur == k) {
-        if (cur == 0ull) atomicAdd(cnt, 1u);
+      ulonglong2 cur = key[slot];  // plain read first: repeated strings skip the atomics
+      if ((cur.x | cur.y) == 0ull) {
+        cur = cas128(key + slot, make_ulonglong2(0ull, 0ull), k);
+        if ((cur.x | cur.y) == 0ull) {
+          atomicAdd(cnt, 1u);
+          cur = k;
+        }
+      }
+      if (cur.x == k.x && cur.y == k.y) {
         if (*(volatile uint32_t*)(first + slot) > (uint32_t)i) atomicMin(first + slot, (uint32_t)i);
+        tslot[i] = slot;
         break;
       }
       slot = (slot + 1) & (cap - 1);
@@ -1019,44 +1053,35 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
   }
 }
 
-// per occupied slot of the raw table: what a token needs to verify and resolve its entry
-// (second hash and length of the entry's first token, its entry's id and kept flag), packed
-// in one 16-byte record so a token's lookup touches two sectors (key, record)
-struct RawSlot {
-  uint64_t h2;
-  uint32_t len;
-  uint32_t ik;  // entry id (31 bits: ids < 2^31 or kNew) | kept << 31
-};
-
-__global__ void k_raw_slots(const uint64_t* __restrict__ key, const uint32_t* __restrict__ first,
-                            const uint32_t* __restrict__ rank, uint32_t cap, const uint64_t* __restrict__ h2,
-                            const uint32_t* __restrict__ tlen, const uint32_t* __restrict__ rkeep,
-                            const uint32_t* __restrict__ rid, int build, RawSlot* __restrict__ rs) {
-  for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < cap; sl += gridDim.x * blockDim.x) {
-    if (!key[sl]) continue;
-    const uint32_t f = first[sl], r = rank[sl];
-    const uint32_t t = rid[r];
-    const bool kept = rkeep[r] && (build || t != kNew);
-    rs[sl] = RawSlot{h2[f], tlen[f], (t & 0x7FFFFFFFu) | (kept ? 0x80000000u : 0u)};
+__global__ void k_slot_flags128(const ulonglong2* __restrict__ key, uint32_t cap, uint32_t* __restrict__ flag) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += gridDim.x * blockDim.x) {
+    const ulonglong2 k = key[s];
+    flag[s] = (k.x | k.y) != 0ull;
   }
 }
 
-// per token: its raw entry (identity checked against the entry's first token: second hash,
-// length), then the entry's id and the kept flag (build: not a stopword; query: also in the
-// vocabulary)
-__global__ void k_raw_assign(const uint64_t* __restrict__ h1, const uint64_t* __restrict__ h2,
-                             const uint32_t* __restrict__ tlen, uint64_t n, const uint64_t* __restrict__ key,
-                             const RawSlot* __restrict__ rs, uint32_t cap, uint32_t* __restrict__ id,
-                             uint32_t* __restrict__ kflag, uint32_t* __restrict__ err) {
+// per occupied slot of the raw table: its entry's id (31 bits: ids < 2^31 or kNew) and the
+// kept flag (build: not a stopword; query: also in the vocabulary) in one word
+__global__ void k_raw_slots(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank, uint32_t cap,
+                            const uint32_t* __restrict__ rkeep, const uint32_t* __restrict__ rid, int build,
+                            uint32_t* __restrict__ rs) {
+  for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < cap; sl += gridDim.x * blockDim.x) {
+    if (!flag[sl]) continue;
+    const uint32_t r = rank[sl];
+    const uint32_t t = rid[r];
+    const bool kept = rkeep[r] && (build || t != kNew);
+    rs[sl] = (t & 0x7FFFFFFFu) | (kept ? 0x80000000u : 0u);
+  }
+}
+
+// per token: its raw entry's id and kept flag
+__global__ void k_raw_assign(const uint32_t* __restrict__ tslot, uint64_t n, const uint32_t* __restrict__ rs,
+                             uint32_t* __restrict__ id, uint32_t* __restrict__ kflag) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = h1[i];
-    uint32_t slot = (uint32_t)k & (cap - 1);
-    while (key[slot] != k) slot = (slot + 1) & (cap - 1);
-    const RawSlot r = rs[slot];
-    if (r.h2 != h2[i] || r.len != tlen[i]) atomicOr(err, 1u);
-    const uint32_t t = r.ik & 0x7FFFFFFFu;
+    const uint32_t ik = __ldg(rs + __ldg(tslot + i));
+    const uint32_t t = ik & 0x7FFFFFFFu;
     id[i] = t == 0x7FFFFFFFu ? kNew : t;
-    kflag[i] = r.ik >> 31;
+    kflag[i] = ik >> 31;
   }
 }
 
@@ -1328,30 +1353,22 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   uint32_t R = 0;
   uint64_t* rbeg = nullptr;
   uint32_t* rlen = nullptr;
-  uint64_t *r_h1 = nullptr, *r_h2 = nullptr, *r_key = nullptr;
-  uint32_t *r_first = nullptr, *r_rank = nullptr;
+  uint32_t *r_flag = nullptr, *r_rank = nullptr, *r_tslot = nullptr;
   uint64_t r_cap = 0;
   if (n_tok) {
-    uint64_t *rh1, *rh2;
-    SL_TTRY(scr.alloc(&rh1, n_tok));
-    SL_TTRY(scr.alloc(&rh2, n_tok));
+    SL_TTRY(scr.alloc(&r_tslot, n_tok));
     // sized for a Zipf vocabulary (grows 4x and retries when more than half full)
     uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 19));
-    uint64_t* key = nullptr;
+    ulonglong2* key = nullptr;
     uint32_t *first = nullptr, *cntr = nullptr;
     SL_TTRY(scr.alloc(&cntr, 2));
-    for (bool hashed = false;; hashed = true) {
+    for (;;) {
       SL_TTRY(scr.alloc(&key, cap));
       SL_TTRY(scr.alloc(&first, cap));
-      if (cudaMemsetAsync(key, 0, cap * 8, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
+      if (cudaMemsetAsync(key, 0, cap * 16, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
           cudaMemsetAsync(cntr, 0, 8, st) != cudaSuccess)
         return fail((set_error("memset"), SL_ECUDA));
-      if (!hashed)
-        k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, rh1, rh2, n_tok, key, first,
-                                                            (uint32_t)cap, cntr);
-      else
-        k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, rh1, rh2, n_tok, key, first,
-                                                             (uint32_t)cap, cntr);
+      k_raw_insert<<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr, r_tslot);
       ++t_launches;
       uint32_t h[2];
       SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 8, cudaMemcpyDeviceToHost, st));
@@ -1364,7 +1381,7 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     SL_TTRY(scr.alloc(&sflag, cap));
     SL_TTRY(scr.alloc(&spos, cap));
     SL_TTRY(scr.alloc(&rank, cap));
-    k_slot_flags<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
+    k_slot_flags128<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
     SL_TTRY(exclusive_scan_u32(sflag, spos, cap, st, &R));
     SL_TTRY(scr.alloc(&slots, R));
     SL_TTRY(scr.alloc(&fk, R));
@@ -1378,10 +1395,7 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     SL_TTRY(radix_sort_pairs(fk, slots, R, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
     SL_CUDA_TRY(cudaMemcpyAsync(repf, fs, R * 4ull, cudaMemcpyDeviceToDevice, st));  // first token of entry r
     k_group_rank<<<grid_for(R), 256, 0, st>>>(ss, R, rank); ++t_launches;            // slot -> r
-    r_h1 = rh1;
-    r_h2 = rh2;
-    r_key = key;
-    r_first = first;
+    r_flag = sflag;
     r_rank = rank;
     r_cap = cap;
     SL_TTRY(scr.alloc(&rbeg, R));
@@ -1524,12 +1538,11 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   SL_TTRY(scr.alloc(&kflag, n_all));
   SL_TTRY(scr.alloc(&kpos, n_all));
   if (n_all) {
-    RawSlot* rslot;
+    uint32_t* rslot;
     SL_TTRY(scr.alloc(&rslot, r_cap));
-    k_raw_slots<<<grid_for(r_cap), 256, 0, st>>>(r_key, r_first, r_rank, (uint32_t)r_cap, r_h2, tlen, na.keep, na.id,
-                                                build ? 1 : 0, rslot); ++t_launches;
-    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_h1, r_h2, tlen, n_all, r_key, rslot, (uint32_t)r_cap, tid, kflag,
-                                                  err); ++t_launches;
+    k_raw_slots<<<grid_for(r_cap), 256, 0, st>>>(r_flag, r_rank, (uint32_t)r_cap, na.keep, na.id, build ? 1 : 0, rslot);
+    ++t_launches;
+    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_tslot, n_all, rslot, tid, kflag); ++t_launches;
   }
   uint32_t T = 0;
   SL_TTRY(exclusive_scan_u32(kflag, kpos, n_all, st, &T));
