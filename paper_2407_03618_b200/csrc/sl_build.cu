@@ -151,6 +151,27 @@ __global__ void k_doc_expand(const uint64_t* __restrict__ off, uint32_t N, uint6
   }
 }
 
+// |D| per document, offset validation, and tile_doc[k] = the document holding the first
+// position of radix-sort tile k (the first sort pass derives every position's document from
+// it instead of reading a materialised doc-id array)
+__global__ void k_doc_meta(const uint64_t* __restrict__ off, uint32_t N, uint64_t o0, uint32_t tile,
+                           uint32_t n_tiles, uint32_t* __restrict__ doclens, uint32_t* __restrict__ tile_doc,
+                           uint32_t* err) {
+  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < N; d += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = off[d], e = off[d + 1];
+    if (e < b || b < o0) {
+      atomicOr(err, kErrOffsets);
+      doclens[d] = 0;
+      continue;
+    }
+    if (e - b > 0xFFFFFFFFull) atomicOr(err, kErrDocLen);
+    doclens[d] = (uint32_t)(e - b);
+    if (e == b) continue;
+    const uint64_t k0 = (b - o0 + tile - 1) / tile, k1 = min((e - o0 - 1) / tile, (uint64_t)n_tiles - 1);
+    for (uint64_t k = k0; k <= k1; ++k) tile_doc[k] = (uint32_t)d;
+  }
+}
+
 __global__ void k_check_tokens(const uint32_t* __restrict__ keys, uint64_t n, uint32_t V,
                                uint32_t* err) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -213,11 +234,11 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32_t* __r
 // ranks, and an element's rank = its counter's scanned value + the earlier elements of the
 // same digit in its own thread. The tile is then staged in shared memory in rank order and
 // every digit's run written to its global offset (coalesced). No warp votes per element.
-template <int LOGD>
+template <int LOGD, bool DOCS>
 __global__ void __launch_bounds__(kSortThreads, SL_SORT_MINB) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n, int shift, uint32_t mask, const uint32_t* __restrict__ offs,
-    uint32_t n_tiles) {
+    uint32_t n_tiles, DocSrc ds) {
   constexpr int ND = 1 << LOGD, LANES = ND / 2;
   constexpr int R = LANES;                        // counter words per thread in the raking scan
   constexpr int NWORDS = LANES * kSortThreads;
@@ -232,21 +253,44 @@ __global__ void __launch_bounds__(kSortThreads, SL_SORT_MINB) k_radix_scatter(
   const uint64_t b = tile0 + (uint64_t)tid * kSortIPT;
   const uint32_t cnt = (uint32_t)min((uint64_t)kSortTile, n - tile0);
   uint32_t kk[kSortIPT], vv[kSortIPT];
-  const bool full = cnt == kSortTile && ((((uintptr_t)(kin + b)) | ((uintptr_t)(vin + b))) & 15) == 0;
+  if constexpr (DOCS) {
+    // document of every position: the last document starting at or before the thread's first
+    // position (binary search between the tile's and the next tile's first documents), then
+    // walked forward (empty documents are skipped)
+    const uint32_t tdoc = ds.tile_doc[blockIdx.x];
+    uint32_t lo = min(tdoc, ds.N - 1);
+    uint32_t hi = blockIdx.x + 1 < n_tiles ? min(ds.tile_doc[blockIdx.x + 1], ds.N - 1) : ds.N - 1;
+    if (hi < lo) hi = lo;
+    const uint64_t pb = ds.o0 + b;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(ds.off + mid) <= pb) lo = mid; else hi = mid - 1;
+    }
+    uint32_t d = lo;
+    uint64_t nxt = __ldg(ds.off + d + 1);
+#pragma unroll
+    for (int j = 0; j < kSortIPT; ++j) {
+      while (nxt <= pb + j && d + 1 < ds.N) nxt = __ldg(ds.off + (++d) + 1);
+      vv[j] = d;
+    }
+  }
+  const bool full = cnt == kSortTile && ((((uintptr_t)(kin + b)) | (DOCS ? 0 : ((uintptr_t)(vin + b)))) & 15) == 0;
   if (full) {
 #pragma unroll
     for (int j = 0; j < kSortIPT; j += 4) {
       const uint4 a = *reinterpret_cast<const uint4*>(kin + b + j);
-      const uint4 c = *reinterpret_cast<const uint4*>(vin + b + j);
       kk[j] = a.x; kk[j + 1] = a.y; kk[j + 2] = a.z; kk[j + 3] = a.w;
-      vv[j] = c.x; vv[j + 1] = c.y; vv[j + 2] = c.z; vv[j + 3] = c.w;
+      if constexpr (!DOCS) {
+        const uint4 c = *reinterpret_cast<const uint4*>(vin + b + j);
+        vv[j] = c.x; vv[j + 1] = c.y; vv[j + 2] = c.z; vv[j + 3] = c.w;
+      }
     }
   } else {
 #pragma unroll
     for (int j = 0; j < kSortIPT; ++j) {
       const bool valid = b + j < n;
       kk[j] = valid ? kin[b + j] : 0u;
-      vv[j] = valid ? vin[b + j] : 0u;
+      if constexpr (!DOCS) vv[j] = valid ? vin[b + j] : 0u;
     }
   }
   __syncthreads();
@@ -694,9 +738,11 @@ struct Temps {
 // digits, widths balanced over the passes). Pass p reads the previous output and writes
 // k{p&1}/v{p&1}; kin/vin are only read by the first pass, so v1 may alias vin. When
 // v_check != 0, keys >= v_check set err bit 2 during the first histogram pass.
+int sort_tile_elems() { return kSortTile; }
+
 int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, int bits, uint32_t* k0, uint32_t* k1,
                          uint32_t* v0, uint32_t* v1, cudaStream_t st, const uint32_t** kout, const uint32_t** vout,
-                         uint32_t v_check, uint32_t* err) {
+                         uint32_t v_check, uint32_t* err, const DocSrc* docs) {
   *kout = kin;
   *vout = vin;
   if (bits <= 0 || n == 0) return SL_OK;
@@ -708,9 +754,13 @@ int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, i
   if (n_tiles > 0x7FFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "radix sort: too many tiles");
   static bool attr_set = false;
   if (!attr_set) {
-    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)scatter_smem<6>()));
-    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<7, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter_smem<7>()));
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)scatter_smem<6>()));
+    SL_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)scatter_smem<7>()));
     attr_set = true;
   }
@@ -726,12 +776,21 @@ int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, i
                                                              v_check ? v_check : 0xFFFFFFFFu,
                                                              p == 0 && v_check ? err : nullptr); ++t_launches;
     SL_TRY(exclusive_scan_u32(hist, hist, n_tiles * (uint64_t)(mask + 1), st, nullptr));
-    if (logd == 6)
-      k_radix_scatter<6><<<(unsigned)n_tiles, kSortThreads, scatter_smem<6>(), st>>>(
-          ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist, (uint32_t)n_tiles);
+    const bool from_docs = p == 0 && docs;
+    const DocSrc ds = from_docs ? *docs : DocSrc{};
+    const unsigned g = (unsigned)n_tiles;
+    if (logd == 6 && from_docs)
+      k_radix_scatter<6, true><<<g, kSortThreads, scatter_smem<6>(), st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift,
+                                                                           mask, hist, (uint32_t)n_tiles, ds);
+    else if (logd == 6)
+      k_radix_scatter<6, false><<<g, kSortThreads, scatter_smem<6>(), st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift,
+                                                                            mask, hist, (uint32_t)n_tiles, ds);
+    else if (from_docs)
+      k_radix_scatter<7, true><<<g, kSortThreads, scatter_smem<7>(), st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift,
+                                                                           mask, hist, (uint32_t)n_tiles, ds);
     else
-      k_radix_scatter<7><<<(unsigned)n_tiles, kSortThreads, scatter_smem<7>(), st>>>(
-          ki, vi, kb[p & 1], vb[p & 1], n, shift, mask, hist, (uint32_t)n_tiles);
+      k_radix_scatter<7, false><<<g, kSortThreads, scatter_smem<7>(), st>>>(ki, vi, kb[p & 1], vb[p & 1], n, shift,
+                                                                            mask, hist, (uint32_t)n_tiles, ds);
     ++t_launches;
     ki = kb[p & 1];
     vi = vb[p & 1];
@@ -1029,26 +1088,32 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   SL_TRY(tmp.alloc(&err, 1));
   SL_CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
 
-  // ---- K1: doc expansion
+  // ---- K1: stable LSD radix sort of (token, doc) by token; the first pass takes every
+  // position's doc id from the offsets (k_doc_meta), later passes from the ping-pong buffers
+  int bits = 0;
+  while (bits < 32 && (V - 1) >> bits) ++bits;
   uint32_t *docs, *kb0, *kb1, *vb1;
   SL_TRY(tmp.alloc(&docs, T));
   SL_TRY(dalloc(ix, &ix->doclens, N));
-  k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err); ++t_launches;
-  tr.mark("doc_expand");
-
-  // ---- K1: stable LSD radix sort of (token, doc) by token
-  int bits = 0;
-  while (bits < 32 && (V - 1) >> bits) ++bits;
   const uint32_t* ksorted = tokens;
   const uint32_t* vsorted = docs;
   if (bits == 0) {
+    k_doc_expand<<<grid_for((uint64_t)N * 32, 256), 256, 0, st>>>(off, N, o0, docs, ix->doclens, err); ++t_launches;
     k_check_tokens<<<grid_for(T, 256), 256, 0, st>>>(tokens, T, V, err); ++t_launches;
   } else {
+    const uint64_t n_tiles = (T + kSortTile - 1) / kSortTile;
+    uint32_t* tile_doc;
+    SL_TRY(tmp.alloc(&tile_doc, n_tiles));
+    SL_CUDA_TRY(cudaMemsetAsync(tile_doc, 0, n_tiles * 4, st));
+    k_doc_meta<<<grid_for(N, 256), 256, 0, st>>>(off, N, o0, kSortTile, (uint32_t)n_tiles, ix->doclens, tile_doc,
+                                                 err); ++t_launches;
+    tr.mark("doc_meta");
     SL_TRY(tmp.alloc(&kb0, T));
     SL_TRY(tmp.alloc(&kb1, T));
     SL_TRY(tmp.alloc(&vb1, T));
-    // values ping-pong between vb1 and docs (docs is consumed by the first pass)
-    SL_TRY(radix_sort_pairs(tokens, docs, T, bits, kb0, kb1, vb1, docs, st, &ksorted, &vsorted, V, err));
+    const DocSrc ds{off, o0, N, tile_doc};
+    // values ping-pong between vb1 and docs
+    SL_TRY(radix_sort_pairs(tokens, nullptr, T, bits, kb0, kb1, vb1, docs, st, &ksorted, &vsorted, V, err, &ds));
   }
   SL_CUDA_TRY(cudaGetLastError());
   tr.mark("sort");

@@ -170,8 +170,18 @@ struct IndexView {
 // host launchers shared between sl_build.cu and sl_query.cu
 int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st,
                            uint32_t* total_host);
+// Values of the first pass taken from document offsets instead of vin (index build: the
+// value of token position p is its document): tile_doc[k] = document holding the first
+// position of sort tile k.
+struct DocSrc {
+  const uint64_t* off;  // [N+1] absolute
+  uint64_t o0;
+  uint32_t N;
+  const uint32_t* tile_doc;
+};
 int32_t radix_sort_pairs(const uint32_t* kin, const uint32_t* vin, uint64_t n, int bits, uint32_t* k0, uint32_t* k1,
                          uint32_t* v0, uint32_t* v1, cudaStream_t st, const uint32_t** kout, const uint32_t** vout,
-                         uint32_t v_check, uint32_t* err);
+                         uint32_t v_check, uint32_t* err, const DocSrc* docs = nullptr);
+int sort_tile_elems();  // elements per radix-sort tile
 
 }  // namespace sl
