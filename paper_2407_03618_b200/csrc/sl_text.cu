@@ -318,6 +318,60 @@ __global__ void k_classify4(TextView t, uint32_t* __restrict__ wbits, uint32_t* 
   }
 }
 
+// word-byte mask of four ASCII bytes (SWAR: [0-9], letters after | 0x20, '_'); bit j = byte j
+__device__ __forceinline__ uint32_t ascii_word_mask4(uint32_t v) {
+  const uint32_t dg = (v + 0x50505050u) & ~(v + 0x46464646u);  // >= '0' and < ':'
+  const uint32_t u = v | 0x20202020u;
+  const uint32_t al = (u + 0x1F1F1F1Fu) & ~(u + 0x05050505u);  // >= 'a' and < '{'
+  const uint32_t x = v ^ 0x5F5F5F5Fu;
+  const uint32_t nz = ((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x;    // bit 7: byte != '_'
+  const uint32_t w = (dg | al | ~nz) & 0x80808080u;
+  return ((w >> 7) & 1u) | ((w >> 14) & 2u) | ((w >> 21) & 4u) | ((w >> 28) & 8u);
+}
+
+// 16 bytes per thread from one 16-byte load (text 16-byte aligned): all-ASCII groups classify
+// with SWAR arithmetic; any other group takes classify_byte per byte. Two lanes form one
+// 32-byte bitmap word (one shuffle each for the word and start bitmaps).
+__global__ void k_classify16(TextView t, uint32_t* __restrict__ wbits, uint32_t* __restrict__ sbits) {
+  const uint64_t ng = (t.n + 15) >> 4;
+  const uint64_t ng_pad = ((ng + 31) >> 5) << 5;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng_pad; g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t wm = 0, sm = 0;
+    const uint64_t b0 = g << 4;
+    if (b0 + 16 <= t.n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(t.text) + g);
+      if (!((v.x | v.y | v.z | v.w) & 0x80808080u)) {
+        wm = ascii_word_mask4(v.x) | (ascii_word_mask4(v.y) << 4) | (ascii_word_mask4(v.z) << 8) |
+             (ascii_word_mask4(v.w) << 12);
+        sm = wm;  // ASCII bytes are codepoint starts
+      } else {
+        for (int j = 0; j < 16; ++j) {
+          bool w, st;
+          classify_byte(t, b0 + j, w, st);
+          wm |= (uint32_t)w << j;
+          sm |= (uint32_t)(w && st) << j;
+        }
+      }
+    } else if (b0 < t.n) {
+      for (int j = 0; j < 16 && b0 + j < t.n; ++j) {
+        bool w, st;
+        classify_byte(t, b0 + j, w, st);
+        wm |= (uint32_t)w << j;
+        sm |= (uint32_t)(w && st) << j;
+      }
+    }
+    const int sh = 16 * (int)(g & 1);
+    uint32_t wv = wm << sh, sv = sm << sh;
+    wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+    sv |= __shfl_xor_sync(0xffffffffu, sv, 1);
+    const uint64_t word_idx = g >> 1;
+    if (!(g & 1) && (word_idx << 5) < t.n) {
+      wbits[word_idx] = wv;
+      sbits[word_idx] = sv;
+    }
+  }
+}
+
 // token ending at the first non-word byte or document start after p; codepoint count
 __device__ __forceinline__ void token_extent(const uint32_t* wbits, const uint32_t* sbits, const uint32_t* dbits,
                                              uint64_t nw, uint64_t p, uint64_t* end, uint32_t* ncp) {
@@ -988,26 +1042,57 @@ __global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __r
 // table of distinct raw strings: key = a 128-bit hash of the bytes (two 64-bit lanes, the
 // second mixed with the length), inserted with one 128-bit CAS, so strings that share one lane
 // simply occupy different slots; first = smallest token index; tslot[i] = token i's slot.
-__device__ __forceinline__ ulonglong2 raw_key(const uint8_t* __restrict__ s, uint32_t n) {
-  // 8 bytes per mixing round on two independent lanes (batch-local: never compared with
-  // hashes from elsewhere)
-  uint64_t a = 0x243f6a8885a308d3ull ^ n, b = 0x13198a2e03707344ull + 0x9e3779b97f4a7c15ull * n;
-  uint32_t i = 0;
-  while (i < n) {
-    uint64_t w = 0;
-    const uint32_t m = min(8u, n - i);
-    for (uint32_t j = 0; j < m; ++j) w |= (uint64_t)__ldg(s + i + j) << (8 * j);
+struct RawMix {
+  uint64_t a, b;
+  __device__ __forceinline__ RawMix(uint32_t n) : a(0x243f6a8885a308d3ull ^ n), b(0x13198a2e03707344ull + 0x9e3779b97f4a7c15ull * n) {}
+  __device__ __forceinline__ void add(uint64_t w) {  // the next (up to) 8 bytes, little-endian
     a = (a ^ w) * 0x100000001b3ull;
     a ^= a >> 29;
     b = (b + w) * 0xd6e8feb86659fd93ull;
     b ^= b >> 32;
-    i += m;
   }
-  ulonglong2 k;
-  k.x = fmix64(a);
-  k.y = fmix64(b ^ (a >> 7));
-  if ((k.x | k.y) == 0ull) k.y = 1ull;  // (0, 0) marks an empty slot
-  return k;
+  __device__ __forceinline__ ulonglong2 key() const {
+    ulonglong2 k;
+    k.x = fmix64(a);
+    k.y = fmix64(b ^ (a >> 7));
+    if ((k.x | k.y) == 0ull) k.y = 1ull;  // (0, 0) marks an empty slot
+    return k;
+  }
+};
+
+// 8 bytes per mixing round on two independent lanes (batch-local: never compared with hashes
+// from elsewhere). ALIGNED (text 4-byte aligned): the rounds' bytes come from aligned 32-bit
+// words joined by funnel shifts (never a word past the one holding the token's last byte);
+// otherwise byte loads. Both feed identical 8-byte words.
+template <bool ALIGNED>
+__device__ __forceinline__ ulonglong2 raw_key(const uint8_t* __restrict__ text, uint64_t beg, uint32_t n) {
+  RawMix h(n);
+  if (ALIGNED) {
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(text);
+    uint64_t p = beg;
+    const uint64_t e = beg + n;
+    while (p < e) {
+      const uint32_t m = (uint32_t)min((uint64_t)8, e - p);
+      const uint32_t sh = (uint32_t)(p & 3) * 8;
+      const uint64_t wi = p >> 2, wl = (p + m - 1) >> 2;  // words holding the round's first / last byte
+      const uint32_t w0 = __ldg(w32 + wi);
+      const uint32_t w1 = wl > wi ? __ldg(w32 + wi + 1) : 0u;
+      const uint32_t w2 = wl > wi + 1 ? __ldg(w32 + wi + 2) : 0u;
+      uint64_t w = ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
+      if (m < 8) w &= (1ull << (8 * m)) - 1ull;
+      h.add(w);
+      p += m;
+    }
+  } else {
+    const uint8_t* s = text + beg;
+    for (uint32_t i = 0; i < n; i += 8) {
+      uint64_t w = 0;
+      const uint32_t m = min(8u, n - i);
+      for (uint32_t j = 0; j < m; ++j) w |= (uint64_t)__ldg(s + i + j) << (8 * j);
+      h.add(w);
+    }
+  }
+  return h.key();
 }
 
 __device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
@@ -1023,12 +1108,13 @@ __device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulon
   return old;
 }
 
+template <bool ALIGNED>
 __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
                              const uint32_t* __restrict__ tlen, uint64_t n, ulonglong2* __restrict__ key,
                              uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt,
                              uint32_t* __restrict__ tslot) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ulonglong2 k = raw_key(text + tbeg[i], tlen[i]);
+    const ulonglong2 k = raw_key<ALIGNED>(text, tbeg[i], tlen[i]);
     uint32_t slot = (uint32_t)k.x & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
@@ -1044,7 +1130,8 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
         }
       }
       if (cur.x == k.x && cur.y == k.y) {
-        if (*(volatile uint32_t*)(first + slot) > (uint32_t)i) atomicMin(first + slot, (uint32_t)i);
+        // a stale (larger) cached value only costs an atomicMin that changes nothing
+        if (first[slot] > (uint32_t)i) atomicMin(first + slot, (uint32_t)i);
         tslot[i] = slot;
         break;
       }
@@ -1313,7 +1400,9 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     if (cudaMemsetAsync(dbits, 0, nw * 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
     k_doc_marks<<<grid_for(N), 256, 0, st>>>(doc_off, N, nb, dbits); ++t_launches;
     const TextView tv{text, nb, dbits};
-    if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0) {
+    if ((reinterpret_cast<uintptr_t>(text) & 15u) == 0) {
+      k_classify16<<<grid_for((nb + 15) / 16), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+    } else if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0) {
       k_classify4<<<grid_for((nb + 3) / 4), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
     } else {
       k_classify<<<grid_for(nw * 32), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
@@ -1368,7 +1457,12 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
       if (cudaMemsetAsync(key, 0, cap * 16, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
           cudaMemsetAsync(cntr, 0, 8, st) != cudaSuccess)
         return fail((set_error("memset"), SL_ECUDA));
-      k_raw_insert<<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr, r_tslot);
+      if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0)
+        k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
+                                                            r_tslot);
+      else
+        k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
+                                                             r_tslot);
       ++t_launches;
       uint32_t h[2];
       SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 8, cudaMemcpyDeviceToHost, st));

@@ -208,14 +208,15 @@ def test_text_index_errors(cuda_ok):
 
 
 def test_device_input_unaligned(cuda_ok, port):
-    """Device-resident text (zero-copy) at an odd address takes the byte-wise classifier."""
+    """Device-resident text (zero-copy): 16-byte aligned input takes the 16-byte SWAR classifier,
+    4-byte aligned the 4-byte one, odd addresses the byte-wise classifier; all identical."""
     import torch
     from paper_2407_03618_b200._lib import SL_MEM_DEVICE
     words = make_words(2000, seed=61, unicode_frac=0.1)
     text, off = make_corpus(500, words, seed=3, malformed_frac=0.02)
     want = port.tokenize_corpus(text, off, 1, 1, 1)
-    for shift in (0, 1, 3):
-        buf = torch.zeros(len(text) + 8, dtype=torch.uint8, device="cuda")
+    for shift in (0, 1, 3, 4, 8):
+        buf = torch.zeros(len(text) + 16, dtype=torch.uint8, device="cuda")
         buf[shift:shift + len(text)] = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
         doff = torch.from_numpy(off.view(np.int64)).cuda()
         v = T.Vocabulary()
@@ -248,3 +249,27 @@ def test_many_distinct_strings_table_growth(cuda_ok):
     _, ids = b.to_numpy()
     assert len(seen) > 1_000_000 and v.size() == len(seen)
     assert np.array_equal(ids, np.array(ref_ids, np.uint32))
+
+
+def test_all_ascii_bytes_classifier(cuda_ok, port):
+    """Every ASCII byte value (controls, punctuation, digits, both cases, '_', DEL) in random
+    documents: the SWAR fast path of the 16-byte classifier against the oracle port."""
+    import torch
+    from paper_2407_03618_b200._lib import SL_MEM_DEVICE
+    rng = np.random.default_rng(29)
+    alphabet = np.arange(1, 128, dtype=np.uint8)
+    weights = np.where((alphabet >= ord("a")) & (alphabet <= ord("z")), 8.0, 1.0)
+    weights /= weights.sum()
+    lens = rng.integers(0, 400, 600)
+    off = np.zeros(len(lens) + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    text = rng.choice(alphabet, int(off[-1]), p=weights).astype(np.uint8).tobytes()
+    for cfg in ((1, 1, 1), (0, 0, 0)):
+        want = port.tokenize_corpus(text, off, *cfg)
+        buf = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+        assert buf.data_ptr() % 16 == 0
+        doff = torch.from_numpy(off.view(np.int64)).cuda()
+        v = T.Vocabulary()
+        b = T._tokenize_raw(buf.data_ptr(), doff.data_ptr(), len(off) - 1, cfg_of(*cfg), v, True, SL_MEM_DEVICE)
+        got_off, got_ids = b.to_numpy()
+        assert np.array_equal(got_off, want[0]) and np.array_equal(got_ids, want[1]) and v.tokens() == want[2], cfg
