@@ -997,16 +997,6 @@ __global__ void k_table_rehash(const uint64_t* __restrict__ offs, const uint8_t*
   }
 }
 
-__global__ void k_out_ids(const uint32_t* __restrict__ kept_idx, uint64_t n, const uint32_t* __restrict__ id,
-                          const uint64_t* __restrict__ tbeg, uint32_t* __restrict__ out_ids,
-                          uint64_t* __restrict__ out_beg) {
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = kept_idx[j];
-    out_ids[j] = id[t];
-    out_beg[j] = tbeg[t];
-  }
-}
-
 // token offsets per document: lower_bound of the document's first byte among kept tokens
 __global__ void k_doc_token_offsets(const uint64_t* __restrict__ doc_off, uint32_t N,
                                     const uint64_t* __restrict__ kbeg, uint64_t T, uint64_t* __restrict__ out) {
@@ -1161,14 +1151,84 @@ __global__ void k_raw_slots(const uint32_t* __restrict__ flag, const uint32_t* _
   }
 }
 
-// per token: its raw entry's id and kept flag
-__global__ void k_raw_assign(const uint32_t* __restrict__ tslot, uint64_t n, const uint32_t* __restrict__ rs,
-                             uint32_t* __restrict__ id, uint32_t* __restrict__ kflag) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t ik = __ldg(rs + __ldg(tslot + i));
-    const uint32_t t = ik & 0x7FFFFFFFu;
-    id[i] = t == 0x7FFFFFFFu ? kNew : t;
-    kflag[i] = ik >> 31;
+// Kept tokens in order, in two passes over tiles of kKeepTile tokens: round j of a tile is
+// tokens [j*256, j*256 + 256) (thread tid takes token j*256 + tid: coalesced loads). The kept
+// flag is the token's raw entry's flag, read through its slot. k_keep_count counts each tile's
+// kept tokens, one scan of the tile counts, then k_keep_emit ranks every kept token by the
+// ballots of its (round, warp) and writes its id and first byte (coalesced runs).
+constexpr int kKeepThreads = 256, kKeepRounds = 16, kKeepTile = kKeepThreads * kKeepRounds;
+constexpr int kKeepWarps = kKeepThreads / 32;
+
+__global__ void __launch_bounds__(kKeepThreads) k_keep_count(const uint32_t* __restrict__ tslot, uint64_t n,
+                                                             const uint32_t* __restrict__ rs,
+                                                             uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t s_c[kKeepWarps];
+  const uint64_t t0 = (uint64_t)blockIdx.x * kKeepTile + threadIdx.x;
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kKeepRounds; ++j) {
+    const uint64_t i = t0 + (uint64_t)j * kKeepThreads;
+    const bool kept = i < n && (__ldg(rs + __ldg(tslot + i)) >> 31);
+    c += __popc(__ballot_sync(0xffffffffu, kept));
+  }
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < kKeepWarps; ++w) tot += s_c[w];
+    tile_cnt[blockIdx.x] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(kKeepThreads) k_keep_emit(const uint32_t* __restrict__ tslot, uint64_t n,
+                                                            const uint32_t* __restrict__ rs,
+                                                            const uint64_t* __restrict__ tbeg,
+                                                            const uint32_t* __restrict__ tile_off,
+                                                            uint32_t* __restrict__ ids, uint64_t* __restrict__ kbeg) {
+  __shared__ uint32_t s_off[kKeepRounds * kKeepWarps];  // (round, warp) -> first output index in the tile
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t t0 = (uint64_t)blockIdx.x * kKeepTile + threadIdx.x;
+  uint32_t ik[kKeepRounds], bal[kKeepRounds];
+#pragma unroll
+  for (int j = 0; j < kKeepRounds; ++j) {
+    const uint64_t i = t0 + (uint64_t)j * kKeepThreads;
+    ik[j] = i < n ? __ldg(rs + __ldg(tslot + i)) : 0u;
+    bal[j] = __ballot_sync(0xffffffffu, ik[j] >> 31);
+    if (lane == 0) s_off[j * kKeepWarps + w] = __popc(bal[j]);
+  }
+  __syncthreads();
+  if (w == 0) {  // exclusive scan of the 128 (round, warp) counts, 4 per lane
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[q] = s_off[lane * 4 + q];
+      sum += v[q];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    uint32_t run = x - sum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s_off[lane * 4 + q] = run;
+      run += v[q];
+    }
+  }
+  __syncthreads();
+  const uint32_t o = tile_off[blockIdx.x];
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kKeepRounds; ++j) {
+    if (ik[j] >> 31) {
+      const uint64_t i = t0 + (uint64_t)j * kKeepThreads;
+      const uint32_t pos = o + s_off[j * kKeepWarps + w] + __popc(bal[j] & lt);
+      const uint32_t t = ik[j] & 0x7FFFFFFFu;
+      ids[pos] = t == 0x7FFFFFFFu ? kNew : t;
+      kbeg[pos] = __ldg(tbeg + i);
+    }
   }
 }
 
@@ -1627,22 +1687,17 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     }
   }
   // ---- every token takes its raw entry's id; kept flags
-  uint32_t *tid, *kflag, *kpos, *kidx;
-  SL_TTRY(scr.alloc(&tid, n_all));
-  SL_TTRY(scr.alloc(&kflag, n_all));
-  SL_TTRY(scr.alloc(&kpos, n_all));
+  uint32_t T = 0;
+  uint32_t* rslot = nullptr;
+  uint32_t* tile_off = nullptr;
+  const uint64_t keep_tiles = (n_all + kKeepTile - 1) / kKeepTile;
   if (n_all) {
-    uint32_t* rslot;
     SL_TTRY(scr.alloc(&rslot, r_cap));
     k_raw_slots<<<grid_for(r_cap), 256, 0, st>>>(r_flag, r_rank, (uint32_t)r_cap, na.keep, na.id, build ? 1 : 0, rslot);
     ++t_launches;
-    k_raw_assign<<<grid_for(n_all), 256, 0, st>>>(r_tslot, n_all, rslot, tid, kflag); ++t_launches;
-  }
-  uint32_t T = 0;
-  SL_TTRY(exclusive_scan_u32(kflag, kpos, n_all, st, &T));
-  SL_TTRY(scr.alloc(&kidx, T));
-  if (n_all) {
-    k_compact_idx<<<grid_for(n_all), 256, 0, st>>>(kflag, kpos, n_all, kidx); ++t_launches;
+    SL_TTRY(scr.alloc(&tile_off, keep_tiles));
+    k_keep_count<<<(unsigned)keep_tiles, kKeepThreads, 0, st>>>(r_tslot, n_all, rslot, tile_off); ++t_launches;
+    SL_TTRY(exclusive_scan_u32(tile_off, tile_off, keep_tiles, st, &T));
   }
   // ---- outputs
   tb->T = T;
@@ -1651,7 +1706,8 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   uint64_t* kbeg;
   SL_TTRY(scr.alloc(&kbeg, T));
   if (T) {
-    k_out_ids<<<grid_for(T), 256, 0, st>>>(kidx, T, tid, tbeg, tb->ids, kbeg); ++t_launches;
+    k_keep_emit<<<(unsigned)keep_tiles, kKeepThreads, 0, st>>>(r_tslot, n_all, rslot, tbeg, tile_off, tb->ids, kbeg);
+    ++t_launches;
   }
   k_doc_token_offsets<<<grid_for((uint64_t)N + 1), 256, 0, st>>>(doc_off, N, kbeg, T, tb->offs); ++t_launches;
   uint32_t h_err = 0;
