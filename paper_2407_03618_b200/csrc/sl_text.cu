@@ -396,33 +396,80 @@ __device__ __forceinline__ void token_extent(const uint32_t* wbits, const uint32
   *ncp = cnt;
 }
 
+// Token starts with >= 2 codepoints, one thread per 32-byte bitmap word, tiles of 256 words.
+// Count pass: per-word counts (u8: at most 16 starts per word) and per-tile totals; the tile
+// totals are scanned; emit pass: a block scan of the word counts gives every word's first
+// output slot (no word-sized scan).
+constexpr int kTokThreads = 256;
+
 template <bool EMIT>
-__global__ void k_tokens(const uint32_t* __restrict__ wbits, const uint32_t* __restrict__ sbits,
-                         const uint32_t* __restrict__ dbits, uint64_t nw, uint32_t* __restrict__ cnt,
-                         const uint32_t* __restrict__ pos, uint64_t* __restrict__ tbeg, uint32_t* __restrict__ tlen) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t W = wbits[i], D = dbits[i];
-    const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
-    uint32_t B = W & (D | ~((W << 1) | prev));
-    uint32_t c = 0, o = EMIT ? pos[i] : 0;
-    while (B) {
-      const uint32_t j = __ffs(B) - 1;
-      B &= B - 1;
-      const uint64_t p = (i << 5) + j;
-      uint64_t e;
-      uint32_t ncp;
-      token_extent(wbits, sbits, dbits, nw, p, &e, &ncp);
-      if (ncp >= 2) {
-        if (EMIT) {
-          tbeg[o] = p;
-          tlen[o] = (uint32_t)(e - p);
-          ++o;
-        } else {
-          ++c;
-        }
+__global__ void __launch_bounds__(kTokThreads) k_tokens(const uint32_t* __restrict__ wbits,
+                                                        const uint32_t* __restrict__ sbits,
+                                                        const uint32_t* __restrict__ dbits, uint64_t nw,
+                                                        uint8_t* __restrict__ wcnt, uint32_t* __restrict__ tile,
+                                                        uint64_t* __restrict__ tbeg, uint32_t* __restrict__ tlen) {
+  __shared__ uint32_t sw[kTokThreads / 32 + 1];
+  const uint64_t i = (uint64_t)blockIdx.x * kTokThreads + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t c = 0;
+  if (!EMIT) {
+    if (i < nw) {
+      const uint32_t W = wbits[i], D = dbits[i];
+      const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
+      uint32_t B = W & (D | ~((W << 1) | prev));
+      while (B) {
+        const uint32_t j = __ffs(B) - 1;
+        B &= B - 1;
+        uint64_t e;
+        uint32_t ncp;
+        token_extent(wbits, sbits, dbits, nw, (i << 5) + j, &e, &ncp);
+        c += ncp >= 2;
       }
+      wcnt[i] = (uint8_t)c;
     }
-    if (!EMIT) cnt[i] = c;
+  } else {
+    c = i < nw ? wcnt[i] : 0u;
+  }
+  // block exclusive scan of c (EMIT) / block total (count)
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sw[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < kTokThreads / 32; ++k) {
+      const uint32_t t = sw[k];
+      sw[k] = run;
+      run += t;
+    }
+    sw[kTokThreads / 32] = run;
+  }
+  __syncthreads();
+  if (!EMIT) {
+    if (threadIdx.x == 0) tile[blockIdx.x] = sw[kTokThreads / 32];
+    return;
+  }
+  if (!c) return;
+  uint32_t o = tile[blockIdx.x] + sw[w] + x - c;
+  const uint32_t W = wbits[i], D = dbits[i];
+  const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
+  uint32_t B = W & (D | ~((W << 1) | prev));
+  while (B) {
+    const uint32_t j = __ffs(B) - 1;
+    B &= B - 1;
+    const uint64_t p = (i << 5) + j;
+    uint64_t e;
+    uint32_t ncp;
+    token_extent(wbits, sbits, dbits, nw, p, &e, &ncp);
+    if (ncp >= 2) {
+      tbeg[o] = p;
+      tlen[o] = (uint32_t)(e - p);
+      ++o;
+    }
   }
 }
 
@@ -1448,11 +1495,10 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     return fail((set_error("tokenize: allocation failed"), SL_ENOMEM));
   // ---- segmentation
   const uint64_t nw = (nb + 31) / 32;
-  uint32_t *dbits, *wbits, *sbits, *cnt;
+  uint32_t *dbits, *wbits, *sbits;
   SL_TTRY(scr.alloc(&dbits, nw));
   SL_TTRY(scr.alloc(&wbits, nw));
   SL_TTRY(scr.alloc(&sbits, nw));
-  SL_TTRY(scr.alloc(&cnt, nw));
   uint64_t n_tok = 0;
   uint64_t *tbeg = nullptr;
   uint32_t* tlen = nullptr;
@@ -1467,14 +1513,21 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     } else {
       k_classify<<<grid_for(nw * 32), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
     }
-    k_tokens<false><<<grid_for(nw), 256, 0, st>>>(wbits, sbits, dbits, nw, cnt, nullptr, nullptr, nullptr);
+    const uint64_t tok_tiles = (nw + kTokThreads - 1) / kTokThreads;
+    uint8_t* wcnt;
+    uint32_t* tok_tile;
+    SL_TTRY(scr.alloc(&wcnt, nw));
+    SL_TTRY(scr.alloc(&tok_tile, tok_tiles));
+    k_tokens<false><<<(unsigned)tok_tiles, kTokThreads, 0, st>>>(wbits, sbits, dbits, nw, wcnt, tok_tile, nullptr,
+                                                                  nullptr);
     ++t_launches;
     uint32_t tot = 0;
-    SL_TTRY(exclusive_scan_u32(cnt, cnt, nw, st, &tot));
+    SL_TTRY(exclusive_scan_u32(tok_tile, tok_tile, tok_tiles, st, &tot));
     n_tok = tot;
     SL_TTRY(scr.alloc(&tbeg, n_tok));
     SL_TTRY(scr.alloc(&tlen, n_tok));
-    k_tokens<true><<<grid_for(nw), 256, 0, st>>>(wbits, sbits, dbits, nw, nullptr, cnt, tbeg, tlen); ++t_launches;
+    k_tokens<true><<<(unsigned)tok_tiles, kTokThreads, 0, st>>>(wbits, sbits, dbits, nw, wcnt, tok_tile, tbeg, tlen);
+    ++t_launches;
   }
   // ---- normalisation + vocabulary probe
   std::vector<std::string> sw;
