@@ -100,8 +100,14 @@ def dist_setup():
     return world, rank, local
 
 
-def workload_name(cfg_i, k):
-    return {1: "c1", 2: "c2", 3: "c3", 4: "c4", 5: "c5"}[cfg_i] + f" lucene k1=1.5 b=0.75 top-{k}"
+# c3 (BASELINE.json configs[2]) pins delta = 0.5 for BM25L and BM25+; tfldp needs delta > 1/e
+VARIANT_DELTA = {"lucene": 0.0, "robertson": 0.0, "atire": 0.0, "bm25l": 0.5, "bm25plus": 0.5, "tfldp": 0.5}
+
+
+def workload_name(cfg_i, k, variant="lucene"):
+    d = VARIANT_DELTA[variant]
+    return ({1: "c1", 2: "c2", 3: "c3", 4: "c4", 5: "c5"}[cfg_i] + f" {variant} k1=1.5 b=0.75"
+            + (f" delta={d}" if d else "") + f" top-{k}")
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -111,13 +117,14 @@ def cpu_corpus(cfg_i):
     return synth.corpus_host(cfg, threads=os.cpu_count() or 8)
 
 
-def cpu_reference_run(cfg_i, k, steps, warmup, sample_q, workers, corp=None):
+def cpu_reference_run(cfg_i, k, steps, warmup, sample_q, workers, corp=None, variant="lucene"):
     """Times the CPU port (oracle/) of the reference path: build single-thread, retrieve_batch with `workers`."""
     import oracle
-    from paper_2407_03618_b200 import synth
+    from paper_2407_03618_b200 import Variant, synth
     corp = corp or cpu_corpus(cfg_i)
     t0 = time.perf_counter()
-    ox = oracle.OracleIndex(corp.offsets, corp.tokens, corp.cfg.vocab, 2, 1.5, 0.75, 0.0)
+    ox = oracle.OracleIndex(corp.offsets, corp.tokens, corp.cfg.vocab, int(Variant[variant]), 1.5, 0.75,
+                            VARIANT_DELTA[variant])
     build_s = time.perf_counter() - t0
     qoff, qtok = synth.queries(corp.cfg, corp.cdf, 0, sample_q)
     times = []
@@ -137,13 +144,14 @@ def run_reference(args):
         return 0
     cores = os.cpu_count() or 1
     sample_q = args.ref_sample
-    r = cpu_reference_run(args.config, args.k, args.steps, args.warmup, sample_q, cores)
+    r = cpu_reference_run(args.config, args.k, args.steps, args.warmup, sample_q, cores, variant=args.variant)
     line = {
         "metric": METRIC, "impl": "reference", "value": r["qps"], "unit": "queries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sample_q / r["qps"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle accumulator)",
         "data": "synthetic (seeded Zipf corpus/queries, BASELINE.md §5)",
-        "config": {"workload": workload_name(args.config, args.k), "queries_per_step": sample_q, "k": args.k,
+        "config": {"workload": workload_name(args.config, args.k, args.variant), "queries_per_step": sample_q,
+                   "k": args.k,
                    "docs": int(len(r["corp"].offsets) - 1), "vocab": int(r["corp"].cfg.vocab)},
         "index_tokens_per_s": r["tokens"] / r["build_s"],
         "cpu_baseline": {"value": r["qps"], "unit": "queries/s", "cores": cores, "kind": "port",
@@ -265,7 +273,7 @@ def run_ours(args):
         uid = [Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = Comm(uid[0], world, rank, local)
-    params = BM25Params(Variant.lucene, 1.5, 0.75, 0.0)
+    params = BM25Params(Variant[args.variant], 1.5, 0.75, VARIANT_DELTA[args.variant])
     # build: warm once (allocator, module load), then the measured build
     idx = build_index(loff, tok, cfg.vocab, params, device=local, doc_base=d0, comm=comm,
                       dense_min_density=args.dense_density)
@@ -363,7 +371,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 accumulate (f64 build math)",
             "data": "synthetic (seeded Zipf corpus/queries, BASELINE.md §5; BEIR absent)",
-            "config": {"workload": workload_name(args.config, k), "docs": cfg.num_docs, "vocab": cfg.vocab,
+            "config": {"workload": workload_name(args.config, k, args.variant), "docs": cfg.num_docs, "vocab": cfg.vocab,
                        "tokens": T_total, "nnz_local": int(info.nnz_local), "queries_per_step": B, "k": k,
                        "parallelism": f"doc-shard x{world}", "l2": "flushed between steps (256 MiB memset)",
                        "dense_rows": int(info.dense_rows), "skip_rows": int(info.skip_rows),
@@ -397,7 +405,7 @@ def run_ours(args):
         line["index_build"]["frac"] = line["index_build"]["achieved_GBps"] / hbm
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            r = cpu_reference_run(args.config, k, 1, 1, args.cpu_sample, cores)
+            r = cpu_reference_run(args.config, k, 1, 1, args.cpu_sample, cores, variant=args.variant)
             line["cpu_baseline"] = {"value": r["qps"], "unit": "queries/s", "cores": cores, "kind": "port",
                                     "sample": f"first {args.cpu_sample} queries of c{args.config}, full 1M-doc "
                                               f"index; CPU build (1 thread) {r['build_s']:.1f}s = "
@@ -423,6 +431,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--variant", choices=list(VARIANT_DELTA), default="lucene",
+                    help="BM25 variant (c3 sweeps robertson, atire, bm25l, bm25plus on c2's corpus)")
     ap.add_argument("--dense-density", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-text", action="store_true", help="skip the text-pipeline block")
