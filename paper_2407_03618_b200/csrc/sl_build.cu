@@ -1117,13 +1117,8 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   }
   SL_CUDA_TRY(cudaGetLastError());
   tr.mark("sort");
-  uint32_t herr = 0;
+  uint32_t herr = 0;  // checked after the run-count sync below (one host round trip)
   SL_CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
-  SL_CUDA_TRY(cudaStreamSynchronize(st));
-  if (herr & kErrOffsets) SL_FAIL(SL_EINVAL, "build_index: doc offsets must be non-decreasing");
-  if (herr & kErrToken) SL_FAIL(SL_EINVAL, "build_index: token id >= vocab size");
-  if (herr & kErrDocLen) SL_FAIL(SL_EUNSUPPORTED, "build_index: document longer than 2^32-1 tokens");
-  tr.mark("err_sync");
 
   // ---- K1': run-length encode (t,d) runs
   const uint64_t rle_tiles = (T + kRleTile - 1) / kRleTile;
@@ -1132,6 +1127,9 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   k_rle_count<<<(unsigned)rle_tiles, kRleThreads, 0, st>>>(ksorted, vsorted, T, tile_offs); ++t_launches;
   uint32_t nnz32 = 0;
   SL_TRY(exclusive_scan_u32(tile_offs, tile_offs, rle_tiles, st, &nnz32));
+  if (herr & kErrOffsets) SL_FAIL(SL_EINVAL, "build_index: doc offsets must be non-decreasing");
+  if (herr & kErrToken) SL_FAIL(SL_EINVAL, "build_index: token id >= vocab size");
+  if (herr & kErrDocLen) SL_FAIL(SL_EUNSUPPORTED, "build_index: document longer than 2^32-1 tokens");
   const uint64_t nnz = nnz32;
   ix->nnz = nnz;
   tr.mark("rle_count+sync");
