@@ -241,6 +241,16 @@ int32_t sl_token_batch_info(const sl_token_batch* batch, uint32_t* num_docs, uin
 int32_t sl_token_batch_copy(const sl_token_batch* batch, uint64_t* host_offsets, uint32_t* host_ids);
 int32_t sl_token_batch_destroy(sl_token_batch* batch);
 
+/* Streaming tokenize of a HOST corpus (same output as sl_tokenize + sl_token_batch_copy): the
+ * corpus is cut into document-aligned chunks of about chunk_bytes (0: 64 MiB); chunk i+1 is
+ * copied to the device while chunk i is tokenized, and each chunk's ids / token offsets are
+ * copied back while the next chunk runs (separate H2D and D2H streams). out_offsets:
+ * u64[num_docs+1]; out_ids: room for ids_capacity ids (SL_EINVAL when the corpus has more
+ * tokens); *num_tokens = total. Pinned host buffers give full PCIe bandwidth. */
+int32_t sl_tokenize_stream(sl_vocab* vocab, const sl_tokenizer_config* config, int32_t build, const char* text,
+                           const uint64_t* doc_offsets, uint32_t num_docs, uint64_t chunk_bytes,
+                           uint64_t* out_offsets, uint32_t* out_ids, uint64_t ids_capacity, uint64_t* num_tokens);
+
 /* stem_english for n words (host buffers): out has the input's byte size, word i's stem is
  * out[offsets[i] .. offsets[i] + out_len[i]) */
 int32_t sl_stem_batch(const char* words, const uint64_t* offsets, uint32_t n, int32_t device, char* out,

@@ -102,6 +102,8 @@ SIGNATURES = {
     "sl_vocab_export": (_i32, [_vp, _vp, _vp, C.POINTER(_u64)]),
     "sl_vocab_import": (_i32, [_vp, _vp, _vp, _u32]),
     "sl_tokenize": (_i32, [_vp, C.POINTER(TokenizerConfig), _i32, _vp, _vp, _u32, _i32, C.POINTER(C.c_void_p)]),
+    "sl_tokenize_stream": (_i32, [_vp, C.POINTER(TokenizerConfig), _i32, _vp, _vp, _u32, _u64, _vp, _vp, _u64,
+                                  C.POINTER(_u64)]),
     "sl_token_batch_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_vp), C.POINTER(_vp)]),
     "sl_token_batch_copy": (_i32, [_vp, _vp, _vp]),
     "sl_token_batch_destroy": (_i32, [_vp]),

@@ -1284,6 +1284,11 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* _
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
 }
 
+__global__ void k_add_u64(const uint64_t* __restrict__ in, uint64_t n, uint64_t add, uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] + add;
+}
+
 // ------------------------------------------------------------------ host side
 inline unsigned grid_for(uint64_t n, int per = 256) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, 148ull * 64));
@@ -1861,6 +1866,126 @@ int32_t sl_vocab_import(sl_vocab* v, const uint64_t* offsets, const char* bytes,
 int32_t sl_tokenize(sl_vocab* vocab, const sl_tokenizer_config* cfg, int32_t build, const char* text,
                     const uint64_t* doc_offsets, uint32_t num_docs, int32_t mem, sl_token_batch** out) {
   return tokenize_impl(vocab, cfg, build, text, doc_offsets, num_docs, mem, out);
+}
+
+int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build, const char* text,
+                           const uint64_t* off, uint32_t N, uint64_t chunk_bytes, uint64_t* out_off,
+                           uint32_t* out_ids, uint64_t cap, uint64_t* num_tokens) {
+  if (!v || !cfg || !num_tokens || !out_off || (N && !off)) SL_FAIL(SL_EINVAL, "tokenize_stream: null argument");
+  *num_tokens = 0;
+  out_off[0] = 0;
+  if (N == 0) return SL_OK;
+  if (off[0] != 0) SL_FAIL(SL_EINVAL, "tokenize: doc_offsets[0] must be 0");
+  for (uint32_t d = 0; d < N; ++d)
+    if (off[d + 1] < off[d]) SL_FAIL(SL_EINVAL, "tokenize: document offsets must be non-decreasing");
+  if (off[N] && !text) SL_FAIL(SL_EINVAL, "tokenize: null text");
+  if (!chunk_bytes) chunk_bytes = 64ull << 20;
+  // document-aligned chunks [d_a, d_b) of about chunk_bytes
+  std::vector<uint32_t> cut{0};
+  while (cut.back() < N) {
+    const uint32_t a = cut.back();
+    const uint64_t target = off[a] + chunk_bytes;
+    uint32_t b = (uint32_t)(std::upper_bound(off + a + 1, off + N + 1, target) - off) - 1;
+    if (b <= a) b = a + 1;  // a document longer than a chunk travels alone
+    cut.push_back(b);
+  }
+  const size_t K = cut.size() - 1;
+  uint64_t max_bytes = 0, max_docs = 0;
+  for (size_t i = 0; i < K; ++i) {
+    max_bytes = std::max<uint64_t>(max_bytes, off[cut[i + 1]] - off[cut[i]]);
+    max_docs = std::max<uint64_t>(max_docs, cut[i + 1] - cut[i]);
+  }
+  cudaStream_t st;
+  SL_TRY(text_stream(v->device, &st));
+  cudaStream_t h2d, d2h;
+  SL_CUDA_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  SL_CUDA_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  cudaEvent_t in_ready[2], out_done[2];
+  for (int i = 0; i < 2; ++i) {
+    SL_CUDA_TRY(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
+    SL_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+  }
+  uint8_t* dtext[2] = {nullptr, nullptr};
+  uint64_t *draw[2] = {nullptr, nullptr}, *doff[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
+  sl_token_batch* pending[2] = {nullptr, nullptr};
+  int32_t rc = SL_OK;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(h2d);
+    cudaStreamSynchronize(d2h);
+    for (int i = 0; i < 2; ++i) {
+      if (pending[i]) sl_token_batch_destroy(pending[i]);
+      cudaFree(dtext[i]);
+      cudaFree(draw[i]);
+      cudaFree(doff[i]);
+      cudaFree(dout[i]);
+      cudaEventDestroy(in_ready[i]);
+      cudaEventDestroy(out_done[i]);
+    }
+    cudaStreamDestroy(h2d);
+    cudaStreamDestroy(d2h);
+  };
+  auto cuda_ok = [&](cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return true;
+    set_error(std::string("tokenize_stream: ") + what + ": " + cudaGetErrorString(e));
+    rc = e == cudaErrorMemoryAllocation ? SL_ENOMEM : SL_ECUDA;
+    return false;
+  };
+  for (int i = 0; i < 2 && rc == SL_OK; ++i) {
+    if (!cuda_ok(cudaMalloc(&dtext[i], std::max<uint64_t>(max_bytes, 1)), "allocation") ||
+        !cuda_ok(cudaMalloc(&draw[i], (max_docs + 1) * 8), "allocation") ||
+        !cuda_ok(cudaMalloc(&doff[i], (max_docs + 1) * 8), "allocation") ||
+        !cuda_ok(cudaMalloc(&dout[i], (max_docs + 1) * 8), "allocation"))
+      break;
+  }
+  // chunk i -> buffer i % 2: text bytes and the chunk's offsets rebased to its first byte
+  auto issue_h2d = [&](size_t i) {
+    const int bsel = (int)(i & 1);
+    const uint32_t a = cut[i], b = cut[i + 1];
+    const uint64_t bytes = off[b] - off[a];
+    if (bytes && !cuda_ok(cudaMemcpyAsync(dtext[bsel], text + off[a], bytes, cudaMemcpyHostToDevice, h2d), "copy"))
+      return;
+    if (!cuda_ok(cudaMemcpyAsync(draw[bsel], off + a, (b - a + 1ull) * 8, cudaMemcpyHostToDevice, h2d), "copy"))
+      return;
+    k_add_u64<<<grid_for(b - a + 1ull), 256, 0, h2d>>>(draw[bsel], b - a + 1ull, 0ull - off[a], doff[bsel]);
+    ++t_launches;
+    cuda_ok(cudaEventRecord(in_ready[bsel], h2d), "event");
+  };
+  uint64_t tok_base = 0;
+  if (rc == SL_OK) issue_h2d(0);
+  for (size_t i = 0; i < K && rc == SL_OK; ++i) {
+    const int bsel = (int)(i & 1);
+    const uint32_t a = cut[i], b = cut[i + 1];
+    // buffer (i+1)%2 was last read by chunk i-1's tokenize (finished: the call is synchronous)
+    if (i + 1 < K) issue_h2d(i + 1);
+    if (rc != SL_OK || !cuda_ok(cudaEventSynchronize(in_ready[bsel]), "event")) break;
+    sl_token_batch* tb = nullptr;
+    rc = tokenize_impl(v, cfg, build, reinterpret_cast<const char*>(dtext[bsel]), doff[bsel], b - a, SL_MEM_DEVICE,
+                       &tb);
+    if (rc != SL_OK) break;
+    // the batch that used this output slot two chunks ago must have been copied out
+    if (pending[bsel]) {
+      if (!cuda_ok(cudaEventSynchronize(out_done[bsel]), "event")) break;
+      sl_token_batch_destroy(pending[bsel]);
+    }
+    pending[bsel] = tb;
+    if (tok_base + tb->T > cap) {
+      set_error("tokenize_stream: ids_capacity too small for the corpus's tokens");
+      rc = SL_EINVAL;
+      break;
+    }
+    k_add_u64<<<grid_for(b - a + 1ull), 256, 0, d2h>>>(tb->offs, b - a + 1ull, tok_base, dout[bsel]);
+    ++t_launches;
+    if (tb->T && !cuda_ok(cudaMemcpyAsync(out_ids + tok_base, tb->ids, tb->T * 4, cudaMemcpyDeviceToHost, d2h), "copy"))
+      break;
+    if (!cuda_ok(cudaMemcpyAsync(out_off + a, dout[bsel], (b - a + 1ull) * 8, cudaMemcpyDeviceToHost, d2h), "copy"))
+      break;
+    if (!cuda_ok(cudaEventRecord(out_done[bsel], d2h), "event")) break;
+    tok_base += tb->T;
+  }
+  if (rc == SL_OK) cuda_ok(cudaStreamSynchronize(d2h), "sync");
+  cleanup();
+  if (rc == SL_OK) *num_tokens = tok_base;
+  return rc;
 }
 
 int32_t sl_token_batch_info(const sl_token_batch* b, uint32_t* num_docs, uint64_t* num_tokens,

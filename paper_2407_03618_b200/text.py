@@ -247,6 +247,48 @@ def tokenize_query(texts, config: TokenizerConfig, vocab: Vocabulary, mem=None) 
     return _tokenize(texts, config, vocab, False, mem)
 
 
+def _tokenize_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, build: bool, chunk_bytes: int,
+                     out_ids=None, out_offsets=None):
+    """sl_tokenize_stream: host corpus in, host (offsets, ids) out, chunked with the copies in
+    both directions overlapping the device work. text: bytes / uint8 array / pinned uint8
+    torch tensor; out_* (optional, e.g. pinned): preallocated output arrays."""
+    if hasattr(text, "data_ptr"):  # torch tensor in host memory
+        tp, nb = text.data_ptr(), text.numel()
+    else:
+        tb = np.frombuffer(text, np.uint8) if not isinstance(text, np.ndarray) else text
+        tp, nb = (tb.ctypes.data if tb.size else 0), tb.size
+    if hasattr(offsets, "data_ptr"):  # 64-bit torch tensor in host memory (e.g. pinned)
+        off_ptr, n = offsets.data_ptr(), offsets.numel() - 1
+    else:
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        off_ptr, n = off.ctypes.data, len(off) - 1
+    if out_offsets is None:
+        out_offsets = np.empty(n + 1, np.uint64)
+    if out_ids is None:
+        out_ids = np.empty(max(1, nb // 2 + 1), np.uint32)  # >= 2 bytes per token
+    op = out_offsets.data_ptr() if hasattr(out_offsets, "data_ptr") else out_offsets.ctypes.data
+    ip = out_ids.data_ptr() if hasattr(out_ids, "data_ptr") else out_ids.ctypes.data
+    cap = out_ids.numel() if hasattr(out_ids, "numel") else out_ids.size
+    cfg, blob = config.to_c()
+    nt = C.c_uint64()
+    check(lib().sl_tokenize_stream(vocab.handle, C.byref(cfg), int(build), tp, off_ptr, n, int(chunk_bytes), op, ip,
+                                   cap, C.byref(nt)))
+    return out_offsets, out_ids[:nt.value]
+
+
+def tokenize_build_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 64 << 20,
+                          out_ids=None, out_offsets=None):
+    """tokenize_build over a host corpus (text bytes + u64 doc offsets), pipelined in
+    document-aligned chunks; returns host (token offsets u64[N+1], ids u32[T])."""
+    return _tokenize_stream(text, offsets, config, vocab, True, chunk_bytes, out_ids, out_offsets)
+
+
+def tokenize_query_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 64 << 20,
+                          out_ids=None, out_offsets=None):
+    """tokenize_query counterpart of tokenize_build_stream (frozen vocabulary)."""
+    return _tokenize_stream(text, offsets, config, vocab, False, chunk_bytes, out_ids, out_offsets)
+
+
 def split_text(text: str | bytes, lowercase: bool = True) -> list:
     """split_text (tokenizer.hpp:31-34): maximal runs of >= 2 word codepoints, in order."""
     v = Vocabulary()

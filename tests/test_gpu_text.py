@@ -273,3 +273,28 @@ def test_all_ascii_bytes_classifier(cuda_ok, port):
         b = T._tokenize_raw(buf.data_ptr(), doff.data_ptr(), len(off) - 1, cfg_of(*cfg), v, True, SL_MEM_DEVICE)
         got_off, got_ids = b.to_numpy()
         assert np.array_equal(got_off, want[0]) and np.array_equal(got_ids, want[1]) and v.tokens() == want[2], cfg
+
+
+@pytest.mark.parametrize("chunk", [1 << 10, 1 << 14, 64 << 20])
+def test_stream_tokenize_matches_single_call(cuda_ok, port, chunk):
+    """sl_tokenize_stream (document-aligned chunks, overlapped copies) gives exactly the
+    single-call result: ids, token offsets and vocabulary order, build and query; chunks smaller
+    than some documents, empty documents, a document longer than a chunk."""
+    words = make_words(3000, seed=71, unicode_frac=0.05)
+    text, off = make_corpus(1500, words, seed=9, malformed_frac=0.01, case_frac=0.2)
+    # an empty document and one long document
+    text = text + " ".join(words[:900]).encode("utf-8")
+    off = np.concatenate([off, [off[-1], len(text)]]).astype(np.uint64)
+    cfg = cfg_of(1, 1, 1)
+    want = port.tokenize_corpus(text, off, 1, 1, 1)
+    v = T.Vocabulary()
+    got_off, got_ids = T.tokenize_build_stream(text, off, cfg, v, chunk_bytes=chunk)
+    assert np.array_equal(got_off, want[0]) and np.array_equal(got_ids, want[1]) and v.tokens() == want[2]
+    # query mode against the single call on the frozen vocabulary
+    b = T.tokenize_query((text, off), cfg, v)
+    qo, qi = b.to_numpy()
+    so, si = T.tokenize_query_stream(text, off, cfg, v, chunk_bytes=chunk)
+    assert np.array_equal(so, qo) and np.array_equal(si, qi)
+    # capacity too small fails loudly
+    with pytest.raises(ValueError, match="ids_capacity"):
+        T.tokenize_query_stream(text, off, cfg, v, chunk_bytes=chunk, out_ids=np.empty(3, np.uint32))
