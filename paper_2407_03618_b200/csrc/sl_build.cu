@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kSortThreads, SL_SORT_MINB) k_radix_scatter(
   static_assert(NPAD >= 2 * kSortTile, "staging aliases the counters");
   extern __shared__ uint32_t smem[];
   uint32_t* cw = smem;                            // packed counters, then the staged tile
-  __shared__ uint32_t dstart[ND], gstart[ND], sw[33];
+  __shared__ uint32_t delta[ND], sw[33];  // per digit: global start - tile-local start
   const int tid = threadIdx.x;
   for (int i = tid; i < NPAD; i += kSortThreads) cw[i] = 0;
   const uint64_t tile0 = (uint64_t)blockIdx.x * kSortTile;
@@ -325,28 +325,25 @@ __global__ void __launch_bounds__(kSortThreads, SL_SORT_MINB) k_radix_scatter(
   __syncthreads();
   for (uint32_t dg = tid; dg < ND; dg += kSortThreads) {
     const uint32_t w = (dg & (LANES - 1)) * kSortThreads;  // thread 0's counter
-    dstart[dg] = reinterpret_cast<const uint16_t*>(cw + w + (w >> 5))[dg >> (LOGD - 1)];
-    gstart[dg] = dg <= mask ? offs[(uint64_t)dg * n_tiles + blockIdx.x] : 0u;
+    const uint32_t ds = reinterpret_cast<const uint16_t*>(cw + w + (w >> 5))[dg >> (LOGD - 1)];
+    delta[dg] = (dg <= mask ? offs[(uint64_t)dg * n_tiles + blockIdx.x] : 0u) - ds;
   }
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j)
     if (b + j < n) pre[j] += *cptr((kk[j] >> shift) & mask);
   __syncthreads();
-  uint32_t* skey = cw;
-  uint32_t* sval = cw + kSortTile;
+  // (key, value) staged as one 8-byte word in rank order
+  uint64_t* stage = reinterpret_cast<uint64_t*>(cw);
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j)
-    if (b + j < n) {
-      skey[pre[j]] = kk[j];
-      sval[pre[j]] = vv[j];
-    }
+    if (b + j < n) stage[pre[j]] = ((uint64_t)vv[j] << 32) | kk[j];
   __syncthreads();
   for (uint32_t i = tid; i < cnt; i += kSortThreads) {
-    const uint32_t k = skey[i];
-    const uint32_t dg = (k >> shift) & mask;
-    const uint32_t pos = gstart[dg] + (i - dstart[dg]);
+    const uint64_t e = stage[i];
+    const uint32_t k = (uint32_t)e;
+    const uint32_t pos = delta[(k >> shift) & mask] + i;
     kout[pos] = k;
-    vout[pos] = sval[i];
+    vout[pos] = (uint32_t)(e >> 32);
   }
 }
 
