@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         ++nd;
       } else if (e < 32) {
 #ifdef SL_DEBUG_CHECKS
-        if (e >= ra.R * ra.qmax) {
+        if (e >= 32u) {
           printf("entry overflow: run %u lane %d nr %u R %u qmax %u e %u incl %u ns %u q %u qlen %llu\n", run, lane, nr,
                  ra.R, ra.qmax, e, incl, ns, q, (unsigned long long)(qe - qb));
           __trap();
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   const int E = s.ebeg[nr];
   const int nd = s.nd[0];
 #ifdef SL_DEBUG_CHECKS
-  if (lane == 0 && (nr > ra.R || nr == 0 || (uint32_t)E > ra.R * ra.qmax || (uint32_t)nd > ra.qmax)) {
+  if (lane == 0 && (nr > ra.R || nr == 0 || (uint32_t)E > 32u || (uint32_t)nd > ra.qmax)) {
     printf("k_score_runs invariant: run %u nr %u R %u E %d qmax %u nd %d\n", run, nr, ra.R, E, ra.qmax, nd);
     __trap();
   }
@@ -934,7 +934,7 @@ __global__ void k_rank_emit(const uint32_t* __restrict__ key, const uint32_t* __
 // Per query: sorted dense signature (slots of rows with a dense copy) and its hash.
 __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
                             IndexView ix, uint32_t qmax, int32_t* __restrict__ qdense, uint32_t* __restrict__ nden,
-                            uint32_t* __restrict__ hkey, uint32_t* __restrict__ hval) {
+                            uint32_t* __restrict__ ngath, uint32_t* __restrict__ hkey, uint32_t* __restrict__ hval) {
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
     int32_t* d = qdense + (uint64_t)q * qmax;
     uint32_t n = 0, ng = 0;
@@ -957,6 +957,7 @@ __global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* 
     uint32_t h = 2166136261u ^ n;  // FNV-1a over the sorted slots
     for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
     nden[q] = n;
+    ngath[q] = ng;
     // > 32 gathered rows: sorts after every short query (key 0xFFFFFFFF) -> k_score_long
     hkey[q] = (ng > 32 || n > (uint32_t)NDMAX) ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
     hval[q] = q;
@@ -977,7 +978,8 @@ __device__ __forceinline__ bool same_signature(const int32_t* qdense, const uint
 // every R queries. One block of 1024 threads walks the batch in chunks.
 __global__ void __launch_bounds__(1024) k_build_runs(const uint32_t* __restrict__ perm, uint32_t B,
                                                      const int32_t* __restrict__ qdense,
-                                                     const uint32_t* __restrict__ nden, uint32_t qmax, uint32_t R,
+                                                     const uint32_t* __restrict__ nden,
+                                                     const uint32_t* __restrict__ ngath, uint32_t qmax, uint32_t R,
                                                      uint32_t* __restrict__ run_begin, uint32_t* __restrict__ n_runs) {
   __shared__ uint32_t sw[40];
   __shared__ uint32_t wmax[32];
@@ -1013,7 +1015,10 @@ __global__ void __launch_bounds__(1024) k_build_runs(const uint32_t* __restrict_
     __syncthreads();
     const uint32_t prev = w > 0 ? wmax[w - 1] : 0u;
     const uint32_t start = max(max(m, prev), carry_start);
-    const bool head = valid && ((i - start) % R == 0);
+    // chunks of R queries from the signature run's start; a member whose gathered rows would
+    // push the run past 32 entries (one lane each) starts its own run (pairwise rule: RMAX <= 2)
+    static_assert(RMAX <= 2, "k_build_runs' entry budget checks pairs only");
+    const bool head = valid && ((i - start) % R == 0 || ngath[perm[i - 1]] + ngath[perm[i]] > 32u);
     uint32_t tot;
     const uint32_t off = block_excl_scan(head ? 1u : 0u, sw, &tot) + carry_count;
     if (head) run_begin[off] = i;
@@ -1259,7 +1264,7 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   p->C = kept_capacity(k);
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
   if (R == 0) R = RMAX;
-  R = std::min(R, std::max(1u, (uint32_t)kQMax / std::max(1u, qmax)));  // <= 32 gathered entries per warp
+  // the run builder keeps every run within 32 gathered entries (one lane each)
   p->R = std::max(1u, std::min<uint32_t>(R, RMAX));
   p->wpc = WPC;
   p->smem = SL_DYN_WSMEM ? sizeof(WarpSmem) * WPC : 0;  // static layout unless it exceeds 48 KB
@@ -1442,6 +1447,8 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   uint32_t *nden, *hk, *hv, *k0, *k1, *v0, *v1, *run_begin, *n_runs;
   SL_TRY(scr.alloc(&qdense, (uint64_t)B * qmax));
   SL_TRY(scr.alloc(&nden, B));
+  uint32_t* ngath;
+  SL_TRY(scr.alloc(&ngath, B));
   SL_TRY(scr.alloc(&hk, B));
   SL_TRY(scr.alloc(&hv, B));
   SL_TRY(scr.alloc(&k0, B));
@@ -1450,10 +1457,11 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   SL_TRY(scr.alloc(&v1, B));
   SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
   SL_TRY(scr.alloc(&n_runs, 2));
-  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, hk, hv); ++t_launches;
+  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, ngath, hk, hv); ++t_launches;
   const uint32_t *sk, *perm;
   SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
-  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, qmax, plan.R, run_begin, n_runs); ++t_launches;
+  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, ngath, qmax, plan.R, run_begin, n_runs);
+  ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;
