@@ -242,7 +242,7 @@ int32_t sl_token_batch_copy(const sl_token_batch* batch, uint64_t* host_offsets,
 int32_t sl_token_batch_destroy(sl_token_batch* batch);
 
 /* Streaming tokenize of a HOST corpus (same output as sl_tokenize + sl_token_batch_copy): the
- * corpus is cut into document-aligned chunks of about chunk_bytes (0: 64 MiB); chunk i+1 is
+ * corpus is cut into document-aligned chunks of about chunk_bytes (0: 256 MiB); chunk i+1 is
  * copied to the device while chunk i is tokenized, and each chunk's ids / token offsets are
  * copied back while the next chunk runs (separate H2D and D2H streams). out_offsets:
  * u64[num_docs+1]; out_ids: room for ids_capacity ids (SL_EINVAL when the corpus has more

@@ -29,6 +29,9 @@
 //                   reference's first-encounter order; open-addressing device hash table
 //   query mode      tokens absent from the frozen vocabulary are dropped (SPEC OOV rule)
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <string>
@@ -1879,7 +1882,7 @@ int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t 
   for (uint32_t d = 0; d < N; ++d)
     if (off[d + 1] < off[d]) SL_FAIL(SL_EINVAL, "tokenize: document offsets must be non-decreasing");
   if (off[N] && !text) SL_FAIL(SL_EINVAL, "tokenize: null text");
-  if (!chunk_bytes) chunk_bytes = 64ull << 20;
+  if (!chunk_bytes) chunk_bytes = 256ull << 20;  // 16-64 MiB chunks: per-call overhead (~1.7 ms) dominates
   // document-aligned chunks [d_a, d_b) of about chunk_bytes
   std::vector<uint32_t> cut{0};
   while (cut.back() < N) {
@@ -1951,17 +1954,27 @@ int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t 
     cuda_ok(cudaEventRecord(in_ready[bsel], h2d), "event");
   };
   uint64_t tok_base = 0;
+  const char* tenv = std::getenv("SL_STREAM_TRACE");
+  const bool trace = tenv && std::atoi(tenv);
   if (rc == SL_OK) issue_h2d(0);
   for (size_t i = 0; i < K && rc == SL_OK; ++i) {
     const int bsel = (int)(i & 1);
     const uint32_t a = cut[i], b = cut[i + 1];
     // buffer (i+1)%2 was last read by chunk i-1's tokenize (finished: the call is synchronous)
     if (i + 1 < K) issue_h2d(i + 1);
+    const auto tw0 = std::chrono::steady_clock::now();
     if (rc != SL_OK || !cuda_ok(cudaEventSynchronize(in_ready[bsel]), "event")) break;
+    const auto tw1 = std::chrono::steady_clock::now();
     sl_token_batch* tb = nullptr;
     rc = tokenize_impl(v, cfg, build, reinterpret_cast<const char*>(dtext[bsel]), doff[bsel], b - a, SL_MEM_DEVICE,
                        &tb);
     if (rc != SL_OK) break;
+    if (trace) {
+      const auto tw2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[stream] chunk %zu: %llu bytes, wait %.3f ms, tokenize %.3f ms\n", i,
+              (unsigned long long)(off[b] - off[a]), std::chrono::duration<double, std::milli>(tw1 - tw0).count(),
+              std::chrono::duration<double, std::milli>(tw2 - tw1).count());
+    }
     // the batch that used this output slot two chunks ago must have been copied out
     if (pending[bsel]) {
       if (!cuda_ok(cudaEventSynchronize(out_done[bsel]), "event")) break;

@@ -276,14 +276,14 @@ def _tokenize_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, 
     return out_offsets, out_ids[:nt.value]
 
 
-def tokenize_build_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 64 << 20,
+def tokenize_build_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 256 << 20,
                           out_ids=None, out_offsets=None):
     """tokenize_build over a host corpus (text bytes + u64 doc offsets), pipelined in
     document-aligned chunks; returns host (token offsets u64[N+1], ids u32[T])."""
     return _tokenize_stream(text, offsets, config, vocab, True, chunk_bytes, out_ids, out_offsets)
 
 
-def tokenize_query_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 64 << 20,
+def tokenize_query_stream(text, offsets, config: TokenizerConfig, vocab: Vocabulary, chunk_bytes: int = 256 << 20,
                           out_ids=None, out_offsets=None):
     """tokenize_query counterpart of tokenize_build_stream (frozen vocabulary)."""
     return _tokenize_stream(text, offsets, config, vocab, False, chunk_bytes, out_ids, out_offsets)
