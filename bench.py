@@ -219,7 +219,8 @@ def text_pipeline_block(cfg_i, hbm, reps=3, cpu_docs=20000):
            "tokens": T_out, "vocab": V, "ms": ms, "bytes_per_s": nb / (ms / 1e3), "tokens_per_s": T_out / (ms / 1e3),
            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                         "algorithmic_bytes": alg,
-                        "note": "per-token string work (raw-string hashing + table probe ~30%, token extraction ~23%, byte classification ~9%), well below the HBM roofline"},
+                        "note": "per-token string work (raw-string hashing + table probe ~30%, token extraction "
+                                "~23%, byte classification ~9%), well below the HBM roofline"},
            "e2e": {"ms": min(e2e_ms), "bytes_per_s": nb / (min(e2e_ms) / 1e3), "h2d_bytes": nb + 8 * (N + 1),
                    "d2h_bytes": 4 * T_out + 8 * (N + 1)}}
     try:
@@ -375,7 +376,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 accumulate (f64 build math)",
             "data": "synthetic (seeded Zipf corpus/queries, BASELINE.md §5; BEIR absent)",
-            "config": {"workload": workload_name(args.config, k, args.variant), "docs": cfg.num_docs, "vocab": cfg.vocab,
+            "config": {"workload": workload_name(args.config, k, args.variant), "docs": cfg.num_docs,
+                       "vocab": cfg.vocab,
                        "tokens": T_total, "nnz_local": int(info.nnz_local), "queries_per_step": B, "k": k,
                        "parallelism": f"doc-shard x{world}", "l2": "flushed between steps (256 MiB memset)",
                        "dense_rows": int(info.dense_rows), "skip_rows": int(info.skip_rows),
