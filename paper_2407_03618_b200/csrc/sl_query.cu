@@ -403,9 +403,10 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const float x = f4c(v, c);
-      if ((x > tf || tau == 0) && (FULL || dl + c < nvalid)) {
-        if (make_key(x, gdoc0 + dl + c) >= tau) pm |= 1u << (4 * rr + c);
-      }
+      // x > tf already implies key(x) > tau: tf is tau's own score (or one ordinal below a
+      // published split threshold, or -inf below every finite score, also for tau == 0), so
+      // no 64-bit key here
+      if (x > tf && (FULL || dl + c < nvalid)) pm |= 1u << (4 * rr + c);
     }
   }
   const float* bf = buf;
