@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
                                                uint32_t per_split, uint64_t split_stride, uint64_t query_stride,
                                                uint32_t k, const double* __restrict__ qconst, uint32_t* out_ids,
                                                float* out_scores, uint64_t* out_keys,
-                                               const uint64_t* __restrict__ gtau) {
+                                               const uint64_t* __restrict__ gtau, uint32_t cap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* buf = (uint64_t*)smem_raw;  // [p2]
   const uint32_t p2 = next_pow2(max(k, 2u));
@@ -1135,18 +1135,40 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
       }
     }
   };
-  uint32_t mine = 0;
-  visit([&](uint64_t) { ++mine; });
-  uint32_t nvalid;
-  block_excl_scan(mine, sw, &nvalid);
+  // when every candidate slot fits shared memory, one pass stages the valid candidates (>= g;
+  // order is irrelevant: keys are unique and the winners are sorted) and the select and the
+  // copy run on them; otherwise every pass reads the candidate buffers.
+  uint64_t* cbuf = reinterpret_cast<uint64_t*>(sw + 40);
+  uint32_t* s_n = sw + 39;
+  uint32_t nvalid = 0;
+  const bool staged = total <= cap;  // every slot fits: stage (cap = 0: candidate sets too large)
+  if (staged) {
+    if (threadIdx.x == 0) *s_n = 0;
+    __syncthreads();
+    visit([&](uint64_t x) { cbuf[atomicAdd(s_n, 1u)] = x; });
+    __syncthreads();
+    nvalid = *s_n;
+    __syncthreads();
+  } else {
+    uint32_t mine = 0;
+    visit([&](uint64_t) { ++mine; });
+    block_excl_scan(mine, sw, &nvalid);
+  }
+  auto visit_s = [&](auto&& f) {
+    if (staged) {
+      for (uint32_t i = threadIdx.x; i < nvalid; i += blockDim.x) f(cbuf[i]);
+    } else {
+      visit(f);
+    }
+  };
   uint64_t tau = 1;
-  if (nvalid > k) tau = block_select_kth(visit, k, hist, sw + 36);
+  if (nvalid > k) tau = block_select_kth(visit_s, k, hist, sw + 36);
   uint32_t m2 = 0;
-  visit([&](uint64_t x) { m2 += x >= tau; });
+  visit_s([&](uint64_t x) { m2 += x >= tau; });
   uint32_t m;
   const uint32_t o = block_excl_scan(m2, sw, &m);
   uint64_t* dst = buf + o;
-  visit([&](uint64_t x) {
+  visit_s([&](uint64_t x) {
     if (x >= tau) *dst++ = x;
   });
   for (uint32_t i = m + threadIdx.x; i < p2; i += blockDim.x) buf[i] = kInvalidKey;
@@ -1302,10 +1324,14 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
 int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32_t per_split, uint64_t split_stride,
                      uint64_t query_stride, uint32_t k, const double* qconst, uint32_t* ids, float* scores,
                      uint64_t* keys, cudaStream_t st, const uint64_t* gtau = nullptr) {
-  const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4;
+  // staging room for the candidates when all slots fit 8192 keys (64 KB); larger candidate
+  // sets (top-1000: 37 splits x 2048) are visited in the buffers
+  const uint64_t slots = (uint64_t)n_splits * per_split;
+  const uint32_t cap = slots <= 8192 ? (uint32_t)slots : 0u;
+  const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4 + (size_t)cap * 8;
   SL_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_merge<<<B, 256, smem, st>>>(cand, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores, keys,
-                                gtau); ++t_launches;
+                                gtau, cap); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
