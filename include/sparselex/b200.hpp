@@ -325,6 +325,25 @@ inline TokenizedCorpus tokenize_query(const std::vector<std::string>& texts, con
   return detail::tokenize(texts, cfg, vocab, false);
 }
 
+// tokenize_build / tokenize_query over a corpus already concatenated in host memory (text bytes
+// + u64 doc offsets[N+1]): sl_tokenize_stream, document-aligned chunks with the copies to and
+// from the device overlapping the device work (chunk_bytes 0: the library default)
+inline TokenizedCorpus tokenize_stream(const std::string& text, const std::vector<uint64_t>& doc_offsets,
+                                       const TokenizerConfig& cfg, Vocabulary& vocab, bool build,
+                                       uint64_t chunk_bytes = 0) {
+  if (doc_offsets.empty()) throw std::invalid_argument("tokenize_stream: doc_offsets needs N+1 entries");
+  detail::CfgC c(cfg);
+  const uint32_t n = static_cast<uint32_t>(doc_offsets.size() - 1);
+  TokenizedCorpus out;
+  out.doc_offsets.resize(doc_offsets.size());
+  out.token_ids.resize(text.size() / 2 + 1);  // a token takes >= 2 bytes
+  uint64_t T = 0;
+  check(sl_tokenize_stream(vocab.handle(), &c.c, build ? 1 : 0, text.data(), doc_offsets.data(), n, chunk_bytes,
+                           out.doc_offsets.data(), out.token_ids.data(), out.token_ids.size(), &T));
+  out.token_ids.resize(T);
+  return out;
+}
+
 // stem_english (stemmer.hpp:16-18), on the device
 inline std::vector<std::string> stem_english(const std::vector<std::string>& words, int device = 0) {
   std::string all;

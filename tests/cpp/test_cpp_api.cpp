@@ -69,6 +69,12 @@ int main() {
     EXPECT(toks == (std::vector<std::string>{"cat", "run"}));
     EXPECT(tk.doc(0) == (std::vector<uint32_t>{0, 1}) && tk.doc(1) == (std::vector<uint32_t>{0, 0}));
     EXPECT(tokenize_query({"zebra running"}, tc, v).doc(0) == (std::vector<uint32_t>{1}));
+    {  // the streaming entry point on a pre-concatenated corpus gives the per-call result
+      Vocabulary v2;
+      const std::string all = "the cat is runningcat cat";
+      auto ts = tokenize_stream(all, {0, 18, 25}, tc, v2, true, 8);
+      EXPECT(v2.tokens() == toks && ts.doc(0) == tk.doc(0) && ts.doc(1) == tk.doc(1));
+    }
     EXPECT(stem_english({"running", "skies", "generously"}) ==
            (std::vector<std::string>{"run", "sky", "generous"}));
     TextIndex ti = build_text_index({"cat sat", "dog ran", "cat cat cat"}, BM25Params{}, TokenizerConfig{});
