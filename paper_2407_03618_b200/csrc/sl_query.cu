@@ -24,6 +24,7 @@
 // GPU count. k_merge selects the final top-k per query from the per-split candidates (and
 // is the rank-0 merge of the G x k candidates gathered over NCCL).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1310,10 +1311,16 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   // must stay small enough for its dense-row chunks and posting slices to be served from L2 —
   // at most 128k docs per split (k <= 256; larger candidate sets trade region size for merge
   // cost: 128k x C/512). c5 shard (6.25M docs): 2 -> 48 splits, 38.8k -> 71k QPS.
+  // The region's L2 footprint grows with the bytes per document the sweep touches (dense copies
+  // + postings): the 128k-doc region is tuned at c2 (50 dense rows, 60 nonzeros per document,
+  // ~680 B/doc); denser corpora shrink it by sqrt of the ratio (c5 shard, ~2.3 KB/doc: 72k docs,
+  // 87 splits; 48 -> 96 splits measured 82.0k -> 87.0k QPS, 192 splits 83.0k: merge cost grows).
   const uint64_t f = k <= 16 ? 12 : 8;
   if (ns == 0) {
     const uint64_t by_work = (f * warps + items - 1) / items;
-    const uint64_t region = 131072ull * std::max(1u, p->C / 512);
+    const double bpd = 4.0 * ix->dense_rows + 8.0 * (double)ix->nnz / (double)std::max(1u, ix->N);
+    const double shrink = bpd > 680.0 ? std::sqrt(680.0 / bpd) : 1.0;
+    const uint64_t region = (uint64_t)(131072.0 * shrink) * std::max(1u, p->C / 512);
     const uint64_t by_l2 = ((uint64_t)ix->N + region - 1) / region;
     ns = (uint32_t)std::max<uint64_t>(1, std::max(by_work, by_l2));
   }
