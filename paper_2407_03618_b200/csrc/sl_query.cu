@@ -30,6 +30,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_pipeline.h>
+
 #include "sl_index.cuh"
 
 namespace sl {
@@ -146,6 +148,10 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
   }
   return prefix;
 }
+
+#ifndef SL_DENSE_ASYNC
+#define SL_DENSE_ASYNC 1
+#endif
 
 // warp-level variant with 4-bit digits (16-bin warp-private histogram, 64 bytes)
 template <class Visit>
@@ -662,6 +668,56 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // (2) dense signature of the run, ascending slot order, all loads in flight
     // register passes of DCH float4 per lane, so the tile size does not set the register
     // footprint; returns the lane max of its sums (padding docs included: an upper bound)
+#if SL_DENSE_ASYNC
+    // The first dense row is copied global -> shared with cp.async (no registers: the whole row
+    // in flight at once, one L2 round trip); later rows are added chunk by chunk in registers,
+    // in ascending slot order as before (((r0 + r1) + r2) ...). Preloading the second row's
+    // chunk during the copy spilled 648 B at the 64-register cap.
+    auto dense_pass = [&]() -> float {
+      float m = -INFINITY;
+      constexpr int DCH = F4L < 4 ? F4L : 4;
+      const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane;
+      if (nd == 0) {
+#pragma unroll
+        for (int rr = 0; rr < F4L; ++rr) dsum4[lane + 32 * rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return 0.f;
+      }
+      {
+        const float4* row0 = dbase + (uint64_t)s.dslot[0] * rstride;
+#pragma unroll
+        for (int rr = 0; rr < F4L; ++rr) __pipeline_memcpy_async(dsum4 + lane + 32 * rr, row0 + 32 * rr, 16);
+        __pipeline_commit();
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < F4L; c0 += DCH) {
+        if (c0 == 0) __pipeline_wait_prior(0);
+        float4 a[DCH];
+#pragma unroll
+        for (int rr = 0; rr < DCH; ++rr) a[rr] = dsum4[lane + 32 * (c0 + rr)];
+        for (int i = 1; i < nd; ++i) {
+          float4 v[DCH];
+          {
+            const float4* row = dbase + (uint64_t)s.dslot[i] * rstride + 32 * c0;
+#pragma unroll
+            for (int rr = 0; rr < DCH; ++rr) v[rr] = __ldg(row + 32 * rr);
+          }
+#pragma unroll
+          for (int rr = 0; rr < DCH; ++rr) {
+            a[rr].x += v[rr].x;
+            a[rr].y += v[rr].y;
+            a[rr].z += v[rr].z;
+            a[rr].w += v[rr].w;
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < DCH; ++rr) {
+          if (nd > 1) dsum4[lane + 32 * (c0 + rr)] = a[rr];
+          m = fmaxf(m, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
+        }
+      }
+      return m;
+    };
+#else
     auto dense_pass = [&]() -> float {
       float m = -INFINITY;
       constexpr int DCH = F4L < 4 ? F4L : 4;
@@ -692,6 +748,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       }
       return m;
     };
+#endif
     const float dm = (ra.debug_skip & 4) ? INFINITY : dense_pass();
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
