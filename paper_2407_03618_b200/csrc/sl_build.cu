@@ -525,6 +525,28 @@ __global__ void k_dense_fill(const uint64_t* __restrict__ indptr, const uint32_t
   }
 }
 
+// pair rows P_ab = r_a + r_b (a < b < m) of the leading dense slots: a run whose dense
+// signature starts with a and b starts its dense sum from P_ab — the same f32 addition the
+// scoring kernel would do first, so every sum stays bit-identical
+__global__ void k_dense_pairs(float* __restrict__ dense, uint32_t n_dense, uint32_t m, uint32_t n_pad) {
+  const uint32_t np = m * (m - 1) / 2;
+  for (uint32_t pr = blockIdx.y; pr < np; pr += gridDim.y) {
+    uint32_t a = 0, r = pr;
+    while (r >= m - 1 - a) {
+      r -= m - 1 - a;
+      ++a;
+    }
+    const uint32_t b = a + 1 + r;
+    const float4* ra = reinterpret_cast<const float4*>(dense + (uint64_t)a * n_pad);
+    const float4* rb = reinterpret_cast<const float4*>(dense + (uint64_t)b * n_pad);
+    float4* out = reinterpret_cast<float4*>(dense + (uint64_t)dense_pair_row(n_dense, m, a, b) * n_pad);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad / 4; i += gridDim.x * blockDim.x) {
+      const float4 x = ra[i], y = rb[i];
+      out[i] = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    }
+  }
+}
+
 // skip[s][tile] = first row-relative posting with doc >= tile * kTileDocs; one CTA per row
 // (grid-stride over rows), four postings per thread per step
 __global__ void __launch_bounds__(256) k_skip_fill(const uint64_t* __restrict__ indptr,
@@ -975,11 +997,24 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     }
   }
   if (ix->dense_rows) {
-    SL_TRY(dalloc(ix, &ix->dense, (uint64_t)ix->dense_rows * ix->n_pad));
+    // pair rows for the leading m dense slots, within a 4 GB budget (SL_DENSE_PAIRS=m overrides; 0: none)
+    uint32_t m = std::min<uint32_t>(16, ix->dense_rows);
+    const uint64_t row_bytes = (uint64_t)ix->n_pad * 4;
+    while (m > 1 && (uint64_t)m * (m - 1) / 2 * row_bytes > (4ull << 30)) --m;
+    if (const char* e = std::getenv("SL_DENSE_PAIRS"))
+      if (*e) m = std::min<uint32_t>((uint32_t)std::atoi(e), ix->dense_rows);
+    if (m < 2) m = 0;
+    ix->pair_m = m;
+    const uint64_t rows = (uint64_t)ix->dense_rows + (m ? (uint64_t)m * (m - 1) / 2 : 0);
+    SL_TRY(dalloc(ix, &ix->dense, rows * ix->n_pad));
     SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
     dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
     k_dense_fill<<<g, 256, 0, st>>>(ix->indptr, ix->docids, ix->values, slot_tok, ix->dense_rows, ix->n_pad,
                                     ix->dense); ++t_launches;
+    if (m) {
+      dim3 gp(grid_for(ix->n_pad / 4, 256, 256), std::min<uint32_t>(m * (m - 1) / 2, 65535));
+      k_dense_pairs<<<gp, 256, 0, st>>>(ix->dense, ix->dense_rows, m, ix->n_pad); ++t_launches;
+    }
   }
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));

@@ -38,8 +38,9 @@ struct sl_index {
   uint32_t* tf = nullptr;         // [nnz] (keep_tf only)
 
   int32_t* tokinfo = nullptr;     // [V]
-  float* dense = nullptr;         // [dense_rows * n_pad]
+  float* dense = nullptr;         // [(dense_rows + pair rows) * n_pad]
   uint32_t dense_rows = 0;
+  uint32_t pair_m = 0;            // dense slots [0, pair_m) also have pair rows r_a + r_b (a < b)
   uint32_t* skiptab = nullptr;    // [skip_rows * (num_tiles + 1)]
   // block-max bounds (exact top-k pruning): max(0, S^Δ) over a row / a row's tile slice
   float* rowmax = nullptr;        // [V]
@@ -68,6 +69,8 @@ struct sl_index {
     v.V = V;
     v.N = N;
     v.n_pad = n_pad;
+    v.n_dense = dense_rows;
+    v.pair_m = pair_m;
     v.num_tiles = num_tiles;
     v.doc_base = doc_base;
     return v;

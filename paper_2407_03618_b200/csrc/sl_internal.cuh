@@ -165,7 +165,14 @@ struct IndexView {
   uint32_t n_pad;    // num_tiles * kTileDocs
   uint32_t num_tiles;
   uint32_t doc_base;
+  uint32_t n_dense;  // dense rows (pair rows follow them in `dense`)
+  uint32_t pair_m;   // leading dense slots with pair rows
 };
+
+// row of the pair (a, b), a < b < m, in the dense array: pair rows follow the n_dense single rows
+__host__ __device__ __forceinline__ uint32_t dense_pair_row(uint32_t n_dense, uint32_t m, uint32_t a, uint32_t b) {
+  return n_dense + a * (2 * m - a - 1) / 2 + (b - a - 1);
+}
 
 // host launchers shared between sl_build.cu and sl_query.cu
 int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st,

@@ -341,3 +341,22 @@ def test_dense_cap_planning_path(cuda_ok, c1, monkeypatch, cap):
     q = lambda i: qtok[int(qoff[i]):int(qoff[i + 1])]  # noqa: E731
     assert_topk_match(gid, gsc, rid, rsc, 20, cfg.num_docs, lambda i: ox.score_query(q(i)),
                       lambda i: query_scale(exp, q(i)), f"dense cap {cap}")
+
+
+def test_dense_pair_rows_exact(cuda_ok, c1, monkeypatch):
+    """Pair rows (r_a + r_b for the leading dense slots) are an access path: queries whose dense
+    signature starts with such a pair — including repeated dense tokens, which have none — give
+    bit-identical top-k with pair rows on and off."""
+    cfg, corp, _, _ = c1
+    p = BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)
+    rng = np.random.default_rng(41)
+    queries = [list(rng.integers(0, 12, rng.integers(2, 6))) + list(rng.integers(0, cfg.vocab, 2)) for _ in range(300)]
+    queries += [[0, 0], [1, 0, 1], [0, 1], [2, 2, 2, 3], [0, 1, 2, 3, 4, 5]]
+    qo, qt = csr(queries)
+    out = []
+    for pairs in ("0", "16"):
+        monkeypatch.setenv("SL_DENSE_PAIRS", pairs)
+        with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+            out.append(retrieve_batch(gi, (qo, qt), 20, as_arrays=True))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
