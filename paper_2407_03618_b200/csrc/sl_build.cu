@@ -547,6 +547,26 @@ __global__ void k_dense_pairs(float* __restrict__ dense, uint32_t n_dense, uint3
   }
 }
 
+// triple rows T_abc = P_ab + r_c (a < b < c < m3 <= m2): the kernel's next addition after P_ab
+__global__ void k_dense_triples(float* __restrict__ dense, uint32_t n_dense, uint32_t m2, uint32_t m3,
+                                uint32_t n_pad) {
+  const uint32_t nt = m3 * (m3 - 1) * (m3 - 2) / 6;
+  for (uint32_t tr = blockIdx.y; tr < nt; tr += gridDim.y) {
+    uint32_t c = 2;
+    while ((c + 1) * c * (c - 1) / 6 <= tr) ++c;
+    uint32_t r = tr - c * (c - 1) * (c - 2) / 6, b = 1;
+    while ((b + 1) * b / 2 <= r) ++b;
+    const uint32_t a = r - b * (b - 1) / 2;
+    const float4* pab = reinterpret_cast<const float4*>(dense + (uint64_t)dense_pair_row(n_dense, m2, a, b) * n_pad);
+    const float4* rc = reinterpret_cast<const float4*>(dense + (uint64_t)c * n_pad);
+    float4* out = reinterpret_cast<float4*>(dense + (uint64_t)dense_triple_row(n_dense, m2, a, b, c) * n_pad);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_pad / 4; i += gridDim.x * blockDim.x) {
+      const float4 x = pab[i], y = rc[i];
+      out[i] = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    }
+  }
+}
+
 // skip[s][tile] = first row-relative posting with doc >= tile * kTileDocs; one CTA per row
 // (grid-stride over rows), four postings per thread per step
 __global__ void __launch_bounds__(256) k_skip_fill(const uint64_t* __restrict__ indptr,
@@ -997,15 +1017,26 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     }
   }
   if (ix->dense_rows) {
-    // pair rows for the leading m dense slots, within a 4 GB budget (SL_DENSE_PAIRS=m overrides; 0: none)
+    // pair rows for the leading m dense slots, within 2 GB (c2: 120 rows, 480 MB; c4: 55 rows)
+    // — SL_DENSE_PAIRS=m overrides, 0: none
     uint32_t m = std::min<uint32_t>(16, ix->dense_rows);
     const uint64_t row_bytes = (uint64_t)ix->n_pad * 4;
-    while (m > 1 && (uint64_t)m * (m - 1) / 2 * row_bytes > (4ull << 30)) --m;
+    while (m > 1 && (uint64_t)m * (m - 1) / 2 * row_bytes > (2ull << 30)) --m;
     if (const char* e = std::getenv("SL_DENSE_PAIRS"))
       if (*e) m = std::min<uint32_t>((uint32_t)std::atoi(e), ix->dense_rows);
     if (m < 2) m = 0;
     ix->pair_m = m;
-    const uint64_t rows = (uint64_t)ix->dense_rows + (m ? (uint64_t)m * (m - 1) / 2 : 0);
+    // triple rows for the leading m3 <= m slots within 512 MB (c2: 56 rows, 224 MB). Larger
+    // dense arrays fragmented the allocator's pool between rebuilds (c4 with 3.7 GB of pairs
+    // and 2 GB of triples rebuilt in 84-259 ms instead of 21) — SL_DENSE_TRIPLES=m3 overrides
+    uint32_t m3 = std::min<uint32_t>(8, m);
+    while (m3 > 2 && (uint64_t)m3 * (m3 - 1) * (m3 - 2) / 6 * row_bytes > (512ull << 20)) --m3;
+    if (const char* e = std::getenv("SL_DENSE_TRIPLES"))
+      if (*e) m3 = std::min<uint32_t>((uint32_t)std::atoi(e), m);
+    if (m3 < 3) m3 = 0;
+    ix->triple_m = m3;
+    const uint64_t rows = (uint64_t)ix->dense_rows + (m ? (uint64_t)m * (m - 1) / 2 : 0) +
+                          (m3 ? (uint64_t)m3 * (m3 - 1) * (m3 - 2) / 6 : 0);
     SL_TRY(dalloc(ix, &ix->dense, rows * ix->n_pad));
     SL_CUDA_TRY(cudaMemsetAsync(ix->dense, 0, (uint64_t)ix->dense_rows * ix->n_pad * 4, st));
     dim3 g(grid_for(N, 256, 1024), std::min<uint32_t>(ix->dense_rows, 65535));
@@ -1014,6 +1045,10 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
     if (m) {
       dim3 gp(grid_for(ix->n_pad / 4, 256, 256), std::min<uint32_t>(m * (m - 1) / 2, 65535));
       k_dense_pairs<<<gp, 256, 0, st>>>(ix->dense, ix->dense_rows, m, ix->n_pad); ++t_launches;
+    }
+    if (m3) {
+      dim3 gt(grid_for(ix->n_pad / 4, 256, 256), std::min<uint32_t>(m3 * (m3 - 1) * (m3 - 2) / 6, 65535));
+      k_dense_triples<<<gt, 256, 0, st>>>(ix->dense, ix->dense_rows, m, m3, ix->n_pad); ++t_launches;
     }
   }
   if (ix->skip_rows) {

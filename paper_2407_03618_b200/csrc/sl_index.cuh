@@ -41,6 +41,7 @@ struct sl_index {
   float* dense = nullptr;         // [(dense_rows + pair rows) * n_pad]
   uint32_t dense_rows = 0;
   uint32_t pair_m = 0;            // dense slots [0, pair_m) also have pair rows r_a + r_b (a < b)
+  uint32_t triple_m = 0;          // ... and [0, triple_m) triple rows (r_a + r_b) + r_c (a < b < c)
   uint32_t* skiptab = nullptr;    // [skip_rows * (num_tiles + 1)]
   // block-max bounds (exact top-k pruning): max(0, S^Δ) over a row / a row's tile slice
   float* rowmax = nullptr;        // [V]
@@ -71,6 +72,7 @@ struct sl_index {
     v.n_pad = n_pad;
     v.n_dense = dense_rows;
     v.pair_m = pair_m;
+    v.triple_m = triple_m;
     v.num_tiles = num_tiles;
     v.doc_base = doc_base;
     return v;

@@ -167,7 +167,14 @@ struct IndexView {
   uint32_t doc_base;
   uint32_t n_dense;  // dense rows (pair rows follow them in `dense`)
   uint32_t pair_m;   // leading dense slots with pair rows
+  uint32_t triple_m; // leading dense slots with triple rows (after the pair rows)
 };
+
+// row of the triple (a, b, c), a < b < c < m3 (colex order): triple rows follow the pair rows
+__host__ __device__ __forceinline__ uint32_t dense_triple_row(uint32_t n_dense, uint32_t m2, uint32_t a, uint32_t b,
+                                                              uint32_t c) {
+  return n_dense + m2 * (m2 - 1) / 2 + c * (c - 1) * (c - 2) / 6 + b * (b - 1) / 2 + a;
+}
 
 // row of the pair (a, b), a < b < m, in the dense array: pair rows follow the n_dense single rows
 __host__ __device__ __forceinline__ uint32_t dense_pair_row(uint32_t n_dense, uint32_t m, uint32_t a, uint32_t b) {

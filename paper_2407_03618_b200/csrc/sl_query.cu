@@ -565,8 +565,14 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       }
       // a signature led by two slots with a pair row starts from it (one dense row fewer)
       // (a repeated token repeats its slot: equal leading slots have no pair row)
-      if (!PRUNE && nd >= 2 && nd <= (uint32_t)NDMAX && (uint32_t)s.dslot[1] < ix.pair_m &&
-          s.dslot[0] < s.dslot[1]) {
+      if (!PRUNE && nd >= 3 && nd <= (uint32_t)NDMAX && (uint32_t)s.dslot[2] < ix.triple_m &&
+          s.dslot[0] < s.dslot[1] && s.dslot[1] < s.dslot[2]) {  // three leading slots: a triple row
+        s.dslot[0] = (int32_t)dense_triple_row(ix.n_dense, ix.pair_m, (uint32_t)s.dslot[0], (uint32_t)s.dslot[1],
+                                               (uint32_t)s.dslot[2]);
+        for (uint32_t a = 1; a + 2 < nd; ++a) s.dslot[a] = s.dslot[a + 2];
+        nd -= 2;
+      } else if (!PRUNE && nd >= 2 && nd <= (uint32_t)NDMAX && (uint32_t)s.dslot[1] < ix.pair_m &&
+                 s.dslot[0] < s.dslot[1]) {
         s.dslot[0] = (int32_t)dense_pair_row(ix.n_dense, ix.pair_m, (uint32_t)s.dslot[0], (uint32_t)s.dslot[1]);
         for (uint32_t a = 1; a + 1 < nd; ++a) s.dslot[a] = s.dslot[a + 1];
         --nd;

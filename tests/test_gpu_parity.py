@@ -344,9 +344,9 @@ def test_dense_cap_planning_path(cuda_ok, c1, monkeypatch, cap):
 
 
 def test_dense_pair_rows_exact(cuda_ok, c1, monkeypatch):
-    """Pair rows (r_a + r_b for the leading dense slots) are an access path: queries whose dense
-    signature starts with such a pair — including repeated dense tokens, which have none — give
-    bit-identical top-k with pair rows on and off."""
+    """Pair rows (r_a + r_b) and triple rows ((r_a + r_b) + r_c) of the leading dense slots are
+    access paths: queries whose dense signature starts with them — including repeated dense
+    tokens, which have none — give bit-identical top-k with them on and off."""
     cfg, corp, _, _ = c1
     p = BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)
     rng = np.random.default_rng(41)
@@ -354,9 +354,11 @@ def test_dense_pair_rows_exact(cuda_ok, c1, monkeypatch):
     queries += [[0, 0], [1, 0, 1], [0, 1], [2, 2, 2, 3], [0, 1, 2, 3, 4, 5]]
     qo, qt = csr(queries)
     out = []
-    for pairs in ("0", "16"):
+    for pairs, triples in (("0", "0"), ("16", "0"), ("16", "8")):  # none, pair rows, pair + triple rows
         monkeypatch.setenv("SL_DENSE_PAIRS", pairs)
+        monkeypatch.setenv("SL_DENSE_TRIPLES", triples)
         with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
             out.append(retrieve_batch(gi, (qo, qt), 20, as_arrays=True))
-    np.testing.assert_array_equal(out[0][0], out[1][0])
-    np.testing.assert_array_equal(out[0][1], out[1][1])
+    for o in out[1:]:
+        np.testing.assert_array_equal(out[0][0], o[0])
+        np.testing.assert_array_equal(out[0][1], o[1])
