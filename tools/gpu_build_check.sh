@@ -14,4 +14,4 @@ if [ -n "$NCU" ]; then
     --log-file gpurun_out/build_launches_new_c$c.csv python tools/prof_build.py --config $c > /dev/null 2>&1
   done
 fi
-tail -3 gpurun_out/t_build_paths.log gpurun_out/memcheck_build.log gpurun_out/prof_build_new.log
+tail -n 3 gpurun_out/t_build_paths.log gpurun_out/memcheck_build.log gpurun_out/prof_build_new.log

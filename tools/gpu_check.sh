@@ -4,4 +4,4 @@ timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/py
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_c2.log 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -c 600 gpurun_out/bench_c2.log; tail -c 400 gpurun_out/bench_ref.log
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -c 600 gpurun_out/bench_c2.log; tail -c 400 gpurun_out/bench_ref.log
