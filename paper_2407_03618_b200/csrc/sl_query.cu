@@ -212,8 +212,12 @@ __host__ __device__ inline uint32_t kept_capacity(uint32_t k) {
 }
 
 // float lower bound of every key >= tau (for the cheap pre-test)
+// x > tau_float(tau) <=> orderable(x) > hi(tau). hi = 0x7FFFFFFF (a split threshold published
+// one ordinal below a score of 0) is no float's ordinal since -0 and +0 share one: its float
+// would be -0.0, and +0 > -0 is false, so it maps to the largest negative float instead.
 __device__ __forceinline__ float tau_float(uint64_t tau) {
   const uint32_t hi = (uint32_t)(tau >> 32);
+  if (hi == 0x7FFFFFFFu) return __uint_as_float(0x80000001u);
   return hi < 0x00800000u ? -INFINITY : ord_to_float(hi);
 }
 

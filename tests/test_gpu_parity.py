@@ -362,3 +362,25 @@ def test_dense_pair_rows_exact(cuda_ok, c1, monkeypatch):
     for o in out[1:]:
         np.testing.assert_array_equal(out[0][0], o[0])
         np.testing.assert_array_equal(out[0][1], o[1])
+
+
+def test_zero_score_ties_across_splits(cuda_ok, c1, monkeypatch):
+    """Robertson head-token queries: documents containing them score below 0, the rest exactly 0,
+    so the top-k is score-0 ties resolved by the smallest doc ids. Splits publish their k-th key
+    one score ordinal lower as a shared threshold; one ordinal below 0 is not a float of its own
+    (-0 and +0 share it) and must still let exact zeros through — in every split, whatever the
+    order the splits run in."""
+    cfg, corp, _, _ = c1
+    p = BM25Params(Variant.robertson, 1.5, 0.75)
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    heads = [t for t in range(50) if exp["df"][t] > cfg.num_docs // 2][:6]
+    assert heads, "c1 has tokens in more than half of the documents"
+    queries = [[t] for t in heads] * 20 + [heads[:2]] * 20
+    qo, qt = csr(queries)
+    rid, rsc = ox.retrieve_batch(qo, qt, 64, True, 4)
+    monkeypatch.setenv("SL_SPLITS", "8")
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        for _ in range(5):
+            gid, gsc = retrieve_batch(gi, (qo, qt), 64, as_arrays=True)
+            np.testing.assert_array_equal(gid, rid.astype(np.uint32))
