@@ -384,3 +384,32 @@ def test_zero_score_ties_across_splits(cuda_ok, c1, monkeypatch):
         for _ in range(5):
             gid, gsc = retrieve_batch(gi, (qo, qt), 64, as_arrays=True)
             np.testing.assert_array_equal(gid, rid.astype(np.uint32))
+
+
+def test_zero_ties_after_split_threshold_published(cuda_ok, monkeypatch):
+    """The one-ordinal-below-zero split threshold: token 0 sits in more than half of the
+    documents (Robertson idf < 0, so they score below 0) except 5 documents at 10235..10239 and
+    the tail from 12240. Later splits meet their exact zeros early and publish their k-th key;
+    the split holding 10235..10239 reaches them after reading that threshold, and they are the
+    best documents (smallest ids among the ties). With the threshold mapped to -0.0 the 5-split
+    plan lost them (+0 > -0 is false)."""
+    N, T = 20480, 1024
+    in0 = np.zeros(N, bool)
+    in0[:10235] = True
+    in0[10240:12240] = True
+    docs = [[0, 1] if in0[d] else [2, 1] for d in range(N)]
+    off = np.zeros(N + 1, np.uint64)
+    off[1:] = np.cumsum([len(x) for x in docs])
+    tok = np.concatenate([np.asarray(x, np.uint32) for x in docs])
+    p = BM25Params(Variant.robertson, 1.5, 0.75)
+    ox = oracle.OracleIndex(off, tok, 3, int(p.variant), p.k1, p.b, p.delta)
+    qo, qt = csr([[0]])
+    rid, rsc = ox.retrieve_batch(qo, qt, 10, True, 1)
+    assert list(rid[0]) == [10235, 10236, 10237, 10238, 10239, 12240, 12241, 12242, 12243, 12244]
+    for splits in ("2", "5", "20"):
+        monkeypatch.setenv("SL_SPLITS", splits)
+        with build_index(off, tok, 3, p) as gi:
+            for _ in range(3):
+                gid, gsc = retrieve_batch(gi, (qo, qt), 10, as_arrays=True)
+                np.testing.assert_array_equal(gid[0], rid[0].astype(np.uint32), err_msg=f"splits {splits}")
+    assert T * 20 == N
