@@ -17,6 +17,8 @@
  *   sl_params_validate  <- BM25Params::validate                                proj/src/scoring.cpp:47-58
  *   sl_index_save       <- save_index(index, directory)                        SPEC.md [MODULE] index
  *   sl_index_load       <- load_index(directory)                               SPEC.md [MODULE] index
+ *   sl_retrieve_local / sl_merge_candidates <- retrieve_batch split at the rank boundary
+ *                          (per-shard top-k keys; rank-0 merge), for callers with their own transport
  *   sl_index_destroy / sl_last_error : ownership + error plumbing (the reference throws
  *                          std::invalid_argument with fixed messages, scoring.cpp:15-138;
  *                          here a status code + thread-local message).
@@ -186,18 +188,29 @@ int32_t sl_score_query(const sl_index* index, const uint32_t* q_tokens, uint32_t
 int32_t sl_top_k(const float* scores, uint32_t n, uint32_t k, int32_t ordered, int32_t mem,
                  int32_t device, uint32_t* out_ids, float* out_scores);
 
+/* Multi-rank building blocks for callers that move candidates over their own transport (the
+ * library's NCCL path runs the same two steps internally):
+ *   sl_retrieve_local   <- the per-rank half of retrieve_batch: this shard's best k candidates per
+ *                          query as 64-bit keys [num_queries x k], key = (order-preserving bits of
+ *                          the f32 accumulated score, query constant excluded) << 32 | ~global_doc_id,
+ *                          larger key = better (ties -> smaller doc id), 0 = empty slot; plus the
+ *                          query constant Σ S^θ (f64, identical on every shard) in out_qconst[B].
+ *   sl_merge_candidates <- the rank-0 merge: keys of num_shards shards laid out
+ *                          [num_shards][num_queries][k] -> the [num_queries x k] (ids, scores) that
+ *                          sl_retrieve_batch on the unsharded index returns (same padding).
+ * k <= 4096. With mem == SL_MEM_HOST every buffer is host memory; SL_MEM_DEVICE: all on `device`
+ * (sl_retrieve_local: the index's device). */
+int32_t sl_retrieve_local(const sl_index* index, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                          uint32_t num_queries, uint32_t k, int32_t mem, uint64_t* out_keys, double* out_qconst);
+int32_t sl_merge_candidates(const uint64_t* keys, uint32_t num_shards, uint32_t num_queries, uint32_t k,
+                            const double* qconst, int32_t mem, int32_t device, uint32_t* out_ids, float* out_scores);
+
 /* Multi-GPU (one process per GPU). The unique id (128 bytes) is created on rank 0 and
  * shipped to every rank by the caller (any transport), then each rank joins. */
 int32_t sl_comm_unique_id(uint8_t out_id[128]);
 int32_t sl_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
                      sl_comm** out);
 void sl_comm_destroy(sl_comm* comm);
-
-/* Synthetic corpus generation on the device (bench/test input only; bit-identical to
- * the host generator in libsl_synth): token_ids[i] = Zipf token at global position
- * begin + i, using the f64 CDF `cdf` (host or device per mem). */
-int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed, uint64_t begin,
-                               uint64_t count, int32_t cdf_mem, uint32_t* token_ids_dev);
 
 /* ---- Text pipeline (SPEC.md [MODULE] tokenizer) ---------------
  *   sl_tokenize(build=1)  <- tokenize_build(text, TokenizerConfig, Vocabulary&) per document

@@ -36,6 +36,11 @@ _SIG = {
     "orc_score": (_d, [_d, _u32, _d, _u32, _d, _i32, _d, _d, _d]),
     "orc_nonoccurrence": (_d, [_u32, _u32, _i32, _d, _d, _d]),
     "orc_validate": (_i32, [_i32, _d, _d, _d]),
+    "orc_stream_df": (_i32, [_vp, _vp, _u32, _u32, _i32, _vp, _vp]),
+    "orc_stream_rows": (_i32, [_vp, _vp, _u32, _u32, _vp, _u32, _vp, _u32, _d, _i32, _d, _d, _d, _i32, _vp, _vp, _vp,
+                               _vp]),
+    "orc_stream_topk": (_i32, [_vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _d, _i32, _d, _d, _d, _u32,
+                               _i32, _vp, _vp]),
 }
 _REF_SIG = {
     "ref_last_error": (C.c_char_p, []),
@@ -189,3 +194,53 @@ def score(tf, df, dl, n, avg, v, k1=1.5, b=0.75, delta=0.0):
 
 def nonoccurrence(df, n, v, k1=1.5, b=0.75, delta=0.0):
     return lib().orc_nonoccurrence(df, n, v, k1, b, delta)
+
+
+# ---- streaming checks (corpora too large for OracleIndex: c5) ----
+def stream_df(offsets, tokens, V, threads=16, df=None):
+    """DF by streaming count over one shard (added into `df`, u64[V]); returns (df, Σ|D|)."""
+    off = np.ascontiguousarray(offsets, np.uint64)
+    tok = np.ascontiguousarray(tokens, np.uint32)
+    df = np.zeros(V, np.uint64) if df is None else df
+    tot = C.c_uint64(0)
+    if lib().orc_stream_df(_p(off), _p(tok) if len(tok) else None, len(off) - 1, V, threads, _p(df), C.byref(tot)):
+        raise ValueError(_err())
+    return df, tot.value
+
+
+def stream_rows(offsets, tokens, V, sel, global_stats, variant=2, k1=1.5, b=0.75, delta=0.0, threads=16):
+    """Rows `sel` of a shard's score matrix from its tokens with global statistics
+    (gdf[V], N_global, avg_len): dict token -> (docs u32, tf u32, values f32)."""
+    off = np.ascontiguousarray(offsets, np.uint64)
+    tok = np.ascontiguousarray(tokens, np.uint32)
+    sel = np.ascontiguousarray(sel, np.uint32)
+    gdf = np.ascontiguousarray(global_stats[0], np.uint32)
+    args = (_p(off), _p(tok), len(off) - 1, V, _p(sel), len(sel), _p(gdf), int(global_stats[1]),
+            float(global_stats[2]), variant, k1, b, delta, threads)
+    ro = np.zeros(len(sel) + 1, np.uint64)
+    if lib().orc_stream_rows(*args, _p(ro), None, None, None):
+        raise ValueError(_err())
+    n = int(ro[-1])
+    docs, tfs, vals = np.empty(max(n, 1), np.uint32), np.empty(max(n, 1), np.uint32), np.empty(max(n, 1), np.float32)
+    if lib().orc_stream_rows(*args, _p(ro), _p(docs), _p(tfs), _p(vals)):
+        raise ValueError(_err())
+    return {int(t): (docs[ro[i]:ro[i + 1]], tfs[ro[i]:ro[i + 1]], vals[ro[i]:ro[i + 1]]) for i, t in enumerate(sel)}
+
+
+def stream_topk(offsets, tokens, V, doc_base, q_offsets, q_tokens, global_stats, k, variant=2, k1=1.5, b=0.75,
+                delta=0.0, threads=16):
+    """Streaming naive dense scorer over one shard: best k (global ids, f64 B(Q,D)) per query,
+    global statistics (gdf[V], N_global, avg_len)."""
+    off = np.ascontiguousarray(offsets, np.uint64)
+    tok = np.ascontiguousarray(tokens, np.uint32)
+    qo = np.ascontiguousarray(q_offsets, np.uint64)
+    qt = np.ascontiguousarray(q_tokens if len(q_tokens) else np.zeros(1), np.uint32)
+    gdf = np.ascontiguousarray(global_stats[0], np.uint32)
+    B = len(qo) - 1
+    ids = np.empty((B, k), np.uint32)
+    sc = np.empty((B, k), np.float64)
+    if lib().orc_stream_topk(_p(off), _p(tok), len(off) - 1, doc_base, V, _p(qo), _p(qt), B, _p(gdf),
+                             int(global_stats[1]), float(global_stats[2]), variant, k1, b, delta, k, threads, _p(ids),
+                             _p(sc)):
+        raise ValueError(_err())
+    return ids, sc

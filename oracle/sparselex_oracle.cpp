@@ -10,7 +10,7 @@
 //             nonoccurrence_score) — restated below expression-for-expression
 //             and pinned against the reference's own scoring.cpp, compiled by
 //             oracle/Makefile into oracle/_ref/libref_scoring.so
-//             (tests/test_oracle_pin.py);
+//             (tests/test_oracle.py::test_restatement_pinned_to_reference_scoring);
 //   counting  proj/src/tokenizer.cpp:162-168 (count_terms: tf per id,
 //             length = #ids) and proj/include/sparselex/vocabulary.hpp:37-42 (DF);
 //   index     SPEC.md [MODULE] index: two-pass build_index (pass 1 DF + lengths,
@@ -270,6 +270,17 @@ int guarded(F&& f) {
   }
 }
 
+template <class F>
+void for_doc_ranges(uint32_t N, int threads, F&& f) {
+  threads = std::max(1, threads);
+  std::vector<std::thread> th;
+  for (int t = 0; t < threads; ++t) {
+    const uint32_t a = (uint32_t)((uint64_t)N * t / threads), b = (uint32_t)((uint64_t)N * (t + 1) / threads);
+    th.emplace_back([&f, t, a, b] { f(t, a, b); });
+  }
+  for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 extern "C" {
@@ -416,6 +427,221 @@ double orc_nonoccurrence(uint32_t df, uint32_t N, int v, double k1, double b, do
 }
 int orc_validate(int v, double k1, double b, double delta) {
   return guarded([&] { validate(Params{v, k1, b, delta}); });
+}
+
+
+// ---- streaming checks for corpora too large to index on the CPU (c5: 1.65e10 tokens) ----
+// Each runs over one shard's tokens in `threads` contiguous document ranges and keeps only
+// what the check needs, so host memory stays at one shard's tokens.
+
+
+// DF by streaming count (vocabulary.hpp:37-42 semantics: one bump per distinct id per
+// document), ADDED into df_out[V]; *total_len_out += Σ|D|.
+int orc_stream_df(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, int threads,
+                  uint64_t* df_out, uint64_t* total_len_out) {
+  return guarded([&] {
+    threads = std::max(1, threads);
+    std::vector<std::vector<uint32_t>> local(threads);
+    std::vector<uint64_t> tot(threads, 0);
+    std::atomic<int> bad{0};
+    for_doc_ranges(N, threads, [&](int t, uint32_t a, uint32_t b) {
+      auto& df = local[t];
+      df.assign(V, 0);
+      std::vector<uint32_t> scratch;
+      std::vector<std::pair<uint32_t, uint32_t>> counts;
+      for (uint32_t d = a; d < b; ++d) {
+        const uint64_t o = offsets[d], e = offsets[d + 1];
+        for (uint64_t i = o; i < e; ++i)
+          if (tokens[i] >= V) bad = 1;
+        if (bad) return;
+        count_terms(tokens + o, e - o, scratch, counts);
+        for (auto& c : counts) ++df[c.first];
+        tot[t] += e - o;
+      }
+    });
+    if (bad) throw std::invalid_argument("stream_df: token id >= vocab size");
+    for (int t = 0; t < threads; ++t) {
+      for (uint32_t v = 0; v < V; ++v) df_out[v] += local[t][v];
+      *total_len_out += tot[t];
+    }
+  });
+}
+
+// Selected rows of a shard's score matrix by streaming: for the nsel tokens in sel, the
+// documents containing them (ascending, local ids), their tf and the stored value
+// f32(S - S^θ) computed with the GLOBAL statistics (gdf, gN, avg) exactly as pass 2 of
+// build() does. row_off[nsel+1] is always written; docs/tfs/values (may be null) are
+// filled in row order when given (sized row_off[nsel]).
+int orc_stream_rows(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t V, const uint32_t* sel,
+                    uint32_t nsel, const uint32_t* gdf, uint32_t gN, double avg, int variant, double k1, double b,
+                    double delta, int threads, uint64_t* row_off, uint32_t* docs, uint32_t* tfs, float* values) {
+  return guarded([&] {
+    const Params p{variant, k1, b, delta};
+    validate(p);
+    threads = std::max(1, threads);
+    std::vector<int32_t> slot(V, -1);
+    for (uint32_t i = 0; i < nsel; ++i) {
+      if (sel[i] >= V) throw std::invalid_argument("stream_rows: selected token >= vocab size");
+      slot[sel[i]] = (int32_t)i;
+    }
+    auto doc_counts = [&](uint32_t d, std::vector<uint32_t>& scratch, std::vector<std::pair<uint32_t, uint32_t>>& out) {
+      scratch.clear();
+      for (uint64_t i = offsets[d]; i < offsets[d + 1]; ++i)
+        if (slot[tokens[i]] >= 0) scratch.push_back(tokens[i]);
+      std::sort(scratch.begin(), scratch.end());
+      out.clear();
+      for (size_t i = 0; i < scratch.size();) {
+        size_t j = i + 1;
+        while (j < scratch.size() && scratch[j] == scratch[i]) ++j;
+        out.emplace_back(scratch[i], (uint32_t)(j - i));
+        i = j;
+      }
+    };
+    std::vector<std::vector<uint64_t>> cnt(threads, std::vector<uint64_t>(nsel, 0));
+    for_doc_ranges(N, threads, [&](int t, uint32_t a, uint32_t bb) {
+      std::vector<uint32_t> scratch;
+      std::vector<std::pair<uint32_t, uint32_t>> c;
+      for (uint32_t d = a; d < bb; ++d) {
+        doc_counts(d, scratch, c);
+        for (auto& x : c) ++cnt[t][slot[x.first]];
+      }
+    });
+    row_off[0] = 0;
+    for (uint32_t i = 0; i < nsel; ++i) {
+      uint64_t s = 0;
+      for (int t = 0; t < threads; ++t) s += cnt[t][i];
+      row_off[i + 1] = row_off[i] + s;
+    }
+    if (!docs) return;
+    // per-thread write cursors: rows in doc order = thread order
+    std::vector<std::vector<uint64_t>> cur(threads, std::vector<uint64_t>(nsel));
+    for (uint32_t i = 0; i < nsel; ++i) {
+      uint64_t c = row_off[i];
+      for (int t = 0; t < threads; ++t) {
+        cur[t][i] = c;
+        c += cnt[t][i];
+      }
+    }
+    std::vector<double> theta64(nsel, 0.0);
+    for (uint32_t i = 0; i < nsel; ++i)
+      if (gdf[sel[i]]) theta64[i] = nonoccurrence(gdf[sel[i]], gN, p);
+    for_doc_ranges(N, threads, [&](int t, uint32_t a, uint32_t bb) {
+      std::vector<uint32_t> scratch;
+      std::vector<std::pair<uint32_t, uint32_t>> c;
+      for (uint32_t d = a; d < bb; ++d) {
+        doc_counts(d, scratch, c);
+        const double dl = (double)(offsets[d + 1] - offsets[d]);
+        for (auto& x : c) {
+          const int32_t i = slot[x.first];
+          const uint64_t pos = cur[t][i]++;
+          docs[pos] = d;
+          if (tfs) tfs[pos] = x.second;
+          if (values) {
+            const double sc = score((double)x.second, gdf[x.first], dl, gN, avg, p);
+            values[pos] = (float)(sc - theta64[i]);
+          }
+        }
+      }
+    });
+  });
+}
+
+// Streaming naive dense scorer (SPEC.md [MODULE] retrieval property "naive dense scorer",
+// AC1/AC6): for each query, B(Q,D) = Σ_i S(q_i, D) from raw tf / global df / |D| for every
+// document of the shard (query tokens in query order, repeats counted), and the best k by
+// (score desc, doc asc) over the shard. Documents containing none of a query's tokens all
+// score Σ_i S(q_i, tf=0) (length-independent); of those only the k smallest ids can place.
+// Outputs [B x k]: global doc ids (doc_base + local), f64 scores; unused slots id 0xFFFFFFFF.
+int orc_stream_topk(const uint64_t* offsets, const uint32_t* tokens, uint32_t N, uint32_t doc_base, uint32_t V,
+                    const uint64_t* q_off, const uint32_t* q_tok, uint32_t B, const uint32_t* gdf, uint32_t gN,
+                    double avg, int variant, double k1, double b, double delta, uint32_t k, int threads,
+                    uint32_t* out_ids, double* out_scores) {
+  return guarded([&] {
+    const Params p{variant, k1, b, delta};
+    validate(p);
+    if (k == 0) throw std::invalid_argument("top_k: k must be >= 1");
+    threads = std::max(1, threads);
+    // compact ids of the distinct query tokens with df > 0 (OOV drop)
+    std::vector<int32_t> cid(V, -1);
+    std::vector<uint32_t> utok;
+    std::vector<std::vector<int32_t>> qc(B);
+    for (uint32_t q = 0; q < B; ++q)
+      for (uint64_t j = q_off[q]; j < q_off[q + 1]; ++j) {
+        const uint32_t t = q_tok[j];
+        if (t >= V) throw std::invalid_argument("score_query: token id >= vocab size");
+        if (gdf[t] == 0) continue;
+        if (cid[t] < 0) {
+          cid[t] = (int32_t)utok.size();
+          utok.push_back(t);
+        }
+        qc[q].push_back(cid[t]);
+      }
+    const uint32_t U = (uint32_t)utok.size();
+    std::vector<double> s0(U);
+    for (uint32_t u = 0; u < U; ++u) s0[u] = score(0.0, gdf[utok[u]], 1.0, gN, avg, p);
+    std::vector<double> base(B, 0.0);
+    for (uint32_t q = 0; q < B; ++q)
+      for (int32_t c : qc[q]) base[q] += s0[c];
+    using Cand = std::pair<double, uint32_t>;  // (score, global doc)
+    auto better = [](const Cand& x, const Cand& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); };
+    std::vector<std::vector<std::vector<Cand>>> heaps(threads, std::vector<std::vector<Cand>>(B));
+    std::vector<std::vector<std::vector<uint32_t>>> untouched(threads, std::vector<std::vector<uint32_t>>(B));
+    for_doc_ranges(N, threads, [&](int t, uint32_t a, uint32_t bb) {
+      std::vector<uint32_t> tfc(U, 0), touched;
+      std::vector<double> val(U);
+      for (uint32_t d = a; d < bb; ++d) {
+        touched.clear();
+        for (uint64_t i = offsets[d]; i < offsets[d + 1]; ++i) {
+          const int32_t c = cid[tokens[i]];
+          if (c >= 0 && tfc[c]++ == 0) touched.push_back((uint32_t)c);
+        }
+        const double dl = (double)(offsets[d + 1] - offsets[d]);
+        for (uint32_t c : touched) val[c] = score((double)tfc[c], gdf[utok[c]], dl, gN, avg, p);
+        const uint32_t g = doc_base + d;
+        for (uint32_t q = 0; q < B; ++q) {
+          bool hit = false;
+          double s = 0.0;
+          for (int32_t c : qc[q]) {
+            if (tfc[c]) {
+              hit = true;
+              s += val[c];
+            } else {
+              s += s0[c];
+            }
+          }
+          if (!hit) {
+            if (untouched[t][q].size() < k) untouched[t][q].push_back(g);
+            continue;
+          }
+          auto& h = heaps[t][q];  // min-heap on `better` of the best k
+          const Cand cd{s, g};
+          if (h.size() < k) {
+            h.push_back(cd);
+            std::push_heap(h.begin(), h.end(), better);
+          } else if (better(cd, h.front())) {
+            std::pop_heap(h.begin(), h.end(), better);
+            h.back() = cd;
+            std::push_heap(h.begin(), h.end(), better);
+          }
+        }
+        for (uint32_t c : touched) tfc[c] = 0;
+      }
+    });
+    for (uint32_t q = 0; q < B; ++q) {
+      std::vector<Cand> all;
+      std::vector<uint32_t> un;
+      for (int t = 0; t < threads; ++t) {
+        all.insert(all.end(), heaps[t][q].begin(), heaps[t][q].end());
+        un.insert(un.end(), untouched[t][q].begin(), untouched[t][q].end());  // thread order = doc order
+      }
+      for (uint32_t i = 0; i < un.size() && i < k; ++i) all.emplace_back(base[q], un[i]);
+      std::sort(all.begin(), all.end(), better);
+      for (uint32_t i = 0; i < k; ++i) {
+        out_ids[(uint64_t)q * k + i] = i < all.size() ? all[i].second : 0xFFFFFFFFu;
+        out_scores[(uint64_t)q * k + i] = i < all.size() ? all[i].first : -INFINITY;
+      }
+    }
+  });
 }
 
 }  // extern "C"

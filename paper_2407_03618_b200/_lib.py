@@ -95,7 +95,8 @@ SIGNATURES = {
     "sl_comm_unique_id": (_i32, [_u8p]),
     "sl_comm_init": (_i32, [_u8p, _i32, _i32, _i32, C.POINTER(C.c_void_p)]),
     "sl_comm_destroy": (None, [_vp]),
-    "sl_synth_tokens_device": (_i32, [_vp, _u32, _u32, _u64, _u64, _i32, _vp]),
+    "sl_retrieve_local": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _vp, _vp]),
+    "sl_merge_candidates": (_i32, [_vp, _u32, _u32, _u32, _vp, _i32, _i32, _vp, _vp]),
     "sl_vocab_create": (_i32, [_i32, C.POINTER(C.c_void_p)]),
     "sl_vocab_destroy": (_i32, [_vp]),
     "sl_vocab_size": (_i32, [_vp, C.POINTER(_u32)]),
@@ -166,5 +167,8 @@ def synth_lib() -> C.CDLL:
     if _synth is None:
         if not os.path.exists(SYNTH_PATH):
             raise RuntimeError(f"{SYNTH_PATH} is missing: build with `make -C paper_2407_03618_b200/csrc`")
-        _synth = C.CDLL(SYNTH_PATH)
+        L = C.CDLL(SYNTH_PATH)
+        L.sl_synth_tokens_device.restype = _i32
+        L.sl_synth_tokens_device.argtypes = [_vp, _u32, _u32, _u64, _u64, _i32, _vp]
+        _synth = L
     return _synth

@@ -127,22 +127,20 @@ class SearchIndex:
     def avg_len(self) -> float:
         return self.info().avg_len
 
-    def export(self, tf: bool = False) -> dict:
-        """Host copies of the ScoreMatrix + SearchIndex arrays (SPEC index External Interfaces)."""
+    def export(self, tf: bool = False, fields=None) -> dict:
+        """Host copies of the ScoreMatrix + SearchIndex arrays (SPEC index External Interfaces);
+        `fields` limits the copy to some of indptr / docids / values / df / theta / doclens."""
         inf = self.info()
         V, nnz, N = inf.vocab_size, inf.nnz_local, inf.num_docs_local
-        out = {
-            "indptr": np.empty(V + 1, np.uint64),
-            "docids": np.empty(nnz, np.uint32),
-            "values": np.empty(nnz, np.float32),
-            "df": np.empty(V, np.uint32),
-            "theta": np.empty(V, np.float32),
-            "doclens": np.empty(N, np.uint32),
-        }
+        shapes = {"indptr": (V + 1, np.uint64), "docids": (nnz, np.uint32), "values": (nnz, np.float32),
+                  "df": (V, np.uint32), "theta": (V, np.float32), "doclens": (N, np.uint32)}
+        want = set(shapes) if fields is None else set(fields)
+        out = {key: np.empty(n, dt) for key, (n, dt) in shapes.items() if key in want}
         tfa = np.empty(nnz, np.uint32) if tf else None
         p = lambda a: None if a is None else a.ctypes.data  # noqa: E731
-        check(lib().sl_index_export(self.handle, SL_MEM_HOST, p(out["indptr"]), p(out["docids"]),
-                                    p(out["values"]), p(out["df"]), p(out["theta"]), p(out["doclens"]), p(tfa)))
+        g = out.get
+        check(lib().sl_index_export(self.handle, SL_MEM_HOST, p(g("indptr")), p(g("docids")), p(g("values")),
+                                    p(g("df")), p(g("theta")), p(g("doclens")), p(tfa)))
         if tf:
             out["tf"] = tfa
         out["avg_len"] = inf.avg_len
@@ -182,8 +180,13 @@ def build_index(doc_offsets, token_ids, vocab_size: int, params: BM25Params | No
     if m1 != m2:
         raise ValueError("doc_offsets and token_ids must live in the same memory space")
     n = (len(keep1) - 1) if num_docs is None else num_docs
-    if n < 0:
+    if n < 0 or n + 1 > len(keep1):
         raise ValueError("build_index: doc_offsets must have num_docs + 1 entries")
+    if m1 == SL_MEM_HOST and n >= 0 and len(keep1):
+        # the library copies tokens [offsets[0], offsets[n]) from the host pointer: keep it in bounds
+        o0, on = int(keep1[0]), int(keep1[n])
+        if on > len(keep2) or o0 > on:
+            raise ValueError("build_index: doc offsets exceed the token array (offsets[num_docs] > len(token_ids))")
     d = _lib.BuildDesc()
     d.doc_offsets, d.token_ids = off_p, tok_p
     d.num_docs, d.vocab_size, d.doc_base, d.mem = n, vocab_size, doc_base, m1
@@ -235,6 +238,8 @@ def retrieve_batch(index: SearchIndex, queries, k: int, ordered: bool = True, wo
     if m1 != m2:
         raise ValueError("query offsets and tokens must live in the same memory space")
     B = len(k1) - 1
+    if m1 == SL_MEM_HOST and B >= 0 and int(k1[B]) > (len(tok) if len(tok) else 0):
+        raise ValueError("retrieve_batch: query offsets exceed the token array")
     if m1 == SL_MEM_DEVICE:
         import torch
         ids = torch.empty((B, k), dtype=torch.uint32, device=k1.device)
@@ -250,6 +255,42 @@ def retrieve_batch(index: SearchIndex, queries, k: int, ordered: bool = True, wo
         return ids, sc
     m = min(k, index.num_docs)
     return [QueryResult(ids[b, :m].copy(), sc[b, :m].copy()) for b in range(B)]
+
+
+def retrieve_local(index: SearchIndex, queries, k: int):
+    """Per-shard half of retrieve_batch (sl_retrieve_local): this shard's best k candidate keys
+    per query, u64[B, k] (0 = empty slot), and the per-query constant Σ S^θ, f64[B]. Feed the
+    keys of every shard to merge_candidates (any transport in between)."""
+    if k <= 0:
+        raise ValueError("top_k: k must be >= 1")
+    off, tok = _queries_to_csr(queries)
+    off = np.ascontiguousarray(off, np.uint64)
+    tok = np.ascontiguousarray(tok if len(tok) else np.zeros(1, np.uint32), np.uint32)
+    B = len(off) - 1
+    if B >= 0 and int(off[B]) > len(tok):
+        raise ValueError("retrieve_batch: query offsets exceed the token array")
+    keys = np.zeros((max(B, 0), k), np.uint64)
+    qc = np.zeros(max(B, 0), np.float64)
+    check(lib().sl_retrieve_local(index.handle, off.ctypes.data, tok.ctypes.data, B, k, SL_MEM_HOST,
+                                  keys.ctypes.data, qc.ctypes.data))
+    return keys, qc
+
+
+def merge_candidates(keys, qconst, device: int = 0):
+    """Rank-0 merge (sl_merge_candidates): keys u64[G, B, k] of G shards + the query constants
+    -> (ids u32[B, k], scores f32[B, k]), exactly what retrieve_batch on the unsharded index returns."""
+    keys = np.ascontiguousarray(keys, np.uint64)
+    if keys.ndim != 3:
+        raise ValueError("merge_candidates: keys must be [shards, queries, k]")
+    G, B, k = keys.shape
+    qc = np.ascontiguousarray(qconst, np.float64)
+    if len(qc) != B:
+        raise ValueError("merge_candidates: one query constant per query")
+    ids = np.empty((B, k), np.uint32)
+    sc = np.empty((B, k), np.float32)
+    check(lib().sl_merge_candidates(keys.ctypes.data, G, B, k, qc.ctypes.data, SL_MEM_HOST, device, ids.ctypes.data,
+                                    sc.ctypes.data))
+    return ids, sc
 
 
 def retrieve(index: SearchIndex, query_tokens, k: int, ordered: bool = True) -> QueryResult:

@@ -723,7 +723,18 @@ __global__ void k_skip_tile_max(const uint64_t* __restrict__ indptr, const uint3
   }
 }
 
-int grid_for(uint64_t n, int threads, int max_blocks = 148 * 32) {
+// SMs of the current device (queried once per device; grids are sized in multiples of it)
+int dev_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] > 0 ? cache[dev] : 1;
+}
+
+int grid_for(uint64_t n, int threads, int max_blocks = 0) {
+  if (max_blocks <= 0) max_blocks = 32 * dev_sms();
   uint64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
   if (b > (uint64_t)max_blocks) b = max_blocks;
@@ -845,6 +856,24 @@ int32_t nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return SL_OK;
   set_error(std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
   return SL_ENCCL;
+}
+
+int32_t comm_agree(sl_comm* c, int32_t status) {
+  if (!c || c->nranks <= 1) return status;
+  const std::string own = get_error();
+  int32_t worst = status;
+  const bool ok = cudaMemcpyAsync(c->dflag, &worst, 4, cudaMemcpyHostToDevice, c->st) == cudaSuccess &&
+                  nccl().AllReduce(c->dflag, c->dflag, 1, ncclInt32, ncclMax, c->comm, c->st) == ncclSuccess &&
+                  cudaMemcpyAsync(&worst, c->dflag, 4, cudaMemcpyDeviceToHost, c->st) == cudaSuccess &&
+                  cudaStreamSynchronize(c->st) == cudaSuccess;
+  if (status != SL_OK) {
+    set_error(own);
+    return status;
+  }
+  if (!ok) SL_FAIL(SL_ENCCL, "status agreement with the peer ranks failed");
+  if (worst != SL_OK)
+    SL_FAIL(worst, std::string("a peer rank failed (") + sl_status_string(worst) + "); see that rank's error");
+  return SL_OK;
 }
 
 void free_index(sl_index* ix) {
@@ -1053,7 +1082,7 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   }
   if (ix->skip_rows) {
     SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
-    k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 148 * 8), 256, 0, st>>>(
+    k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 8 * dev_sms()), 256, 0, st>>>(
         ix->indptr, ix->docids, slot_tok + ix->dense_rows, ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
   }
   // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
@@ -1112,7 +1141,7 @@ struct PhaseTrace {
   }
 };
 
-int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
+int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st, bool* agreed) {
   PhaseTrace tr(st);
   const uint32_t N = d->num_docs, V = d->vocab_size;
   // ---- inputs on the device
@@ -1230,6 +1259,8 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st) {
   } else if (d->comm) {
     uint64_t* dstats;
     SL_TRY(tmp.alloc(&dstats, 2));
+    *agreed = true;  // from here on every rank takes part in the collectives below
+    SL_TRY(comm_agree(d->comm, SL_OK));
     SL_CUDA_TRY(cudaMemcpyAsync(dstats, stats, 16, cudaMemcpyHostToDevice, st));
     SL_TRY(nccl_check(nccl().AllReduce(ix->df_global, ix->df_global, V, ncclUint32, ncclSum, d->comm->comm, st),
                       "ncclAllReduce(df)"));
@@ -1301,7 +1332,10 @@ int32_t build_index_impl(const sl_build_desc* d, sl_index** out) {
     }
   }
   t_build_stream = st;
-  const int32_t rc = build_body(d, ix, st);
+  bool agreed = false;
+  int32_t rc = build_body(d, ix, st, &agreed);
+  // a rank that failed before the statistics all-reduce still takes part in the agreement
+  if (rc != SL_OK && d->comm && !d->global_df && !agreed) rc = comm_agree(d->comm, rc);
   t_build_stream = nullptr;
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);

@@ -4,7 +4,6 @@
 #include <string>
 
 #include "sl_index.cuh"
-#include "sl_synth.h"
 
 namespace sl {
 thread_local uint32_t t_launches = 0;
@@ -17,17 +16,13 @@ const std::string& get_error() { return t_error; }
 int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
                       uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats);
 int32_t score_query_impl(const sl_index* ix, const uint32_t* q_tokens, uint32_t q_len, int32_t mem, float* out);
+int32_t retrieve_local_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
+                            uint32_t k, int32_t mem, uint64_t* out_keys, double* out_qconst);
+int32_t merge_candidates_impl(const uint64_t* keys, uint32_t G, uint32_t B, uint32_t k, const double* qconst,
+                              int32_t mem, int32_t device, uint32_t* out_ids, float* out_scores);
 int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int32_t device, uint32_t* out_ids,
                    float* out_scores);
 
-namespace {
-__global__ void k_synth_tokens(const double* __restrict__ cdf, uint32_t V, uint32_t seed, uint64_t begin,
-                               uint64_t count, uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = sl_corpus_token(cdf, V, seed, begin + i);
-}
-}  // namespace
 }  // namespace sl
 
 using namespace sl;
@@ -157,8 +152,16 @@ int32_t sl_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, int32_
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc((void**)&c->dflag, 4) != cudaSuccess) {
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+    SL_FAIL(SL_ECUDA, "sl_comm_init: stream / flag allocation failed");
+  }
   const int32_t rc = nccl_check(nccl().CommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
   if (rc != SL_OK) {
+    cudaFree(c->dflag);
+    cudaStreamDestroy(c->st);
     delete c;
     return rc;
   }
@@ -166,31 +169,23 @@ int32_t sl_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, int32_
   return SL_OK;
 }
 
+int32_t sl_retrieve_local(const sl_index* index, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                          uint32_t num_queries, uint32_t k, int32_t mem, uint64_t* out_keys, double* out_qconst) {
+  return retrieve_local_impl(index, q_offsets, q_tokens, num_queries, k, mem, out_keys, out_qconst);
+}
+
+int32_t sl_merge_candidates(const uint64_t* keys, uint32_t num_shards, uint32_t num_queries, uint32_t k,
+                            const double* qconst, int32_t mem, int32_t device, uint32_t* out_ids, float* out_scores) {
+  return merge_candidates_impl(keys, num_shards, num_queries, k, qconst, mem, device, out_ids, out_scores);
+}
+
 void sl_comm_destroy(sl_comm* c) {
   if (!c) return;
   if (c->comm) nccl().CommDestroy(c->comm);
+  cudaSetDevice(c->device);
+  if (c->dflag) cudaFree(c->dflag);
+  if (c->st) cudaStreamDestroy(c->st);
   delete c;
-}
-
-int32_t sl_synth_tokens_device(const double* cdf, uint32_t vocab, uint32_t seed, uint64_t begin, uint64_t count,
-                               int32_t cdf_mem, uint32_t* token_ids_dev) {
-  if (!cdf || !token_ids_dev || vocab == 0) SL_FAIL(SL_EINVAL, "sl_synth_tokens_device: bad arguments");
-  const double* dcdf = cdf;
-  double* tmp = nullptr;
-  if (cdf_mem == SL_MEM_HOST) {
-    SL_CUDA_TRY(cudaMalloc(&tmp, (uint64_t)vocab * 8));
-    SL_CUDA_TRY(cudaMemcpy(tmp, cdf, (uint64_t)vocab * 8, cudaMemcpyHostToDevice));
-    dcdf = tmp;
-  }
-  uint64_t blocks = (count + 255) / 256;
-  if (blocks > 148ull * 64) blocks = 148ull * 64;
-  if (blocks == 0) blocks = 1;
-  k_synth_tokens<<<(unsigned)blocks, 256>>>(dcdf, vocab, seed, begin, count, token_ids_dev); ++t_launches;
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (tmp) cudaFree(tmp);
-  if (e != cudaSuccess) SL_FAIL(SL_ECUDA, std::string("sl_synth_tokens_device: ") + cudaGetErrorString(e));
-  return SL_OK;
 }
 
 }  // extern "C"

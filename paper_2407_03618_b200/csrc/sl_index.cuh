@@ -12,6 +12,8 @@ struct sl_comm {
   int nranks = 1;
   int rank = 0;
   int device = 0;
+  cudaStream_t st = nullptr;  // the status agreement's stream (usable whatever state the caller's work is in)
+  int32_t* dflag = nullptr;   // device word for the status agreement
 };
 
 // SPEC.md [MODULE] index, SearchIndex: matrix (indptr/docids/values), stats, params,
@@ -96,4 +98,9 @@ int32_t load_index_from_host(const HostIndex& h, int device, float dense_min_den
 int32_t build_index_impl(const sl_build_desc* desc, sl_index** out);
 void free_index(sl_index* ix);
 int32_t nccl_check(ncclResult_t r, const char* what);
+// Status agreement before a data collective: every rank passes its own status (SL_OK or the
+// error it hit) and gets back its own error, or, when it was fine but a peer was not, the
+// largest peer status. A rank that fails before a collective calls this instead of returning
+// straight away, so its peers fail too instead of blocking in the collective.
+int32_t comm_agree(sl_comm* c, int32_t status);
 }  // namespace sl

@@ -1293,8 +1293,17 @@ __global__ void k_query_prep(const uint64_t* __restrict__ q_off, const uint32_t*
   }
 }
 
+// The split-threshold pre-test relies on denormal compares (tau_float: 0 > -denorm_min). A
+// build with flush-to-zero (-ftz=true / --use_fast_math) would silently drop exact-zero ties
+// across doc splits; nvcc defines no macro for it, so every stream checks it once on the device.
+__global__ void k_ftz_probe(const float* __restrict__ zero, uint32_t* __restrict__ out) {
+  const float x = zero[0];
+  out[0] = (x > tau_float(0x7FFFFFFFull << 32)) ? 1u : 0u;
+}
+
 struct StreamCache {
   int device = -1;
+  bool ftz = false;  // built with flush-to-zero: every call fails (k_ftz_probe)
   cudaStream_t st = nullptr;
   cudaEvent_t ev[4] = {};
 };
@@ -1307,6 +1316,17 @@ int32_t get_stream(int device, StreamCache** out) {
     SL_CUDA_TRY(cudaSetDevice(device));
     SL_CUDA_TRY(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
     for (auto& e : c.ev) SL_CUDA_TRY(cudaEventCreate(&e));
+    {
+      void* buf;
+      SL_CUDA_TRY(cudaMalloc(&buf, 8));
+      SL_CUDA_TRY(cudaMemset(buf, 0, 8));
+      k_ftz_probe<<<1, 1, 0, c.st>>>((const float*)buf, (uint32_t*)buf + 1); ++t_launches;
+      uint32_t ok = 0;
+      SL_CUDA_TRY(cudaMemcpyAsync(&ok, (uint32_t*)buf + 1, 4, cudaMemcpyDeviceToHost, c.st));
+      SL_CUDA_TRY(cudaStreamSynchronize(c.st));
+      cudaFree(buf);
+      c.ftz = !ok;
+    }
     c.device = device;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1314,6 +1334,8 @@ int32_t get_stream(int device, StreamCache** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
+  if (c.ftz) SL_FAIL(SL_EUNSUPPORTED, "libsparselex_b200 was compiled with flush-to-zero; the top-k threshold "
+                                      "pre-test needs denormal compares (rebuild without -ftz / --use_fast_math)");
   SL_CUDA_TRY(cudaSetDevice(device));
   *out = &c;
   return SL_OK;
@@ -1344,6 +1366,12 @@ int num_sms(int device) {
   static int cache[16] = {0};
   if (!cache[device]) cudaDeviceGetAttribute(&cache[device], cudaDevAttrMultiProcessorCount, device);
   return cache[device];
+}
+
+int cur_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return num_sms(dev);
 }
 
 int env_int(const char* name, int dflt) {
@@ -1435,11 +1463,11 @@ struct RankBufs {
 int32_t rank_full(const float* scores, uint32_t n, uint32_t k, uint32_t id_base, double qc, uint32_t* ids,
                   float* out, cudaStream_t st, const RankBufs& rb) {
   uint32_t *k0 = rb.k0, *v0 = rb.v0, *k1 = rb.k1, *v1 = rb.v1, *k2 = rb.k2, *v2 = rb.v2;
-  const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256 + 1, 148 * 32);
+  const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256 + 1, 32 * cur_sms());
   if (n) k_rank_keys<<<g, 256, 0, st>>>(scores, n, id_base, k0, v0); ++t_launches;
   const uint32_t *ks = k0, *vs = v0;
   if (n) SL_TRY(radix_sort_pairs(k0, v0, n, 32, k1, k2, v1, v2, st, &ks, &vs, 0, nullptr));
-  k_rank_emit<<<(unsigned)std::min<uint64_t>((k + 255) / 256, 148 * 32), 256, 0, st>>>(ks, vs, n, k, qc, ids, out); ++t_launches;
+  k_rank_emit<<<(unsigned)std::min<uint64_t>((k + 255) / 256, 32 * cur_sms()), 256, 0, st>>>(ks, vs, n, k, qc, ids, out); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   return SL_OK;
 }
@@ -1447,46 +1475,51 @@ int32_t rank_full(const float* scores, uint32_t n, uint32_t k, uint32_t id_base,
 }  // namespace
 
 // ------------------------------------------------------------------ entry points
-int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
-                      uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats) {
-  if (!ix) SL_FAIL(SL_EINVAL, "retrieve_batch: null index");
-  if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
-  if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "retrieve_batch: bad mem kind");
-  const bool dist = ix->comm != nullptr;  // any communicator, 1 rank included
-  const bool want_out = !dist || ix->comm->rank == 0;
-  if (B == 0) return SL_OK;
-  if (!q_offsets || !q_tokens) SL_FAIL(SL_EINVAL, "retrieve_batch: null query pointers");
-  if (want_out && (!out_ids || !out_scores)) SL_FAIL(SL_EINVAL, "retrieve_batch: null output pointers");
-  StreamCache* sc;
-  SL_TRY(get_stream(ix->device, &sc));
+namespace {
+// Host query offsets must be non-decreasing before anything is staged: the copy takes
+// q_offsets[B] tokens and the device kernels index the staged tokens with every offset.
+int32_t validate_host_offsets(const uint64_t* off, uint32_t B) {
+  for (uint32_t q = 0; q < B; ++q)
+    if (off[q + 1] < off[q]) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
+  return SL_OK;
+}
+
+// Candidate scratch of one chunk is [chunk][n_splits][C] keys; batches whose scratch would
+// exceed the budget (SL_CAND_MB, default 4096 MB) are scored in equal chunks of queries.
+// Results are identical for any chunking (a query's keys depend on the query only).
+int32_t chunk_size(const sl_index* ix, uint32_t B, uint32_t k, uint32_t* out) {
+  const uint64_t budget = (uint64_t)std::max(1, env_int("SL_CAND_MB", 4096)) << 20;
+  RunPlan p;
+  SL_TRY(plan_runs(ix, B, k, 1, &p));
+  uint64_t per_q = (uint64_t)p.n_splits * p.C * 8;
+  uint64_t bc = B;
+  if ((uint64_t)B * per_q > budget) {
+    bc = std::max<uint64_t>(1, budget / per_q);
+    SL_TRY(plan_runs(ix, (uint32_t)bc, k, 1, &p));  // fewer queries -> possibly more splits
+    per_q = (uint64_t)p.n_splits * p.C * 8;
+    bc = std::max<uint64_t>(1, std::min<uint64_t>(bc, budget / per_q));
+    const uint64_t nch = (B + bc - 1) / bc;
+    bc = (B + nch - 1) / nch;
+  }
+  *out = (uint32_t)bc;
+  return SL_OK;
+}
+
+// One chunk of queries through the fused scorer: validation and query constants
+// (k_query_prep), grouping by dense signature, k_score_runs (+ k_score_long for queries with
+// more than 32 gathered rows), then the per-query merge of the split candidates into the
+// final (ids, scores) or, for a multi-rank index, into this rank's top-k keys. d_off / qconst
+// point at the chunk's first query (offsets stay absolute into d_tok).
+int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, const uint32_t* d_tok, uint32_t B,
+                    uint32_t k, double* qconst, uint32_t* ids, float* scores, uint64_t* keys,
+                    unsigned long long* bytes, float* score_ms) {
   cudaStream_t st = sc->st;
   Scratch scr(st);
-
-  const uint64_t* d_off = q_offsets;
-  const uint32_t* d_tok = q_tokens;
-  if (mem == SL_MEM_HOST) {
-    const uint64_t ntok = q_offsets[B];
-    uint64_t* o;
-    uint32_t* t;
-    SL_TRY(scr.alloc(&o, (uint64_t)B + 1));
-    SL_TRY(scr.alloc(&t, ntok));
-    SL_CUDA_TRY(cudaMemcpyAsync(o, q_offsets, ((uint64_t)B + 1) * 8, cudaMemcpyHostToDevice, st));
-    if (ntok) SL_CUDA_TRY(cudaMemcpyAsync(t, q_tokens, ntok * 4, cudaMemcpyHostToDevice, st));
-    d_off = o;
-    d_tok = t;
-  }
-  const uint32_t launches0 = t_launches;
-  SL_CUDA_TRY(cudaEventRecord(sc->ev[0], st));
   const IndexView v = ix->view();
   const bool have_bounds = v.rowmax && (!ix->dense_rows || v.dmax) && (!ix->skip_rows || v.smax);
-  double* qconst;
   uint32_t* info;
-  unsigned long long* bytes;
-  SL_TRY(scr.alloc(&qconst, B));
   SL_TRY(scr.alloc(&info, 4));
-  SL_TRY(scr.alloc(&bytes, 1));
   SL_CUDA_TRY(cudaMemsetAsync(info, 0, 16, st));
-  SL_CUDA_TRY(cudaMemsetAsync(bytes, 0, 8, st));
   k_query_prep<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   uint32_t h_info[4];
@@ -1497,66 +1530,13 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   const uint32_t qmax = std::max(1u, h_info[1]);
   const uint32_t n_long = h_info[2];   // queries with > 32 gathered rows -> k_score_long
   const uint32_t B_short = B - n_long;  // they sort after every other query
-  if (k > kMaxK) {
-    // SPEC top_k for large k (up to |C|): dense score vector per query + full stable ranking
-    if (dist) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: k > 4096 is not supported across ranks");
-    uint32_t* ids_dev = out_ids;
-    float* sc_dev = out_scores;
-    if (mem == SL_MEM_HOST) {
-      SL_TRY(scr.alloc(&ids_dev, (uint64_t)B * k));
-      SL_TRY(scr.alloc(&sc_dev, (uint64_t)B * k));
-    }
-    float* vec;
-    double* zero;
-    uint32_t* iota;
-    SL_TRY(scr.alloc(&vec, std::max(1u, ix->N)));
-    SL_TRY(scr.alloc(&zero, B));
-    SL_TRY(scr.alloc(&iota, B));
-    SL_CUDA_TRY(cudaMemsetAsync(zero, 0, (uint64_t)B * 8, st));
-    std::vector<uint32_t> h_iota(B);
-    for (uint32_t i = 0; i < B; ++i) h_iota[i] = i;
-    SL_CUDA_TRY(cudaMemcpyAsync(iota, h_iota.data(), (uint64_t)B * 4, cudaMemcpyHostToDevice, st));
-    std::vector<double> h_qc(B);
-    SL_CUDA_TRY(cudaMemcpyAsync(h_qc.data(), qconst, (uint64_t)B * 8, cudaMemcpyDeviceToHost, st));
-    SL_CUDA_TRY(cudaStreamSynchronize(st));
-    RunArgs ra{};
-    ra.q_off = d_off;
-    ra.q_tok = d_tok;
-    ra.qconst = zero;  // rank by the accumulated score; the constant is added on output
-    ra.perm = iota;
-    ra.k = 1;
-    ra.C = kept_capacity(1);
-    ra.n_splits = std::max(1u, ix->num_tiles);
-    ra.dense_out = vec;
-    const size_t lsm = long_smem_bytes(qmax);
-    if (lsm > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: query too long for the device scorer");
-    SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-    RankBufs rbuf;
-    SL_TRY(rbuf.alloc(scr, std::max(1u, ix->N)));
-    SL_CUDA_TRY(cudaEventRecord(sc->ev[1], st));
-    for (uint32_t b = 0; b < B; ++b) {
-      k_score_long<GM_DENSE><<<ra.n_splits, NT, lsm, st>>>(v, ra, b, 1, qmax); ++t_launches;
-      SL_TRY(rank_full(vec, ix->N, k, ix->doc_base, h_qc[b], ids_dev + (uint64_t)b * k, sc_dev + (uint64_t)b * k, st,
-                       rbuf));
-    }
-    SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
-    SL_CUDA_TRY(cudaEventRecord(sc->ev[3], st));
-    if (mem == SL_MEM_HOST) {
-      SL_CUDA_TRY(cudaMemcpyAsync(out_ids, ids_dev, (uint64_t)B * k * 4, cudaMemcpyDeviceToHost, st));
-      SL_CUDA_TRY(cudaMemcpyAsync(out_scores, sc_dev, (uint64_t)B * k * 4, cudaMemcpyDeviceToHost, st));
-    }
-    SL_CUDA_TRY(cudaStreamSynchronize(st));
-    if (stats) std::memset(stats, 0, sizeof(*stats));
-    return SL_OK;
-  }
   RunPlan plan;
   SL_TRY(plan_runs(ix, B, k, qmax, &plan));
   // group queries by dense signature: sort by signature hash, cut runs of <= R identical ones
   int32_t* qdense;
-  uint32_t *nden, *hk, *hv, *k0, *k1, *v0, *v1, *run_begin, *n_runs;
+  uint32_t *nden, *hk, *hv, *k0, *k1, *v0, *v1, *run_begin, *n_runs, *ngath;
   SL_TRY(scr.alloc(&qdense, (uint64_t)B * qmax));
   SL_TRY(scr.alloc(&nden, B));
-  uint32_t* ngath;
   SL_TRY(scr.alloc(&ngath, B));
   SL_TRY(scr.alloc(&hk, B));
   SL_TRY(scr.alloc(&hv, B));
@@ -1615,7 +1595,127 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   }
   SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
+  const uint64_t qstride = (uint64_t)plan.n_splits * plan.C;
+  if (keys) {
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, keys, st,
+                        ra.gtau));
+  } else {
+    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids, scores, nullptr, st,
+                        ra.gtau));
+  }
+  if (score_ms) {
+    float ms = 0.f;
+    SL_CUDA_TRY(cudaEventSynchronize(sc->ev[2]));
+    SL_CUDA_TRY(cudaEventElapsedTime(&ms, sc->ev[1], sc->ev[2]));
+    *score_ms += ms;
+  }
+  return SL_OK;
+}
 
+// Rank-local part of retrieval for a batch already on the device: every chunk scored and
+// merged into this rank's keys (keys != nullptr) or straight into the final results.
+int32_t local_topk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, const uint32_t* d_tok, uint32_t B,
+                   uint32_t k, double* qconst, uint32_t* ids, float* scores, uint64_t* keys,
+                   unsigned long long* bytes, float* score_ms) {
+  uint32_t bc = B;
+  SL_TRY(chunk_size(ix, B, k, &bc));
+  for (uint32_t b0 = 0; b0 < B; b0 += bc) {
+    const uint32_t n = std::min(bc, B - b0);
+    const uint64_t o = (uint64_t)b0 * k;
+    SL_TRY(score_chunk(ix, sc, d_off + b0, d_tok, n, k, qconst + b0, ids ? ids + o : nullptr,
+                       scores ? scores + o : nullptr, keys ? keys + o : nullptr, bytes, score_ms));
+  }
+  return SL_OK;
+}
+
+// k > kMaxK (SPEC top_k up to |C|): dense score vector per query + full stable ranking; single rank.
+int32_t retrieve_large_k(const sl_index* ix, StreamCache* sc, Scratch& scr, const uint64_t* d_off,
+                         const uint32_t* d_tok, uint32_t B, uint32_t k, uint32_t* ids_dev, float* sc_dev) {
+  cudaStream_t st = sc->st;
+  const IndexView v = ix->view();
+  double* qconst;
+  uint32_t* info;
+  SL_TRY(scr.alloc(&qconst, B));
+  SL_TRY(scr.alloc(&info, 4));
+  SL_CUDA_TRY(cudaMemsetAsync(info, 0, 16, st));
+  k_query_prep<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, nullptr); ++t_launches;
+  uint32_t h_info[4];
+  SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_info[0] & 2u) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
+  if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
+  const uint32_t qmax = std::max(1u, h_info[1]);
+  float* vec;
+  double* zero;
+  uint32_t* iota;
+  SL_TRY(scr.alloc(&vec, std::max(1u, ix->N)));
+  SL_TRY(scr.alloc(&zero, B));
+  SL_TRY(scr.alloc(&iota, B));
+  SL_CUDA_TRY(cudaMemsetAsync(zero, 0, (uint64_t)B * 8, st));
+  std::vector<uint32_t> h_iota(B);
+  for (uint32_t i = 0; i < B; ++i) h_iota[i] = i;
+  SL_CUDA_TRY(cudaMemcpyAsync(iota, h_iota.data(), (uint64_t)B * 4, cudaMemcpyHostToDevice, st));
+  std::vector<double> h_qc(B);
+  SL_CUDA_TRY(cudaMemcpyAsync(h_qc.data(), qconst, (uint64_t)B * 8, cudaMemcpyDeviceToHost, st));
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  RunArgs ra{};
+  ra.q_off = d_off;
+  ra.q_tok = d_tok;
+  ra.qconst = zero;  // rank by the accumulated score; the constant is added on output
+  ra.perm = iota;
+  ra.k = 1;
+  ra.C = kept_capacity(1);
+  ra.n_splits = std::max(1u, ix->num_tiles);
+  ra.dense_out = vec;
+  const size_t lsm = long_smem_bytes(qmax);
+  if (lsm > 227 * 1024) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: query too long for the device scorer");
+  SL_CUDA_TRY(cudaFuncSetAttribute(k_score_long<GM_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+  RankBufs rbuf;
+  SL_TRY(rbuf.alloc(scr, std::max(1u, ix->N)));
+  for (uint32_t b = 0; b < B; ++b) {
+    k_score_long<GM_DENSE><<<ra.n_splits, NT, lsm, st>>>(v, ra, b, 1, qmax); ++t_launches;
+    SL_TRY(rank_full(vec, ix->N, k, ix->doc_base, h_qc[b], ids_dev + (uint64_t)b * k, sc_dev + (uint64_t)b * k, st,
+                     rbuf));
+  }
+  return SL_OK;
+}
+
+// Stage host queries on the device (validated first) or take device pointers as they are.
+int32_t stage_queries(Scratch& scr, cudaStream_t st, const uint64_t* q_offsets, const uint32_t* q_tokens,
+                      uint32_t B, int32_t mem, const uint64_t** d_off, const uint32_t** d_tok) {
+  *d_off = q_offsets;
+  *d_tok = q_tokens;
+  if (mem != SL_MEM_HOST) return SL_OK;
+  SL_TRY(validate_host_offsets(q_offsets, B));
+  const uint64_t ntok = q_offsets[B];
+  uint64_t* o;
+  uint32_t* t;
+  SL_TRY(scr.alloc(&o, (uint64_t)B + 1));
+  SL_TRY(scr.alloc(&t, ntok));
+  SL_CUDA_TRY(cudaMemcpyAsync(o, q_offsets, ((uint64_t)B + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (ntok) SL_CUDA_TRY(cudaMemcpyAsync(t, q_tokens, ntok * 4, cudaMemcpyHostToDevice, st));
+  *d_off = o;
+  *d_tok = t;
+  return SL_OK;
+}
+
+// Rank-local retrieval + (multi-rank) gather of the G x B x k keys on rank 0 and the final
+// merge there. *agreed is set once this rank has entered the status agreement that precedes
+// the gather (retrieve_impl's caller-facing wrapper agrees on the failure otherwise).
+int32_t retrieve_body(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
+                      uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats,
+                      bool* agreed) {
+  const bool dist = ix->comm != nullptr;  // any communicator, 1 rank included
+  const bool want_out = !dist || ix->comm->rank == 0;
+  StreamCache* sc;
+  SL_TRY(get_stream(ix->device, &sc));
+  cudaStream_t st = sc->st;
+  Scratch scr(st);
+  const uint64_t* d_off;
+  const uint32_t* d_tok;
+  SL_TRY(stage_queries(scr, st, q_offsets, q_tokens, B, mem, &d_off, &d_tok));
+  const uint32_t launches0 = t_launches;
+  SL_CUDA_TRY(cudaEventRecord(sc->ev[0], st));
   uint32_t* ids_dev = nullptr;
   float* sc_dev = nullptr;
   if (want_out) {
@@ -1627,29 +1727,48 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
       SL_TRY(scr.alloc(&sc_dev, (uint64_t)B * k));
     }
   }
-  const uint64_t qstride = (uint64_t)plan.n_splits * plan.C;
-  if (!dist) {
-    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids_dev, sc_dev, nullptr, st,
-                        ra.gtau));
+  float score_ms = 0.f, merge_ms = 0.f;
+  unsigned long long* bytes;
+  SL_TRY(scr.alloc(&bytes, 1));
+  SL_CUDA_TRY(cudaMemsetAsync(bytes, 0, 8, st));
+  if (k > kMaxK) {
+    if (dist) SL_FAIL(SL_EUNSUPPORTED, "retrieve_batch: k > 4096 is not supported across ranks");
+    SL_TRY(retrieve_large_k(ix, sc, scr, d_off, d_tok, B, k, ids_dev, sc_dev));
   } else {
-    // local merge -> keys, gather the G x k candidates on rank 0 (NCCL), merge there
-    const sl_comm* cm = ix->comm;
-    uint64_t* local;
-    SL_TRY(scr.alloc(&local, (uint64_t)B * k));
-    SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, local, st,
-                        ra.gtau));
-    uint64_t* gathered = nullptr;
-    if (cm->rank == 0) SL_TRY(scr.alloc(&gathered, (uint64_t)cm->nranks * B * k));
-    const size_t cnt = (size_t)B * k;
-    SL_TRY(nccl_check(nccl().GroupStart(), "ncclGroupStart"));
-    if (cm->rank == 0) {
-      for (int r = 0; r < cm->nranks; ++r)
-        SL_TRY(nccl_check(nccl().Recv(gathered + (uint64_t)r * cnt, cnt, ncclUint64, r, cm->comm, st), "ncclRecv"));
+    double* qconst;
+    SL_TRY(scr.alloc(&qconst, B));
+    if (!dist) {
+      SL_TRY(local_topk(ix, sc, d_off, d_tok, B, k, qconst, ids_dev, sc_dev, nullptr, bytes,
+                        stats ? &score_ms : nullptr));
+    } else {
+      // local top-k keys -> gather the G x k candidates of every query on rank 0 (NCCL) -> merge there
+      sl_comm* cm = ix->comm;
+      uint64_t* local;
+      SL_TRY(scr.alloc(&local, (uint64_t)B * k));
+      SL_TRY(local_topk(ix, sc, d_off, d_tok, B, k, qconst, nullptr, nullptr, local, bytes,
+                        stats ? &score_ms : nullptr));
+      uint64_t* gathered = nullptr;
+      if (cm->rank == 0) SL_TRY(scr.alloc(&gathered, (uint64_t)cm->nranks * B * k));
+      SL_CUDA_TRY(cudaStreamSynchronize(st));
+      *agreed = true;
+      SL_TRY(comm_agree(cm, SL_OK));
+      SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
+      const size_t cnt = (size_t)B * k;
+      SL_TRY(nccl_check(nccl().GroupStart(), "ncclGroupStart"));
+      if (cm->rank == 0) {
+        for (int r = 0; r < cm->nranks; ++r)
+          SL_TRY(nccl_check(nccl().Recv(gathered + (uint64_t)r * cnt, cnt, ncclUint64, r, cm->comm, st), "ncclRecv"));
+      }
+      SL_TRY(nccl_check(nccl().Send(local, cnt, ncclUint64, 0, cm->comm, st), "ncclSend"));
+      SL_TRY(nccl_check(nccl().GroupEnd(), "ncclGroupEnd"));
+      if (cm->rank == 0)
+        SL_TRY(launch_merge(gathered, B, (uint32_t)cm->nranks, k, cnt, k, k, qconst, ids_dev, sc_dev, nullptr, st));
+      SL_CUDA_TRY(cudaEventRecord(sc->ev[3], st));
+      if (stats) {
+        SL_CUDA_TRY(cudaEventSynchronize(sc->ev[3]));
+        SL_CUDA_TRY(cudaEventElapsedTime(&merge_ms, sc->ev[2], sc->ev[3]));
+      }
     }
-    SL_TRY(nccl_check(nccl().Send(local, cnt, ncclUint64, 0, cm->comm, st), "ncclSend"));
-    SL_TRY(nccl_check(nccl().GroupEnd(), "ncclGroupEnd"));
-    if (cm->rank == 0)
-      SL_TRY(launch_merge(gathered, B, (uint32_t)cm->nranks, k, cnt, k, k, qconst, ids_dev, sc_dev, nullptr, st));
   }
   SL_CUDA_TRY(cudaEventRecord(sc->ev[3], st));
   if (want_out && mem == SL_MEM_HOST) {
@@ -1658,20 +1777,110 @@ int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint3
   }
   SL_CUDA_TRY(cudaStreamSynchronize(st));
   if (stats) {
-    float a = 0, b = 0, c = 0;
+    float a = 0;
     cudaEventElapsedTime(&a, sc->ev[0], sc->ev[3]);
-    cudaEventElapsedTime(&b, sc->ev[1], sc->ev[2]);
-    cudaEventElapsedTime(&c, sc->ev[2], sc->ev[3]);
     unsigned long long hb = 0;
-    cudaMemcpy(&hb, bytes, 8, cudaMemcpyDeviceToHost);
+    SL_CUDA_TRY(cudaMemcpy(&hb, bytes, 8, cudaMemcpyDeviceToHost));
+    std::memset(stats, 0, sizeof(*stats));
     stats->total_ms = a;
-    stats->score_kernel_ms = b;
-    stats->merge_ms = c;
+    stats->score_kernel_ms = score_ms;
+    stats->merge_ms = merge_ms;
     stats->posting_bytes = hb;
     stats->scorevec_bytes = 4ull * ix->N * B;
-    stats->unique_posting_bytes = 0;
     stats->kernels_launched = t_launches - launches0;  // every kernel of this call
   }
+  return SL_OK;
+}
+}  // namespace
+
+int32_t retrieve_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
+                      uint32_t k, int32_t mem, uint32_t* out_ids, float* out_scores, sl_retrieve_stats* stats) {
+  if (!ix) SL_FAIL(SL_EINVAL, "retrieve_batch: null index");
+  if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
+  if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "retrieve_batch: bad mem kind");
+  const bool dist = ix->comm != nullptr;
+  const bool want_out = !dist || ix->comm->rank == 0;
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (B == 0) return SL_OK;
+  if (!q_offsets || !q_tokens) SL_FAIL(SL_EINVAL, "retrieve_batch: null query pointers");
+  if (want_out && (!out_ids || !out_scores)) SL_FAIL(SL_EINVAL, "retrieve_batch: null output pointers");
+  bool agreed = false;
+  int32_t rc = retrieve_body(ix, q_offsets, q_tokens, B, k, mem, out_ids, out_scores, stats, &agreed);
+  // a rank that failed before the candidate gather still takes part in the status agreement,
+  // so its peers return an error instead of waiting in ncclRecv / ncclSend
+  if (rc != SL_OK && dist && !agreed) rc = comm_agree(ix->comm, rc);
+  return rc;
+}
+
+// Multi-rank building blocks (include/sparselex_b200.h sl_retrieve_local / sl_merge_candidates).
+int32_t retrieve_local_impl(const sl_index* ix, const uint64_t* q_offsets, const uint32_t* q_tokens, uint32_t B,
+                            uint32_t k, int32_t mem, uint64_t* out_keys, double* out_qconst) {
+  if (!ix) SL_FAIL(SL_EINVAL, "retrieve_local: null index");
+  if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
+  if (k > kMaxK) SL_FAIL(SL_EUNSUPPORTED, "retrieve_local: k > 4096 has no candidate form");
+  if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "retrieve_local: bad mem kind");
+  if (B == 0) return SL_OK;
+  if (!q_offsets || !q_tokens || !out_keys || !out_qconst) SL_FAIL(SL_EINVAL, "retrieve_local: null argument");
+  StreamCache* sc;
+  SL_TRY(get_stream(ix->device, &sc));
+  cudaStream_t st = sc->st;
+  Scratch scr(st);
+  const uint64_t* d_off;
+  const uint32_t* d_tok;
+  SL_TRY(stage_queries(scr, st, q_offsets, q_tokens, B, mem, &d_off, &d_tok));
+  uint64_t* keys = out_keys;
+  double* qconst = out_qconst;
+  if (mem == SL_MEM_HOST) {
+    SL_TRY(scr.alloc(&keys, (uint64_t)B * k));
+    SL_TRY(scr.alloc(&qconst, B));
+  }
+  SL_TRY(local_topk(ix, sc, d_off, d_tok, B, k, qconst, nullptr, nullptr, keys, nullptr, nullptr));
+  if (mem == SL_MEM_HOST) {
+    SL_CUDA_TRY(cudaMemcpyAsync(out_keys, keys, (uint64_t)B * k * 8, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(out_qconst, qconst, (uint64_t)B * 8, cudaMemcpyDeviceToHost, st));
+  }
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
+  return SL_OK;
+}
+
+int32_t merge_candidates_impl(const uint64_t* keys, uint32_t G, uint32_t B, uint32_t k, const double* qconst,
+                              int32_t mem, int32_t device, uint32_t* out_ids, float* out_scores) {
+  if (k == 0) SL_FAIL(SL_EINVAL, "top_k: k must be >= 1");
+  if (k > kMaxK) SL_FAIL(SL_EUNSUPPORTED, "merge_candidates: k > 4096 has no candidate form");
+  if (G == 0) SL_FAIL(SL_EINVAL, "merge_candidates: no shards");
+  if (mem != SL_MEM_HOST && mem != SL_MEM_DEVICE) SL_FAIL(SL_EINVAL, "merge_candidates: bad mem kind");
+  if (B == 0) return SL_OK;
+  if (!keys || !qconst || !out_ids || !out_scores) SL_FAIL(SL_EINVAL, "merge_candidates: null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    SL_FAIL(SL_ECUDA, "merge_candidates: no CUDA device available (there is no CPU fallback)");
+  StreamCache* sc;
+  SL_TRY(get_stream(device, &sc));
+  cudaStream_t st = sc->st;
+  Scratch scr(st);
+  const uint64_t cnt = (uint64_t)B * k;
+  const uint64_t* d_keys = keys;
+  const double* d_qc = qconst;
+  uint32_t* ids = out_ids;
+  float* scs = out_scores;
+  if (mem == SL_MEM_HOST) {
+    uint64_t* kk;
+    double* qq;
+    SL_TRY(scr.alloc(&kk, cnt * G));
+    SL_TRY(scr.alloc(&qq, B));
+    SL_TRY(scr.alloc(&ids, cnt));
+    SL_TRY(scr.alloc(&scs, cnt));
+    SL_CUDA_TRY(cudaMemcpyAsync(kk, keys, cnt * G * 8, cudaMemcpyHostToDevice, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(qq, qconst, (uint64_t)B * 8, cudaMemcpyHostToDevice, st));
+    d_keys = kk;
+    d_qc = qq;
+  }
+  SL_TRY(launch_merge(d_keys, B, G, k, cnt, k, k, d_qc, ids, scs, nullptr, st));
+  if (mem == SL_MEM_HOST) {
+    SL_CUDA_TRY(cudaMemcpyAsync(out_ids, ids, cnt * 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(out_scores, scs, cnt * 4, cudaMemcpyDeviceToHost, st));
+  }
+  SL_CUDA_TRY(cudaStreamSynchronize(st));
   return SL_OK;
 }
 
@@ -1765,7 +1974,7 @@ int32_t top_k_impl(const float* scores, uint32_t n, uint32_t k, int32_t mem, int
   }
   const uint32_t C = std::max(512u, kept_capacity(k));
   const uint32_t n_tiles = std::max(1u, (n + TILE - 1) / TILE);
-  const uint32_t n_splits = std::min<uint32_t>(n_tiles, 148 * 4);
+  const uint32_t n_splits = std::min<uint32_t>(n_tiles, 4 * num_sms(device));
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)n_splits * C));
   if (n) {

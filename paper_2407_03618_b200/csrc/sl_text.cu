@@ -1293,8 +1293,17 @@ __global__ void k_add_u64(const uint64_t* __restrict__ in, uint64_t n, uint64_t 
 }
 
 // ------------------------------------------------------------------ host side
+inline int text_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] > 0 ? cache[dev] : 1;
+}
+
 inline unsigned grid_for(uint64_t n, int per = 256) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, 148ull * 64));
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, 64ull * text_sms()));
 }
 
 struct TScratch {

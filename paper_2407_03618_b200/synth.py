@@ -86,6 +86,15 @@ def tokens_host(cfg: SynthConfig, cdf: np.ndarray, begin: int, count: int, threa
     return out
 
 
+def tokens_device(cfg: SynthConfig, cdf: np.ndarray, begin: int, count: int, out_ptr: int) -> None:
+    """Corpus tokens [begin, begin+count) generated on the current CUDA device into out_ptr
+    (bit-identical to tokens_host; libsl_synth's device generator, not the product library)."""
+    e = _lib.synth_lib().sl_synth_tokens_device(_ptr(cdf), cfg.vocab, cfg.corpus_seed, int(begin), int(count), 0,
+                                                out_ptr)
+    if e != 0:
+        raise RuntimeError(f"sl_synth_tokens_device failed (cudaError {e})")
+
+
 def queries(cfg: SynthConfig, cdf: np.ndarray, q_begin: int = 0, nq: int | None = None):
     nq = cfg.n_queries - q_begin if nq is None else nq
     off = np.empty(nq + 1, dtype=np.uint64)

@@ -17,8 +17,7 @@ def main():
     cdf = synth.zipf_cdf(cfg)
     off = synth.doc_offsets(cfg)
     tok = torch.empty(int(off[-1]), dtype=torch.uint32, device="cuda")
-    check(lib().sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, 0, int(off[-1]), SL_MEM_HOST,
-                                       tok.data_ptr()))
+    synth.tokens_device(cfg, cdf, 0, int(off[-1]), tok.data_ptr())
     doff = torch.from_numpy(off).cuda()
     for _ in range(2):
         idx = build_index(doff, tok, cfg.vocab, BM25Params())

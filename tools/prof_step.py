@@ -25,7 +25,7 @@ def main():
     off = synth.doc_offsets(cfg)
     T = int(off[-1])
     tok = torch.empty(T, dtype=torch.uint32, device="cuda")
-    check(lib().sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, 0, T, SL_MEM_HOST, tok.data_ptr()))
+    synth.tokens_device(cfg, cdf, 0, T, tok.data_ptr())
     idx = build_index(torch.from_numpy(off).cuda(), tok, cfg.vocab, BM25Params(), dense_min_density=a.dense_density)
     del tok
     qoff, qtok = synth.queries(cfg, cdf, 0, a.queries or None)

@@ -35,8 +35,7 @@ def main():
         base = 0
     T = int(off[-1])
     tok = torch.empty(T, dtype=torch.uint32, device="cuda")
-    check(lib().sl_synth_tokens_device(cdf.ctypes.data, cfg.vocab, cfg.corpus_seed, base, T, SL_MEM_HOST,
-                                       tok.data_ptr()))
+    synth.tokens_device(cfg, cdf, base, T, tok.data_ptr())
     idx = build_index(torch.from_numpy(off).cuda(), tok, cfg.vocab, BM25Params(), dense_min_density=a.dense_density)
     inf = idx.info()
     print(json.dumps({"build_ms": inf.build_ms, "dense_rows": inf.dense_rows, "skip_rows": inf.skip_rows,
