@@ -18,15 +18,19 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
+#include "sparselex/bm25.hpp"
 #include "sparselex_b200.h"
 
 namespace sparselex::b200 {
 
-// bm25.hpp:16-23 (same order)
-enum class Variant : int32_t { robertson = 0, atire = 1, lucene = 2, bm25l = 3, bm25plus = 4, tfldp = 5 };
+// bm25.hpp:16-47: the reference's own scoring types (include/sparselex/bm25.hpp), implemented by
+// this library — a BM25Params built by reference code is passed straight through.
+using sparselex::BM25Params;
+using sparselex::Variant;
 
 inline void check(int32_t status) {
   if (status == SL_OK) return;
@@ -35,23 +39,7 @@ inline void check(int32_t status) {
   throw std::runtime_error(std::string(sl_status_string(status)) + ": " + msg);
 }
 
-// bm25.hpp:31-47
-struct BM25Params {
-  Variant variant = Variant::lucene;
-  double k1 = 1.5;
-  double b = 0.75;
-  double delta = 0.0;
-
-  static double default_delta(Variant v) { return sl_default_delta(static_cast<int32_t>(v)); }
-  static BM25Params for_variant(Variant v, double k1 = 1.5, double b = 0.75) {
-    return BM25Params{v, k1, b, default_delta(v)};
-  }
-  sl_params c() const { return sl_params{static_cast<int32_t>(variant), k1, b, delta}; }
-  void validate() const {
-    const sl_params p = c();
-    check(sl_params_validate(&p));
-  }
-};
+inline sl_params to_c(const BM25Params& p) { return sl_params{static_cast<int32_t>(p.variant), p.k1, p.b, p.delta}; }
 
 // A tokenised corpus: document d holds token_ids[doc_offsets[d] .. doc_offsets[d+1]).
 struct TokenCorpus {
@@ -68,9 +56,11 @@ struct BuildOptions {
   sl_comm* comm = nullptr;        // NCCL communicator for a document-sharded corpus
 };
 
-// SPEC retrieval QueryResult: doc indices with exact B(Q,D) scores, descending.
+// SPEC retrieval QueryResult: doc indices with exact B(Q,D) scores, descending;
+// external_ids for a text index.
 struct QueryResult {
   std::vector<uint32_t> doc_indices;
+  std::vector<std::string> external_ids;
   std::vector<float> scores;
 };
 
@@ -136,7 +126,10 @@ class SearchIndex {
 };
 
 inline SearchIndex build_index(const TokenCorpus& corpus, const BM25Params& params, const BuildOptions& opt = {}) {
-  if (corpus.doc_offsets.empty()) throw std::invalid_argument("build_index: empty corpus");
+  if (corpus.doc_offsets.size() < 2) throw std::invalid_argument("build_index: empty corpus");
+  // the library copies tokens [doc_offsets[0], doc_offsets[N]) from the host pointer
+  if (corpus.doc_offsets.back() > corpus.token_ids.size() || corpus.doc_offsets.front() > corpus.doc_offsets.back())
+    throw std::invalid_argument("build_index: doc offsets exceed the token array");
   sl_build_desc d{};
   d.doc_offsets = corpus.doc_offsets.data();
   d.token_ids = corpus.token_ids.data();
@@ -144,7 +137,7 @@ inline SearchIndex build_index(const TokenCorpus& corpus, const BM25Params& para
   d.vocab_size = corpus.vocab_size;
   d.doc_base = opt.doc_base;
   d.mem = SL_MEM_HOST;
-  d.params = params.c();
+  d.params = to_c(params);
   d.device = opt.device;
   d.keep_tf = opt.keep_tf ? 1 : 0;
   d.dense_min_density = opt.dense_min_density;
@@ -361,27 +354,156 @@ inline std::vector<std::string> stem_english(const std::vector<std::string>& wor
   return r;
 }
 
-// SPEC build_index(corpus texts, params, tokenizer_config) -> index + vocabulary
-struct TextIndex {
-  SearchIndex index;
-  Vocabulary vocab;
-  TokenizerConfig config;
+// ---------------------------------------------------------------- text-level SearchIndex
+// SPEC SearchIndex with vocabulary, tokenizer config and external document ids,
+// move-only RAII over the library's sl_text_index.
+class TextIndex {
+ public:
+  TextIndex() = default;
+  explicit TextIndex(sl_text_index* h) : h_(h) {}
+  TextIndex(TextIndex&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  TextIndex& operator=(TextIndex&& o) noexcept {
+    if (this != &o) {
+      if (h_) sl_text_index_destroy(h_);
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  TextIndex(const TextIndex&) = delete;
+  TextIndex& operator=(const TextIndex&) = delete;
+  ~TextIndex() {
+    if (h_) sl_text_index_destroy(h_);
+  }
+  sl_text_index* handle() const {
+    if (!h_) throw std::invalid_argument("TextIndex: empty handle");
+    return h_;
+  }
+  uint32_t num_docs() const {
+    uint32_t n = 0;
+    check(sl_text_index_num_docs(handle(), &n));
+    return n;
+  }
+  std::string external_id(uint32_t doc) const {
+    const char* p = nullptr;
+    uint64_t n = 0;
+    check(sl_text_index_external_id(handle(), doc, &p, &n));
+    return std::string(p, n);
+  }
+  std::vector<std::string> doc_external_ids() const {
+    std::vector<std::string> out(num_docs());
+    for (uint32_t d = 0; d < out.size(); ++d) out[d] = external_id(d);
+    return out;
+  }
+  // vocabulary tokens in id order (vocabulary.hpp:13-48)
+  std::vector<std::string> vocab_tokens() const {
+    sl_vocab* v = sl_text_index_vocab(handle());
+    uint32_t n = 0;
+    check(sl_vocab_size(v, &n));
+    std::vector<uint64_t> off(n + 1ull);
+    uint64_t total = 0;
+    check(sl_vocab_export(v, nullptr, nullptr, &total));
+    std::string bytes(total, '\0');
+    check(sl_vocab_export(v, off.data(), bytes.data(), &total));
+    std::vector<std::string> out(n);
+    for (uint32_t i = 0; i < n; ++i) out[i] = bytes.substr(off[i], off[i + 1] - off[i]);
+    return out;
+  }
+  TokenizerConfig tokenizer_config() const {
+    sl_tokenizer_config c{};
+    check(sl_text_index_config(handle(), &c));
+    TokenizerConfig t;
+    t.lowercase = c.lowercase != 0;
+    t.stemmer = static_cast<StemmerKind>(c.stemmer);
+    std::string cur;
+    for (uint64_t i = 0; i <= c.stopwords_bytes; ++i) {
+      if (i == c.stopwords_bytes || c.stopwords[i] == '\n') {
+        if (!cur.empty()) t.stopwords.push_back(cur);
+        cur.clear();
+      } else {
+        cur += c.stopwords[i];
+      }
+    }
+    return t;
+  }
+  // token-id level view of the same index (score_query / export_arrays); owned by this TextIndex
+  const sl_index* index() const { return sl_text_index_index(handle()); }
+
+ private:
+  sl_text_index* h_ = nullptr;
 };
+
+// SPEC build_index(corpus: sequence of (external_id, text), params, tokenizer_config) SPEC.md:201-209;
+// throws std::invalid_argument on an empty corpus, a degenerate corpus or duplicate external ids
+inline TextIndex build_text_index(const std::vector<std::pair<std::string, std::string>>& corpus,
+                                  const BM25Params& params, const TokenizerConfig& cfg, int device = 0,
+                                  float dense_min_density = 0.f) {
+  std::string ids, text;
+  std::vector<uint64_t> ioff{0}, toff{0};
+  for (const auto& [id, t] : corpus) {
+    ids += id;
+    ioff.push_back(ids.size());
+    text += t;
+    toff.push_back(text.size());
+  }
+  if (ids.empty()) ids.push_back('\0');
+  if (text.empty()) text.push_back('\0');
+  detail::CfgC c(cfg);
+  const sl_params p = to_c(params);
+  sl_text_index* h = nullptr;
+  check(sl_text_index_build(ids.data(), ioff.data(), text.data(), toff.data(), static_cast<uint32_t>(corpus.size()),
+                            &p, &c.c, device, dense_min_density, &h));
+  return TextIndex(h);
+}
+// documents without ids of their own get their position ("0", "1", ...) as external id
 inline TextIndex build_text_index(const std::vector<std::string>& docs, const BM25Params& params,
                                   const TokenizerConfig& cfg, int device = 0) {
-  if (docs.empty()) throw std::invalid_argument("build_index: empty corpus");
-  Vocabulary v(device);
-  TokenizedCorpus tc = tokenize_build(docs, cfg, v);
-  if (tc.token_ids.empty()) throw std::invalid_argument("build_index: degenerate corpus");
-  BuildOptions o;
-  o.device = device;
-  SearchIndex ix = build_index({tc.doc_offsets, tc.token_ids, v.size()}, params, o);
-  return TextIndex{std::move(ix), std::move(v), cfg};
+  std::vector<std::pair<std::string, std::string>> corpus;
+  corpus.reserve(docs.size());
+  for (size_t i = 0; i < docs.size(); ++i) corpus.emplace_back(std::to_string(i), docs[i]);
+  return build_text_index(corpus, params, cfg, device);
 }
-// SPEC retrieve(index, text, k, ordered): frozen vocabulary, OOV tokens dropped
-inline QueryResult retrieve(TextIndex& t, const std::string& text, uint32_t k, bool ordered = true) {
-  TokenizedCorpus q = tokenize_query({text}, t.config, t.vocab);
-  return retrieve(t.index, q.doc(0), k, ordered);
+
+// SPEC save_index / load_index for a text index
+inline void save_index(const TextIndex& t, const std::string& directory) {
+  check(sl_text_index_save(t.handle(), directory.c_str()));
+}
+inline TextIndex load_text_index(const std::string& directory, int device = 0) {
+  sl_text_index* h = nullptr;
+  check(sl_text_index_load(directory.c_str(), device, 0.f, &h));
+  return TextIndex(h);
+}
+
+// SPEC retrieve_batch(index, queries, k, ordered, workers) over query texts
+inline std::vector<QueryResult> retrieve_batch(const TextIndex& t, const std::vector<std::string>& queries,
+                                               uint32_t k, bool ordered = true, int workers = 1) {
+  if (workers < 1) throw std::invalid_argument("retrieve_batch: workers must be >= 1");
+  if (k == 0) throw std::invalid_argument("top_k: k must be >= 1");
+  std::string all;
+  std::vector<uint64_t> off{0};
+  for (const auto& q : queries) {
+    all += q;
+    off.push_back(all.size());
+  }
+  if (all.empty()) all.push_back('\0');
+  const size_t B = queries.size();
+  std::vector<uint32_t> ids(B * k);
+  std::vector<float> sc(B * k);
+  if (B)
+    check(sl_text_index_retrieve(t.handle(), all.data(), off.data(), static_cast<uint32_t>(B), k, ordered ? 1 : 0,
+                                 ids.data(), sc.data()));
+  const uint32_t n = t.num_docs();
+  const size_t m = k < n ? k : n;
+  std::vector<QueryResult> out(B);
+  for (size_t b = 0; b < B; ++b) {
+    out[b].doc_indices.assign(ids.begin() + b * k, ids.begin() + b * k + m);
+    out[b].scores.assign(sc.begin() + b * k, sc.begin() + b * k + m);
+    for (uint32_t d : out[b].doc_indices) out[b].external_ids.push_back(t.external_id(d));
+  }
+  return out;
+}
+// SPEC retrieve(index, text, k, ordered): frozen vocabulary, OOV tokens dropped, external ids mapped
+inline QueryResult retrieve(const TextIndex& t, const std::string& text, uint32_t k, bool ordered = true) {
+  return std::move(retrieve_batch(t, std::vector<std::string>{text}, k, ordered)[0]);
 }
 
 }  // namespace sparselex::b200

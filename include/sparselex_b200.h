@@ -126,6 +126,21 @@ const char* sl_status_string(int32_t status);
 int32_t sl_params_validate(const sl_params* p);
 double sl_default_delta(int32_t variant); /* bm25.hpp:37-39 / scoring.cpp:34-41 */
 
+/* The scoring functions of proj/include/sparselex/bm25.hpp:25-72 (scoring.cpp:8-145) as C:
+ * the same arithmetic as the C++ symbols of include/sparselex/bm25.hpp (exported by this library
+ * for reference code that links against them) and as the GPU build's per-nonzero math.
+ * Contract violations return SL_EINVAL with the reference's std::invalid_argument message. */
+int32_t sl_variant_from_string(const char* name, int32_t* out);  /* variant_from_string, scoring.cpp:8-16 */
+const char* sl_variant_to_string(int32_t variant);              /* to_string, scoring.cpp:18-28; NULL if invalid */
+int32_t sl_is_sparse_variant(int32_t variant);                  /* is_sparse_variant, scoring.cpp:30-32: 1 / 0 */
+int32_t sl_idf(int32_t variant, uint32_t df, uint32_t num_docs, double* out);  /* idf, scoring.cpp:60-79 */
+int32_t sl_tf_component(double tf, double doc_len, uint32_t num_docs, double avg_len, const sl_params* p,
+                        double* out);                             /* tf_component, scoring.cpp:81-114 */
+int32_t sl_score(double tf, uint32_t df, double doc_len, uint32_t num_docs, double avg_len, const sl_params* p,
+                 double* out);                                    /* score, scoring.cpp:116-123 */
+int32_t sl_nonoccurrence_score(uint32_t df, uint32_t num_docs, const sl_params* p,
+                               double* out);                      /* nonoccurrence_score, scoring.cpp:125-145 */
+
 /* Index build (SPEC build_index). Token ids must be < vocab_size; num_docs >= 1; the
  * corpus must not be all-empty ("degenerate corpus"). */
 int32_t sl_index_build(const sl_build_desc* desc, sl_index** out);
@@ -263,6 +278,39 @@ int32_t sl_token_batch_destroy(sl_token_batch* batch);
 int32_t sl_tokenize_stream(sl_vocab* vocab, const sl_tokenizer_config* config, int32_t build, const char* text,
                            const uint64_t* doc_offsets, uint32_t num_docs, uint64_t chunk_bytes,
                            uint64_t* out_offsets, uint32_t* out_ids, uint64_t ids_capacity, uint64_t* num_tokens);
+
+/* ---- Text-level SearchIndex (SPEC.md [MODULE] index / retrieval over texts) -------------------
+ *   sl_text_index_build    <- build_index(corpus: sequence of (external_id, text), params,
+ *                             tokenizer_config) SPEC.md:201-209: tokenize_build on the device, then
+ *                             sl_index_build on the device-resident ids. Errors (SL_EINVAL): empty
+ *                             corpus, degenerate corpus (every document tokenizes to empty),
+ *                             duplicate external ids. ids / texts: byte ranges [off[d], off[d+1]).
+ *   sl_text_index_save/load<- save_index / load_index SPEC.md:210-227: the 9-file layout with the real
+ *                             vocab.json {token: id}, docs.json [external ids] and meta.json tokenizer
+ *                             {lowercase, stopwords_hash, stemmer} (+ the stopword list); load checks
+ *                             the list against the hash (SL_ECORRUPT on mismatch).
+ *   sl_text_index_retrieve <- retrieve / retrieve_batch over query texts SPEC.md:296-313: tokenize_query
+ *                             with the index's config and frozen vocabulary, then score + top-k; host
+ *                             outputs [num_queries x k] padded as sl_retrieve_batch.
+ *   sl_text_index_external_id <- QueryResult.external_ids / SearchIndex.doc_external_ids (borrowed bytes)
+ * The index, vocabulary and configuration returned by the accessors are borrowed from the text index. */
+typedef struct sl_text_index sl_text_index;
+
+int32_t sl_text_index_build(const char* ext_ids, const uint64_t* id_offsets, const char* text,
+                            const uint64_t* text_offsets, uint32_t num_docs, const sl_params* params,
+                            const sl_tokenizer_config* config, int32_t device, float dense_min_density,
+                            sl_text_index** out);
+void sl_text_index_destroy(sl_text_index* index);
+int32_t sl_text_index_save(const sl_text_index* index, const char* directory);
+int32_t sl_text_index_load(const char* directory, int32_t device, float dense_min_density, sl_text_index** out);
+const sl_index* sl_text_index_index(const sl_text_index* index);
+sl_vocab* sl_text_index_vocab(const sl_text_index* index);
+int32_t sl_text_index_config(const sl_text_index* index, sl_tokenizer_config* out);
+int32_t sl_text_index_num_docs(const sl_text_index* index, uint32_t* out);
+int32_t sl_text_index_external_id(const sl_text_index* index, uint32_t doc, const char** id, uint64_t* len);
+int32_t sl_text_index_retrieve(const sl_text_index* index, const char* text, const uint64_t* offsets,
+                               uint32_t num_queries, uint32_t k, int32_t ordered, uint32_t* out_ids,
+                               float* out_scores);
 
 /* stem_english for n words (host buffers): out has the input's byte size, word i's stem is
  * out[offsets[i] .. offsets[i] + out_len[i]) */

@@ -2,7 +2,7 @@
 //
 // Compiled by oracle/Makefile together with /root/reference/proj/src/scoring.cpp
 // (read in place, never copied) into oracle/_ref/libref_scoring.so. Test
-// infrastructure only: tests/test_oracle_pin.py calls these to pin the oracle's
+// infrastructure only: tests/test_oracle.py::test_restatement_pinned_to_reference_scoring calls these to pin the oracle's
 // restated formulas against the reference implementation itself.
 // Declarations come from the reference header proj/include/sparselex/bm25.hpp:25-72.
 #include <cmath>

@@ -82,6 +82,13 @@ SIGNATURES = {
     "sl_status_string": (C.c_char_p, [_i32]),
     "sl_params_validate": (_i32, [C.POINTER(Params)]),
     "sl_default_delta": (C.c_double, [_i32]),
+    "sl_variant_from_string": (_i32, [C.c_char_p, C.POINTER(_i32)]),
+    "sl_variant_to_string": (C.c_char_p, [_i32]),
+    "sl_is_sparse_variant": (_i32, [_i32]),
+    "sl_idf": (_i32, [_i32, _u32, _u32, C.POINTER(C.c_double)]),
+    "sl_tf_component": (_i32, [C.c_double, C.c_double, _u32, C.c_double, C.POINTER(Params), C.POINTER(C.c_double)]),
+    "sl_score": (_i32, [C.c_double, _u32, C.c_double, _u32, C.c_double, C.POINTER(Params), C.POINTER(C.c_double)]),
+    "sl_nonoccurrence_score": (_i32, [_u32, _u32, C.POINTER(Params), C.POINTER(C.c_double)]),
     "sl_index_build": (_i32, [C.POINTER(BuildDesc), C.POINTER(C.c_void_p)]),
     "sl_index_destroy": (None, [_vp]),
     "sl_index_get_info": (_i32, [_vp, C.POINTER(IndexInfo)]),
@@ -109,6 +116,17 @@ SIGNATURES = {
     "sl_token_batch_copy": (_i32, [_vp, _vp, _vp]),
     "sl_token_batch_destroy": (_i32, [_vp]),
     "sl_stem_batch": (_i32, [_vp, _vp, _u32, _i32, _vp, _vp]),
+    "sl_text_index_build": (_i32, [_vp, _vp, _vp, _vp, _u32, C.POINTER(Params), C.POINTER(TokenizerConfig), _i32,
+                                   C.c_float, C.POINTER(C.c_void_p)]),
+    "sl_text_index_destroy": (None, [_vp]),
+    "sl_text_index_save": (_i32, [_vp, C.c_char_p]),
+    "sl_text_index_load": (_i32, [C.c_char_p, _i32, C.c_float, C.POINTER(C.c_void_p)]),
+    "sl_text_index_index": (_vp, [_vp]),
+    "sl_text_index_vocab": (_vp, [_vp]),
+    "sl_text_index_config": (_i32, [_vp, C.POINTER(TokenizerConfig)]),
+    "sl_text_index_num_docs": (_i32, [_vp, C.POINTER(_u32)]),
+    "sl_text_index_external_id": (_i32, [_vp, _u32, C.POINTER(C.c_void_p), C.POINTER(_u64)]),
+    "sl_text_index_retrieve": (_i32, [_vp, _vp, _vp, _u32, _u32, _i32, _vp, _vp]),
 }
 
 _lib = None

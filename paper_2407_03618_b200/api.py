@@ -87,18 +87,21 @@ def _as_arg(x, dtype):
 
 @dataclass
 class QueryResult:
-    """SPEC retrieval QueryResult: doc indices (global) and exact B(Q,D) scores, descending."""
+    """SPEC retrieval QueryResult: doc indices (global), exact B(Q,D) scores (descending) and, for
+    a text index, the matching external ids."""
     doc_indices: np.ndarray
     scores: np.ndarray
+    external_ids: list | None = None
 
 
 class SearchIndex:
     """A device-resident index shard (SPEC SearchIndex minus vocabulary / external ids)."""
 
-    def __init__(self, handle: int, device: int, comm=None):
+    def __init__(self, handle: int, device: int, comm=None, owned: bool = True):
         self._h = C.c_void_p(handle)
         self.device = device
         self.comm = comm
+        self._owned = owned  # False: a view of the index inside a TextIndex
 
     @property
     def handle(self):
@@ -153,9 +156,9 @@ class SearchIndex:
         check(lib().sl_index_save(self.handle, str(directory).encode()))
 
     def close(self) -> None:
-        if self._h:
+        if self._h and self._owned:
             lib().sl_index_destroy(self._h)
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __del__(self):
         try:

@@ -741,15 +741,8 @@ int grid_for(uint64_t n, int threads, int max_blocks = 0) {
   return (int)b;
 }
 
-int32_t host_validate(const sl_params& p) {
-  if (p.variant < 0 || p.variant > 5) SL_FAIL(SL_EINVAL, "invalid Variant value");
-  if (!(p.k1 > 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: k1 must be > 0");
-  if (!(p.b >= 0.0 && p.b <= 1.0)) SL_FAIL(SL_EINVAL, "BM25Params: b must be in [0, 1]");
-  if (!(p.delta >= 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: delta must be >= 0");
-  if (p.variant == SL_TFLDP && !(p.delta > std::exp(-1.0)))
-    SL_FAIL(SL_EINVAL, "BM25Params: tfldp requires delta > exp(-1)");
-  return SL_OK;
-}
+// BM25Params::validate (scoring.cpp:47-58) — one implementation, in sl_bm25.cpp
+int32_t host_validate(const sl_params& p) { return sl_params_validate(&p); }
 
 // RAII set of stream-ordered temporaries
 struct Temps {

@@ -47,25 +47,7 @@ const char* sl_status_string(int32_t s) {
   }
 }
 
-int32_t sl_params_validate(const sl_params* p) {
-  if (!p) SL_FAIL(SL_EINVAL, "null params");
-  if (p->variant < 0 || p->variant > 5) SL_FAIL(SL_EINVAL, "invalid Variant value");
-  if (!(p->k1 > 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: k1 must be > 0");
-  if (!(p->b >= 0.0 && p->b <= 1.0)) SL_FAIL(SL_EINVAL, "BM25Params: b must be in [0, 1]");
-  if (!(p->delta >= 0.0)) SL_FAIL(SL_EINVAL, "BM25Params: delta must be >= 0");
-  if (p->variant == SL_TFLDP && !(p->delta > std::exp(-1.0)))
-    SL_FAIL(SL_EINVAL, "BM25Params: tfldp requires delta > exp(-1)");
-  return SL_OK;
-}
-
-double sl_default_delta(int32_t v) {
-  switch (v) {
-    case SL_BM25L: return 0.5;
-    case SL_BM25PLUS: return 1.0;
-    case SL_TFLDP: return 0.5;
-    default: return 0.0;
-  }
-}
+// sl_params_validate / sl_default_delta and the scoring functions live in sl_bm25.cpp.
 
 int32_t sl_index_build(const sl_build_desc* desc, sl_index** out) { return build_index_impl(desc, out); }
 

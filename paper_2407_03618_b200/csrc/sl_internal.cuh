@@ -6,6 +6,7 @@
 
 #include <string>
 
+#include "sl_bm25_math.h"
 #include "sparselex_b200.h"
 
 namespace sl {
@@ -54,63 +55,18 @@ constexpr uint32_t kMaxK = 4096;       // max k for the fused top-k path
 constexpr uint64_t kInvalidKey = 0ull; // never produced by a real (score, doc) key
 
 // ---------------------------------------------------------------- BM25 math (f64)
-// Exact restatement of proj/src/scoring.cpp:60-145 with every operation explicitly
-// rounded (no FMA contraction), matching the reference's C++ expression trees.
-__device__ __forceinline__ double d_idf(int v, double n, double d) {
-  switch (v) {
-    case SL_LUCENE:  // log(1.0 + (n - d + 0.5) / (d + 0.5))
-      return log(__dadd_rn(1.0, __ddiv_rn(__dadd_rn(__dsub_rn(n, d), 0.5), __dadd_rn(d, 0.5))));
-    case SL_ROBERTSON:  // log((n - d + 0.5) / (d + 0.5))
-      return log(__ddiv_rn(__dadd_rn(__dsub_rn(n, d), 0.5), __dadd_rn(d, 0.5)));
-    case SL_ATIRE:  // log(n / d)
-      return log(__ddiv_rn(n, d));
-    case SL_BM25L:  // log((n + 1.0) / (d + 0.5))
-      return log(__ddiv_rn(__dadd_rn(n, 1.0), __dadd_rn(d, 0.5)));
-    default:  // bm25plus, tfldp: log((n + 1.0) / d)
-      return log(__ddiv_rn(__dadd_rn(n, 1.0), d));
-  }
-}
+// proj/src/scoring.cpp:60-145 as written once in sl_bm25_math.h; the device instantiation
+// rounds every operation explicitly (no FMA contraction), matching the reference's C++
+// expression trees. Preconditions are validated on the host.
+__device__ __forceinline__ double d_idf(int v, double n, double d) { return bm25::idf<bm25::DevOps>(v, n, d); }
 
-// scoring.cpp:81-114 (preconditions validated on the host)
 __device__ __forceinline__ double d_tf_component(int v, double tf, double dl, double avg, double k1,
                                                  double b, double delta) {
-  // norm = 1.0 - b + b * doc_len / avg_len  ==  ((1.0 - b) + ((b * dl) / avg))
-  const double norm = __dadd_rn(__dsub_rn(1.0, b), __ddiv_rn(__dmul_rn(b, dl), avg));
-  switch (v) {
-    case SL_LUCENE:
-      return __ddiv_rn(tf, __dadd_rn(tf, __dmul_rn(k1, norm)));
-    case SL_ROBERTSON:
-    case SL_ATIRE:
-      return __ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), tf), __dadd_rn(tf, __dmul_rn(k1, norm)));
-    case SL_BM25L: {
-      const double c = __ddiv_rn(tf, norm);
-      return __ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), __dadd_rn(c, delta)),
-                       __dadd_rn(__dadd_rn(k1, c), delta));
-    }
-    case SL_BM25PLUS: {
-      const double c = __ddiv_rn(tf, norm);
-      return __dadd_rn(__ddiv_rn(__dmul_rn(__dadd_rn(k1, 1.0), c), __dadd_rn(k1, c)), delta);
-    }
-    default: {  // tfldp
-      const double c = __ddiv_rn(tf, norm);
-      const double inner = __dadd_rn(1.0, log(__dadd_rn(c, delta)));
-      return __dadd_rn(1.0, log(inner));
-    }
-  }
+  return bm25::tf_component<bm25::DevOps>(v, tf, bm25::norm<bm25::DevOps>(dl, avg, b), k1, delta);
 }
 
-// scoring.cpp:125-145 given idf
 __device__ __forceinline__ double d_nonoccurrence(int v, double idf, double k1, double delta) {
-  switch (v) {
-    case SL_BM25L:  // i * ((k1 + 1.0) * delta) / (k1 + delta)
-      return __ddiv_rn(__dmul_rn(idf, __dmul_rn(__dadd_rn(k1, 1.0), delta)), __dadd_rn(k1, delta));
-    case SL_BM25PLUS:
-      return __dmul_rn(idf, delta);
-    case SL_TFLDP:
-      return __dmul_rn(idf, __dadd_rn(1.0, log(__dadd_rn(1.0, log(delta)))));
-    default:
-      return 0.0;
-  }
+  return bm25::nonoccurrence<bm25::DevOps>(v, idf, k1, delta);
 }
 
 __host__ __device__ __forceinline__ bool is_sparse_variant(int v) {

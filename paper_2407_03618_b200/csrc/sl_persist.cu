@@ -21,6 +21,8 @@
 #include <vector>
 
 #include "sl_index.cuh"
+#include "sl_json.h"
+#include "sl_persist.h"
 
 namespace sl {
 namespace {
@@ -75,27 +77,6 @@ int32_t read_array(const std::string& path, std::vector<T>& v, uint64_t expect, 
   return SL_OK;
 }
 
-// value of "key": in a flat JSON object we wrote ourselves (numbers or strings)
-bool json_field(const std::string& js, const std::string& key, std::string& val) {
-  const std::string k = "\"" + key + "\"";
-  size_t p = js.find(k);
-  if (p == std::string::npos) return false;
-  p = js.find(':', p + k.size());
-  if (p == std::string::npos) return false;
-  ++p;
-  while (p < js.size() && (js[p] == ' ' || js[p] == '\n')) ++p;
-  if (p < js.size() && js[p] == '"') {
-    const size_t e = js.find('"', p + 1);
-    if (e == std::string::npos) return false;
-    val = js.substr(p + 1, e - p - 1);
-    return true;
-  }
-  size_t e = p;
-  while (e < js.size() && js[e] != ',' && js[e] != '}' && js[e] != '\n') ++e;
-  val = js.substr(p, e - p);
-  return true;
-}
-
 template <class T>
 int32_t d2h(std::vector<T>& v, const T* src, uint64_t n) {
   v.resize(n);
@@ -108,14 +89,14 @@ int32_t d2h(std::vector<T>& v, const T* src, uint64_t n) {
 
 using namespace sl;
 
-extern "C" {
+namespace sl {
 
-int32_t sl_index_save(const sl_index* ix, const char* directory) {
-  if (!ix || !directory) SL_FAIL(SL_EINVAL, "save_index: null argument");
-  const std::string dir(directory);
+int32_t save_index_impl(const sl_index* ix, const std::string& dir, const TextMeta* tm) {
   struct stat sb;
   if (stat(dir.c_str(), &sb) != 0 && mkdir(dir.c_str(), 0755) != 0)
     SL_FAIL(SL_EIO, "save_index: cannot create directory " + dir + ": " + std::strerror(errno));
+  if (tm && ((tm->tokens && tm->tokens->size() != ix->V) || (tm->ext_ids && tm->ext_ids->size() != ix->N)))
+    SL_FAIL(SL_EINVAL, "save_index: vocabulary / external ids do not match the index");
   SL_CUDA_TRY(cudaSetDevice(ix->device));
   std::vector<uint64_t> indptr;
   std::vector<uint32_t> docids, df, doclens;
@@ -126,22 +107,41 @@ int32_t sl_index_save(const sl_index* ix, const char* directory) {
   SL_TRY(d2h(df, ix->df_global, ix->V));
   SL_TRY(d2h(theta, ix->theta, ix->V));
   SL_TRY(d2h(doclens, ix->doclens, ix->N));
+  std::string tok;
+  if (tm && tm->tokens) {
+    tok = std::string("{\"lowercase\": ") + (tm->lowercase ? "true" : "false") +
+          ", \"stopwords_hash\": " + std::to_string(tm->stopwords_hash) + ", \"stemmer\": \"" +
+          (tm->stemmer == SL_STEMMER_SNOWBALL_ENGLISH ? "snowball-english" : "none") + "\"}";
+  } else {
+    tok = "{\"lowercase\": false, \"stopwords_hash\": \"none\", \"stemmer\": \"none\", \"input\": \"token-ids\"}";
+  }
   char meta[2048];
   std::snprintf(meta, sizeof(meta),
                 "{\n \"format_version\": %d,\n \"variant\": \"%s\",\n \"k1\": %.17g,\n \"b\": %.17g,\n"
                 " \"delta\": %.17g,\n \"num_docs\": %u,\n \"avg_len\": %.17g,\n \"num_tokens\": %llu,\n"
-                " \"num_nonzeros\": %llu,\n \"tokenizer\": {\"lowercase\": false, \"stopwords_hash\": \"none\","
-                " \"stemmer\": \"none\", \"input\": \"token-ids\"},\n \"vocab_size\": %u,\n"
-                " \"num_docs_global\": %u,\n \"doc_base\": %u,\n \"total_len_global\": %llu\n}\n",
+                " \"num_nonzeros\": %llu,\n \"tokenizer\": %s,\n \"vocab_size\": %u,\n"
+                " \"num_docs_global\": %u,\n \"doc_base\": %u,\n \"total_len_global\": %llu",
                 kFormatVersion, variant_name(ix->params.variant), ix->params.k1, ix->params.b, ix->params.delta,
-                ix->N, ix->avg_len, (unsigned long long)ix->total_len, (unsigned long long)ix->nnz, ix->V,
+                ix->N, ix->avg_len, (unsigned long long)ix->total_len, (unsigned long long)ix->nnz, tok.c_str(), ix->V,
                 ix->N_global, ix->doc_base, (unsigned long long)ix->total_len);
-  SL_TRY(write_file(join(dir, "meta.json"), meta, std::strlen(meta)));
+  std::string m(meta);
+  if (tm && tm->stopwords) {  // extension: the list itself, so load_index restores the set (SPEC keeps the hash)
+    m += ",\n \"stopwords\": [";
+    for (size_t i = 0; i < tm->stopwords->size(); ++i) {
+      if (i) m += ", ";
+      json::escape_into(m, (*tm->stopwords)[i]);
+    }
+    m += "]";
+  }
+  m += "\n}\n";
+  SL_TRY(write_file(join(dir, "meta.json"), m.data(), m.size()));
   std::string vocab = "{";
   vocab.reserve((size_t)ix->V * 20);
   for (uint32_t t = 0; t < ix->V; ++t) {
     if (t) vocab += ", ";
-    vocab += "\"" + std::to_string(t) + "\": " + std::to_string(t);
+    if (tm && tm->tokens) json::escape_into(vocab, (*tm->tokens)[t]);
+    else vocab += "\"" + std::to_string(t) + "\"";
+    vocab += ": " + std::to_string(t);
   }
   vocab += "}\n";
   SL_TRY(write_file(join(dir, "vocab.json"), vocab.data(), vocab.size()));
@@ -149,7 +149,8 @@ int32_t sl_index_save(const sl_index* ix, const char* directory) {
   docs.reserve((size_t)ix->N * 12);
   for (uint32_t d = 0; d < ix->N; ++d) {
     if (d) docs += ", ";
-    docs += "\"" + std::to_string((uint64_t)ix->doc_base + d) + "\"";
+    if (tm && tm->ext_ids) json::escape_into(docs, (*tm->ext_ids)[d]);
+    else docs += "\"" + std::to_string((uint64_t)ix->doc_base + d) + "\"";
   }
   docs += "]\n";
   SL_TRY(write_file(join(dir, "docs.json"), docs.data(), docs.size()));
@@ -162,30 +163,32 @@ int32_t sl_index_save(const sl_index* ix, const char* directory) {
   return SL_OK;
 }
 
-int32_t sl_index_load(const char* directory, int32_t device, float dense_min_density, sl_index** out) {
-  if (!directory || !out) SL_FAIL(SL_EINVAL, "load_index: null argument");
+int32_t load_index_impl(const std::string& dir, int32_t device, float dense_min_density, sl_index** out,
+                        LoadedText* text) {
   *out = nullptr;
-  const std::string dir(directory);
-  std::string meta, f;
+  std::string meta, err;
   SL_TRY(read_file(join(dir, "meta.json"), meta));
-  if (!json_field(meta, "format_version", f) || std::atoi(f.c_str()) != kFormatVersion)
+  json::Value mv;
+  if (!json::Parser(meta).parse(mv, err) || mv.kind != json::Value::kObject)
+    SL_FAIL(SL_ECORRUPT, "load_index: corrupt meta.json (" + err + ")");
+  const json::Value* fv = mv.get("format_version");
+  if (!fv || fv->kind != json::Value::kNumber || fv->num() != kFormatVersion)
     SL_FAIL(SL_EUNSUPPORTED, "load_index: format version mismatch (expected " + std::to_string(kFormatVersion) +
-                                 ", found " + f + ")");
-  HostIndex h;
+                                 ", found " + (fv ? fv->text : std::string("none")) + ")");
   auto num = [&](const char* k, double& v) -> bool {
-    std::string s;
-    if (!json_field(meta, k, s)) return false;
-    char* e = nullptr;
-    v = std::strtod(s.c_str(), &e);
-    return e != s.c_str();
+    const json::Value* x = mv.get(k);
+    if (!x || x->kind != json::Value::kNumber) return false;
+    v = x->num();
+    return true;
   };
+  HostIndex h;
   double k1, b, delta, nd, nnzd, avg, ntok;
-  std::string vname;
-  if (!json_field(meta, "variant", vname) || !num("k1", k1) || !num("b", b) || !num("delta", delta) ||
+  const json::Value* vn = mv.get("variant");
+  if (!vn || vn->kind != json::Value::kString || !num("k1", k1) || !num("b", b) || !num("delta", delta) ||
       !num("num_docs", nd) || !num("avg_len", avg) || !num("num_nonzeros", nnzd) || !num("num_tokens", ntok))
     SL_FAIL(SL_ECORRUPT, "load_index: corrupt meta.json (missing fields)");
-  h.params = sl_params{variant_from_name(vname), k1, b, delta};
-  if (h.params.variant < 0) SL_FAIL(SL_ECORRUPT, "load_index: corrupt meta.json (unknown variant " + vname + ")");
+  h.params = sl_params{variant_from_name(vn->text), k1, b, delta};
+  if (h.params.variant < 0) SL_FAIL(SL_ECORRUPT, "load_index: corrupt meta.json (unknown variant " + vn->text + ")");
   h.N = (uint32_t)nd;
   h.avg_len = avg;
   h.total_len = (uint64_t)ntok;
@@ -202,11 +205,24 @@ int32_t sl_index_load(const char* directory, int32_t device, float dense_min_den
   std::memcpy(h.indptr.data(), raw.data(), raw.size());
   std::string vocab;
   SL_TRY(read_file(join(dir, "vocab.json"), vocab));
-  uint64_t entries = 0;
-  for (char c : vocab) entries += c == ':';
-  if (entries != h.V)
-    SL_FAIL(SL_ECORRUPT, "load_index: structural error (vocab.json has " + std::to_string(entries) +
+  std::vector<std::pair<std::string, uint64_t>> ventries;
+  if (!json::Parser(vocab).string_u64_object(ventries, err))
+    SL_FAIL(SL_ECORRUPT, "load_index: structural error (vocab.json: " + err + ")");
+  if (ventries.size() != h.V)
+    SL_FAIL(SL_ECORRUPT, "load_index: structural error (vocab.json has " + std::to_string(ventries.size()) +
                              " tokens, indptr.bin describes " + std::to_string(h.V) + ")");
+  if (text) {  // tokens in id order: the ids must be a permutation of 0..V-1
+    text->tokens.assign(h.V, std::string());
+    std::vector<uint8_t> seen(h.V, 0);
+    for (auto& e : ventries) {
+      if (e.second >= h.V || seen[e.second])
+        SL_FAIL(SL_ECORRUPT, "load_index: structural error (vocab.json ids are not 0..V-1)");
+      seen[e.second] = 1;
+      text->tokens[e.second] = std::move(e.first);
+    }
+  }
+  ventries.clear();
+  ventries.shrink_to_fit();
   const uint64_t nnz = h.indptr.back();
   if (nnz != (uint64_t)nnzd) SL_FAIL(SL_ECORRUPT, "load_index: corrupt matrix (num_nonzeros != indptr[V])");
   SL_TRY(read_array(join(dir, "docids.bin"), h.docids, nnz, "docids.bin"));
@@ -216,10 +232,51 @@ int32_t sl_index_load(const char* directory, int32_t device, float dense_min_den
   SL_TRY(read_array(join(dir, "doclens.bin"), h.doclens, h.N, "doclens.bin"));
   std::string docs;
   SL_TRY(read_file(join(dir, "docs.json"), docs));
-  uint64_t quotes = 0;
-  for (char c : docs) quotes += c == '"';
-  if (quotes != 2ull * h.N) SL_FAIL(SL_ECORRUPT, "load_index: structural error (docs.json does not list num_docs ids)");
+  std::vector<std::string> ids;
+  if (!json::Parser(docs).string_array(ids, err))
+    SL_FAIL(SL_ECORRUPT, "load_index: structural error (docs.json: " + err + ")");
+  if (ids.size() != h.N) SL_FAIL(SL_ECORRUPT, "load_index: structural error (docs.json does not list num_docs ids)");
+  if (text) {
+    text->ext_ids = std::move(ids);
+    const json::Value* tk = mv.get("tokenizer");
+    text->lowercase = false;
+    text->stemmer = SL_STEMMER_NONE;
+    text->has_hash = false;
+    text->stopwords.clear();
+    if (tk && tk->kind == json::Value::kObject) {
+      const json::Value* lc = tk->get("lowercase");
+      text->lowercase = lc && lc->kind == json::Value::kBool && lc->b;
+      const json::Value* st = tk->get("stemmer");
+      if (st && st->kind == json::Value::kString) {
+        if (st->text == "snowball-english" || st->text == "snowball_english") text->stemmer = SL_STEMMER_SNOWBALL_ENGLISH;
+        else if (st->text != "none") SL_FAIL(SL_ECORRUPT, "load_index: corrupt meta.json (unknown stemmer " + st->text + ")");
+      }
+      const json::Value* hv = tk->get("stopwords_hash");
+      if (hv && hv->kind == json::Value::kNumber) {
+        text->has_hash = true;
+        text->stopwords_hash = hv->u64();
+      }
+    }
+    const json::Value* sw = mv.get("stopwords");
+    if (sw && sw->kind == json::Value::kArray)
+      for (const auto& w : sw->arr)
+        if (w.kind == json::Value::kString) text->stopwords.push_back(w.text);
+  }
   return load_index_from_host(h, device, dense_min_density, out);
+}
+
+}  // namespace sl
+
+extern "C" {
+
+int32_t sl_index_save(const sl_index* ix, const char* directory) {
+  if (!ix || !directory) SL_FAIL(SL_EINVAL, "save_index: null argument");
+  return save_index_impl(ix, directory, nullptr);
+}
+
+int32_t sl_index_load(const char* directory, int32_t device, float dense_min_density, sl_index** out) {
+  if (!directory || !out) SL_FAIL(SL_EINVAL, "load_index: null argument");
+  return load_index_impl(directory, device, dense_min_density, out, nullptr);
 }
 
 }  // extern "C"

@@ -19,7 +19,6 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
-import json
 import os
 from dataclasses import dataclass, field
 
@@ -27,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import SL_MEM_DEVICE, SL_MEM_HOST, check, lib
-from .api import BM25Params, QueryResult, SearchIndex, load_index
+from .api import BM25Params, QueryResult, SearchIndex
 
 _DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
 STOPWORDS_EN = os.path.join(_DATA, "stopwords_en.txt")
@@ -168,10 +167,17 @@ class Vocabulary:
         check(lib().sl_vocab_import(v.handle, off.ctypes.data, blob or b"\0", len(enc)))
         return v
 
+    @staticmethod
+    def borrowed(handle, device: int = 0) -> "Vocabulary":
+        """A view of a vocabulary owned by someone else (a TextIndex): never destroyed here."""
+        v = Vocabulary.__new__(Vocabulary)
+        v._h, v.device, v._cache, v._index, v._owned = C.c_void_p(handle), device, None, None, False
+        return v
+
     def close(self):
-        if self._h:
+        if self._h and getattr(self, "_owned", True):
             lib().sl_vocab_destroy(self._h)
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __del__(self):
         try:
@@ -322,102 +328,124 @@ def stem_english(word: str) -> str:
 
 # ---------------------------------------------------------------- text-level index (SPEC build_index)
 class TextIndex:
-    """SPEC SearchIndex with its vocabulary, tokenizer config and external document ids."""
+    """SPEC SearchIndex with its vocabulary, tokenizer config and external document ids — the
+    library's sl_text_index (C++), this class only holds the handle."""
 
-    def __init__(self, index: SearchIndex, vocab: Vocabulary, config: TokenizerConfig, doc_ids, params):
-        self.index, self.vocab, self.config, self.doc_ids, self.params = index, vocab, config, list(doc_ids), params
+    def __init__(self, handle, device: int = 0, params: BM25Params | None = None):
+        self._h = C.c_void_p(handle)
+        self.device = device
+        self.params = params
+        L = lib()
+        self.index = SearchIndex(L.sl_text_index_index(self._h), device, owned=False)
+        self.vocab = Vocabulary.borrowed(L.sl_text_index_vocab(self._h), device)
+        c = _lib.TokenizerConfig()
+        check(L.sl_text_index_config(self._h, C.byref(c)))
+        sw = C.string_at(c.stopwords, c.stopwords_bytes).decode("utf-8") if c.stopwords_bytes else ""
+        self.config = TokenizerConfig(bool(c.lowercase), frozenset(w for w in sw.split("\n") if w),
+                                      StemmerKind(c.stemmer))
+        self._ids = None
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise ValueError("TextIndex is closed")
+        return self._h
+
+    @property
+    def num_docs(self) -> int:
+        n = C.c_uint32()
+        check(lib().sl_text_index_num_docs(self.handle, C.byref(n)))
+        return n.value
+
+    @property
+    def doc_ids(self) -> list:
+        """SearchIndex.doc_external_ids (SPEC.md:194-197)."""
+        if self._ids is None:
+            p, n = C.c_void_p(), C.c_uint64()
+            out = []
+            for d in range(self.num_docs):
+                check(lib().sl_text_index_external_id(self.handle, d, C.byref(p), C.byref(n)))
+                out.append(C.string_at(p, n.value).decode("utf-8", errors="surrogateescape"))
+            self._ids = out
+        return self._ids
+
+    def external_ids(self, doc_indices) -> list:
+        ids = self.doc_ids
+        return [ids[int(d)] for d in doc_indices]
 
     def save(self, directory: str) -> None:
-        """SPEC save_index (9 files): the device arrays via sl_index_save, then the text
-        metadata the token-id layout leaves generic (vocab.json tokens, docs.json ids,
-        meta.json tokenizer)."""
-        self.index.save(directory)
-        toks = self.vocab.tokens()
-        with open(os.path.join(directory, "vocab.json"), "w", encoding="utf-8") as f:
-            json.dump({t: i for i, t in enumerate(toks)}, f, ensure_ascii=False)
-        with open(os.path.join(directory, "docs.json"), "w", encoding="utf-8") as f:
-            json.dump(self.doc_ids, f, ensure_ascii=False)
-        mp = os.path.join(directory, "meta.json")
-        with open(mp, encoding="utf-8") as f:
-            meta = json.load(f)
-        meta["tokenizer"] = self.config.to_json()
-        meta["stopwords"] = sorted(self.config.stopwords)  # lets load_text_index restore the set
-        meta.pop("input", None)
-        with open(mp, "w", encoding="utf-8") as f:
-            json.dump(meta, f, indent=1)
+        """SPEC save_index: the 9 files with the real vocab.json, docs.json and tokenizer metadata."""
+        check(lib().sl_text_index_save(self.handle, str(directory).encode()))
+
+    def close(self) -> None:
+        if self._h:
+            lib().sl_text_index_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def _blob(items):
+    enc = [x.encode("utf-8") if isinstance(x, str) else bytes(x) for x in items]
+    off = np.zeros(len(enc) + 1, np.uint64)
+    if enc:
+        off[1:] = np.cumsum([len(e) for e in enc])
+    return b"".join(enc) or b"\0", off
 
 
 def build_text_index(corpus, params: BM25Params | None = None, config: TokenizerConfig | None = None, *,
                      device: int = 0, dense_min_density: float = 0.0) -> TextIndex:
-    """SPEC build_index(corpus: sequence of (external_id, text), params, tokenizer_config).
-
-    Errors as the SPEC: empty corpus; every document tokenizing to nothing ("degenerate
-    corpus"); duplicate external ids."""
+    """SPEC build_index(corpus: sequence of (external_id, text), params, tokenizer_config), in the
+    library (sl_text_index_build). Errors as the SPEC: empty corpus; every document tokenizing to
+    nothing ("degenerate corpus"); duplicate external ids."""
     params = params or BM25Params()
     config = config or TokenizerConfig.english()
     corpus = list(corpus)
-    if not corpus:
-        raise ValueError("build_index: empty corpus")
-    ids = [c[0] for c in corpus]
-    if len(set(ids)) != len(ids):
-        raise ValueError("build_index: duplicate external ids")
-    vocab = Vocabulary(device)
-    batch = tokenize_build([c[1] for c in corpus], config, vocab)
-    if batch.num_tokens == 0:
-        raise ValueError("build_index: degenerate corpus (every document tokenizes to empty)")
-    d = _lib.BuildDesc()
-    d.doc_offsets, d.token_ids = batch.d_offsets, batch.d_ids
-    d.num_docs, d.vocab_size, d.doc_base, d.mem = batch.num_docs, vocab.size(), 0, SL_MEM_DEVICE
-    d.params = params.to_c()
-    d.device, d.keep_tf, d.dense_min_density = device, 0, float(dense_min_density)
+    ids, ioff = _blob([str(c[0]) for c in corpus])
+    text, toff = _blob([c[1] for c in corpus])
+    cfg, keep = config.to_c()
+    p = params.to_c()
     h = C.c_void_p()
-    check(lib().sl_index_build(C.byref(d), C.byref(h)))
-    batch.close()
-    return TextIndex(SearchIndex(h.value, device), vocab, config, ids, params)
+    check(lib().sl_text_index_build(ids, ioff.ctypes.data, text, toff.ctypes.data, len(corpus), C.byref(p),
+                                    C.byref(cfg), device, float(dense_min_density), C.byref(h)))
+    return TextIndex(h.value, device, params)
 
 
-def load_text_index(directory: str, *, device: int = 0) -> TextIndex:
-    """SPEC load_index for an index saved by TextIndex.save."""
-    index = load_index(directory, device=device)
-    with open(os.path.join(directory, "vocab.json"), encoding="utf-8") as f:
-        vj = json.load(f)
-    toks = [None] * len(vj)
-    for t, i in vj.items():
-        toks[i] = t
-    with open(os.path.join(directory, "docs.json"), encoding="utf-8") as f:
-        doc_ids = json.load(f)
-    with open(os.path.join(directory, "meta.json"), encoding="utf-8") as f:
-        meta = json.load(f)
-    tk = meta.get("tokenizer", {})
-    cfg = TokenizerConfig(bool(tk.get("lowercase", True)), frozenset(meta.get("stopwords", [])),
-                          StemmerKind.from_string(tk.get("stemmer", "none")))
-    if stopwords_hash(cfg.stopwords) != int(tk.get("stopwords_hash", stopwords_hash(cfg.stopwords))):
-        raise ValueError("load_index: stopword configuration does not match the index")
-    return TextIndex(index, Vocabulary.from_tokens(toks, device), cfg, doc_ids, None)
+def load_text_index(directory: str, *, device: int = 0, dense_min_density: float = 0.0) -> TextIndex:
+    """SPEC load_index for a text index (sl_text_index_load): the stopword list is checked against
+    meta.json's stopwords_hash."""
+    h = C.c_void_p()
+    check(lib().sl_text_index_load(str(directory).encode(), device, float(dense_min_density), C.byref(h)))
+    return TextIndex(h.value, device)
 
 
 def retrieve_text_batch(tindex: TextIndex, queries, k: int, ordered: bool = True, workers: int = 1):
-    """SPEC retrieve_batch over query texts: tokenize_query with the index's config and frozen
-    vocabulary (on the device), then score + top-k; doc_ids maps to external ids."""
+    """SPEC retrieve_batch over query texts (sl_text_index_retrieve: tokenize_query with the index's
+    config and frozen vocabulary on the device, score + top-k); each QueryResult carries the
+    external ids of its documents."""
     if workers < 1:
         raise ValueError("retrieve_batch: workers must be >= 1")
     if k <= 0:
         raise ValueError("top_k: k must be >= 1")
-    qb = tokenize_query(queries, tindex.config, tindex.vocab)
-    B = qb.num_docs
-    ids = np.empty((B, k), np.uint32)
-    sc = np.empty((B, k), np.float32)
-    # token ids are on the device; results come back to the host
-    import torch  # device output buffers (torch is the allocator, not the compute)
-    dids = torch.empty((B, k), dtype=torch.uint32, device=f"cuda:{tindex.index.device}")
-    dsc = torch.empty((B, k), dtype=torch.float32, device=f"cuda:{tindex.index.device}")
-    check(lib().sl_retrieve_batch(tindex.index.handle, qb.d_offsets, qb.d_ids or qb.d_offsets, B, k, int(ordered),
-                                  SL_MEM_DEVICE, dids.data_ptr(), dsc.data_ptr()))
-    ids[:] = dids.cpu().numpy()
-    sc[:] = dsc.cpu().numpy()
-    qb.close()
-    m = min(k, tindex.index.num_docs)
-    return [QueryResult(ids[b, :m].copy(), sc[b, :m].copy()) for b in range(B)]
+    text, off = _blob(list(queries))
+    B = len(off) - 1
+    ids = np.empty((max(B, 1), k), np.uint32)
+    sc = np.empty((max(B, 1), k), np.float32)
+    check(lib().sl_text_index_retrieve(tindex.handle, text, off.ctypes.data, B, k, int(ordered), ids.ctypes.data,
+                                       sc.ctypes.data))
+    m = min(k, tindex.num_docs)
+    ext = tindex.doc_ids
+    return [QueryResult(ids[b, :m].copy(), sc[b, :m].copy(), [ext[int(d)] for d in ids[b, :m]]) for b in range(B)]
 
 
 def retrieve_text(tindex: TextIndex, text: str, k: int, ordered: bool = True) -> QueryResult:

@@ -3,6 +3,8 @@
 // dog=2 ran=3; expected values verified against the reference's scoring.cpp.
 #include <cmath>
 #include <cstdio>
+#include <string>
+#include <unistd.h>
 #include <stdexcept>
 #include <vector>
 
@@ -78,9 +80,53 @@ int main() {
     EXPECT(stem_english({"running", "skies", "generously"}) ==
            (std::vector<std::string>{"run", "sky", "generous"}));
     TextIndex ti = build_text_index({"cat sat", "dog ran", "cat cat cat"}, BM25Params{}, TokenizerConfig{});
-    EXPECT(ti.vocab.tokens() == (std::vector<std::string>{"cat", "sat", "dog", "ran"}));
+    EXPECT(ti.vocab_tokens() == (std::vector<std::string>{"cat", "sat", "dog", "ran"}));
     auto rt = retrieve(ti, "Cat!", 2);
     EXPECT(rt.doc_indices == (std::vector<uint32_t>{2, 0}) && rt.scores[0] == 0.292446703f);
+    EXPECT(rt.external_ids == (std::vector<std::string>{"2", "0"}));
+  }
+  // SPEC build_index over (external_id, text) pairs -> save -> load -> retrieve with external ids
+  {
+    const std::vector<std::pair<std::string, std::string>> corpus = {
+        {"doc-a", "The cats sat on the mat"}, {"doc \"b\"", "Dogs ran; a dog runs."}, {"c/\u00e9", "cat cat cat"}};
+    TokenizerConfig tc{true, {"the", "on", "a"}, StemmerKind::snowball_english};
+    TextIndex t = build_text_index(corpus, BM25Params::for_variant(Variant::bm25plus), tc);
+    EXPECT(t.num_docs() == 3 && t.doc_external_ids()[1] == "doc \"b\"");
+    auto r1 = retrieve_batch(t, {"cat", "dogs running", "zebra"}, 2);
+    EXPECT(r1.size() == 3 && r1[0].external_ids == (std::vector<std::string>{"c/\u00e9", "doc-a"}));
+    EXPECT(r1[1].external_ids[0] == "doc \"b\"");
+    const std::string dir = "/tmp/sl_cpp_text_index_" + std::to_string(::getpid());
+    save_index(t, dir);
+    TextIndex u = load_text_index(dir);
+    EXPECT(u.doc_external_ids() == t.doc_external_ids() && u.vocab_tokens() == t.vocab_tokens());
+    auto tcu = u.tokenizer_config();
+    EXPECT(tcu.lowercase && tcu.stemmer == StemmerKind::snowball_english && tcu.stopwords.size() == 3);
+    auto r2 = retrieve_batch(u, {"cat", "dogs running", "zebra"}, 2);
+    for (size_t i = 0; i < r1.size(); ++i)
+      EXPECT(r2[i].doc_indices == r1[i].doc_indices && r2[i].scores == r1[i].scores &&
+             r2[i].external_ids == r1[i].external_ids);
+    bool dup = false;
+    try {
+      build_text_index(std::vector<std::pair<std::string, std::string>>{{"x", "cat"}, {"x", "dog"}}, BM25Params{}, tc);
+    } catch (const std::invalid_argument& e) {
+      dup = std::string(e.what()).find("duplicate external ids") != std::string::npos;
+    }
+    EXPECT(dup);
+    bool degenerate = false;
+    try {
+      build_text_index(std::vector<std::pair<std::string, std::string>>{{"x", "the"}, {"y", "! ?"}}, BM25Params{}, tc);
+    } catch (const std::invalid_argument& e) {
+      degenerate = std::string(e.what()).find("degenerate corpus") != std::string::npos;
+    }
+    EXPECT(degenerate);
+  }
+  // the reference's scoring functions are this library's too (bm25.hpp)
+  {
+    EXPECT(sparselex::variant_from_string("bm25l") == Variant::bm25l && sparselex::to_string(Variant::atire) == "atire");
+    sparselex::CorpusStats st;
+    st.num_docs = 3;
+    st.avg_len = 7.0 / 3.0;
+    EXPECT(static_cast<float>(sparselex::score(3.0, 2, 3.0, st, BM25Params{})) == 0.292446703f);
   }
   std::printf("cpp api ok\n");
   return 0;

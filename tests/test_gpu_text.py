@@ -185,6 +185,33 @@ def test_text_index_retrieval_vs_oracle(cuda_ok, port, tmp_path):
     res2 = T.retrieve_text_batch(tl, queries, 10)
     for a, b in zip(res, res2):
         assert np.array_equal(a.doc_indices, b.doc_indices) and np.array_equal(a.scores, b.scores)
+        assert a.external_ids == b.external_ids == [corpus[int(d)][0] for d in a.doc_indices]
+    with open(tmp_path / "ix" / "meta.json", encoding="utf-8") as f:
+        meta = json.load(f)
+    assert meta["tokenizer"] == {"lowercase": True, "stopwords_hash": T.stopwords_hash(cfg.stopwords),
+                                 "stemmer": "snowball-english"}
+    assert tl.config.stopwords == cfg.stopwords and tl.config.stemmer == cfg.stemmer
+
+
+def test_text_index_external_ids_json_roundtrip(cuda_ok, tmp_path):
+    """External ids with quotes, backslashes, control characters and non-ASCII survive save/load
+    (docs.json is parsed as JSON, not by counting quote characters); int ids become strings."""
+    corpus = [('a "quoted" id', "cat sat"), ("back\\slash\ttab", "dog ran"), ("ünï/€", "cat cat cat"), (7, "dog dog")]
+    ti = T.build_text_index(corpus, BM25Params(), T.TokenizerConfig())
+    assert ti.doc_ids == [str(c[0]) for c in corpus]
+    ti.save(str(tmp_path / "ix"))
+    with open(tmp_path / "ix" / "docs.json", encoding="utf-8") as f:
+        assert json.load(f) == [str(c[0]) for c in corpus]
+    tl = T.load_text_index(str(tmp_path / "ix"))
+    assert tl.doc_ids == ti.doc_ids
+    r = T.retrieve_text(tl, "cat", 2)
+    assert r.external_ids == ["ünï/€", 'a "quoted" id']
+    # a stopword list that no longer matches meta.json's hash is refused
+    meta = json.load(open(tmp_path / "ix" / "meta.json", encoding="utf-8"))
+    meta["stopwords"] = ["the"]
+    json.dump(meta, open(tmp_path / "ix" / "meta.json", "w", encoding="utf-8"))
+    with pytest.raises(RuntimeError, match="stopwords_hash"):
+        T.load_text_index(str(tmp_path / "ix"))
 
 
 def test_text_index_errors(cuda_ok):
