@@ -61,6 +61,7 @@ struct sl_vocab {
   uint64_t* tkey = nullptr;  // [tcap] first hash (0 = empty)
   uint32_t* tval = nullptr;  // [tcap] id
   uint32_t tcap = 0;         // power of two
+  int32_t weak = 0;          // test hook (SL_TEXT_WEAK_HASH=1): degenerate hashes exercise the collision paths
 };
 
 struct sl_token_batch {
@@ -167,6 +168,19 @@ __device__ __forceinline__ H2 hash2(const uint8_t* s, uint32_t n) {
   a = fmix64(a ^ n);
   b = fmix64(b);
   return H2{a ? a : 1ull, b};
+}
+
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\tmov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+      : "memory");
+  return old;
 }
 
 // ------------------------------------------------------------------ segmentation
@@ -799,7 +813,8 @@ struct NormArgs {
   uint64_t* h1;
   uint64_t* h2;
   uint32_t* long_flag;       // token deferred to the global-scratch pass
-  uint32_t* err;             // bit 0: vocabulary hash collision
+  uint32_t* err;
+  int32_t weak;              // test hook: degenerate first hashes (collision paths)
 };
 
 __device__ bool is_stopword(const StopView& s, const uint8_t* w, uint32_t n) {
@@ -816,19 +831,17 @@ __device__ bool is_stopword(const StopView& s, const uint8_t* w, uint32_t n) {
   }
 }
 
-__device__ uint32_t vocab_find(const VocabView& v, const uint8_t* w, uint32_t n, H2 h, uint32_t* err) {
+__device__ uint32_t vocab_find(const VocabView& v, const uint8_t* w, uint32_t n, H2 h) {
   if (!v.tcap) return kNew;
   for (uint32_t slot = (uint32_t)h.a & (v.tcap - 1);; slot = (slot + 1) & (v.tcap - 1)) {
     const uint64_t e = v.tkey[slot];
     if (!e) return kNew;
-    if (e == h.a) {
+    if (e == h.a) {  // identity = bytes: a string sharing the first hash keeps probing
       const uint32_t id = v.tval[slot];
       const uint64_t o = v.offs[id];
       bool eq = v.h2[id] == h.b && v.offs[id + 1] - o == n;
       for (uint32_t i = 0; i < n && eq; ++i) eq = v.bytes[o + i] == w[i];
       if (eq) return id;
-      atomicOr(err, 1u);  // same first hash, different string: refuse rather than merge
-      return kNew;
     }
   }
 }
@@ -868,11 +881,12 @@ __device__ void norm_one(const NormArgs& a, uint64_t i, uint8_t* nb, uint8_t* sh
     fl = stem_utf8(nb, nl, sh, fb);
     fin = fb;
   }
-  const H2 h = hash2(fin, fl);
+  H2 h = hash2(fin, fl);
+  if (a.weak) h.a = (h.a & 7ull) | 1ull;  // test hook (SL_TEXT_WEAK_HASH): first-hash collisions everywhere
   a.flen[i] = fl;
   a.h1[i] = h.a;
   a.h2[i] = h.b;
-  a.id[i] = vocab_find(a.voc, fin, fl, h, a.err);
+  a.id[i] = vocab_find(a.voc, fin, fl, h);
   if (a.arena)
     for (uint32_t k = 0; k < fl; ++k) a.arena[2 * b + k] = fin[k];
 }
@@ -920,35 +934,61 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* _
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = src[idx[j]];
 }
 
-// batch-local distinct-string table: key = first hash, first = smallest token index
-__global__ void k_dedup_insert(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ h1,
-                               uint64_t* __restrict__ key, uint32_t* __restrict__ first, uint32_t cap,
-                               uint32_t* __restrict__ cnt /*[0] inserted [1] overflow*/) {
-  // whole warps iterate together (the match below needs every lane)
-  for (uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; j0 < M; j0 += gridDim.x * blockDim.x) {
-    const uint32_t j = j0 + (threadIdx.x & 31);
-    const bool act = j < M;
-    const uint32_t i = act ? ntok[j] : 0xFFFFFFFFu;
-    const uint64_t k = act ? h1[i] : 0ull;
-    // Zipf head tokens repeat within a warp: one lane per distinct hash (the lowest lane =
-    // the smallest token index, ntok is ascending) touches the table
-    const uint32_t grp = __match_any_sync(0xffffffffu, (unsigned long long)k);
-    if (!act || (__ffs(grp) - 1) != (int)(threadIdx.x & 31)) continue;
-    uint32_t slot = (uint32_t)k & (cap - 1);
+// batch-local distinct-string table of the NEW normalised strings: 128-bit key per string
+// (kx, ky: the two 64-bit hashes, or a reseeded pair after a verified collision), first =
+// smallest raw-entry index. A plain read comes first, so repeated strings stay read-only.
+__global__ void k_dedup_insert(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ kx,
+                               const uint64_t* __restrict__ ky, ulonglong2* __restrict__ key,
+                               uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+    const uint32_t i = ntok[j];
+    ulonglong2 k = make_ulonglong2(kx[j], ky[j]);
+    if ((k.x | k.y) == 0ull) k.y = 1ull;  // (0, 0) marks an empty slot
+    uint32_t slot = (uint32_t)k.x & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
         atomicOr(cnt + 1, 1u);
         break;
       }
-      unsigned long long cur = key[slot];
-      if (cur == 0ull) cur = atomicCAS((unsigned long long*)key + slot, 0ull, (unsigned long long)k);
-      if (cur == 0ull || cur == k) {
-        if (cur == 0ull) atomicAdd(cnt, 1u);
-        if (*(volatile uint32_t*)(first + slot) > i) atomicMin(first + slot, i);
+      ulonglong2 cur = key[slot];
+      if ((cur.x | cur.y) == 0ull) {
+        cur = cas128(key + slot, make_ulonglong2(0ull, 0ull), k);
+        if ((cur.x | cur.y) == 0ull) {
+          atomicAdd(cnt, 1u);
+          cur = k;
+        }
+      }
+      if (cur.x == k.x && cur.y == k.y) {
+        if (first[slot] > i) atomicMin(first + slot, i);
         break;
       }
       slot = (slot + 1) & (cap - 1);
     }
+  }
+}
+
+// 128-bit dedup keys of the new strings: seed 0 = the normalisation's own (h1, h2); a reseeded
+// pair from the normalised bytes (arena) after a verified collision
+__global__ void k_new_keys(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ h1,
+                           const uint64_t* __restrict__ h2, const uint8_t* __restrict__ arena,
+                           const uint64_t* __restrict__ tbeg, const uint32_t* __restrict__ flen, uint32_t seed,
+                           int32_t weak, uint64_t* __restrict__ kx, uint64_t* __restrict__ ky) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
+    const uint32_t i = ntok[j];
+    if (seed == 0) {
+      kx[j] = weak ? (uint64_t)flen[i] : h1[i];  // weak: test hook, every equal-length string collides
+      ky[j] = weak ? 1ull : h2[i];
+      continue;
+    }
+    const uint8_t* w = arena + 2 * tbeg[i];
+    uint64_t a = 0x8ebc6af09c88c6e3ull * seed, b = 0x589965cc75374cc3ull + seed;
+    for (uint32_t k = 0; k < flen[i]; ++k) {
+      a = (a ^ w[k]) * 0x100000001b3ull;
+      b = (b + w[k] + 1) * 0xd6e8feb86659fd93ull;
+      b ^= b >> 29;
+    }
+    kx[j] = fmix64(a ^ flen[i]);
+    ky[j] = fmix64(b);
   }
 }
 
@@ -967,20 +1007,28 @@ __global__ void k_slot_list(const uint32_t* __restrict__ flag, const uint32_t* _
     }
 }
 
-// id of every new token; the second hash and length must agree with the group's first
-// occurrence (otherwise two distinct strings share the first hash: refuse)
-__global__ void k_dedup_assign(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ h1,
-                               const uint64_t* __restrict__ h2, const uint32_t* __restrict__ flen,
-                               const uint64_t* __restrict__ key, const uint32_t* __restrict__ first,
+// id of every new token; its normalised bytes must equal its group's first occurrence's
+// (a mismatch is a verified 128-bit collision: err bit 2, the host redoes the dedup reseeded)
+__global__ void k_dedup_assign(const uint32_t* __restrict__ ntok, uint32_t M, const uint64_t* __restrict__ kx,
+                               const uint64_t* __restrict__ ky, const uint32_t* __restrict__ flen,
+                               const uint8_t* __restrict__ arena, const uint64_t* __restrict__ tbeg,
+                               const ulonglong2* __restrict__ key, const uint32_t* __restrict__ first,
                                const uint32_t* __restrict__ rank, uint32_t cap, uint32_t V0, uint32_t* __restrict__ id,
                                uint32_t* __restrict__ err) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < M; j += gridDim.x * blockDim.x) {
     const uint32_t i = ntok[j];
-    const uint64_t k = h1[i];
-    uint32_t slot = (uint32_t)k & (cap - 1);
-    while (key[slot] != k) slot = (slot + 1) & (cap - 1);
+    ulonglong2 k = make_ulonglong2(kx[j], ky[j]);
+    if ((k.x | k.y) == 0ull) k.y = 1ull;
+    uint32_t slot = (uint32_t)k.x & (cap - 1);
+    while (key[slot].x != k.x || key[slot].y != k.y) slot = (slot + 1) & (cap - 1);
     const uint32_t f = first[slot];
-    if (h2[f] != h2[i] || flen[f] != flen[i]) atomicOr(err, 1u);
+    if (f != i) {
+      bool eq = flen[f] == flen[i];
+      const uint8_t* a = arena + 2 * tbeg[i];
+      const uint8_t* b = arena + 2 * tbeg[f];
+      for (uint32_t c = 0; c < flen[i] && eq; ++c) eq = a[c] == b[c];
+      if (!eq) atomicOr(err, 4u);
+    }
     id[i] = V0 + rank[slot];
   }
 }
@@ -1023,10 +1071,7 @@ __global__ void k_table_insert(const uint64_t* __restrict__ h1tok, const uint32_
         tval[slot] = V0 + r;
         break;
       }
-      if (prev == k) {  // cannot happen (groups have distinct first hashes)
-        atomicOr(err, 1u);
-        break;
-      }
+      // prev == k: another string with the same first hash (vocab_find compares bytes): probe on
     }
   }
 }
@@ -1034,9 +1079,10 @@ __global__ void k_table_insert(const uint64_t* __restrict__ h1tok, const uint32_
 // re-insert an existing vocabulary into a larger table: hash recomputed from the bytes
 __global__ void k_table_rehash(const uint64_t* __restrict__ offs, const uint8_t* __restrict__ bytes, uint32_t V,
                                uint64_t* __restrict__ tkey, uint32_t* __restrict__ tval, uint32_t tcap,
-                               uint64_t* __restrict__ h2v) {
+                               uint64_t* __restrict__ h2v, int32_t weak) {
   for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < V; id += gridDim.x * blockDim.x) {
-    const H2 h = hash2(bytes + offs[id], (uint32_t)(offs[id + 1] - offs[id]));
+    H2 h = hash2(bytes + offs[id], (uint32_t)(offs[id + 1] - offs[id]));
+    if (weak) h.a = (h.a & 7ull) | 1ull;  // the same degenerate first hash as norm_one
     h2v[id] = h.b;
     for (uint32_t slot = (uint32_t)h.a & (tcap - 1);; slot = (slot + 1) & (tcap - 1)) {
       if (atomicCAS((unsigned long long*)tkey + slot, 0ull, (unsigned long long)h.a) == 0ull) {
@@ -1084,7 +1130,10 @@ __global__ void k_stem_batch(const uint8_t* __restrict__ in, const uint64_t* __r
 // simply occupy different slots; first = smallest token index; tslot[i] = token i's slot.
 struct RawMix {
   uint64_t a, b;
-  __device__ __forceinline__ RawMix(uint32_t n) : a(0x243f6a8885a308d3ull ^ n), b(0x13198a2e03707344ull + 0x9e3779b97f4a7c15ull * n) {}
+  // seed > 0 only after a verified collision (k_raw_verify): the table is rebuilt with new hashes
+  __device__ __forceinline__ RawMix(uint32_t n, uint32_t seed)
+      : a((0x243f6a8885a308d3ull ^ n) + 0xa0761d6478bd642full * seed),
+        b(0x13198a2e03707344ull + 0x9e3779b97f4a7c15ull * n + 0xe7037ed1a0b428dbull * seed) {}
   __device__ __forceinline__ void add(uint64_t w) {  // the next (up to) 8 bytes, little-endian
     a = (a ^ w) * 0x100000001b3ull;
     a ^= a >> 29;
@@ -1104,57 +1153,54 @@ struct RawMix {
 // from elsewhere). ALIGNED (text 4-byte aligned): the rounds' bytes come from aligned 32-bit
 // words joined by funnel shifts (never a word past the one holding the token's last byte);
 // otherwise byte loads. Both feed identical 8-byte words.
+// the (up to) 8 bytes [p, p + m) of text as a little-endian word, zero-padded. ALIGNED (text
+// 4-byte aligned): from aligned 32-bit words joined by funnel shifts (never a word past the one
+// holding the last byte); otherwise byte loads.
 template <bool ALIGNED>
-__device__ __forceinline__ ulonglong2 raw_key(const uint8_t* __restrict__ text, uint64_t beg, uint32_t n) {
-  RawMix h(n);
+__device__ __forceinline__ uint64_t load_word8(const uint8_t* __restrict__ text, uint64_t p, uint32_t m) {
   if (ALIGNED) {
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(text);
-    uint64_t p = beg;
-    const uint64_t e = beg + n;
-    while (p < e) {
-      const uint32_t m = (uint32_t)min((uint64_t)8, e - p);
-      const uint32_t sh = (uint32_t)(p & 3) * 8;
-      const uint64_t wi = p >> 2, wl = (p + m - 1) >> 2;  // words holding the round's first / last byte
-      const uint32_t w0 = __ldg(w32 + wi);
-      const uint32_t w1 = wl > wi ? __ldg(w32 + wi + 1) : 0u;
-      const uint32_t w2 = wl > wi + 1 ? __ldg(w32 + wi + 2) : 0u;
-      uint64_t w = ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
-      if (m < 8) w &= (1ull << (8 * m)) - 1ull;
-      h.add(w);
-      p += m;
-    }
-  } else {
-    const uint8_t* s = text + beg;
-    for (uint32_t i = 0; i < n; i += 8) {
-      uint64_t w = 0;
-      const uint32_t m = min(8u, n - i);
-      for (uint32_t j = 0; j < m; ++j) w |= (uint64_t)__ldg(s + i + j) << (8 * j);
-      h.add(w);
-    }
+    const uint32_t sh = (uint32_t)(p & 3) * 8;
+    const uint64_t wi = p >> 2, wl = (p + m - 1) >> 2;  // words holding the first / last byte
+    const uint32_t w0 = __ldg(w32 + wi);
+    const uint32_t w1 = wl > wi ? __ldg(w32 + wi + 1) : 0u;
+    const uint32_t w2 = wl > wi + 1 ? __ldg(w32 + wi + 2) : 0u;
+    uint64_t w = ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
+    if (m < 8) w &= (1ull << (8 * m)) - 1ull;
+    return w;
   }
+  uint64_t w = 0;
+  for (uint32_t j = 0; j < m; ++j) w |= (uint64_t)__ldg(text + p + j) << (8 * j);
+  return w;
+}
+
+template <bool ALIGNED>
+__device__ __forceinline__ ulonglong2 raw_key(const uint8_t* __restrict__ text, uint64_t beg, uint32_t n,
+                                              uint32_t seed) {
+  RawMix h(n, seed);
+  for (uint32_t i = 0; i < n; i += 8) h.add(load_word8<ALIGNED>(text, beg + i, min(8u, n - i)));
   return h.key();
 }
 
-__device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
-  ulonglong2 old;
-  asm volatile(
-      "{\n\t.reg .b128 c, v, o;\n\t"
-      "mov.b128 c, {%2, %3};\n\tmov.b128 v, {%4, %5};\n\t"
-      "atom.global.cas.b128 o, [%6], c, v;\n\t"
-      "mov.b128 {%0, %1}, o;\n\t}"
-      : "=l"(old.x), "=l"(old.y)
-      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
-      : "memory");
-  return old;
+// byte equality of text[a, a + n) and text[b, b + n), 8 bytes per step
+template <bool ALIGNED>
+__device__ __forceinline__ bool bytes_equal(const uint8_t* __restrict__ text, uint64_t a, uint64_t b, uint32_t n) {
+  for (uint32_t i = 0; i < n; i += 8) {
+    const uint32_t m = min(8u, n - i);
+    if (load_word8<ALIGNED>(text, a + i, m) != load_word8<ALIGNED>(text, b + i, m)) return false;
+  }
+  return true;
 }
 
 template <bool ALIGNED>
 __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
                              const uint32_t* __restrict__ tlen, uint64_t n, ulonglong2* __restrict__ key,
                              uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ tslot) {
+                             uint32_t* __restrict__ tslot, uint32_t seed, int32_t weak) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const ulonglong2 k = raw_key<ALIGNED>(text, tbeg[i], tlen[i]);
+    // weak (test hook): at seed 0 every equal-length string collides, so verification must reseed
+    const ulonglong2 k = weak && seed == 0 ? make_ulonglong2((uint64_t)tlen[i] | 1ull, 1ull)
+                                           : raw_key<ALIGNED>(text, tbeg[i], tlen[i], seed);
     uint32_t slot = (uint32_t)k.x & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
@@ -1177,6 +1223,21 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
       }
       slot = (slot + 1) & (cap - 1);
     }
+  }
+}
+
+// Identity of raw strings is BYTE equality (the reference's string map, vocabulary.hpp:26-33):
+// every token is compared with its slot's first occurrence. A mismatch is a 128-bit collision
+// of distinct strings; the host then rebuilds the table with another seed (cnt[2] flags it).
+template <bool ALIGNED>
+__global__ void k_raw_verify(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
+                             const uint32_t* __restrict__ tlen, uint64_t n, const uint32_t* __restrict__ tslot,
+                             const uint32_t* __restrict__ first, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = first[tslot[i]];
+    if (f == (uint32_t)i) continue;
+    const uint32_t len = tlen[i];
+    if (tlen[f] != len || !bytes_equal<ALIGNED>(text, tbeg[i], tbeg[f], len)) atomicOr(cnt + 2, 1u);
   }
 }
 
@@ -1444,7 +1505,8 @@ int32_t vocab_reserve(sl_vocab* v, uint64_t n_entries, uint64_t n_bytes, cudaStr
     SL_CUDA_TRY(cudaMemsetAsync(v->tkey, 0, want * 8, st));
     v->tcap = (uint32_t)want;
     if (v->V) {
-      k_table_rehash<<<grid_for(v->V), 256, 0, st>>>(v->offs, v->bytes, v->V, v->tkey, v->tval, v->tcap, v->h2);
+      k_table_rehash<<<grid_for(v->V), 256, 0, st>>>(v->offs, v->bytes, v->V, v->tkey, v->tval, v->tcap, v->h2,
+                                                         v->weak);
       ++t_launches;
     }
   }
@@ -1580,24 +1642,32 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 19));
     ulonglong2* key = nullptr;
     uint32_t *first = nullptr, *cntr = nullptr;
-    SL_TTRY(scr.alloc(&cntr, 2));
-    for (;;) {
+    SL_TTRY(scr.alloc(&cntr, 3));
+    const bool al = (reinterpret_cast<uintptr_t>(text) & 3u) == 0;
+    for (uint32_t seed = 0;;) {
       SL_TTRY(scr.alloc(&key, cap));
       SL_TTRY(scr.alloc(&first, cap));
       if (cudaMemsetAsync(key, 0, cap * 16, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
-          cudaMemsetAsync(cntr, 0, 8, st) != cudaSuccess)
+          cudaMemsetAsync(cntr, 0, 12, st) != cudaSuccess)
         return fail((set_error("memset"), SL_ECUDA));
-      if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0)
+      if (al) {
         k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
-                                                            r_tslot);
-      else
+                                                            r_tslot, seed, v->weak);
+        k_raw_verify<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, first, cntr);
+      } else {
         k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
-                                                             r_tslot);
-      ++t_launches;
-      uint32_t h[2];
-      SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 8, cudaMemcpyDeviceToHost, st));
+                                                             r_tslot, seed, v->weak);
+        k_raw_verify<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, first, cntr);
+      }
+      t_launches += 2;
+      uint32_t h[3];
+      SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 12, cudaMemcpyDeviceToHost, st));
       SL_CUDA_TRY(cudaStreamSynchronize(st));
-      if (!h[1] && (uint64_t)h[0] * 2 <= cap) break;
+      if (!h[1] && (uint64_t)h[0] * 2 <= cap && !h[2]) break;
+      if (h[2]) {  // verified collision of distinct raw strings: new hashes, same table size
+        if (++seed > 8) return fail((set_error("tokenize: raw-string hash collisions persist across seeds"), SL_ECUDA));
+        continue;
+      }
       if (cap >= (1ull << 31)) return fail((set_error("tokenize: too many distinct tokens in one batch"), SL_EUNSUPPORTED));
       cap = std::min<uint64_t>(cap * 4, 1ull << 31);
     }
@@ -1639,6 +1709,7 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
   na.stop = sv;
   na.voc = VocabView{v->tkey, v->tval, v->V ? v->tcap : 0u, v->offs, v->h2, v->bytes};
   na.err = err;
+  na.weak = v->weak;
   const uint64_t nR = R;
   SL_TTRY(scr.alloc(&na.keep, nR));
   SL_TTRY(scr.alloc(&na.id, nR));
@@ -1689,65 +1760,74 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
       uint32_t *ntok, *slots, *fk, *k0, *k1, *v0, *v1, *elen, *epos, *cnt2;
       SL_TTRY(scr.alloc(&ntok, M));
       k_compact_idx<<<grid_for(nR), 256, 0, st>>>(nflag, npos, nR, ntok); ++t_launches;
-      // distinct new strings: batch-local hash table keyed by the first hash, value = the
-      // smallest token index (first occurrence); grows and retries on overflow
+      // distinct new strings: batch-local table keyed by 128-bit hashes, value = the smallest
+      // raw-entry index (first occurrence); grows and retries on overflow; identity verified by
+      // bytes (k_dedup_assign), a verified collision redoes the dedup with reseeded keys
       uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(M, 1ull << 22));
-      uint64_t* key = nullptr;
-      uint32_t *first = nullptr, *rank = nullptr, *sflag = nullptr, *spos = nullptr;
+      ulonglong2* key = nullptr;
+      uint32_t *first = nullptr, *rank = nullptr, *sflag = nullptr, *spos = nullptr, *gs_k = nullptr;
+      uint64_t *kx, *ky;
       SL_TTRY(scr.alloc(&cnt2, 2));
-      for (;;) {
-        SL_TTRY(scr.alloc(&key, cap));
-        SL_TTRY(scr.alloc(&first, cap));
-        if (cudaMemsetAsync(key, 0, cap * 8, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
-            cudaMemsetAsync(cnt2, 0, 8, st) != cudaSuccess)
-          return fail((set_error("memset"), SL_ECUDA));
-        k_dedup_insert<<<grid_for(M), 256, 0, st>>>(ntok, M, na.h1, key, first, (uint32_t)cap, cnt2); ++t_launches;
-        uint32_t h[2];
-        SL_CUDA_TRY(cudaMemcpyAsync(h, cnt2, 8, cudaMemcpyDeviceToHost, st));
-        SL_CUDA_TRY(cudaStreamSynchronize(st));
-        if (!h[1] && (uint64_t)h[0] * 2 <= cap) break;
-        if (cap >= (1ull << 31)) return fail((set_error("tokenize: too many distinct tokens in one batch"), SL_EUNSUPPORTED));
-        cap = std::min<uint64_t>(cap * 4, 1ull << 31);
-      }
-      SL_TTRY(scr.alloc(&sflag, cap));
-      SL_TTRY(scr.alloc(&spos, cap));
-      SL_TTRY(scr.alloc(&rank, cap));
-      k_slot_flags<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
+      SL_TTRY(scr.alloc(&kx, M));
+      SL_TTRY(scr.alloc(&ky, M));
       uint32_t G = 0;
-      SL_TTRY(exclusive_scan_u32(sflag, spos, cap, st, &G));
-      SL_TTRY(scr.alloc(&slots, G));
-      SL_TTRY(scr.alloc(&fk, G));
-      SL_TTRY(scr.alloc(&k0, G));
-      SL_TTRY(scr.alloc(&k1, G));
-      SL_TTRY(scr.alloc(&v0, G));
-      SL_TTRY(scr.alloc(&v1, G));
-      SL_TTRY(scr.alloc(&elen, G));
-      SL_TTRY(scr.alloc(&epos, G));
-      k_slot_list<<<grid_for(cap), 256, 0, st>>>(sflag, spos, first, (uint32_t)cap, slots, fk); ++t_launches;
-      // groups in first-occurrence order (document order, then position)
-      const uint32_t *fs, *ss;
-      SL_TTRY(radix_sort_pairs(fk, slots, G, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
-      uint32_t *gs_k, *gs_slot;
-      SL_TTRY(scr.alloc(&gs_k, G));
-      SL_TTRY(scr.alloc(&gs_slot, G));
-      SL_CUDA_TRY(cudaMemcpyAsync(gs_k, fs, G * 4ull, cudaMemcpyDeviceToDevice, st));     // first token per rank
-      SL_CUDA_TRY(cudaMemcpyAsync(gs_slot, ss, G * 4ull, cudaMemcpyDeviceToDevice, st));  // slot per rank
-      k_group_rank<<<grid_for(G), 256, 0, st>>>(gs_slot, G, rank); ++t_launches;
       const uint32_t V0 = v->V;
-      k_dedup_assign<<<grid_for(M), 256, 0, st>>>(ntok, M, na.h1, na.h2, na.flen, key, first, rank, (uint32_t)cap, V0,
-                                                  na.id, err);
-      ++t_launches;
+      for (uint32_t seed = 0;; ++seed) {
+        k_new_keys<<<grid_for(M), 256, 0, st>>>(ntok, M, na.h1, na.h2, na.arena, na.tbeg, na.flen, seed, na.weak, kx,
+                                                ky);
+        ++t_launches;
+        for (;;) {
+          SL_TTRY(scr.alloc(&key, cap));
+          SL_TTRY(scr.alloc(&first, cap));
+          if (cudaMemsetAsync(key, 0, cap * 16, st) != cudaSuccess ||
+              cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess || cudaMemsetAsync(cnt2, 0, 8, st) != cudaSuccess)
+            return fail((set_error("memset"), SL_ECUDA));
+          k_dedup_insert<<<grid_for(M), 256, 0, st>>>(ntok, M, kx, ky, key, first, (uint32_t)cap, cnt2); ++t_launches;
+          uint32_t h[2];
+          SL_CUDA_TRY(cudaMemcpyAsync(h, cnt2, 8, cudaMemcpyDeviceToHost, st));
+          SL_CUDA_TRY(cudaStreamSynchronize(st));
+          if (!h[1] && (uint64_t)h[0] * 2 <= cap) break;
+          if (cap >= (1ull << 31))
+            return fail((set_error("tokenize: too many distinct tokens in one batch"), SL_EUNSUPPORTED));
+          cap = std::min<uint64_t>(cap * 4, 1ull << 31);
+        }
+        SL_TTRY(scr.alloc(&sflag, cap));
+        SL_TTRY(scr.alloc(&spos, cap));
+        SL_TTRY(scr.alloc(&rank, cap));
+        k_slot_flags128<<<grid_for(cap), 256, 0, st>>>(key, (uint32_t)cap, sflag); ++t_launches;
+        SL_TTRY(exclusive_scan_u32(sflag, spos, cap, st, &G));
+        SL_TTRY(scr.alloc(&slots, G));
+        SL_TTRY(scr.alloc(&fk, G));
+        SL_TTRY(scr.alloc(&k0, G));
+        SL_TTRY(scr.alloc(&k1, G));
+        SL_TTRY(scr.alloc(&v0, G));
+        SL_TTRY(scr.alloc(&v1, G));
+        SL_TTRY(scr.alloc(&elen, G));
+        SL_TTRY(scr.alloc(&epos, G));
+        k_slot_list<<<grid_for(cap), 256, 0, st>>>(sflag, spos, first, (uint32_t)cap, slots, fk); ++t_launches;
+        // groups in first-occurrence order (document order, then position)
+        const uint32_t *fs, *ss;
+        SL_TTRY(radix_sort_pairs(fk, slots, G, 32, k0, k1, v0, v1, st, &fs, &ss, 0, nullptr));
+        uint32_t* gs_slot;
+        SL_TTRY(scr.alloc(&gs_k, G));
+        SL_TTRY(scr.alloc(&gs_slot, G));
+        SL_CUDA_TRY(cudaMemcpyAsync(gs_k, fs, G * 4ull, cudaMemcpyDeviceToDevice, st));     // first token per rank
+        SL_CUDA_TRY(cudaMemcpyAsync(gs_slot, ss, G * 4ull, cudaMemcpyDeviceToDevice, st));  // slot per rank
+        k_group_rank<<<grid_for(G), 256, 0, st>>>(gs_slot, G, rank); ++t_launches;
+        if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return fail((set_error("memset"), SL_ECUDA));
+        k_dedup_assign<<<grid_for(M), 256, 0, st>>>(ntok, M, kx, ky, na.flen, na.arena, na.tbeg, key, first, rank,
+                                                    (uint32_t)cap, V0, na.id, err);
+        ++t_launches;
+        uint32_t h_err = 0;
+        SL_CUDA_TRY(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+        SL_CUDA_TRY(cudaStreamSynchronize(st));
+        if (!(h_err & 4u)) break;
+        if (seed >= 8) return fail((set_error("tokenize: normalised-string hash collisions persist across seeds"), SL_ECUDA));
+      }
       // append strings
       k_new_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, na.flen, elen); ++t_launches;
       uint32_t ebytes = 0;
       SL_TTRY(exclusive_scan_u32(elen, epos, G, st, &ebytes));
-      uint32_t h_err = 0;
-      SL_CUDA_TRY(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-      SL_CUDA_TRY(cudaStreamSynchronize(st));
-      if (h_err) {
-        set_error("tokenize: 128-bit token hash collision between distinct strings");
-        return fail(SL_EUNSUPPORTED);
-      }
       SL_TTRY(vocab_reserve(v, (uint64_t)V0 + G, v->bused + ebytes, st));
       k_copy_entries<<<grid_for(G), 256, 0, st>>>(gs_k, G, na.tbeg, na.flen, na.arena, epos, v->bused, V0, na.h2,
                                                   v->bytes, v->offs, v->h2); ++t_launches;
@@ -1786,8 +1866,8 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     return fail((set_error(std::string("tokenize: CUDA failure: ") + cudaGetErrorString(cudaGetLastError())),
                  SL_ECUDA));
   if (h_err) {
-    set_error("tokenize: 128-bit token hash collision between distinct strings");
-    return fail(SL_EUNSUPPORTED);
+    set_error("tokenize: internal table error");
+    return fail(SL_ECUDA);
   }
 #undef SL_TTRY
   *out = tb;
@@ -1807,6 +1887,7 @@ int32_t sl_vocab_create(int32_t device, sl_vocab** out) {
   SL_TRY(text_stream(device, &st));
   auto* v = new sl_vocab();
   v->device = device;
+  if (const char* e = std::getenv("SL_TEXT_WEAK_HASH")) v->weak = *e && *e != '0';
   const int32_t rc = vocab_reserve(v, 16, 256, st);
   cudaStreamSynchronize(st);
   if (rc != SL_OK) {
@@ -1867,7 +1948,7 @@ int32_t sl_vocab_import(sl_vocab* v, const uint64_t* offsets, const char* bytes,
     SL_CUDA_TRY(cudaMemsetAsync(v->tkey, 0, v->tcap * 8ull, st));
     v->V = n;
     v->bused = nbytes;
-    k_table_rehash<<<grid_for(n), 256, 0, st>>>(v->offs, v->bytes, n, v->tkey, v->tval, v->tcap, v->h2);
+    k_table_rehash<<<grid_for(n), 256, 0, st>>>(v->offs, v->bytes, n, v->tkey, v->tval, v->tcap, v->h2, v->weak);
     ++t_launches;
   }
   SL_CUDA_TRY(cudaStreamSynchronize(st));

@@ -325,3 +325,31 @@ def test_stream_tokenize_matches_single_call(cuda_ok, port, chunk):
     # capacity too small fails loudly
     with pytest.raises(ValueError, match="ids_capacity"):
         T.tokenize_query_stream(text, off, cfg, v, chunk_bytes=chunk, out_ids=np.empty(3, np.uint32))
+
+
+@pytest.mark.parametrize("lc,stop,stem", [(True, True, True), (False, False, False)])
+def test_identity_is_bytes_under_forced_collisions(cuda_ok, port, monkeypatch, lc, stop, stem):
+    """Vocabulary identity is byte equality (vocabulary.hpp:26-33), not a hash: with
+    SL_TEXT_WEAK_HASH=1 every raw string of one length collides in the raw-string table, every
+    new normalised string of one length collides in the dedup table and all vocabulary first
+    hashes fall into 4 values. Byte verification reseeds the tables / keeps probing, and the
+    ids, offsets and vocabulary stay identical to the oracle (incremental builds and query mode
+    included)."""
+    monkeypatch.setenv("SL_TEXT_WEAK_HASH", "1")
+    words = make_words(3000, seed=12, unicode_frac=0.08)
+    t1, o1 = make_corpus(1500, words[:2000], seed=8, malformed_frac=0.02, case_frac=0.3)
+    t2, o2 = make_corpus(800, words, seed=9, case_frac=0.3)
+    v = T.Vocabulary()
+    g1 = gpu_tokenize(t1, o1, lc, stop, stem, v)
+    g2 = gpu_tokenize(t2, o2, lc, stop, stem, v)
+    ov = port.vocab_new()
+    w1 = port.tokenize_corpus(t1, o1, lc, stop, stem, vocab=ov)
+    w2 = port.tokenize_corpus(t2, o2, lc, stop, stem, vocab=ov)
+    for g, w in ((g1, w1), (g2, w2)):
+        assert np.array_equal(g[0], w[0]) and np.array_equal(g[1], w[1])
+    assert v.tokens() == port.vocab_tokens(ov)
+    tq, oq = make_corpus(200, words + make_words(300, seed=98), seed=5, mean_words=6)
+    lists = T.tokenize_query((tq, oq), cfg_of(lc, stop, stem), v).lists()
+    for d in range(len(oq) - 1):
+        assert lists[d] == port.tokenize(ov, tq[oq[d]:oq[d + 1]], False, lc, stop, stem)
+    port.vocab_free(ov)
