@@ -144,7 +144,10 @@ def lib() -> C.CDLL:
         # library's lazily-resolved NCCL binds to the same copy torch.distributed uses.
         import torch  # noqa: F401
         L = C.CDLL(LIB_PATH)
+        ab_build = bool(os.environ.get("SPARSELEX_LIB"))  # A/B tuning builds may predate some entry points
         for name, (res, args) in SIGNATURES.items():
+            if ab_build and not hasattr(L, name):
+                continue
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

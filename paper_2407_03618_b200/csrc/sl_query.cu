@@ -229,7 +229,7 @@ enum GroupMode { GM_TOPK = 0, GM_DENSE = 1 };
 
 constexpr int ULOG = 8;  // undo-log capacity in gather slots
 #ifndef SL_RMAX_CT
-#define SL_RMAX_CT 2  // two queries of one dense signature per warp item, the second via the undo log
+#define SL_RMAX_CT 4  // up to four queries of one dense signature per warp item (all but the last via the undo log)
 #endif
 constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) handled by one warp
 #ifndef SL_UNROLL
@@ -1051,62 +1051,52 @@ __device__ __forceinline__ bool same_signature(const int32_t* qdense, const uint
   return true;
 }
 
-// Runs over the signature-sorted queries: maximal stretches of identical signatures, cut
-// every R queries. One block of 1024 threads walks the batch in chunks.
-__global__ void __launch_bounds__(1024) k_build_runs(const uint32_t* __restrict__ perm, uint32_t B,
-                                                     const int32_t* __restrict__ qdense,
-                                                     const uint32_t* __restrict__ nden,
-                                                     const uint32_t* __restrict__ ngath, uint32_t qmax, uint32_t R,
-                                                     uint32_t* __restrict__ run_begin, uint32_t* __restrict__ n_runs) {
-  __shared__ uint32_t sw[40];
-  __shared__ uint32_t wmax[32];
-  __shared__ uint32_t carry_start, carry_count;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    carry_start = 0;
-    carry_count = 0;
+// Runs over the signature-sorted queries: a run is <= R consecutive queries of one dense
+// signature whose gathered rows fit the warp's 32 lanes together. Three steps: signature-group
+// heads (k_sig_heads) -> group starts (k_group_starts, after a scan of the heads) -> one thread
+// per group packs its members greedily in query order (k_pack_runs: count pass, scan of the
+// per-group run counts, write pass).
+__global__ void k_sig_heads(const uint32_t* __restrict__ perm, uint32_t B, const int32_t* __restrict__ qdense,
+                            const uint32_t* __restrict__ nden, uint32_t qmax, uint32_t* __restrict__ flag) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || !same_signature(qdense, nden, qmax, perm[i], perm[i - 1])) ? 1u : 0u;
+}
+
+__global__ void k_group_starts(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint32_t B,
+                               uint32_t* __restrict__ gstart) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
+    if (flag[i]) gstart[pos[i]] = i;
+    if (i == B - 1) gstart[pos[i] + flag[i]] = B;
   }
-  __syncthreads();
-  for (uint32_t base = 0; base < B; base += blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
-    const bool valid = i < B;
-    const bool sighead = valid && (i == 0 || !same_signature(qdense, nden, qmax, perm[i], perm[i - 1]));
-    // inclusive max-scan of signature-run heads -> start of i's signature run
-    uint32_t m = sighead ? i : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, m, o);
-      if (lane >= o) m = max(m, t);
-    }
-    if (lane == 31) wmax[w] = m;
-    __syncthreads();
-    if (w == 0) {
-      uint32_t x = wmax[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x = max(x, t);
+}
+
+template <bool WRITE>
+__global__ void k_pack_runs(const uint32_t* __restrict__ gstart, const uint32_t* __restrict__ flag,
+                            const uint32_t* __restrict__ pos, uint32_t B, const uint32_t* __restrict__ perm,
+                            const uint32_t* __restrict__ ngath, uint32_t R, uint32_t* __restrict__ gcnt,
+                            const uint32_t* __restrict__ goff, uint32_t* __restrict__ run_begin,
+                            uint32_t* __restrict__ n_runs) {
+  const uint32_t G = pos[B - 1] + flag[B - 1];
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    const uint32_t b = gstart[g], e = gstart[g + 1];
+    uint32_t runs = 0, in_run = 0, ent = 0;
+    for (uint32_t i = b; i < e; ++i) {
+      const uint32_t ng = ngath[perm[i]];
+      if (in_run == 0 || in_run == R || ent + ng > 32u) {
+        if (WRITE) run_begin[goff[g] + runs] = i;
+        ++runs;
+        in_run = 0;
+        ent = 0;
       }
-      wmax[lane] = x;
+      ++in_run;
+      ent += ng;
     }
-    __syncthreads();
-    const uint32_t prev = w > 0 ? wmax[w - 1] : 0u;
-    const uint32_t start = max(max(m, prev), carry_start);
-    // chunks of R queries from the signature run's start; a member whose gathered rows would
-    // push the run past 32 entries (one lane each) starts its own run (pairwise rule: RMAX <= 2)
-    static_assert(RMAX <= 2, "k_build_runs' entry budget checks pairs only");
-    const bool head = valid && ((i - start) % R == 0 || ngath[perm[i - 1]] + ngath[perm[i]] > 32u);
-    uint32_t tot;
-    const uint32_t off = block_excl_scan(head ? 1u : 0u, sw, &tot) + carry_count;
-    if (head) run_begin[off] = i;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1 || i == B - 1) carry_start = start;
-    if (threadIdx.x == 0) carry_count += tot;
-    __syncthreads();
+    if (!WRITE) gcnt[g] = runs;
   }
-  if (threadIdx.x == 0) {
-    run_begin[carry_count] = B;
-    n_runs[0] = carry_count;
+  if (WRITE && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t total = goff[G - 1] + gcnt[G - 1];
+    run_begin[total] = B;
+    n_runs[0] = total;
     n_runs[1] = 0;  // work-item counter of k_score_runs
   }
 }
@@ -1390,7 +1380,7 @@ struct RunPlan {
 int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, RunPlan* p) {
   p->C = kept_capacity(k);
   uint32_t R = (uint32_t)env_int("SL_RUN", 0);
-  if (R == 0) R = RMAX;
+  if (R == 0) R = 2;  // SL_RUN up to RMAX
   // the run builder keeps every run within 32 gathered entries (one lane each)
   p->R = std::max(1u, std::min<uint32_t>(R, RMAX));
   p->wpc = WPC;
@@ -1549,8 +1539,29 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, ngath, hk, hv); ++t_launches;
   const uint32_t *sk, *perm;
   SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
-  k_build_runs<<<1, 1024, 0, st>>>(perm, B_short, qdense, nden, ngath, qmax, plan.R, run_begin, n_runs);
-  ++t_launches;
+  if (B_short) {
+    uint32_t *flag, *pos, *gstart, *gcnt, *goff;
+    SL_TRY(scr.alloc(&flag, B_short));
+    SL_TRY(scr.alloc(&pos, B_short));
+    SL_TRY(scr.alloc(&gstart, (uint64_t)B_short + 1));
+    SL_TRY(scr.alloc(&gcnt, B_short));
+    SL_TRY(scr.alloc(&goff, B_short));
+    SL_CUDA_TRY(cudaMemsetAsync(gcnt, 0, (uint64_t)B_short * 4, st));
+    const unsigned g = (B_short + 255) / 256;
+    k_sig_heads<<<g, 256, 0, st>>>(perm, B_short, qdense, nden, qmax, flag); ++t_launches;
+    SL_TRY(exclusive_scan_u32(flag, pos, B_short, st, nullptr));
+    k_group_starts<<<g, 256, 0, st>>>(flag, pos, B_short, gstart); ++t_launches;
+    k_pack_runs<false><<<g, 256, 0, st>>>(gstart, flag, pos, B_short, perm, ngath, plan.R, gcnt, nullptr, nullptr,
+                                          nullptr);
+    ++t_launches;
+    SL_TRY(exclusive_scan_u32(gcnt, goff, B_short, st, nullptr));
+    k_pack_runs<true><<<g, 256, 0, st>>>(gstart, flag, pos, B_short, perm, ngath, plan.R, gcnt, goff, run_begin,
+                                         n_runs);
+    ++t_launches;
+  } else {
+    SL_CUDA_TRY(cudaMemsetAsync(n_runs, 0, 8, st));
+    SL_CUDA_TRY(cudaMemsetAsync(run_begin, 0, 4, st));
+  }
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;

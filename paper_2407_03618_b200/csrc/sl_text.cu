@@ -1192,16 +1192,42 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* __restrict__ text, ui
   return true;
 }
 
+// Identity of raw strings is BYTE equality (the reference's string map, vocabulary.hpp:26-33).
+// A token of at most 15 bytes IS its key: (bytes 0-7, bytes 8-14 | length << 56), so equal keys
+// mean equal strings by construction. Longer tokens key on a 128-bit hash (top byte 0xFF, which
+// no short key has); the claimant of such a slot records its (position << 24 | length) in
+// wrep[slot], and k_raw_verify_long then checks every long token byte by byte against its
+// slot's claimant. A mismatch (a verified 128-bit collision) makes the host rebuild the table
+// with another seed.
+#ifndef SL_EXACT_KEY_BYTES
+#define SL_EXACT_KEY_BYTES 15
+#endif
+constexpr uint32_t kExactKeyBytes = SL_EXACT_KEY_BYTES;
+
 template <bool ALIGNED>
 __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
                              const uint32_t* __restrict__ tlen, uint64_t n, ulonglong2* __restrict__ key,
-                             uint32_t* __restrict__ first, uint32_t cap, uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ tslot, uint32_t seed, int32_t weak) {
+                             uint32_t* __restrict__ first, uint64_t* __restrict__ wrep, uint32_t cap,
+                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ tslot, uint32_t seed, int32_t weak) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    // weak (test hook): at seed 0 every equal-length string collides, so verification must reseed
-    const ulonglong2 k = weak && seed == 0 ? make_ulonglong2((uint64_t)tlen[i] | 1ull, 1ull)
-                                           : raw_key<ALIGNED>(text, tbeg[i], tlen[i], seed);
-    uint32_t slot = (uint32_t)k.x & (cap - 1);
+    const uint64_t beg = tbeg[i];
+    const uint32_t len = tlen[i];
+    const bool exact = len <= kExactKeyBytes;
+    ulonglong2 k;
+    if (exact) {
+      k.x = load_word8<ALIGNED>(text, beg, min(8u, len));
+      k.y = (len > 8 ? load_word8<ALIGNED>(text, beg + 8, len - 8) : 0ull) | ((uint64_t)len << 56);
+    } else if (len >= 0xFFFFFFu) {  // (position, length) packs the length in 24 bits
+      atomicOr(cnt + 2, 2u);
+      continue;
+    } else if (weak && seed == 0) {  // test hook: every long string of one length collides
+      k = make_ulonglong2((uint64_t)len, 0xFFull << 56);
+    } else {
+      k = raw_key<ALIGNED>(text, beg, len, seed);
+      k.y |= 0xFFull << 56;
+    }
+    // probe start: mixed key (a short key's raw bytes are a poor hash); weak: length only
+    uint32_t slot = (uint32_t)(weak ? len * 0x9E3779B1u : fmix64(k.x ^ (k.y * 0x9e3779b97f4a7c15ull))) & (cap - 1);
     for (uint32_t probes = 0;; ++probes) {
       if (probes == cap) {
         atomicOr(cnt + 1, 1u);
@@ -1213,6 +1239,7 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
         if ((cur.x | cur.y) == 0ull) {
           atomicAdd(cnt, 1u);
           cur = k;
+          if (!exact) wrep[slot] = (beg << 24) | len;  // read by k_raw_verify_long (after this kernel)
         }
       }
       if (cur.x == k.x && cur.y == k.y) {
@@ -1226,18 +1253,37 @@ __global__ void k_raw_insert(const uint8_t* __restrict__ text, const uint64_t* _
   }
 }
 
-// Identity of raw strings is BYTE equality (the reference's string map, vocabulary.hpp:26-33):
-// every token is compared with its slot's first occurrence. A mismatch is a 128-bit collision
-// of distinct strings; the host then rebuilds the table with another seed (cnt[2] flags it).
+// Every hashed (long) token against its slot's claimant, byte by byte (cnt[2] on a mismatch).
+// A block takes 2048 tokens, queues its long ones in shared memory and verifies the queue with
+// all threads busy (long tokens are a minority: a per-token loop would idle most lanes).
+constexpr int kVerTile = 2048;
 template <bool ALIGNED>
-__global__ void k_raw_verify(const uint8_t* __restrict__ text, const uint64_t* __restrict__ tbeg,
-                             const uint32_t* __restrict__ tlen, uint64_t n, const uint32_t* __restrict__ tslot,
-                             const uint32_t* __restrict__ first, uint32_t* __restrict__ cnt) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t f = first[tslot[i]];
-    if (f == (uint32_t)i) continue;
-    const uint32_t len = tlen[i];
-    if (tlen[f] != len || !bytes_equal<ALIGNED>(text, tbeg[i], tbeg[f], len)) atomicOr(cnt + 2, 1u);
+__global__ void __launch_bounds__(256) k_raw_verify_long(const uint8_t* __restrict__ text,
+                                                         const uint64_t* __restrict__ tbeg,
+                                                         const uint32_t* __restrict__ tlen, uint64_t n,
+                                                         const uint32_t* __restrict__ tslot,
+                                                         const uint64_t* __restrict__ wrep, uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t q[kVerTile];
+  __shared__ uint32_t qn;
+  if (*(volatile uint32_t*)(cnt + 1)) return;  // the insert overflowed: the table is rebuilt anyway
+  for (uint64_t t0 = (uint64_t)blockIdx.x * kVerTile; t0 < n; t0 += (uint64_t)gridDim.x * kVerTile) {
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < kVerTile; j += blockDim.x) {
+      const uint64_t i = t0 + j;
+      if (i < n && tlen[i] > kExactKeyBytes) q[atomicAdd(&qn, 1u)] = j;
+    }
+    __syncthreads();
+    const uint32_t m = qn;
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      const uint64_t i = t0 + q[j];
+      const uint32_t len = tlen[i];
+      const uint64_t beg = tbeg[i];
+      const uint64_t rp = wrep[tslot[i]];
+      if ((rp >> 24) != beg && ((uint32_t)(rp & 0xFFFFFFu) != len || !bytes_equal<ALIGNED>(text, beg, rp >> 24, len)))
+        atomicOr(cnt + 2, 1u);
+    }
+    __syncthreads();
   }
 }
 
@@ -1640,30 +1686,36 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     SL_TTRY(scr.alloc(&r_tslot, n_tok));
     // sized for a Zipf vocabulary (grows 4x and retries when more than half full)
     uint64_t cap = pow2_at_least(2ull * std::min<uint64_t>(n_tok, 1ull << 19));
-    ulonglong2* key = nullptr;
     uint32_t *first = nullptr, *cntr = nullptr;
+    ulonglong2* key = nullptr;
+    uint64_t* wrep = nullptr;
     SL_TTRY(scr.alloc(&cntr, 3));
     const bool al = (reinterpret_cast<uintptr_t>(text) & 3u) == 0;
+    if (nb >> 40) return fail((set_error("tokenize: batch text beyond 2^40 bytes"), SL_EUNSUPPORTED));
     for (uint32_t seed = 0;;) {
       SL_TTRY(scr.alloc(&key, cap));
       SL_TTRY(scr.alloc(&first, cap));
+      SL_TTRY(scr.alloc(&wrep, cap));
       if (cudaMemsetAsync(key, 0, cap * 16, st) != cudaSuccess || cudaMemsetAsync(first, 0xFF, cap * 4, st) != cudaSuccess ||
           cudaMemsetAsync(cntr, 0, 12, st) != cudaSuccess)
         return fail((set_error("memset"), SL_ECUDA));
+      const unsigned vg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_tok + kVerTile - 1) / kVerTile,
+                                                                           8ull * text_sms()));
       if (al) {
-        k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
-                                                            r_tslot, seed, v->weak);
-        k_raw_verify<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, first, cntr);
+        k_raw_insert<true><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, wrep, (uint32_t)cap,
+                                                            cntr, r_tslot, seed, v->weak);
+        k_raw_verify_long<true><<<vg, 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, wrep, cntr);
       } else {
-        k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, (uint32_t)cap, cntr,
-                                                             r_tslot, seed, v->weak);
-        k_raw_verify<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, first, cntr);
+        k_raw_insert<false><<<grid_for(n_tok), 256, 0, st>>>(text, tbeg, tlen, n_tok, key, first, wrep, (uint32_t)cap,
+                                                             cntr, r_tslot, seed, v->weak);
+        k_raw_verify_long<false><<<vg, 256, 0, st>>>(text, tbeg, tlen, n_tok, r_tslot, wrep, cntr);
       }
       t_launches += 2;
       uint32_t h[3];
       SL_CUDA_TRY(cudaMemcpyAsync(h, cntr, 12, cudaMemcpyDeviceToHost, st));
       SL_CUDA_TRY(cudaStreamSynchronize(st));
       if (!h[1] && (uint64_t)h[0] * 2 <= cap && !h[2]) break;
+      if (h[2] & 2u) return fail((set_error("tokenize: a token longer than 16 MiB"), SL_EUNSUPPORTED));
       if (h[2]) {  // verified collision of distinct raw strings: new hashes, same table size
         if (++seed > 8) return fail((set_error("tokenize: raw-string hash collisions persist across seeds"), SL_ECUDA));
         continue;
