@@ -152,6 +152,34 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
 #ifndef SL_DENSE_ASYNC
 #define SL_DENSE_ASYNC 1
 #endif
+#ifndef SL_DENSE_TMA
+#define SL_DENSE_TMA 1  // first dense row of a tile by one bulk copy (cp.async.bulk + mbarrier) per warp
+#endif
+
+// ---- 1-D bulk copy global -> shared completing on an mbarrier (Hopper+ TMA engine, no tensor map)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one lane: arm the barrier for `bytes` and start the copy (dst, src, bytes: 16-byte multiples)
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
 
 // warp-level variant with 4-bit digits (16-bin warp-private histogram, 64 bytes)
 template <class Visit>
@@ -177,6 +205,67 @@ __device__ uint64_t warp_select_kth(Visit visit, uint32_t k, uint32_t* hist) {
     prefix |= (uint64_t)(15 - src) << shift;
     mask |= 0xFull << shift;
     if (cnt == need) break;
+  }
+  return prefix;
+}
+
+#ifndef SL_BALLOT_SELECT
+#define SL_BALLOT_SELECT 0  // measured: c2 top-10 -2.6%, c4 top-1000 -2.5% (register allocation)
+#endif
+
+// The exact k-th largest among the keys kept[0, nk) and this lane's tile candidates (bits of pm
+// over buf, keys >= lo): MSD radix select with 4-bit digits like warp_select_kth, but the bin
+// counts of each pass come from ballots instead of shared-memory atomics (lane b < 16 counts
+// bin b from the four digit-bit ballots), so a pass costs a few warp-wide instructions per 32
+// keys however skewed the digits are. Warp-synchronous: every lane runs the same trip counts.
+__device__ __forceinline__ uint64_t warp_select_kth_tile(const uint64_t* kept, uint32_t nk, uint32_t pm,
+                                                         const float* bf, uint32_t gdoc0, uint64_t lo, uint32_t k) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t tile_iters = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(pm));
+  uint64_t prefix = 0, mask = 0;
+  uint32_t need = k;
+  for (int shift = 60; shift >= 0; shift -= 4) {
+    uint32_t cnt = 0;
+    auto add = [&](bool v, uint64_t x) {
+      const bool m = v && (x & mask) == prefix;
+      const uint32_t bm = __ballot_sync(0xffffffffu, m);
+      if (!bm) return;
+      const uint32_t d = (uint32_t)(x >> shift) & 15u;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, d & 1u), b1 = __ballot_sync(0xffffffffu, d & 2u);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, d & 4u), b3 = __ballot_sync(0xffffffffu, d & 8u);
+      const uint32_t sel = bm & ((lane & 1) ? b0 : ~b0) & ((lane & 2) ? b1 : ~b1) & ((lane & 4) ? b2 : ~b2) &
+                           ((lane & 8) ? b3 : ~b3);
+      cnt += __popc(sel);
+    };
+    for (uint32_t base = 0; base < nk; base += 32) {
+      const uint32_t i = base + lane;
+      add(i < nk, i < nk ? kept[i] : 0ull);
+    }
+    uint32_t m = pm;
+    for (uint32_t it = 0; it < tile_iters; ++it) {
+      bool v = m != 0;
+      uint64_t key = 0;
+      if (v) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t dl = 4 * (lane + 32 * (bit >> 2)) + (bit & 3);
+        key = make_key(bf[dl], gdoc0 + dl);
+        v = key >= lo;
+      }
+      add(v, key);
+    }
+    // buckets high -> low: lane j < 16 takes bin 15 - j
+    const uint32_t cj = __shfl_sync(0xffffffffu, cnt, 15 - (lane & 15));
+    const uint32_t c = lane < 16 ? cj : 0u;
+    const uint32_t incl = warp_incl_scan(c), excl = incl - c;
+    const bool mine = lane < 16 && excl < need && need <= incl;
+    const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    const uint32_t above = __shfl_sync(0xffffffffu, excl, src);
+    const uint32_t cb = __shfl_sync(0xffffffffu, c, src);
+    need -= above;
+    prefix |= (uint64_t)(15 - src) << shift;
+    mask |= 0xFull << shift;
+    if (cb == need) break;
   }
   return prefix;
 }
@@ -293,6 +382,10 @@ struct __align__(16) WarpSmem {
   uint64_t* keptp[RMAX];      // its candidate slot for this split
   int32_t ebeg[RMAX + 1];     // query r owns entries [ebeg[r], ebeg[r+1])
   int32_t nd[1];
+#if SL_DENSE_TMA
+  uint64_t mbar[1];           // completion of the first dense row's bulk copy
+  uint32_t mphase[1];         // parity of its next completion
+#endif
 };
 
 
@@ -439,12 +532,16 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
     __syncwarp();
     if (lane == 0) s.n_kept[r] = nk + P;
   } else {
+#if SL_BALLOT_SELECT
+    const uint64_t nt = warp_select_kth_tile(kept, nk, pm, bf, gdoc0, tau, k);
+#else
     const uint64_t nt = warp_select_kth(
         [&](auto&& fn) {
           for (uint32_t i = lane; i < nk; i += 32) fn(kept[i]);
           tile_visit(tau, fn);
         },
         k, s.hist);
+#endif
     // in-place compaction of kept (destination never passes the source chunk)
     uint32_t out = 0;
     for (uint32_t b = 0; b < nk; b += 32) {
@@ -497,6 +594,13 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   const uint32_t n_runs = *ra.n_runs;
   const uint32_t total = n_runs * ra.n_splits;
   WarpSmem& s = wsm[warp];
+#if SL_DENSE_TMA
+  if (lane == 0) {
+    mbar_init(s.mbar, 1);
+    s.mphase[0] = 0;
+  }
+  __syncwarp();
+#endif
   for (;;) {
   uint32_t it = 0;
   if (lane == 0) it = atomicAdd(ra.work, 1u);
@@ -700,15 +804,33 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         for (int rr = 0; rr < F4L; ++rr) dsum4[lane + 32 * rr] = make_float4(0.f, 0.f, 0.f, 0.f);
         return 0.f;
       }
+#if SL_DENSE_TMA
+      // the whole 4 KB row tile by one bulk copy: order this warp's earlier generic accesses to
+      // the buffer before the async-proxy write, then lane 0 arms the barrier and starts the copy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        bulk_copy_g2s(s.dsum, ix.dense + (uint64_t)s.dslot[0] * ix.n_pad + d0, TILE * 4u, s.mbar);
+#else
       {
         const float4* row0 = dbase + (uint64_t)s.dslot[0] * rstride;
 #pragma unroll
         for (int rr = 0; rr < F4L; ++rr) __pipeline_memcpy_async(dsum4 + lane + 32 * rr, row0 + 32 * rr, 16);
         __pipeline_commit();
       }
+#endif
 #pragma unroll 1
       for (int c0 = 0; c0 < F4L; c0 += DCH) {
+#if SL_DENSE_TMA
+        if (c0 == 0) {
+          const uint32_t ph = s.mphase[0];
+          mbar_wait(s.mbar, ph);
+          __syncwarp();
+          if (lane == 0) s.mphase[0] = ph ^ 1u;
+        }
+#else
         if (c0 == 0) __pipeline_wait_prior(0);
+#endif
         float4 a[DCH];
 #pragma unroll
         for (int rr = 0; rr < DCH; ++rr) a[rr] = dsum4[lane + 32 * (c0 + rr)];

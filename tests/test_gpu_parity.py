@@ -438,7 +438,6 @@ def test_zero_ties_after_split_threshold_published(cuda_ok, monkeypatch):
             for _ in range(3):
                 gid, gsc = retrieve_batch(gi, (qo, qt), 10, as_arrays=True)
                 np.testing.assert_array_equal(gid[0], rid[0].astype(np.uint32), err_msg=f"splits {splits}")
-    assert T * 20 == N
 
 
 @pytest.mark.parametrize("p", [BM25Params(Variant.lucene), BM25Params(Variant.robertson),
