@@ -473,3 +473,24 @@ def test_query_chunking_bit_identical(cuda_ok, c1, monkeypatch, k):
         ids2, sc2 = retrieve_batch(gi, (qoff, qtok), k, as_arrays=True)
     np.testing.assert_array_equal(sc1, sc2)
     np.testing.assert_array_equal(ids1, ids2)
+
+
+@pytest.mark.parametrize("V", [2, 100, 5_000, 300_000, 1 << 22, (1 << 22) + 5])
+def test_build_sort_tiles_and_digit_widths(cuda_ok, V):
+    """The build's stable (token, doc) sort across digit widths (1 .. 23-bit keys: 1 to 4 radix
+    passes) and tile shapes: documents longer than a sort tile, empty documents, one hot token,
+    a tail that is not a whole tile, token ids up to V - 1 — CSC equal to the oracle's."""
+    rng = np.random.default_rng(V)
+    lens = rng.integers(0, 40, 3000)
+    lens[::97] = 0
+    lens[5], lens[1700] = 9000, 13000  # longer than a sort tile
+    off = np.zeros(len(lens) + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    T = int(off[-1])
+    tok = np.minimum(rng.zipf(1.1, T) - 1, V - 1).astype(np.uint32)
+    tok[rng.random(T) < 0.05] = V - 1
+    tok[int(off[5]):int(off[6])] = 0  # one document of a single hot token
+    p = BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)
+    ox = oracle.OracleIndex(off, tok, V, int(p.variant), p.k1, p.b, p.delta).export()
+    with build_index(off, tok, V, p, keep_tf=True) as gi:
+        assert_index_equal(gi.export(tf=True), ox, f"V={V}")
