@@ -389,35 +389,88 @@ __global__ void k_classify16(TextView t, uint32_t* __restrict__ wbits, uint32_t*
   }
 }
 
-// token ending at the first non-word byte or document start after p; codepoint count
-__device__ __forceinline__ void token_extent(const uint32_t* wbits, const uint32_t* sbits, const uint32_t* dbits,
-                                             uint64_t nw, uint64_t p, uint64_t* end, uint32_t* ncp) {
-  uint64_t k = p >> 5;
-  const uint32_t j = (uint32_t)(p & 31);
-  uint32_t stop = (~wbits[k] | dbits[k]) & (j == 31 ? 0u : (0xFFFFFFFFu << (j + 1)));  // bits > j
-  uint32_t from = 0xFFFFFFFFu << j;                                                  // bits >= j
-  uint32_t cnt = 0;
-  while (!stop) {
-    cnt += __popc(sbits[k] & from);
-    from = 0xFFFFFFFFu;
-    if (++k >= nw) {
-      *end = nw << 5;
-      *ncp = cnt;
-      return;
+// 32 bytes (one bitmap word) per thread from two 16-byte loads in flight together (text 16-byte
+// aligned); all-ASCII halves classify with SWAR arithmetic, others per byte (classify_byte).
+__device__ __forceinline__ void classify_half(const TextView& t, uint64_t b0, const uint4& v, uint32_t& wm,
+                                              uint32_t& sm) {
+  if (!((v.x | v.y | v.z | v.w) & 0x80808080u)) {
+    wm = ascii_word_mask4(v.x) | (ascii_word_mask4(v.y) << 4) | (ascii_word_mask4(v.z) << 8) |
+         (ascii_word_mask4(v.w) << 12);
+    sm = wm;  // ASCII bytes are codepoint starts
+  } else {
+    wm = sm = 0;
+    for (int j = 0; j < 16; ++j) {
+      bool w, st;
+      classify_byte(t, b0 + j, w, st);
+      wm |= (uint32_t)w << j;
+      sm |= (uint32_t)(w && st) << j;
     }
+  }
+}
+
+__global__ void k_classify32(TextView t, uint32_t* __restrict__ wbits, uint32_t* __restrict__ sbits) {
+  const uint64_t nw = (t.n + 31) >> 5;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b0 = w << 5;
+    uint32_t wm0 = 0, sm0 = 0, wm1 = 0, sm1 = 0;
+    if (b0 + 32 <= t.n) {
+      const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(t.text) + 2 * w);
+      const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(t.text) + 2 * w + 1);
+      classify_half(t, b0, v0, wm0, sm0);
+      classify_half(t, b0 + 16, v1, wm1, sm1);
+    } else {
+      for (int j = 0; j < 32 && b0 + j < t.n; ++j) {
+        bool wd, st;
+        classify_byte(t, b0 + j, wd, st);
+        (j < 16 ? wm0 : wm1) |= (uint32_t)wd << (j & 15);
+        (j < 16 ? sm0 : sm1) |= (uint32_t)(wd && st) << (j & 15);
+      }
+    }
+    wbits[w] = wm0 | (wm1 << 16);
+    sbits[w] = sm0 | (sm1 << 16);
+  }
+}
+
+// Does the token starting at bit j of word k have >= 2 codepoints (word-codepoint starts,
+// sbits, inside it)? The same count as a walk to the token's end, from words k and k + 1 only:
+// a token running through all of word k + 1 spans more than 32 bytes, hence >= 8 codepoints
+// (a codepoint is at most 4 bytes).
+__device__ __forceinline__ bool token_two_cp(uint32_t W0, uint32_t S0, uint32_t D0, uint32_t W1, uint32_t S1,
+                                             uint32_t D1, bool has1, uint32_t j) {
+  const uint32_t from = 0xFFFFFFFFu << j;
+  const uint32_t stop0 = (~W0 | D0) & (j == 31 ? 0u : (0xFFFFFFFFu << (j + 1)));
+  if (stop0) return __popc(S0 & from & ((stop0 & (0u - stop0)) - 1u)) >= 2;
+  const uint32_t n = __popc(S0 & from);
+  if (n >= 2) return true;
+  if (!has1) return false;
+  const uint32_t stop1 = ~W1 | D1;
+  if (!stop1) return true;
+  return n + __popc(S1 & ((stop1 & (0u - stop1)) - 1u)) >= 2;
+}
+
+// end (exclusive byte position) of the token starting at bit j of word k: the first stop after j
+__device__ __forceinline__ uint64_t token_end(const uint32_t* wbits, const uint32_t* dbits, uint64_t nw, uint64_t k,
+                                              uint32_t j, uint32_t W0, uint32_t D0, uint32_t W1, uint32_t D1) {
+  uint32_t stop = (~W0 | D0) & (j == 31 ? 0u : (0xFFFFFFFFu << (j + 1)));
+  if (stop) return (k << 5) + (__ffs(stop) - 1);
+  if (++k >= nw) return nw << 5;
+  stop = ~W1 | D1;
+  while (!stop) {
+    if (++k >= nw) return nw << 5;
     stop = ~wbits[k] | dbits[k];
   }
-  const uint32_t e = __ffs(stop) - 1;
-  cnt += __popc(sbits[k] & from & ((1u << e) - 1u));
-  *end = (k << 5) + e;
-  *ncp = cnt;
+  return (k << 5) + (__ffs(stop) - 1);
 }
 
 // Token starts with >= 2 codepoints, one thread per 32-byte bitmap word, tiles of 256 words.
 // Count pass: per-word counts (u8: at most 16 starts per word) and per-tile totals; the tile
 // totals are scanned; emit pass: a block scan of the word counts gives every word's first
-// output slot (no word-sized scan).
+// output slot (no word-sized scan). Both read words i - 1 .. i + 1 only (token_two_cp); the
+// emit pass walks on to a token's end when it runs past word i + 1.
 constexpr int kTokThreads = 256;
+#ifndef SL_CLASSIFY32
+#define SL_CLASSIFY32 1  // one 32-byte bitmap word per thread (two 16-byte loads in flight)
+#endif
 
 template <bool EMIT>
 __global__ void __launch_bounds__(kTokThreads) k_tokens(const uint32_t* __restrict__ wbits,
@@ -428,20 +481,24 @@ __global__ void __launch_bounds__(kTokThreads) k_tokens(const uint32_t* __restri
   __shared__ uint32_t sw[kTokThreads / 32 + 1];
   const uint64_t i = (uint64_t)blockIdx.x * kTokThreads + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t W = 0, S = 0, D = 0, W1 = 0, S1 = 0, D1 = 0, B = 0;
+  const bool has1 = i + 1 < nw;
+  if (i < nw) {
+    W = wbits[i];
+    S = sbits[i];
+    D = dbits[i];
+    if (has1) {
+      W1 = wbits[i + 1];
+      S1 = sbits[i + 1];
+      D1 = dbits[i + 1];
+    }
+    const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
+    B = W & (D | ~((W << 1) | prev));
+  }
   uint32_t c = 0;
   if (!EMIT) {
     if (i < nw) {
-      const uint32_t W = wbits[i], D = dbits[i];
-      const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
-      uint32_t B = W & (D | ~((W << 1) | prev));
-      while (B) {
-        const uint32_t j = __ffs(B) - 1;
-        B &= B - 1;
-        uint64_t e;
-        uint32_t ncp;
-        token_extent(wbits, sbits, dbits, nw, (i << 5) + j, &e, &ncp);
-        c += ncp >= 2;
-      }
+      for (uint32_t b = B; b; b &= b - 1) c += token_two_cp(W, S, D, W1, S1, D1, has1, __ffs(b) - 1);
       wcnt[i] = (uint8_t)c;
     }
   } else {
@@ -472,19 +529,13 @@ __global__ void __launch_bounds__(kTokThreads) k_tokens(const uint32_t* __restri
   }
   if (!c) return;
   uint32_t o = tile[blockIdx.x] + sw[w] + x - c;
-  const uint32_t W = wbits[i], D = dbits[i];
-  const uint32_t prev = i ? (wbits[i - 1] >> 31) : 0u;
-  uint32_t B = W & (D | ~((W << 1) | prev));
   while (B) {
     const uint32_t j = __ffs(B) - 1;
     B &= B - 1;
-    const uint64_t p = (i << 5) + j;
-    uint64_t e;
-    uint32_t ncp;
-    token_extent(wbits, sbits, dbits, nw, p, &e, &ncp);
-    if (ncp >= 2) {
+    if (token_two_cp(W, S, D, W1, S1, D1, has1, j)) {
+      const uint64_t p = (i << 5) + j;
       tbeg[o] = p;
-      tlen[o] = (uint32_t)(e - p);
+      tlen[o] = (uint32_t)(token_end(wbits, dbits, nw, i, j, W, D, W1, D1) - p);
       ++o;
     }
   }
@@ -1632,7 +1683,11 @@ int32_t tokenize_impl(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t build
     k_doc_marks<<<grid_for(N), 256, 0, st>>>(doc_off, N, nb, dbits); ++t_launches;
     const TextView tv{text, nb, dbits};
     if ((reinterpret_cast<uintptr_t>(text) & 15u) == 0) {
+#if SL_CLASSIFY32
+      k_classify32<<<grid_for(nw), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+#else
       k_classify16<<<grid_for((nb + 15) / 16), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
+#endif
     } else if ((reinterpret_cast<uintptr_t>(text) & 3u) == 0) {
       k_classify4<<<grid_for((nb + 3) / 4), 256, 0, st>>>(tv, wbits, sbits); ++t_launches;
     } else {
