@@ -26,8 +26,6 @@ namespace sl {
 // ============================================================== scan (u32, exclusive)
 namespace {
 constexpr int kScanThreads = 256;
-constexpr int kScanIPT = 8;
-constexpr int kScanTile = kScanThreads * kScanIPT;
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   const int lane = threadIdx.x & 31;
@@ -58,38 +56,76 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sw, ui
   return r;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_reduce_tiles(const uint32_t* in, uint64_t n,
-                                                               uint32_t* sums) {
-  __shared__ uint32_t sw[33];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
-  uint32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < kScanIPT; ++j) {
-    const uint64_t i = base + (uint64_t)j * kScanThreads + threadIdx.x;
-    if (i < n) s += in[i];
+}  // namespace
+
+namespace {
+// Single-pass exclusive scan (decoupled look-back, Merrill & Garland): a block takes the next
+// tile in launch order from a ticket, scans it, publishes its aggregate in a status word
+// (flag << 32 | value: 1 = aggregate, 2 = inclusive prefix), and warp 0 sums its predecessors'
+// words back to the nearest inclusive prefix, 32 tiles per step. One launch per scan.
+constexpr int kLbIPT = 16, kLbTile = kScanThreads * kLbIPT;
+constexpr unsigned long long kLbAgg = 1ull << 32, kLbPre = 2ull << 32;
+
+__device__ __forceinline__ uint32_t lookback_warp(unsigned long long* status, uint32_t tile, uint32_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) atomicExch(status + tile, (tile == 0 ? 2ull << 32 : 1ull << 32) | agg);
+  if (tile == 0) return 0;
+  uint32_t excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  for (;;) {
+    const int64_t t = base - lane;
+    const unsigned long long v = t >= 0 ? *(volatile unsigned long long*)(status + t) : (unsigned long long)(2ull << 32);
+    const uint32_t flag = (uint32_t)(v >> 32);
+    const uint32_t pm = __ballot_sync(0xffffffffu, flag == 2u);
+    const uint32_t zm = __ballot_sync(0xffffffffu, flag == 0u);
+    const uint32_t low = pm & (0u - pm);
+    const uint32_t need = pm ? (low | (low - 1u)) : 0xffffffffu;  // lanes up to the nearest prefix
+    if (zm & need) continue;                                      // a predecessor has not published
+    excl += __reduce_add_sync(0xffffffffu, ((need >> lane) & 1u) ? (uint32_t)v : 0u);
+    if (pm) break;
+    base -= 32;
   }
-  uint32_t tot;
-  block_excl_scan(s, sw, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+  if (lane == 0) atomicExch(status + tile, kLbPre | (excl + agg));
+  return excl;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* in, uint32_t* out,
-                                                             uint64_t n, const uint32_t* offs) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_1p(const uint32_t* in, uint32_t* out, uint64_t n,
+                                                          unsigned long long* status, uint32_t* ticket,
+                                                          uint32_t* total) {
   __shared__ uint32_t sw[33];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanIPT;
-  uint32_t v[kScanIPT];
+  __shared__ uint32_t s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kLbTile + (uint64_t)threadIdx.x * kLbIPT;
+  uint32_t v[kLbIPT];
   uint32_t s = 0;
+  if (base + kLbIPT <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
 #pragma unroll
-  for (int j = 0; j < kScanIPT; ++j) {
-    const uint64_t i = base + j;
-    v[j] = i < n ? in[i] : 0u;
-    s += v[j];
+    for (int j = 0; j < kLbIPT; j += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(in + base + j);
+      v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kLbIPT; ++j) v[j] = base + j < n ? in[base + j] : 0u;
   }
-  uint32_t run = block_excl_scan(s, sw, nullptr) + (offs ? offs[blockIdx.x] : 0u);
 #pragma unroll
-  for (int j = 0; j < kScanIPT; ++j) {
-    const uint64_t i = base + j;
-    if (i < n) out[i] = run;
+  for (int j = 0; j < kLbIPT; ++j) s += v[j];
+  uint32_t agg;
+  const uint32_t excl = block_excl_scan(s, sw, &agg);
+  if (threadIdx.x < 32) {
+    const uint32_t pre = lookback_warp(status, tile, agg);
+    if (threadIdx.x == 0) {
+      s_prefix = pre;
+      if ((uint64_t)(tile + 1) * kLbTile >= n) *total = pre + agg;  // the last tile
+    }
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + excl;
+#pragma unroll
+  for (int j = 0; j < kLbIPT; ++j) {
+    if (base + j < n) out[base + j] = run;
     run += v[j];
   }
 }
@@ -102,26 +138,21 @@ int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaSt
     if (total_host) *total_host = 0;
     return SL_OK;
   }
-  uint32_t last_in = 0;
-  if (total_host) SL_CUDA_TRY(cudaMemcpyAsync(&last_in, in + n - 1, 4, cudaMemcpyDeviceToHost, st));
-  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-  if (nb == 1) {
-    k_scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr); ++t_launches;
-  } else {
-    uint32_t* sums = nullptr;
-    SL_CUDA_TRY(cudaMallocAsync(&sums, nb * 4, st));
-    k_reduce_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums); ++t_launches;
-    SL_TRY(exclusive_scan_u32(sums, sums, nb, st, nullptr));
-    k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums); ++t_launches;
-    SL_CUDA_TRY(cudaFreeAsync(sums, st));
-  }
+  const uint64_t nb = (n + kLbTile - 1) / kLbTile;
+  if (nb > 0xFFFFFFFFull) SL_FAIL(SL_EUNSUPPORTED, "scan: too many tiles");
+  // status words [nb] | ticket | total (one stream-ordered allocation, zeroed)
+  unsigned long long* status = nullptr;
+  const uint64_t bytes = nb * 8 + 8;
+  SL_CUDA_TRY(cudaMallocAsync(&status, bytes, st));
+  SL_CUDA_TRY(cudaMemsetAsync(status, 0, bytes, st));
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(status + nb);
+  k_scan_1p<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, status, ticket, ticket + 1); ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   if (total_host) {
-    uint32_t last_out = 0;
-    SL_CUDA_TRY(cudaMemcpyAsync(&last_out, out + n - 1, 4, cudaMemcpyDeviceToHost, st));
+    SL_CUDA_TRY(cudaMemcpyAsync(total_host, ticket + 1, 4, cudaMemcpyDeviceToHost, st));
     SL_CUDA_TRY(cudaStreamSynchronize(st));
-    *total_host = last_out + last_in;
   }
+  SL_CUDA_TRY(cudaFreeAsync(status, st));
   return SL_OK;
 }
 
