@@ -152,6 +152,9 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
 #ifndef SL_DENSE_ASYNC
 #define SL_DENSE_ASYNC 1
 #endif
+#ifndef SL_TMA_EARLY
+#define SL_TMA_EARLY 1  // the first dense row's bulk copy starts at the top of the tile
+#endif
 #ifndef SL_DENSE_TMA
 #define SL_DENSE_TMA 1  // first dense row of a tile by one bulk copy (cp.async.bulk + mbarrier) per warp
 #endif
@@ -734,6 +737,19 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint32_t d0 = tile * TILE, d1 = d0 + TILE;
     const uint32_t nvalid = min((uint32_t)TILE, ix.N - d0);
+#if SL_DENSE_TMA
+    // the whole 4 KB first-row tile by one bulk copy: order this warp's earlier generic accesses
+    // to the buffer before the async-proxy write, then lane 0 arms the barrier and starts the copy
+    auto issue_first_row = [&]() {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bulk_copy_g2s(s.dsum, ix.dense + (uint64_t)s.dslot[0] * ix.n_pad + d0, TILE * 4u, s.mbar);
+    };
+#if SL_TMA_EARLY
+    // issued before the tile's slice bookkeeping, whose loads then overlap the copy
+    if (nd > 0 && !(ra.debug_skip & 4)) issue_first_row();
+#endif
+#endif
     // (1) this tile's slice of every gathered row (lane = entry)
     uint32_t sb = 0, cnt = 0;
     if (ent) {
@@ -785,7 +801,17 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         const uint64_t tau = s.tau[r];
         if (tau != 0 && ub + fabsf(ub) * 4e-6f <= tau_float(tau)) live &= ~(1u << r);
       }
-      if (!live) continue;
+      if (!live) {
+#if SL_DENSE_TMA && SL_TMA_EARLY
+        if (nd > 0 && !(ra.debug_skip & 4)) {  // the early copy must complete before the buffer is reused
+          const uint32_t ph = s.mphase[0];
+          mbar_wait(s.mbar, ph);
+          __syncwarp();
+          if (lane == 0) s.mphase[0] = ph ^ 1u;
+        }
+#endif
+        continue;
+      }
     }
     // (2) dense signature of the run, ascending slot order, all loads in flight
     // register passes of DCH float4 per lane, so the tile size does not set the register
@@ -795,7 +821,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // in flight at once, one L2 round trip); later rows are added chunk by chunk in registers,
     // in ascending slot order as before (((r0 + r1) + r2) ...). Preloading the second row's
     // chunk during the copy spilled 648 B at the 64-register cap.
-    auto dense_pass = [&]() -> float {
+    auto dense_pass = [&](bool issued) -> float {
       float m = -INFINITY;
       constexpr int DCH = F4L < 4 ? F4L : 4;
       const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane;
@@ -805,12 +831,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         return 0.f;
       }
 #if SL_DENSE_TMA
-      // the whole 4 KB row tile by one bulk copy: order this warp's earlier generic accesses to
-      // the buffer before the async-proxy write, then lane 0 arms the barrier and starts the copy
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0)
-        bulk_copy_g2s(s.dsum, ix.dense + (uint64_t)s.dslot[0] * ix.n_pad + d0, TILE * 4u, s.mbar);
+      if (!issued) issue_first_row();
 #else
       {
         const float4* row0 = dbase + (uint64_t)s.dslot[0] * rstride;
@@ -858,7 +879,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       return m;
     };
 #else
-    auto dense_pass = [&]() -> float {
+    auto dense_pass = [&](bool) -> float {
       float m = -INFINITY;
       constexpr int DCH = F4L < 4 ? F4L : 4;
 #pragma unroll 1
@@ -889,7 +910,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       return m;
     };
 #endif
-    const float dm = (ra.debug_skip & 4) ? INFINITY : dense_pass();
+    const float dm = (ra.debug_skip & 4) ? INFINITY : dense_pass(SL_TMA_EARLY && SL_DENSE_TMA);
     __syncwarp();
     // (3) per query: gathered rows, then the running top-k
     for (uint32_t r = 0; r < nr; ++r) {
@@ -941,7 +962,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         }
       } else if (undo == 2) {
         __syncwarp();
-        dense_pass();
+        dense_pass(false);
         __syncwarp();
       }
 #endif
