@@ -1223,16 +1223,24 @@ __global__ void k_pack_runs(const uint32_t* __restrict__ gstart, const uint32_t*
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
     const uint32_t b = gstart[g], e = gstart[g + 1];
     uint32_t runs = 0, in_run = 0, ent = 0;
-    for (uint32_t i = b; i < e; ++i) {
-      const uint32_t ng = ngath[perm[i]];
-      if (in_run == 0 || in_run == R || ent + ng > 32u) {
-        if (WRITE) run_begin[goff[g] + runs] = i;
-        ++runs;
-        in_run = 0;
-        ent = 0;
+    // greedy packing in group order; the gathered-row counts are fetched 8 at a time (a large
+    // group, e.g. every query without dense tokens, is one thread's loop)
+    for (uint32_t i0 = b; i0 < e; i0 += 8) {
+      uint32_t ngv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ngv[j] = i0 + j < e ? __ldg(ngath + __ldg(perm + i0 + j)) : 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (i0 + j >= e) break;
+        if (in_run == 0 || in_run == R || ent + ngv[j] > 32u) {
+          if (WRITE) run_begin[goff[g] + runs] = i0 + j;
+          ++runs;
+          in_run = 0;
+          ent = 0;
+        }
+        ++in_run;
+        ent += ngv[j];
       }
-      ++in_run;
-      ent += ng;
     }
     if (!WRITE) gcnt[g] = runs;
   }
@@ -1390,6 +1398,84 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ cand
     if (out_ids) out_ids[(uint64_t)q * k + i] = i < m ? key_doc(key) : 0xFFFFFFFFu;
     if (out_scores)
       out_scores[(uint64_t)q * k + i] = i < m ? __double2float_rn((double)key_score(key) + qc) : -INFINITY;
+  }
+}
+
+// k_merge for small sets (k <= 32, n_splits x per_split <= kMergeWarpCap): one WARP per query.
+// The valid candidates (>= the shared threshold g) are staged in the warp's shared slice, the
+// exact k-th key is found by the warp radix select, and the k winners (one per lane) are ranked
+// by counting (keys are unique): the same keys, order and decoding as k_merge.
+constexpr int kMergeWarps = 4, kMergeWarpCap = 1024;
+__global__ void __launch_bounds__(kMergeWarps * 32) k_merge_warp(const uint64_t* __restrict__ cand, uint32_t B,
+                                                                  uint32_t n_splits, uint32_t per_split,
+                                                                  uint64_t split_stride, uint64_t query_stride,
+                                                                  uint32_t k, const double* __restrict__ qconst,
+                                                                  uint32_t* out_ids, float* out_scores,
+                                                                  uint64_t* out_keys, const uint64_t* __restrict__ gtau) {
+  __shared__ uint64_t sbuf[kMergeWarps][kMergeWarpCap];
+  __shared__ uint32_t shist[kMergeWarps][16];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t q = blockIdx.x * kMergeWarps + w;
+  if (q >= B) return;
+  uint64_t* buf = sbuf[w];
+  const uint64_t* base = cand + (uint64_t)q * query_stride;
+  const uint64_t g = gtau ? gtau[q] : 0ull;
+  uint32_t n = 0;  // staged so far (warp-uniform)
+  for (uint32_t sp = 0; sp < n_splits; ++sp) {
+    const uint64_t* p = base + (uint64_t)sp * split_stride;
+    for (uint32_t j0 = 0; j0 < per_split; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint64_t x = j < per_split ? __ldg(p + j) : kInvalidKey;
+      const bool v = x != kInvalidKey && x >= g;
+      const uint32_t bal = __ballot_sync(0xffffffffu, v);
+      if (v) buf[n + __popc(bal & lanemask_lt())] = x;
+      n += __popc(bal);
+    }
+  }
+  __syncwarp();
+  uint64_t tau = 1;
+  if (n > k)
+    tau = warp_select_kth(
+        [&](auto&& fn) {
+          for (uint32_t i = lane; i < n; i += 32) fn(buf[i]);
+        },
+        k, shist[w]);
+  // the winners (keys >= tau: exactly min(n, k) of them), one per lane
+  uint64_t mine = kInvalidKey;
+  uint32_t m = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint64_t x = i < n ? buf[i] : kInvalidKey;
+    const bool v = i < n && x >= tau;
+    const uint32_t bal = __ballot_sync(0xffffffffu, v);
+    const uint32_t r = m + __popc(bal & lanemask_lt());
+    // the winner of rank r (in staging order) goes to lane r
+    for (uint32_t b = bal; b; b &= b - 1) {
+      const int src = __ffs(b) - 1;
+      const uint64_t y = __shfl_sync(0xffffffffu, x, src);
+      const uint32_t ry = __shfl_sync(0xffffffffu, r, src);
+      if ((uint32_t)lane == ry) mine = y;
+    }
+    m += __popc(bal);
+  }
+  // descending rank of this lane's key among the winners
+  uint32_t rank = 0;
+  for (int j = 0; j < 32; ++j) {
+    const uint64_t y = __shfl_sync(0xffffffffu, mine, j);
+    rank += (uint32_t)j < m && y > mine;
+  }
+  const double qc = qconst ? qconst[q] : 0.0;
+  if ((uint32_t)lane < m) {
+    const uint64_t o = (uint64_t)q * k + rank;
+    if (out_keys) out_keys[o] = mine;
+    if (out_ids) out_ids[o] = key_doc(mine);
+    if (out_scores) out_scores[o] = __double2float_rn((double)key_score(mine) + qc);
+  }
+  for (uint32_t i = m + lane; i < k; i += 32) {  // fewer than k candidates: padding
+    const uint64_t o = (uint64_t)q * k + i;
+    if (out_keys) out_keys[o] = kInvalidKey;
+    if (out_ids) out_ids[o] = 0xFFFFFFFFu;
+    if (out_scores) out_scores[o] = -INFINITY;
   }
 }
 
@@ -1570,6 +1656,13 @@ int32_t launch_merge(const uint64_t* cand, uint32_t B, uint32_t n_splits, uint32
   // staging room for the candidates when all slots fit 8192 keys (64 KB); larger candidate
   // sets (top-1000: 37 splits x 2048) are visited in the buffers
   const uint64_t slots = (uint64_t)n_splits * per_split;
+  if (k <= 32 && slots <= (uint64_t)kMergeWarpCap && env_int("SL_MERGE_WARP", 1)) {
+    k_merge_warp<<<(B + kMergeWarps - 1) / kMergeWarps, kMergeWarps * 32, 0, st>>>(
+        cand, B, n_splits, per_split, split_stride, query_stride, k, qconst, ids, scores, keys, gtau);
+    ++t_launches;
+    SL_CUDA_TRY(cudaGetLastError());
+    return SL_OK;
+  }
   const uint32_t cap = slots <= 8192 ? (uint32_t)slots : 0u;
   const size_t smem = (size_t)next_pow2(std::max(k, 2u)) * 8 + 256 * 4 + 40 * 4 + (size_t)cap * 8;
   SL_CUDA_TRY(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
