@@ -1194,59 +1194,86 @@ __device__ __forceinline__ bool same_signature(const int32_t* qdense, const uint
   return true;
 }
 
-// Runs over the signature-sorted queries: a run is <= R consecutive queries of one dense
-// signature whose gathered rows fit the warp's 32 lanes together. Three steps: signature-group
-// heads (k_sig_heads) -> group starts (k_group_starts, after a scan of the heads) -> one thread
-// per group packs its members greedily in query order (k_pack_runs: count pass, scan of the
-// per-group run counts, write pass).
-__global__ void k_sig_heads(const uint32_t* __restrict__ perm, uint32_t B, const int32_t* __restrict__ qdense,
-                            const uint32_t* __restrict__ nden, uint32_t qmax, uint32_t* __restrict__ flag) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x)
-    flag[i] = (i == 0 || !same_signature(qdense, nden, qmax, perm[i], perm[i - 1])) ? 1u : 0u;
-}
-
-__global__ void k_group_starts(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint32_t B,
-                               uint32_t* __restrict__ gstart) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
-    if (flag[i]) gstart[pos[i]] = i;
-    if (i == B - 1) gstart[pos[i] + flag[i]] = B;
+// Grouping by dense signature without a sort: every short query claims or finds its
+// signature's slot in a hash table (key = hash, value = the claiming query, whose signature is
+// compared on a hash match), takes a position in the group from the slot's counter, and is
+// scattered to its group's range of perm after a scan of the counters. Long queries (more
+// than 32 gathered rows) go to the tail of perm. The order inside a group is the arrival
+// order: scores do not depend on the grouping (fixed per-document summation order).
+__global__ void k_group_insert(const uint32_t* __restrict__ hkey, uint32_t B, const int32_t* __restrict__ qdense,
+                               const uint32_t* __restrict__ nden, uint32_t qmax,
+                               unsigned long long* __restrict__ table, uint32_t cap, uint32_t* __restrict__ cnt,
+                               uint32_t* __restrict__ gslot, uint32_t* __restrict__ gpos,
+                               uint32_t* __restrict__ n_long) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
+    const uint32_t h = hkey[q];
+    if (h == 0xFFFFFFFFu) {
+      gslot[q] = 0xFFFFFFFFu;
+      gpos[q] = atomicAdd(n_long, 1u);
+      continue;
+    }
+    const unsigned long long tag = (unsigned long long)(h | 0x80000000u) << 32;
+    uint32_t s = (h * 0x9E3779B1u) & (cap - 1);
+    for (;;) {
+      unsigned long long cur = table[s];
+      if (cur == 0ull) {
+        cur = atomicCAS(table + s, 0ull, tag | q);
+        if (cur == 0ull) break;  // claimed: this query represents the signature
+      }
+      if ((cur & 0xFFFFFFFF00000000ull) == tag && same_signature(qdense, nden, qmax, (uint32_t)cur, q)) break;
+      s = (s + 1) & (cap - 1);
+    }
+    gslot[q] = s;
+    gpos[q] = atomicAdd(cnt + s, 1u);
   }
 }
 
+__global__ void k_group_scatter(const uint32_t* __restrict__ gslot, const uint32_t* __restrict__ gpos, uint32_t B,
+                                const uint32_t* __restrict__ gofs, const uint32_t* __restrict__ n_long,
+                                uint32_t* __restrict__ perm) {
+  const uint32_t b_short = B - *n_long;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
+    const uint32_t s = gslot[q];
+    perm[s == 0xFFFFFFFFu ? b_short + gpos[q] : gofs[s] + gpos[q]] = q;
+  }
+}
+
+// runs of one slot's group (greedy, in group order): count pass (gcnt per slot) / write pass
 template <bool WRITE>
-__global__ void k_pack_runs(const uint32_t* __restrict__ gstart, const uint32_t* __restrict__ flag,
-                            const uint32_t* __restrict__ pos, uint32_t B, const uint32_t* __restrict__ perm,
-                            const uint32_t* __restrict__ ngath, uint32_t R, uint32_t* __restrict__ gcnt,
-                            const uint32_t* __restrict__ goff, uint32_t* __restrict__ run_begin,
-                            uint32_t* __restrict__ n_runs) {
-  const uint32_t G = pos[B - 1] + flag[B - 1];
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
-    const uint32_t b = gstart[g], e = gstart[g + 1];
-    uint32_t runs = 0, in_run = 0, ent = 0;
-    // greedy packing in group order; the gathered-row counts are fetched 8 at a time (a large
-    // group, e.g. every query without dense tokens, is one thread's loop)
-    for (uint32_t i0 = b; i0 < e; i0 += 8) {
-      uint32_t ngv[8];
+__global__ void k_pack_slots(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ gofs, uint32_t cap,
+                             const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ngath, uint32_t R,
+                             uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
+                             uint32_t* __restrict__ run_begin, uint32_t* __restrict__ n_runs,
+                             const uint32_t* __restrict__ n_long, uint32_t B) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < cap; g += gridDim.x * blockDim.x) {
+    const uint32_t c = cnt[g];
+    uint32_t runs = 0;
+    if (c) {
+      const uint32_t b = gofs[g], e = b + c;
+      uint32_t in_run = 0, ent = 0;
+      for (uint32_t i0 = b; i0 < e; i0 += 8) {
+        uint32_t ngv[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) ngv[j] = i0 + j < e ? __ldg(ngath + __ldg(perm + i0 + j)) : 0u;
+        for (int j = 0; j < 8; ++j) ngv[j] = i0 + j < e ? __ldg(ngath + __ldg(perm + i0 + j)) : 0u;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (i0 + j >= e) break;
-        if (in_run == 0 || in_run == R || ent + ngv[j] > 32u) {
-          if (WRITE) run_begin[goff[g] + runs] = i0 + j;
-          ++runs;
-          in_run = 0;
-          ent = 0;
+        for (int j = 0; j < 8; ++j) {
+          if (i0 + j >= e) break;
+          if (in_run == 0 || in_run == R || ent + ngv[j] > 32u) {
+            if (WRITE) run_begin[goff[g] + runs] = i0 + j;
+            ++runs;
+            in_run = 0;
+            ent = 0;
+          }
+          ++in_run;
+          ent += ngv[j];
         }
-        ++in_run;
-        ent += ngv[j];
       }
     }
     if (!WRITE) gcnt[g] = runs;
   }
   if (WRITE && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t total = goff[G - 1] + gcnt[G - 1];
-    run_begin[total] = B;
+    const uint32_t total = goff[cap - 1] + gcnt[cap - 1];
+    run_begin[total] = B - *n_long;
     n_runs[0] = total;
     n_runs[1] = 0;  // work-item counter of k_score_runs
   }
@@ -1645,6 +1672,14 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
     const uint64_t region = (uint64_t)(131072.0 * shrink) * std::max(1u, p->C / 512);
     const uint64_t by_l2 = ((uint64_t)ix->N + region - 1) / region;
     ns = (uint32_t)std::max<uint64_t>(1, std::max(by_work, by_l2));
+    // but every split keeps ~64 tiles to amortise a work item's setup (query classification,
+    // row cursors, the first tiles' top-k warm-up): the document shards of c2 score best in
+    // 8 / 4 / 2 splits at 1/2, 1/4, 1/8 of the corpus (489 / 245 / 122 tiles; 1/8: 5.75M QPS in
+    // 2 splits against 4.20M in the 12 the work rule asks for). While there are fewer runs than
+    // resident warps, splits still add parallelism (c1).
+    const uint64_t min_tiles = (uint64_t)std::max(1, env_int("SL_MIN_TILES", 64));
+    const uint64_t cap = std::max<uint64_t>((ix->num_tiles + min_tiles / 2) / min_tiles, (warps + items - 1) / items);
+    ns = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(ns, cap));
   }
   p->n_splits = std::max(1u, std::min(ns, std::max(1u, ix->num_tiles)));
   return SL_OK;
@@ -1758,46 +1793,45 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   const uint32_t B_short = B - n_long;  // they sort after every other query
   RunPlan plan;
   SL_TRY(plan_runs(ix, B, k, qmax, &plan));
-  // group queries by dense signature: sort by signature hash, cut runs of <= R identical ones
+  // group queries by dense signature (hash table, no sort), cut runs of <= R identical ones
   int32_t* qdense;
-  uint32_t *nden, *hk, *hv, *k0, *k1, *v0, *v1, *run_begin, *n_runs, *ngath;
+  uint32_t *nden, *hk, *hv, *run_begin, *n_runs, *ngath, *perm_w;
   SL_TRY(scr.alloc(&qdense, (uint64_t)B * qmax));
   SL_TRY(scr.alloc(&nden, B));
   SL_TRY(scr.alloc(&ngath, B));
   SL_TRY(scr.alloc(&hk, B));
   SL_TRY(scr.alloc(&hv, B));
-  SL_TRY(scr.alloc(&k0, B));
-  SL_TRY(scr.alloc(&k1, B));
-  SL_TRY(scr.alloc(&v0, B));
-  SL_TRY(scr.alloc(&v1, B));
+  SL_TRY(scr.alloc(&perm_w, B));
   SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
   SL_TRY(scr.alloc(&n_runs, 2));
   k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, ngath, hk, hv); ++t_launches;
-  const uint32_t *sk, *perm;
-  SL_TRY(radix_sort_pairs(hk, hv, B, 32, k0, k1, v0, v1, st, &sk, &perm, 0, nullptr));
-  if (B_short) {
-    uint32_t *flag, *pos, *gstart, *gcnt, *goff;
-    SL_TRY(scr.alloc(&flag, B_short));
-    SL_TRY(scr.alloc(&pos, B_short));
-    SL_TRY(scr.alloc(&gstart, (uint64_t)B_short + 1));
-    SL_TRY(scr.alloc(&gcnt, B_short));
-    SL_TRY(scr.alloc(&goff, B_short));
-    SL_CUDA_TRY(cudaMemsetAsync(gcnt, 0, (uint64_t)B_short * 4, st));
-    const unsigned g = (B_short + 255) / 256;
-    k_sig_heads<<<g, 256, 0, st>>>(perm, B_short, qdense, nden, qmax, flag); ++t_launches;
-    SL_TRY(exclusive_scan_u32(flag, pos, B_short, st, nullptr));
-    k_group_starts<<<g, 256, 0, st>>>(flag, pos, B_short, gstart); ++t_launches;
-    k_pack_runs<false><<<g, 256, 0, st>>>(gstart, flag, pos, B_short, perm, ngath, plan.R, gcnt, nullptr, nullptr,
-                                          nullptr);
+  {
+    const uint32_t cap = next_pow2(std::max(64u, 2 * B));
+    // one zeroed scratch: table u64[cap] | cnt[cap] | n_long
+    unsigned long long* table;
+    SL_TRY(scr.alloc(&table, (uint64_t)cap + cap / 2 + 1));
+    SL_CUDA_TRY(cudaMemsetAsync(table, 0, ((uint64_t)cap + cap / 2 + 1) * 8, st));
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(table + cap);
+    uint32_t* nl = cnt + cap;
+    uint32_t *gslot, *gpos, *gofs, *gcnt, *goff;
+    SL_TRY(scr.alloc(&gslot, B));
+    SL_TRY(scr.alloc(&gpos, B));
+    SL_TRY(scr.alloc(&gofs, cap));
+    SL_TRY(scr.alloc(&gcnt, cap));
+    SL_TRY(scr.alloc(&goff, cap));
+    const unsigned g = (B + 255) / 256, gc = (cap + 255) / 256;
+    k_group_insert<<<g, 256, 0, st>>>(hk, B, qdense, nden, qmax, table, cap, cnt, gslot, gpos, nl); ++t_launches;
+    SL_TRY(exclusive_scan_u32(cnt, gofs, cap, st, nullptr));
+    k_group_scatter<<<g, 256, 0, st>>>(gslot, gpos, B, gofs, nl, perm_w); ++t_launches;
+    k_pack_slots<false><<<gc, 256, 0, st>>>(cnt, gofs, cap, perm_w, ngath, plan.R, gcnt, nullptr, nullptr, nullptr,
+                                            nl, B);
     ++t_launches;
-    SL_TRY(exclusive_scan_u32(gcnt, goff, B_short, st, nullptr));
-    k_pack_runs<true><<<g, 256, 0, st>>>(gstart, flag, pos, B_short, perm, ngath, plan.R, gcnt, goff, run_begin,
-                                         n_runs);
+    SL_TRY(exclusive_scan_u32(gcnt, goff, cap, st, nullptr));
+    k_pack_slots<true><<<gc, 256, 0, st>>>(cnt, gofs, cap, perm_w, ngath, plan.R, gcnt, goff, run_begin, n_runs, nl,
+                                           B);
     ++t_launches;
-  } else {
-    SL_CUDA_TRY(cudaMemsetAsync(n_runs, 0, 8, st));
-    SL_CUDA_TRY(cudaMemsetAsync(run_begin, 0, 4, st));
   }
+  const uint32_t* perm = perm_w;
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;
