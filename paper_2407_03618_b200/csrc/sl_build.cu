@@ -1137,36 +1137,9 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
   return SL_OK;
 }
 
-// SL_BUILD_TRACE=1: device time between build phases (events on the build stream), stderr
-struct PhaseTrace {
-  bool on = false;
-  cudaStream_t st = nullptr;
-  std::vector<std::pair<const char*, cudaEvent_t>> ev;
-  explicit PhaseTrace(cudaStream_t s) : st(s) {
-    const char* e = std::getenv("SL_BUILD_TRACE");
-    on = e && std::atoi(e);
-  }
-  void mark(const char* name) {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    ev.emplace_back(name, e);
-  }
-  ~PhaseTrace() {
-    if (!on || ev.empty()) return;
-    cudaEventSynchronize(ev.back().second);
-    for (size_t i = 1; i < ev.size(); ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-      fprintf(stderr, "[build] %-14s %8.3f ms\n", ev[i].first, ms);
-    }
-    for (auto& x : ev) cudaEventDestroy(x.second);
-  }
-};
 
 int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st, bool* agreed) {
-  PhaseTrace tr(st);
+  PhaseTrace tr(st, "SL_BUILD_TRACE", "build");
   const uint32_t N = d->num_docs, V = d->vocab_size;
   // ---- inputs on the device
   uint64_t o0 = 0, oN = 0;

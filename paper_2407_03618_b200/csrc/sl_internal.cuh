@@ -1,5 +1,8 @@
 // sl_internal.cuh — shared device/host internals of libsparselex_b200.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -143,6 +146,35 @@ int32_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaSt
 // Values of the first pass taken from document offsets instead of vin (index build: the
 // value of token position p is its document): tile_doc[k] = document holding the first
 // position of sort tile k.
+// SL_BUILD_TRACE=1 / SL_QUERY_TRACE=1: device time between phases (events on the stream), stderr
+struct PhaseTrace {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  const char* tag = "";
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  PhaseTrace(cudaStream_t s, const char* env, const char* t) : st(s), tag(t) {
+    const char* e = std::getenv(env);
+    on = e && std::atoi(e);
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(name, e);
+  }
+  ~PhaseTrace() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "[%s] %-14s %8.3f ms\n", tag, ev[i].first, ms);
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+  }
+};
+
 struct DocSrc {
   const uint64_t* off;  // [N+1] absolute
   uint64_t o0;

@@ -1238,43 +1238,64 @@ __global__ void k_group_scatter(const uint32_t* __restrict__ gslot, const uint32
   }
 }
 
-// runs of one slot's group (greedy, in group order): count pass (gcnt per slot) / write pass
+// runs of one slot's group: a WARP per slot; the group is cut into blocks of R consecutive
+// members (one lane per block) and each block into runs greedily by the 32-lane entry budget,
+// so a large group (e.g. every query without dense tokens) is packed in parallel. Count pass
+// (gcnt per slot) / write pass (run starts at the slot's scanned offset).
 template <bool WRITE>
 __global__ void k_pack_slots(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ gofs, uint32_t cap,
                              const uint32_t* __restrict__ perm, const uint32_t* __restrict__ ngath, uint32_t R,
                              uint32_t* __restrict__ gcnt, const uint32_t* __restrict__ goff,
                              uint32_t* __restrict__ run_begin, uint32_t* __restrict__ n_runs,
                              const uint32_t* __restrict__ n_long, uint32_t B) {
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < cap; g += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < cap; g += nwarps) {
     const uint32_t c = cnt[g];
-    uint32_t runs = 0;
+    uint32_t total = 0;
     if (c) {
-      const uint32_t b = gofs[g], e = b + c;
-      uint32_t in_run = 0, ent = 0;
-      for (uint32_t i0 = b; i0 < e; i0 += 8) {
-        uint32_t ngv[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) ngv[j] = i0 + j < e ? __ldg(ngath + __ldg(perm + i0 + j)) : 0u;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (i0 + j >= e) break;
-          if (in_run == 0 || in_run == R || ent + ngv[j] > 32u) {
-            if (WRITE) run_begin[goff[g] + runs] = i0 + j;
-            ++runs;
-            in_run = 0;
-            ent = 0;
+      const uint32_t b = gofs[g], nblk = (c + R - 1) / R;
+      for (uint32_t k0 = 0; k0 < nblk; k0 += 32) {
+        const uint32_t blk = k0 + lane;
+        const uint32_t i0 = b + blk * R, i1 = min(i0 + R, b + c);
+        uint32_t runs = 0;
+        if (blk < nblk) {
+          uint32_t ent = 0, in_run = 0;
+          for (uint32_t i = i0; i < i1; ++i) {
+            const uint32_t ng = __ldg(ngath + __ldg(perm + i));
+            if (in_run == 0 || ent + ng > 32u) {
+              ++runs;
+              in_run = 0;
+              ent = 0;
+            }
+            ++in_run;
+            ent += ng;
           }
-          ++in_run;
-          ent += ngv[j];
         }
+        const uint32_t incl = warp_incl_scan(runs);
+        if (WRITE && blk < nblk) {
+          uint32_t o = goff[g] + total + incl - runs;
+          uint32_t ent = 0, in_run = 0;
+          for (uint32_t i = i0; i < i1; ++i) {
+            const uint32_t ng = __ldg(ngath + __ldg(perm + i));
+            if (in_run == 0 || ent + ng > 32u) {
+              run_begin[o++] = i;
+              in_run = 0;
+              ent = 0;
+            }
+            ++in_run;
+            ent += ng;
+          }
+        }
+        total += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
-    if (!WRITE) gcnt[g] = runs;
+    if (!WRITE && lane == 0) gcnt[g] = total;
   }
   if (WRITE && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t total = goff[cap - 1] + gcnt[cap - 1];
-    run_begin[total] = B - *n_long;
-    n_runs[0] = total;
+    const uint32_t t = goff[cap - 1] + gcnt[cap - 1];
+    run_begin[t] = B - *n_long;
+    n_runs[0] = t;
     n_runs[1] = 0;  // work-item counter of k_score_runs
   }
 }
@@ -1448,14 +1469,20 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_merge_warp(const uint64_t*
   const uint64_t* base = cand + (uint64_t)q * query_stride;
   const uint64_t g = gtau ? gtau[q] : 0ull;
   uint32_t n = 0;  // staged so far (warp-uniform)
-  for (uint32_t sp = 0; sp < n_splits; ++sp) {
-    const uint64_t* p = base + (uint64_t)sp * split_stride;
-    for (uint32_t j0 = 0; j0 < per_split; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      const uint64_t x = j < per_split ? __ldg(p + j) : kInvalidKey;
-      const bool v = x != kInvalidKey && x >= g;
+  const uint32_t total = n_splits * per_split;
+  for (uint32_t t0 = 0; t0 < total; t0 += 128) {  // four loads per lane in flight
+    uint64_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = t0 + 32u * u + lane;
+      const uint32_t sp = i / per_split;
+      x[u] = i < total ? __ldg(base + (uint64_t)sp * split_stride + (i - sp * per_split)) : kInvalidKey;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool v = x[u] != kInvalidKey && x[u] >= g;
       const uint32_t bal = __ballot_sync(0xffffffffu, v);
-      if (v) buf[n + __popc(bal & lanemask_lt())] = x;
+      if (v) buf[n + __popc(bal & lanemask_lt())] = x[u];
       n += __popc(bal);
     }
   }
@@ -1503,6 +1530,76 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_merge_warp(const uint64_t*
     if (out_keys) out_keys[o] = kInvalidKey;
     if (out_ids) out_ids[o] = 0xFFFFFFFFu;
     if (out_scores) out_scores[o] = -INFINITY;
+  }
+}
+
+// k_query_prep and the dense signature in one pass over each query's tokens (score_chunk):
+// validation, Σ S^θ (f64, query order), max length and posting bytes (warp-aggregated
+// atomics), the sorted dense slots (stride NDMAX: a query with more is scored by k_score_long),
+// gathered-row count and signature hash (0xFFFFFFFF: the long-query path).
+__global__ void k_query_prep_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
+                                 IndexView ix, double* __restrict__ qconst, uint32_t* __restrict__ info,
+                                 unsigned long long* __restrict__ bytes, int32_t* __restrict__ qdense,
+                                 uint32_t* __restrict__ nden, uint32_t* __restrict__ ngath,
+                                 uint32_t* __restrict__ hkey) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < B; q0 += stride) {
+    const uint32_t q = q0 + threadIdx.x;
+    uint32_t len = 0;
+    unsigned long long pb = 0;
+    if (q < B) {
+      const uint64_t b = q_off[q], e = q_off[q + 1];
+      double c = 0.0;
+      uint32_t n = 0, ng = 0;
+      int32_t* d = qdense + (uint64_t)q * NDMAX;
+      if (e < b) {
+        atomicOr(&info[0], 2u);
+      } else {
+        len = (uint32_t)min(e - b, (uint64_t)0xFFFFFFFFu);
+        for (uint64_t j = b; j < e; ++j) {
+          const uint32_t t = q_tok[j];
+          if (t >= ix.V) {
+            atomicOr(&info[0], 1u);
+            continue;
+          }
+          if (ix.df_global[t] == 0) continue;
+          c += (double)ix.theta[t];
+          const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
+          pb += 8ull * (re - rb);
+          if (rb == re) continue;
+          const int32_t tinfo = ix.tokinfo[t];
+          if (tinfo < 0) {
+            ++ng;
+            continue;
+          }
+          if (n < (uint32_t)NDMAX) {  // insertion into the sorted slots
+            int bb = (int)n - 1;
+            while (bb >= 0 && d[bb] > tinfo) {
+              d[bb + 1] = d[bb];
+              --bb;
+            }
+            d[bb + 1] = tinfo;
+          }
+          ++n;
+        }
+      }
+      const bool lng = ng > 32 || n > (uint32_t)NDMAX;
+      if (lng) atomicAdd(&info[2], 1u);
+      uint32_t h = 2166136261u ^ n;  // FNV-1a over the sorted slots
+      if (!lng)
+        for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
+      qconst[q] = c;
+      nden[q] = lng ? 0u : n;
+      ngath[q] = ng;
+      hkey[q] = lng ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
+    }
+    const uint32_t m = __reduce_max_sync(0xffffffffu, len);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    if ((threadIdx.x & 31) == 0) {
+      if (m) atomicMax(&info[1], m);
+      if (bytes && pb) atomicAdd(bytes, pb);
+    }
   }
 }
 
@@ -1774,6 +1871,8 @@ int32_t chunk_size(const sl_index* ix, uint32_t B, uint32_t k, uint32_t* out) {
 int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, const uint32_t* d_tok, uint32_t B,
                     uint32_t k, double* qconst, uint32_t* ids, float* scores, uint64_t* keys,
                     unsigned long long* bytes, float* score_ms) {
+  PhaseTrace tr(sc->st, "SL_QUERY_TRACE", "query");
+  tr.mark("start");
   cudaStream_t st = sc->st;
   Scratch scr(st);
   const IndexView v = ix->view();
@@ -1781,11 +1880,23 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   uint32_t* info;
   SL_TRY(scr.alloc(&info, 4));
   SL_CUDA_TRY(cudaMemsetAsync(info, 0, 16, st));
-  k_query_prep<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes); ++t_launches;
+  // validation, query constants and dense signatures in one kernel, then one host round trip
+  int32_t* qdense;
+  uint32_t *nden, *hk, *run_begin, *n_runs, *ngath, *perm_w;
+  SL_TRY(scr.alloc(&qdense, (uint64_t)B * NDMAX));
+  SL_TRY(scr.alloc(&nden, B));
+  SL_TRY(scr.alloc(&ngath, B));
+  SL_TRY(scr.alloc(&hk, B));
+  SL_TRY(scr.alloc(&perm_w, B));
+  SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
+  SL_TRY(scr.alloc(&n_runs, 2));
+  k_query_prep_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes, qdense, nden, ngath, hk);
+  ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   uint32_t h_info[4];
   SL_CUDA_TRY(cudaMemcpyAsync(h_info, info, 16, cudaMemcpyDeviceToHost, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
+  tr.mark("prep+sync");
   if (h_info[0] & 2u) SL_FAIL(SL_EINVAL, "retrieve_batch: query offsets must be non-decreasing");
   if (h_info[0] & 1u) SL_FAIL(SL_EINVAL, "score_query: token id >= vocab size");
   const uint32_t qmax = std::max(1u, h_info[1]);
@@ -1794,17 +1905,6 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   RunPlan plan;
   SL_TRY(plan_runs(ix, B, k, qmax, &plan));
   // group queries by dense signature (hash table, no sort), cut runs of <= R identical ones
-  int32_t* qdense;
-  uint32_t *nden, *hk, *hv, *run_begin, *n_runs, *ngath, *perm_w;
-  SL_TRY(scr.alloc(&qdense, (uint64_t)B * qmax));
-  SL_TRY(scr.alloc(&nden, B));
-  SL_TRY(scr.alloc(&ngath, B));
-  SL_TRY(scr.alloc(&hk, B));
-  SL_TRY(scr.alloc(&hv, B));
-  SL_TRY(scr.alloc(&perm_w, B));
-  SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
-  SL_TRY(scr.alloc(&n_runs, 2));
-  k_query_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qmax, qdense, nden, ngath, hk, hv); ++t_launches;
   {
     const uint32_t cap = next_pow2(std::max(64u, 2 * B));
     // one zeroed scratch: table u64[cap] | cnt[cap] | n_long
@@ -1819,8 +1919,8 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
     SL_TRY(scr.alloc(&gofs, cap));
     SL_TRY(scr.alloc(&gcnt, cap));
     SL_TRY(scr.alloc(&goff, cap));
-    const unsigned g = (B + 255) / 256, gc = (cap + 255) / 256;
-    k_group_insert<<<g, 256, 0, st>>>(hk, B, qdense, nden, qmax, table, cap, cnt, gslot, gpos, nl); ++t_launches;
+    const unsigned g = (B + 255) / 256, gc = (unsigned)std::min<uint64_t>((cap + 7) / 8, 64ull * num_sms(ix->device));
+    k_group_insert<<<g, 256, 0, st>>>(hk, B, qdense, nden, NDMAX, table, cap, cnt, gslot, gpos, nl); ++t_launches;
     SL_TRY(exclusive_scan_u32(cnt, gofs, cap, st, nullptr));
     k_group_scatter<<<g, 256, 0, st>>>(gslot, gpos, B, gofs, nl, perm_w); ++t_launches;
     k_pack_slots<false><<<gc, 256, 0, st>>>(cnt, gofs, cap, perm_w, ngath, plan.R, gcnt, nullptr, nullptr, nullptr,
@@ -1832,6 +1932,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
     ++t_launches;
   }
   const uint32_t* perm = perm_w;
+  tr.mark("groups+runs");
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
   ra.q_off = d_off;
@@ -1876,6 +1977,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   }
   SL_CUDA_TRY(cudaGetLastError());
   SL_CUDA_TRY(cudaEventRecord(sc->ev[2], st));
+  tr.mark("score");
   const uint64_t qstride = (uint64_t)plan.n_splits * plan.C;
   if (keys) {
     SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, nullptr, nullptr, nullptr, keys, st,
@@ -1884,6 +1986,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
     SL_TRY(launch_merge(cand, B, plan.n_splits, plan.C, plan.C, qstride, k, qconst, ids, scores, nullptr, st,
                         ra.gtau));
   }
+  tr.mark("merge");
   if (score_ms) {
     float ms = 0.f;
     SL_CUDA_TRY(cudaEventSynchronize(sc->ev[2]));
