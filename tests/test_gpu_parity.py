@@ -494,3 +494,32 @@ def test_build_sort_tiles_and_digit_widths(cuda_ok, V):
     ox = oracle.OracleIndex(off, tok, V, int(p.variant), p.k1, p.b, p.delta).export()
     with build_index(off, tok, V, p, keep_tf=True) as gi:
         assert_index_equal(gi.export(tf=True), ox, f"V={V}")
+
+
+@pytest.mark.parametrize("k", [10, 100])
+def test_signature_grouping_extremes(cuda_ok, c1, k):
+    """Query grouping (hash table of dense signatures) and run packing at their extremes: one
+    signature shared by thousands of queries (one group packed by a warp), thousands of empty /
+    OOV-only queries, every query distinct, and long queries (> 32 gathered rows) mixed in at
+    random positions — the results equal the oracle's whatever the grouping."""
+    cfg, corp, qoff, qtok = c1
+    p = BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)
+    ox = _oracle(corp, cfg.vocab, p)
+    exp = ox.export()
+    rng = np.random.default_rng(11)
+    base = [list(qtok[int(qoff[b]):int(qoff[b + 1])]) for b in range(len(qoff) - 1)]
+    heavy = [list(rng.integers(0, cfg.vocab, 60)) for _ in range(20)]  # > 32 gathered rows
+    batches = {
+        "one signature x3000": [base[0]] * 3000,
+        "empty and one-rare-token x2000": [[] for _ in range(1000)] + [[cfg.vocab - 1] * 3 for _ in range(1000)],
+        "distinct + long mixed": base + heavy + base[::-1],
+    }
+    with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
+        for what, queries in batches.items():
+            order = rng.permutation(len(queries))
+            queries = [queries[i] for i in order]
+            qo, qt = csr(queries)
+            gid, gsc = retrieve_batch(gi, (qo, qt), k, as_arrays=True)
+            rid, rsc = ox.retrieve_batch(qo, qt, k, True, 8)
+            assert_topk_match(gid, gsc, rid, rsc, k, cfg.num_docs, lambda b: ox.score_query(queries[b]),
+                              lambda b: query_scale(exp, queries[b]), f"{what} k={k}")
