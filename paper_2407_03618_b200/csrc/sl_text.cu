@@ -1486,6 +1486,7 @@ struct TScratch {
 struct TextStream {
   int device = -1;
   cudaStream_t st = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // sl_tokenize_stream's copy streams (created once)
 };
 thread_local TextStream t_text_stream[16];
 
@@ -2097,9 +2098,10 @@ int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t 
   }
   cudaStream_t st;
   SL_TRY(text_stream(v->device, &st));
-  cudaStream_t h2d, d2h;
-  SL_CUDA_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
-  SL_CUDA_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  TextStream& ts = t_text_stream[v->device];
+  if (!ts.h2d) SL_CUDA_TRY(cudaStreamCreateWithFlags(&ts.h2d, cudaStreamNonBlocking));
+  if (!ts.d2h) SL_CUDA_TRY(cudaStreamCreateWithFlags(&ts.d2h, cudaStreamNonBlocking));
+  cudaStream_t h2d = ts.h2d, d2h = ts.d2h;
   cudaEvent_t in_ready[2], out_done[2];
   for (int i = 0; i < 2; ++i) {
     SL_CUDA_TRY(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
@@ -2109,20 +2111,20 @@ int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t 
   uint64_t *draw[2] = {nullptr, nullptr}, *doff[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
   sl_token_batch* pending[2] = {nullptr, nullptr};
   int32_t rc = SL_OK;
+  // staging buffers come from the device's stream-ordered pool (kept mapped between calls)
   auto cleanup = [&]() {
     cudaStreamSynchronize(h2d);
     cudaStreamSynchronize(d2h);
     for (int i = 0; i < 2; ++i) {
       if (pending[i]) sl_token_batch_destroy(pending[i]);
-      cudaFree(dtext[i]);
-      cudaFree(draw[i]);
-      cudaFree(doff[i]);
-      cudaFree(dout[i]);
+      if (dtext[i]) cudaFreeAsync(dtext[i], st);
+      if (draw[i]) cudaFreeAsync(draw[i], st);
+      if (doff[i]) cudaFreeAsync(doff[i], st);
+      if (dout[i]) cudaFreeAsync(dout[i], st);
       cudaEventDestroy(in_ready[i]);
       cudaEventDestroy(out_done[i]);
     }
-    cudaStreamDestroy(h2d);
-    cudaStreamDestroy(d2h);
+    cudaStreamSynchronize(st);
   };
   auto cuda_ok = [&](cudaError_t e, const char* what) {
     if (e == cudaSuccess) return true;
@@ -2131,12 +2133,14 @@ int32_t sl_tokenize_stream(sl_vocab* v, const sl_tokenizer_config* cfg, int32_t 
     return false;
   };
   for (int i = 0; i < 2 && rc == SL_OK; ++i) {
-    if (!cuda_ok(cudaMalloc(&dtext[i], std::max<uint64_t>(max_bytes, 1)), "allocation") ||
-        !cuda_ok(cudaMalloc(&draw[i], (max_docs + 1) * 8), "allocation") ||
-        !cuda_ok(cudaMalloc(&doff[i], (max_docs + 1) * 8), "allocation") ||
-        !cuda_ok(cudaMalloc(&dout[i], (max_docs + 1) * 8), "allocation"))
+    if (!cuda_ok(cudaMallocAsync(&dtext[i], std::max<uint64_t>(max_bytes, 1), st), "allocation") ||
+        !cuda_ok(cudaMallocAsync(&draw[i], (max_docs + 1) * 8, st), "allocation") ||
+        !cuda_ok(cudaMallocAsync(&doff[i], (max_docs + 1) * 8, st), "allocation") ||
+        !cuda_ok(cudaMallocAsync(&dout[i], (max_docs + 1) * 8, st), "allocation"))
       break;
   }
+  // the copy streams use the buffers only after the allocations are ordered before them
+  if (rc == SL_OK) cuda_ok(cudaStreamSynchronize(st), "sync");
   // chunk i -> buffer i % 2: text bytes and the chunk's offsets rebased to its first byte
   auto issue_h2d = [&](size_t i) {
     const int bsel = (int)(i & 1);

@@ -1,5 +1,5 @@
 cd /root/repo
-for i in 1 2; do for L in old main; do
+for i in 1 2; do for L in ${LIBS:-old} main; do
   if [ $L = main ]; then unset SPARSELEX_LIB; else export SPARSELEX_LIB=$PWD/paper_2407_03618_b200/csrc/build/$L/libsparselex_b200.so; fi
   echo "$L $(python -c "
 import sys, json; sys.path.insert(0,'.')
