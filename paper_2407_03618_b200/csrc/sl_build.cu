@@ -915,6 +915,17 @@ namespace {
 // persistent index arrays come from the device's stream-ordered pool (kept mapped across
 // builds by the release threshold set in get_stream), so rebuilding does not pay page mapping
 thread_local cudaStream_t t_build_stream = nullptr;
+thread_local cudaStream_t t_side_stream[64] = {};
+
+// a second build stream of the current device (work that overlaps the build stream's)
+int32_t side_stream(cudaStream_t* out) {
+  int dev = 0;
+  SL_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) SL_FAIL(SL_EUNSUPPORTED, "device ordinal out of range");
+  if (!t_side_stream[dev]) SL_CUDA_TRY(cudaStreamCreateWithFlags(&t_side_stream[dev], cudaStreamNonBlocking));
+  *out = t_side_stream[dev];
+  return SL_OK;
+}
 
 template <class T>
 int32_t dalloc(sl_index* ix, T** p, uint64_t count) {
@@ -1069,6 +1080,31 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
       ++t_launches;
     }
   }
+  // skip tables on a side stream: their fill is latency-bound (one CTA per row), the dense
+  // copies below are bandwidth-bound, so the two overlap
+  cudaEvent_t fork = nullptr, join = nullptr;
+  struct EvGuard {  // on every exit: the build stream waits for the side stream before the
+    cudaStream_t s;  // temporaries it reads (slot_tok) are freed on the build stream
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~EvGuard() {
+      if (*b) cudaStreamWaitEvent(s, *b, 0);
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } evg{st, &fork, &join};
+  if (ix->skip_rows) {
+    SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
+    cudaStream_t side;
+    SL_TRY(side_stream(&side));
+    SL_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SL_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    SL_CUDA_TRY(cudaEventRecord(fork, st));
+    SL_CUDA_TRY(cudaStreamWaitEvent(side, fork, 0));
+    k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 8 * dev_sms()), 256, 0, side>>>(
+        ix->indptr, ix->docids, slot_tok + ix->dense_rows, ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
+    SL_CUDA_TRY(cudaEventRecord(join, side));
+  }
   if (ix->dense_rows) {
     // pair rows for the leading m dense slots, within 2 GB (c2: 120 rows, 480 MB; c4: 55 rows)
     // — SL_DENSE_PAIRS=m overrides, 0: none
@@ -1104,11 +1140,7 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
       k_dense_triples<<<gt, 256, 0, st>>>(ix->dense, ix->dense_rows, m, m3, ix->n_pad); ++t_launches;
     }
   }
-  if (ix->skip_rows) {
-    SL_TRY(dalloc(ix, &ix->skiptab, (uint64_t)ix->skip_rows * (ix->num_tiles + 1)));
-    k_skip_fill<<<std::min<uint32_t>(ix->skip_rows, 8 * dev_sms()), 256, 0, st>>>(
-        ix->indptr, ix->docids, slot_tok + ix->dense_rows, ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
-  }
+  if (ix->skip_rows) SL_CUDA_TRY(cudaStreamWaitEvent(st, join, 0));  // the skip tables (side stream) are done
   // block-max bounds for exact pruning (opt-in: SL_BLOCKMAX=1; measured slower at 512-doc tiles,
   // DESIGN.md §8)
   const char* bm = std::getenv("SL_BLOCKMAX");
