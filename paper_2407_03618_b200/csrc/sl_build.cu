@@ -915,15 +915,17 @@ namespace {
 // persistent index arrays come from the device's stream-ordered pool (kept mapped across
 // builds by the release threshold set in get_stream), so rebuilding does not pay page mapping
 thread_local cudaStream_t t_build_stream = nullptr;
-thread_local cudaStream_t t_side_stream[64] = {};
+thread_local cudaStream_t t_side_stream[64][2] = {};
 
-// a second build stream of the current device (work that overlaps the build stream's)
-int32_t side_stream(cudaStream_t* out) {
+// side build streams of the current device (work that overlaps the build stream's):
+// 0 = per-nonzero values, 1 = skip tables
+int32_t side_stream(cudaStream_t* out, int which = 1) {
   int dev = 0;
   SL_CUDA_TRY(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) SL_FAIL(SL_EUNSUPPORTED, "device ordinal out of range");
-  if (!t_side_stream[dev]) SL_CUDA_TRY(cudaStreamCreateWithFlags(&t_side_stream[dev], cudaStreamNonBlocking));
-  *out = t_side_stream[dev];
+  cudaStream_t& s = t_side_stream[dev][which & 1];
+  if (!s) SL_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
   return SL_OK;
 }
 
@@ -944,7 +946,8 @@ int32_t dalloc(sl_index* ix, T** p, uint64_t count) {
 // Query-side access structures from a finished CSC (ix->indptr/docids/values/df_global):
 // dense copies of the rows with global df >= density * N_global, per-tile skip offsets of
 // long rows, and the per-token dispatch table. Used by the build and by index loading.
-int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream_t st) {
+int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream_t st,
+                               cudaEvent_t values_ready = nullptr) {
   Temps tmp(st);
   const uint32_t N = ix->N, V = ix->V;
   ix->num_tiles = (N + kTileDocs - 1) / kTileDocs;
@@ -1105,6 +1108,8 @@ int32_t build_query_structures(sl_index* ix, float dense_min_density, cudaStream
         ix->indptr, ix->docids, slot_tok + ix->dense_rows, ix->skip_rows, ix->num_tiles, ix->skiptab); ++t_launches;
     SL_CUDA_TRY(cudaEventRecord(join, side));
   }
+  // the dense copies read the per-nonzero values (computed on a side stream during a build)
+  if (values_ready) SL_CUDA_TRY(cudaStreamWaitEvent(st, values_ready, 0));
   if (ix->dense_rows) {
     // pair rows for the leading m dense slots, within 2 GB (c2: 120 rows, 480 MB; c4: 55 rows)
     // — SL_DENSE_PAIRS=m overrides, 0: none
@@ -1311,12 +1316,34 @@ int32_t build_body(const sl_build_desc* d, sl_index* ix, cudaStream_t st, bool* 
   k_token_stats<<<grid_for(V, 256), 256, 0, st>>>(ix->df_global, V, ix->N_global, d->params, idf64, theta64,
                                                  ix->theta); ++t_launches;
   SL_TRY(dalloc(ix, &ix->values, nnz));
-  k_values<<<grid_for(nnz / 4 + 1, 256), 256, 0, st>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64, nnz,
-                                               d->params, ix->avg_len, ix->values, ix->tf); ++t_launches;
+  // the values run on a side stream while the access structures are planned and the skip
+  // tables filled (they need only indptr / docids / df); the dense copies wait for them
+  cudaStream_t vside;
+  SL_TRY(side_stream(&vside, 0));
+  cudaEvent_t vfork = nullptr, vjoin = nullptr;
+  struct VGuard {  // on every exit the build stream waits for the values before its temporaries
+    cudaStream_t s;  // (rows, runstart, idf64, theta64) are freed
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~VGuard() {
+      if (*b) cudaStreamWaitEvent(s, *b, 0);
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } vg{st, &vfork, &vjoin};
+  SL_CUDA_TRY(cudaEventCreateWithFlags(&vfork, cudaEventDisableTiming));
+  SL_CUDA_TRY(cudaEventCreateWithFlags(&vjoin, cudaEventDisableTiming));
+  SL_CUDA_TRY(cudaEventRecord(vfork, st));
+  SL_CUDA_TRY(cudaStreamWaitEvent(vside, vfork, 0));
+  k_values<<<grid_for(nnz / 4 + 1, 256), 256, 0, vside>>>(rows, ix->docids, runstart, ix->doclens, idf64, theta64,
+                                                         nnz, d->params, ix->avg_len, ix->values, ix->tf);
+  ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
+  SL_CUDA_TRY(cudaEventRecord(vjoin, vside));
   tr.mark("df+stats+values");
 
-  SL_TRY(build_query_structures(ix, d->dense_min_density, st));
+  SL_TRY(build_query_structures(ix, d->dense_min_density, st, vjoin));
+  SL_CUDA_TRY(cudaStreamWaitEvent(st, vjoin, 0));
   tr.mark("structures");
   SL_CUDA_TRY(cudaEventRecord(ev1, st));
   SL_CUDA_TRY(cudaStreamSynchronize(st));
