@@ -1151,38 +1151,6 @@ __global__ void k_rank_emit(const uint32_t* __restrict__ key, const uint32_t* __
   }
 }
 
-// Per query: sorted dense signature (slots of rows with a dense copy) and its hash.
-__global__ void k_query_sig(const uint64_t* __restrict__ q_off, const uint32_t* __restrict__ q_tok, uint32_t B,
-                            IndexView ix, uint32_t qmax, int32_t* __restrict__ qdense, uint32_t* __restrict__ nden,
-                            uint32_t* __restrict__ ngath, uint32_t* __restrict__ hkey, uint32_t* __restrict__ hval) {
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
-    int32_t* d = qdense + (uint64_t)q * qmax;
-    uint32_t n = 0, ng = 0;
-    for (uint64_t j = q_off[q]; j < q_off[q + 1]; ++j) {
-      const uint32_t t = q_tok[j];
-      if (t >= ix.V || ix.df_global[t] == 0 || ix.indptr[t] == ix.indptr[t + 1]) continue;
-      const int32_t info = ix.tokinfo[t];
-      if (info < 0) {
-        ++ng;
-        continue;
-      }
-      int b = (int)n - 1;
-      while (b >= 0 && d[b] > info) {
-        d[b + 1] = d[b];
-        --b;
-      }
-      d[b + 1] = info;
-      ++n;
-    }
-    uint32_t h = 2166136261u ^ n;  // FNV-1a over the sorted slots
-    for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
-    nden[q] = n;
-    ngath[q] = ng;
-    // > 32 gathered rows: sorts after every short query (key 0xFFFFFFFF) -> k_score_long
-    hkey[q] = (ng > 32 || n > (uint32_t)NDMAX) ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
-    hval[q] = q;
-  }
-}
 
 __device__ __forceinline__ bool same_signature(const int32_t* qdense, const uint32_t* nden, uint32_t qmax,
                                                uint32_t a, uint32_t b) {
