@@ -336,6 +336,7 @@ struct RunArgs {
   const uint32_t* perm;       // sorted position -> original query id
   const uint32_t* run_begin;  // [n_runs+1] positions in perm
   const uint32_t* n_runs;     // device scalar
+  const uint32_t* rorder;     // runs in work order (heaviest first), nullptr: run index order
   uint32_t* work;             // device scalar: next work item (zeroed by k_build_runs)
   uint64_t* gtau;             // [B] shared threshold per query across doc splits (nullptr: off)
   uint32_t k;
@@ -612,7 +613,8 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   // split-major order: concurrently resident warps sweep the same doc region, so each CSC
   // slice / dense chunk is fetched from HBM once and served from L2 to every query using it
   const bool smaj = ra.split_major != 0;
-  const uint32_t run = (uint32_t)(smaj ? item % n_runs : item / ra.n_splits);
+  const uint32_t ridx = (uint32_t)(smaj ? item % n_runs : item / ra.n_splits);
+  const uint32_t run = ra.rorder ? ra.rorder[ridx] : ridx;
   const uint32_t split = (uint32_t)(smaj ? item / n_runs : item % ra.n_splits);
   const uint32_t pb = ra.run_begin[run];
   const uint32_t nr = ra.run_begin[run + 1] - pb;
@@ -1268,6 +1270,45 @@ __global__ void k_pack_slots(const uint32_t* __restrict__ cnt, const uint32_t* _
   }
 }
 
+// Work order of the runs, heaviest first (an LPT schedule for the persistent scoring kernel:
+// with few items per warp — document shards, small batches — the heaviest run pulled last
+// would set the kernel's tail). Cost ~ postings of the run's queries + its dense rows x docs / 4;
+// runs are bucketed by log2 of the cost (32 buckets, counting sort, order within a bucket
+// arbitrary — the scores do not depend on it).
+__device__ __forceinline__ uint32_t run_bucket(const uint32_t* run_begin, const uint32_t* perm, const uint32_t* qpost,
+                                               const uint32_t* nden, uint32_t r, uint32_t n_docs) {
+  const uint32_t b = run_begin[r], e = run_begin[r + 1];
+  unsigned long long c = (unsigned long long)nden[perm[b]] * (n_docs / 4 + 1);
+  for (uint32_t i = b; i < e; ++i) c += qpost[perm[i]];
+  c = min(c, 0xFFFFFFFFull);
+  return c ? 31u - (uint32_t)__clz((uint32_t)c) : 0u;  // 0..31
+}
+
+__global__ void k_run_order(const uint32_t* __restrict__ run_begin, const uint32_t* __restrict__ n_runs,
+                            const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpost,
+                            const uint32_t* __restrict__ nden, uint32_t n_docs, uint32_t* __restrict__ bcnt,
+                            uint32_t* __restrict__ rorder) {
+  // one CTA: counts per bucket, exclusive offsets (heaviest bucket first), scatter
+  __shared__ uint32_t cnt[32], off[32];
+  const uint32_t R = *n_runs;
+  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < R; r += blockDim.x)
+    atomicAdd(&cnt[run_bucket(run_begin, perm, qpost, nden, r, n_docs)], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 31; b >= 0; --b) {
+      off[b] = run;
+      run += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < R; r += blockDim.x)
+    rorder[atomicAdd(&off[run_bucket(run_begin, perm, qpost, nden, r, n_docs)], 1u)] = r;
+  (void)bcnt;
+}
+
 // top-k over an arbitrary f32 vector (SPEC top_k on its own): CTA per split of tiles,
 // block-level filter + select, candidates [n_splits][C].
 __global__ void __launch_bounds__(NT) k_topk_vector(const float* __restrict__ vec, uint32_t n, uint32_t k,
@@ -1509,7 +1550,7 @@ __global__ void k_query_prep_sig(const uint64_t* __restrict__ q_off, const uint3
                                  IndexView ix, double* __restrict__ qconst, uint32_t* __restrict__ info,
                                  unsigned long long* __restrict__ bytes, int32_t* __restrict__ qdense,
                                  uint32_t* __restrict__ nden, uint32_t* __restrict__ ngath,
-                                 uint32_t* __restrict__ hkey) {
+                                 uint32_t* __restrict__ hkey, uint32_t* __restrict__ qpost) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t q0 = blockIdx.x * blockDim.x; q0 < B; q0 += stride) {
     const uint32_t q = q0 + threadIdx.x;
@@ -1557,6 +1598,7 @@ __global__ void k_query_prep_sig(const uint64_t* __restrict__ q_off, const uint3
       if (!lng)
         for (uint32_t i = 0; i < n; ++i) h = (h ^ (uint32_t)d[i]) * 16777619u;
       qconst[q] = c;
+      qpost[q] = (uint32_t)min(pb / 8ull, (unsigned long long)0xFFFFFFFFu);  // postings the query reads
       nden[q] = lng ? 0u : n;
       ngath[q] = ng;
       hkey[q] = lng ? 0xFFFFFFFFu : (h & 0x7FFFFFFFu);
@@ -1856,9 +1898,12 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   SL_TRY(scr.alloc(&ngath, B));
   SL_TRY(scr.alloc(&hk, B));
   SL_TRY(scr.alloc(&perm_w, B));
+  uint32_t* qpost;
+  SL_TRY(scr.alloc(&qpost, B));
   SL_TRY(scr.alloc(&run_begin, (uint64_t)B + 1));
   SL_TRY(scr.alloc(&n_runs, 2));
-  k_query_prep_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes, qdense, nden, ngath, hk);
+  k_query_prep_sig<<<(B + 255) / 256, 256, 0, st>>>(d_off, d_tok, B, v, qconst, info, bytes, qdense, nden, ngath, hk,
+                                                     qpost);
   ++t_launches;
   SL_CUDA_TRY(cudaGetLastError());
   uint32_t h_info[4];
@@ -1900,6 +1945,11 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
     ++t_launches;
   }
   const uint32_t* perm = perm_w;
+  uint32_t* rorder = nullptr;
+  if (env_int("SL_RUN_ORDER", 1)) {
+    SL_TRY(scr.alloc(&rorder, B));
+    k_run_order<<<1, 1024, 0, st>>>(run_begin, n_runs, perm, qpost, nden, ix->N, nullptr, rorder); ++t_launches;
+  }
   tr.mark("groups+runs");
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
@@ -1909,6 +1959,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   ra.perm = perm;
   ra.run_begin = run_begin;
   ra.n_runs = n_runs;
+  ra.rorder = rorder;
   ra.work = n_runs + 1;
   ra.k = k;
   ra.C = plan.C;
