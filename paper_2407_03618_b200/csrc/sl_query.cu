@@ -152,6 +152,9 @@ __device__ uint64_t block_select_kth(Visit visit, uint32_t k, uint32_t* hist, ui
 #ifndef SL_DENSE_ASYNC
 #define SL_DENSE_ASYNC 1
 #endif
+#ifndef SL_DCH
+#define SL_DCH 4  // float4 per lane of one dense row in registers at a time (the dense pass's chunk)
+#endif
 #ifndef SL_TMA_EARLY
 #define SL_TMA_EARLY 1  // the first dense row's bulk copy starts at the top of the tile
 #endif
@@ -825,7 +828,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // chunk during the copy spilled 648 B at the 64-register cap.
     auto dense_pass = [&](bool issued) -> float {
       float m = -INFINITY;
-      constexpr int DCH = F4L < 4 ? F4L : 4;
+      constexpr int DCH = F4L < SL_DCH ? F4L : SL_DCH;
       const float4* dbase = reinterpret_cast<const float4*>(ix.dense + d0) + lane;
       if (nd == 0) {
 #pragma unroll
@@ -883,7 +886,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
 #else
     auto dense_pass = [&](bool) -> float {
       float m = -INFINITY;
-      constexpr int DCH = F4L < 4 ? F4L : 4;
+      constexpr int DCH = F4L < SL_DCH ? F4L : SL_DCH;
 #pragma unroll 1
       for (int c0 = 0; c0 < F4L; c0 += DCH) {
         float4 a[DCH];
