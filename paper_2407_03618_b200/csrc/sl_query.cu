@@ -1289,8 +1289,7 @@ __device__ __forceinline__ uint32_t run_bucket(const uint32_t* run_begin, const 
 
 __global__ void k_run_order(const uint32_t* __restrict__ run_begin, const uint32_t* __restrict__ n_runs,
                             const uint32_t* __restrict__ perm, const uint32_t* __restrict__ qpost,
-                            const uint32_t* __restrict__ nden, uint32_t n_docs, uint32_t* __restrict__ bcnt,
-                            uint32_t* __restrict__ rorder) {
+                            const uint32_t* __restrict__ nden, uint32_t n_docs, uint32_t* __restrict__ rorder) {
   // one CTA: counts per bucket, exclusive offsets (heaviest bucket first), scatter
   __shared__ uint32_t cnt[32], off[32];
   const uint32_t R = *n_runs;
@@ -1309,7 +1308,6 @@ __global__ void k_run_order(const uint32_t* __restrict__ run_begin, const uint32
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < R; r += blockDim.x)
     rorder[atomicAdd(&off[run_bucket(run_begin, perm, qpost, nden, r, n_docs)], 1u)] = r;
-  (void)bcnt;
 }
 
 // top-k over an arbitrary f32 vector (SPEC top_k on its own): CTA per split of tiles,
@@ -1953,7 +1951,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   uint32_t* rorder = nullptr;
   if (env_int("SL_RUN_ORDER", 1)) {
     SL_TRY(scr.alloc(&rorder, B));
-    k_run_order<<<1, 1024, 0, st>>>(run_begin, n_runs, perm, qpost, nden, ix->N, nullptr, rorder); ++t_launches;
+    k_run_order<<<1, 1024, 0, st>>>(run_begin, n_runs, perm, qpost, nden, ix->N, rorder); ++t_launches;
   }
   tr.mark("groups+runs");
   SL_CUDA_TRY(cudaGetLastError());
