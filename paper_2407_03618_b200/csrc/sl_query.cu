@@ -1792,6 +1792,10 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
     ns = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(ns, cap));
   }
   p->n_splits = std::max(1u, std::min(ns, std::max(1u, ix->num_tiles)));
+  // few work items per resident warp (document shards, small batches): one query per run — the
+  // run sharing saves dense passes, but with ~2 items per warp the balance matters more (1/8 shard
+  // of c2: +5%)
+  if (env_int("SL_RUN", 0) == 0 && (uint64_t)(B / 2) * p->n_splits < 4 * warps) p->R = 1;
   return SL_OK;
 }
 

@@ -117,16 +117,21 @@ def test_dense_threshold_variants_match_oracle(cuda_ok, c1, density):
                       lambda i: query_scale(exp, q(i)), f"density={density}")
 
 
-def test_group_and_split_invariance(cuda_ok, c1, monkeypatch):
-    """Per-document summation order is fixed: any CTA grouping / doc split gives identical bits."""
+@pytest.mark.parametrize("k", [10, 50])
+def test_group_and_split_invariance(cuda_ok, c1, monkeypatch, k):
+    """Per-document summation order is fixed: any run size (queries of one dense signature per
+    warp item, the undo-log path for R > 1), doc split, work order or dense-chunk kernel gives
+    identical bits."""
     cfg, corp, qoff, qtok = c1
-    p = BM25Params(Variant.lucene)
+    p = BM25Params(Variant.bm25plus, 1.5, 0.75, 0.5)
     with build_index(corp.offsets, corp.tokens, cfg.vocab, p) as gi:
-        ref = retrieve_batch(gi, (qoff, qtok), 50, as_arrays=True)
-        for g, s in [(1, 1), (3, 2), (16, 1), (8, 7)]:
-            monkeypatch.setenv("SL_GROUP", str(g))
+        ref = retrieve_batch(gi, (qoff, qtok), k, as_arrays=True)
+        for r, s, order, narrow in [(1, 1, 1, 4), (2, 3, 0, 4), (4, 1, 1, 0), (3, 7, 1, 1000), (2, 10, 1, 0)]:
+            monkeypatch.setenv("SL_RUN", str(r))
             monkeypatch.setenv("SL_SPLITS", str(s))
-            out = retrieve_batch(gi, (qoff, qtok), 50, as_arrays=True)
+            monkeypatch.setenv("SL_RUN_ORDER", str(order))
+            monkeypatch.setenv("SL_NARROW_ITEMS", str(narrow))
+            out = retrieve_batch(gi, (qoff, qtok), k, as_arrays=True)
             np.testing.assert_array_equal(out[0], ref[0])
             np.testing.assert_array_equal(out[1], ref[1])
 
