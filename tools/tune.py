@@ -49,7 +49,7 @@ def main():
     sc = torch.empty((B, a.k), dtype=torch.float32, device="cuda")
     st = _lib.RetrieveStats()
     for env in json.loads(a.sweep):
-        for key in ("SL_RUN", "SL_SPLITS", "SL_GTAU", "SL_DEBUG_SKIP", "SL_RUN_ORDER", "SL_MERGE_WARP", "SL_MIN_TILES", "SL_SPLIT_GAMMA"):
+        for key in ("SL_RUN", "SL_SPLITS", "SL_GTAU", "SL_DEBUG_SKIP", "SL_RUN_ORDER", "SL_MERGE_WARP", "SL_MIN_TILES", "SL_SPLIT_GAMMA", "SL_MERGE_BIG"):
             os.environ.pop(key, None)
         os.environ.update({k: str(v) for k, v in env.items()})
         ts = []
