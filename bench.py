@@ -532,6 +532,66 @@ def extra_block(L, sh, cfg_i, k, variant, args, world, rank, flush, hbm, hbm_src
     return blk
 
 
+def shard_projection_block(L, sh, args, flush):
+    """Per-GPU work of an N-way document sharding, measured on this one GPU (N = 2, 4, 8): shard 0
+    of the token-balanced split is built with the corpus-wide statistics of the full index (what a
+    rank computes after the NCCL all-reduce), the whole query batch is scored on it (device-timed
+    like the headline), and the rank-0 merge of N x B x k candidate keys is timed on N copies of
+    that shard's keys. Not an N-GPU measurement: the NCCL gather of the keys is not included
+    (its bytes are reported)."""
+    import torch
+    from paper_2407_03618_b200 import BM25Params, Variant, build_index, shard_ranges, synth
+    from paper_2407_03618_b200._lib import SL_MEM_DEVICE, SL_MEM_HOST, check
+    cfg, k = sh.cfg, args.k
+    V, N = cfg.vocab, cfg.num_docs
+    df = np.empty(V, np.uint32)
+    check(L.sl_index_export(sh.idx.handle, SL_MEM_HOST, None, None, None, df.ctypes.data, None, None, None))
+    offsets = synth.doc_offsets(cfg)
+    T = int(offsets[-1])
+    qoff, qtok = synth.queries(cfg, sh.cdf)
+    B = len(qoff) - 1
+    d_off = torch.from_numpy(qoff.astype(np.uint64)).cuda()
+    d_tok = torch.from_numpy(qtok.astype(np.uint32)).cuda()
+    p = BM25Params(Variant[args.variant], 1.5, 0.75, VARIANT_DELTA[args.variant])
+    out = {"note": "shard 0 of an N-way token-balanced document sharding on ONE GPU, corpus-wide statistics; "
+                   "per_rank = its device-timed retrieve_batch of the whole batch; merge = rank-0 merge of N x B "
+                   "x k keys on this GPU; the NCCL gather (gather_bytes) is not measured",
+           "config": f"c{args.config} {args.variant} top-{k}, {B} queries"}
+    for f in (2, 4, 8):
+        d0, d1 = shard_ranges(offsets, f)[0]
+        o0, o1 = int(offsets[d0]), int(offsets[d1])
+        tok = torch.empty(max(1, o1 - o0), dtype=torch.uint32, device="cuda")
+        synth.tokens_device(cfg, sh.cdf, o0, o1 - o0, tok.data_ptr())
+        loff = torch.from_numpy((offsets[d0:d1 + 1] - np.uint64(o0)).astype(np.uint64)).cuda()
+        with build_index(loff, tok, V, p, doc_base=d0, dense_min_density=args.dense_density,
+                         global_stats=(df, N, T)) as ix:
+            r = time_retrieval(L, ix, qoff, qtok, k, args.steps, args.warmup, 0, 1, flush, e2e=False)
+            keys = torch.empty((B, k), dtype=torch.int64, device="cuda")
+            qc = torch.empty(B, dtype=torch.float64, device="cuda")
+            check(L.sl_retrieve_local(ix.handle, d_off.data_ptr(), d_tok.data_ptr(), B, k, SL_MEM_DEVICE,
+                                      keys.data_ptr(), qc.data_ptr()))
+        del tok, loff
+        allk = keys.unsqueeze(0).repeat(f, 1, 1).contiguous()
+        ids = torch.empty((B, k), dtype=torch.uint32, device="cuda")
+        sc = torch.empty((B, k), dtype=torch.float32, device="cuda")
+        ms = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            check(L.sl_merge_candidates(allk.data_ptr(), f, B, k, qc.data_ptr(), SL_MEM_DEVICE, 0, ids.data_ptr(),
+                                        sc.data_ptr()))
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ms.append((time.perf_counter() - t0) * 1e3)
+        merge_ms = float(np.median(ms))
+        out[f"N{f}"] = {"docs": int(d1 - d0), "per_rank_qps": r["value"], "per_rank_ms": r["ms_per_step"],
+                        "merge_ms": merge_ms, "gather_bytes": int(f * B * k * 8),
+                        "projected_qps_before_gather": B / ((r["ms_per_step"] + merge_ms) / 1e3)}
+        del allk, keys, qc
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ncu_child(args):
     """--ncu-child: build the workload's index and run ONE retrieve_batch (profiled by ncu_probe)."""
     import torch
@@ -610,6 +670,8 @@ def run_ours(args):
     if not args.no_extra and args.shard_of == 1:
         if args.config == 2 and args.variant == "lucene":
             blocks["c2_top100"] = extra_block(L, sh, 2, 100, "lucene", args, world, rank, flush, hbm, hbm_src, sms)
+        if world == 1 and not args.no_projection:
+            blocks["shard_projection"] = shard_projection_block(L, sh, args, flush)
         sh.close()
         if args.config == 2 and world == 1:  # c3: the variant sweep on c2's corpus
             for v in ("robertson", "atire", "bm25l", "bm25plus"):
@@ -673,6 +735,8 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the c2 top-100 / c3 / c4 / c5 blocks")
     ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu counters (roofline traffic)")
     ap.add_argument("--c5", action="store_true", help="add the c5 block below 8 GPUs (each rank holds 1/N)")
+    ap.add_argument("--no-projection", action="store_true",
+                    help="skip the one-GPU per-rank measurement of the 2/4/8-way document sharding")
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--ref-sample", type=int, default=0, help="reference arm: queries per step (0 = the whole batch)")
     ap.add_argument("--shard-of", type=int, default=1, help="build one shard of an N-way doc sharding (1 GPU)")
