@@ -359,6 +359,7 @@ struct RunArgs {
 // filter_tile takes this or the warp kernel's WarpSmem
 struct WSmem {
   uint64_t* tau;     // [1]
+  float* tauf;       // [1] tau_float(*tau), kept with it
   uint32_t* n_kept;  // [1]
   uint32_t* hist;    // [16] warp_select_kth histogram
 };
@@ -378,6 +379,7 @@ struct __align__(16) WarpSmem {
 #endif
   uint64_t row_start[32];     // gathered-row entries (lane = entry)
   uint64_t tau[RMAX];         // exact running threshold key per query
+  float tauf[RMAX];           // tau_float(tau[r]), updated with it (the filter's pre-test bound)
   uint32_t row_len[32];
   int32_t skip[32];
   float rmax[32];             // row maxima (block-max pruning)
@@ -479,7 +481,7 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
   const int lane = threadIdx.x & 31;
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   uint64_t tau = s.tau[r];
-  float tf = tau_float(tau);
+  float tf = s.tauf[r];
   float mx = pmax;
   if (isnan(pmax)) {
   mx = -INFINITY;
@@ -577,6 +579,7 @@ __device__ __forceinline__ void filter_tile(SM& s, uint32_t r, uint32_t k, uint3
     if (lane == 0) {
       s.n_kept[r] = out + tot2;
       s.tau[r] = mn;
+      s.tauf[r] = tau_float(mn);
       const uint64_t hi = mn >> 32;
       if (gpub && hi > 1) atomicMax((unsigned long long*)gpub, (unsigned long long)(((hi - 1) << 32) | 0xFFFFFFFFull));
     }
@@ -668,6 +671,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     if (act) {
       s.n_kept[lane] = 0;
       s.tau[lane] = 0;
+      s.tauf[lane] = -INFINITY;
     }
     if (lane == 0) {
       for (uint32_t a = 1; a < nd; ++a) {  // canonical (ascending slot) order of the dense terms
@@ -1004,7 +1008,8 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
   uint32_t* n_kept = reinterpret_cast<uint32_t*>(row_start + qcap);
   uint32_t* hist = n_kept + 1;                                     // [16]
   int32_t* counts = reinterpret_cast<int32_t*>(hist + 16);         // nd, ns
-  int32_t* dslot = counts + 2;                                     // [qcap]
+  float* tauf = reinterpret_cast<float*>(counts + 2);              // [1] (+ 1 pad)
+  int32_t* dslot = counts + 4;                                     // [qcap]
   uint32_t* row_len = reinterpret_cast<uint32_t*>(dslot + qcap);   // [qcap]
   int32_t* skip = reinterpret_cast<int32_t*>(row_len + qcap);      // [qcap]
   uint32_t* cursor = reinterpret_cast<uint32_t*>(skip + qcap);     // [qcap]
@@ -1040,6 +1045,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
     counts[0] = nd;
     counts[1] = ns;
     *tau = 0;
+    *tauf = -INFINITY;
     *n_kept = 0;
   }
   __syncthreads();
@@ -1060,6 +1066,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
   __syncthreads();
   WSmem ws{};
   ws.tau = tau;
+  ws.tauf = tauf;
   ws.n_kept = n_kept;
   ws.hist = hist;
   uint64_t* kept = ra.cand + ((uint64_t)q * ra.n_splits + split) * ra.C;
@@ -1131,7 +1138,7 @@ __global__ void __launch_bounds__(NT) k_score_long(IndexView ix, RunArgs ra, uin
 }
 
 __host__ inline size_t long_smem_bytes(uint32_t qcap) {
-  return (size_t)TILE * 4 + 8 + (size_t)qcap * 8 + 4 + 16 * 4 + 8 + (size_t)qcap * 4 * 7 + 16;
+  return (size_t)TILE * 4 + 8 + (size_t)qcap * 8 + 4 + 16 * 4 + 16 + (size_t)qcap * 4 * 7 + 16;
 }
 
 // Large k (> kMaxK): keys for a stable LSD radix sort that yields (score desc, doc asc).
