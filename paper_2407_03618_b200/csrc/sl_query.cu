@@ -330,6 +330,9 @@ constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) hand
 #ifndef SL_UNROLL
 #define SL_UNROLL 4
 #endif
+#ifndef SL_PAR_SETUP
+#define SL_PAR_SETUP 1  // work-item setup with a lane per query token (0: a lane per query, serial over its tokens)
+#endif
 constexpr int UNROLL = SL_UNROLL;  // gather rounds whose loads are issued together
 
 struct RunArgs {
@@ -627,6 +630,65 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   const uint32_t t0 = (uint32_t)((uint64_t)split * ix.num_tiles / ra.n_splits);
   const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * ix.num_tiles / ra.n_splits);
 
+#if SL_PAR_SETUP
+  // ---- setup, a lane per query token: the tokens of the run's queries, concatenated in query
+  // order, are classified 32 at a time (each lane's df / indptr / tokinfo loads in flight
+  // together: four L2 round trips per chunk instead of four per token), and ballots place the
+  // gathered rows (query order, then token order) and query 0's dense slots
+  {
+    const bool act = (uint32_t)lane < nr;
+    const uint32_t ql = act ? ra.perm[pb + lane] : 0u;
+    const uint64_t qbl = act ? ra.q_off[ql] : 0ull;
+    const uint32_t lenl = act ? (uint32_t)(ra.q_off[ql + 1] - qbl) : 0u;
+    const uint32_t incl = warp_incl_scan(lenl);  // lanes >= nr hold the total
+    const uint32_t excl = incl - lenl;
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t len0 = __shfl_sync(0xffffffffu, incl, 0);  // query 0 owns positions [0, len0)
+    if (act) s.qid[lane] = ql;
+    uint32_t e = 0, nd = 0, eb = 0;  // gathered entries / query 0's dense terms so far (uniform); entries before query `lane`
+    for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
+      const uint32_t p = p0 + lane;
+      uint32_t r = 0;  // the query owning position p
+      for (uint32_t a = 0; a + 1 < nr; ++a) r += p >= __shfl_sync(0xffffffffu, incl, a) ? 1u : 0u;
+      const uint64_t qb = __shfl_sync(0xffffffffu, qbl, r);
+      const uint32_t ex = __shfl_sync(0xffffffffu, excl, r);
+      uint32_t t = 0xFFFFFFFFu;
+      if (p < tot) t = ra.q_tok[qb + (p - ex)];
+      bool ok = p < tot && t < ix.V;
+      uint32_t dfv = 0;
+      uint64_t rb = 0, re = 0;
+      int32_t info = 0;
+      if (ok) {
+        dfv = ix.df_global[t];
+        rb = ix.indptr[t];
+        re = ix.indptr[t + 1];
+        info = ix.tokinfo[t];
+      }
+      ok = ok && dfv != 0 && rb != re;  // OOV drop (SPEC tokenizer decisions); no local postings
+      const bool isg = ok && info < 0, isd = ok && info >= 0 && p < len0;
+      const uint32_t ms = __ballot_sync(0xffffffffu, isg), md = __ballot_sync(0xffffffffu, isd);
+      if (isg) {
+        const uint32_t ee = e + __popc(ms & lanemask_lt());
+        if (ee < 32) {
+          s.row_start[ee] = rb;
+          s.row_len[ee] = (uint32_t)(re - rb);
+          s.skip[ee] = info <= -2 ? -2 - info : -1;
+          if (PRUNE) s.rmax[ee] = ix.rowmax[t];
+        }
+      }
+      if (isd) {  // identical multiset for every query of the run: query 0's
+        const uint32_t di = nd + __popc(md & lanemask_lt());
+        if (di < (uint32_t)NDMAX) s.dslot[di] = info;
+      }
+      const uint32_t w = excl > p0 ? min(excl - p0, 32u) : 0u;  // this chunk's positions before query `lane`
+      eb += __popc(ms & (w >= 32u ? 0xffffffffu : (1u << w) - 1u));
+      e += __popc(ms);
+      nd += __popc(md);
+    }
+    if (act) s.ebeg[lane] = (int32_t)min(eb, 32u);
+    if (lane == 0) s.ebeg[nr] = (int32_t)min(e, 32u);
+    __syncwarp();
+#else
   // ---- setup: lane r classifies query r's tokens; gathered rows are concatenated
   {
     const bool act = (uint32_t)lane < nr;
@@ -668,6 +730,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
         ++e;
       }
     }
+#endif
     if (act) {
       s.n_kept[lane] = 0;
       s.tau[lane] = 0;
