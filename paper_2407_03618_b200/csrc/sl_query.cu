@@ -330,10 +330,24 @@ constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) hand
 #ifndef SL_UNROLL
 #define SL_UNROLL 4
 #endif
-#ifndef SL_PAR_SETUP
-#define SL_PAR_SETUP 1  // work-item setup with a lane per query token (0: a lane per query, serial over its tokens)
-#endif
 constexpr int UNROLL = SL_UNROLL;  // gather rounds whose loads are issued together
+
+constexpr int NDMAX = 64;   // dense rows per query in the warp kernel
+
+// Everything a (run, split) work item of k_score_runs needs to start, written once per run and
+// batch by k_run_desc in work order (the classification of the run's tokens does not depend on
+// the split): members, their gathered-row entries (query order, then token order; at most 32,
+// one lane each), the dense signature in canonical order with its leading pair / triple row.
+struct __align__(16) RunDesc {
+  uint32_t qid[SL_RMAX_CT];       // original query index of member r (~0: none)
+  int32_t ebeg[SL_RMAX_CT + 1];   // member r owns entries [ebeg[r], ebeg[r + 1])
+  int32_t nd;                     // dense rows to sum
+  int32_t dslot[NDMAX];           // ascending slots; dslot[0] may be a pair / triple row
+  uint64_t row_start[32];         // per entry: CSC row start, length, skip-table slot (-1: none), row maximum
+  uint32_t row_len[32];
+  int32_t skip[32];
+  float rmax[32];
+};
 
 struct RunArgs {
   const uint64_t* q_off;      // [B+1]
@@ -343,6 +357,7 @@ struct RunArgs {
   const uint32_t* run_begin;  // [n_runs+1] positions in perm
   const uint32_t* n_runs;     // device scalar
   const uint32_t* rorder;     // runs in work order (heaviest first), nullptr: run index order
+  const RunDesc* rdesc;       // [n_runs] descriptor of the run at each work-order position (k_run_desc)
   uint32_t* work;             // device scalar: next work item (zeroed by k_build_runs)
   uint64_t* gtau;             // [B] shared threshold per query across doc splits (nullptr: off)
   uint32_t k;
@@ -371,7 +386,6 @@ struct WSmem {
 // LDS/STS with an immediate offset (no generic-pointer rematerialisation). Bounds: <= 32
 // gathered rows and <= NDMAX dense rows per run (other queries take k_score_long).
 constexpr int WPC = 8;      // warps per CTA
-constexpr int NDMAX = 64;   // dense rows per query in the warp kernel
 struct __align__(16) WarpSmem {
   float dsum[TILE];           // dense-signature sum of the current tile
 #if SL_RMAX_CT > 1
@@ -380,12 +394,8 @@ struct __align__(16) WarpSmem {
   uint16_t ulog_doc[ULOG * 32];
   float ulog_old[ULOG * 32];
 #endif
-  uint64_t row_start[32];     // gathered-row entries (lane = entry)
   uint64_t tau[RMAX];         // exact running threshold key per query
   float tauf[RMAX];           // tau_float(tau[r]), updated with it (the filter's pre-test bound)
-  uint32_t row_len[32];
-  int32_t skip[32];
-  float rmax[32];             // row maxima (block-max pruning)
   int32_t dslot[NDMAX];       // the run's dense signature, ascending slots
   uint32_t hist[16];          // warp_select_kth histogram
   uint32_t n_kept[RMAX];
@@ -623,167 +633,45 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
   // slice / dense chunk is fetched from HBM once and served from L2 to every query using it
   const bool smaj = ra.split_major != 0;
   const uint32_t ridx = (uint32_t)(smaj ? item % n_runs : item / ra.n_splits);
-  const uint32_t run = ra.rorder ? ra.rorder[ridx] : ridx;
   const uint32_t split = (uint32_t)(smaj ? item / n_runs : item % ra.n_splits);
-  const uint32_t pb = ra.run_begin[run];
-  const uint32_t nr = ra.run_begin[run + 1] - pb;
   const uint32_t t0 = (uint32_t)((uint64_t)split * ix.num_tiles / ra.n_splits);
   const uint32_t t1 = (uint32_t)((uint64_t)(split + 1) * ix.num_tiles / ra.n_splits);
 
-#if SL_PAR_SETUP
-  // ---- setup, a lane per query token: the tokens of the run's queries, concatenated in query
-  // order, are classified 32 at a time (each lane's df / indptr / tokinfo loads in flight
-  // together: four L2 round trips per chunk instead of four per token), and ballots place the
-  // gathered rows (query order, then token order) and query 0's dense slots
+  // ---- setup: the run's descriptor (k_run_desc, work order) — members, gathered-row entries
+  // (lane = entry, straight into registers) and the dense signature; every load is independent,
+  // so a work item starts after one L2 round trip (plus the first slices below)
+  const RunDesc* rd = ra.rdesc + ridx;
+  const uint32_t qm = lane < RMAX ? __ldg(rd->qid + lane) : 0xFFFFFFFFu;
+  const int32_t eb = lane <= RMAX ? __ldg(rd->ebeg + lane) : 0;
+  const int nd = __ldg(&rd->nd);
+  const uint32_t nr = (uint32_t)__popc(__ballot_sync(0xffffffffu, qm != 0xFFFFFFFFu));
+  const int E = __shfl_sync(0xffffffffu, eb, nr);
+  const bool ent = lane < E;
+  const uint64_t rstart = ent ? __ldg(rd->row_start + lane) : 0ull;
+  const uint32_t rlen = ent ? __ldg(rd->row_len + lane) : 0u;
+  const int32_t sk = ent ? __ldg(rd->skip + lane) : -1;
+  const float rmx = PRUNE && ent ? __ldg(rd->rmax + lane) : 0.f;
+  if (lane < nd) s.dslot[lane] = __ldg(rd->dslot + lane);
+  if (lane + 32 < nd) s.dslot[lane + 32] = __ldg(rd->dslot + lane + 32);
   {
-    const bool act = (uint32_t)lane < nr;
-    const uint32_t ql = act ? ra.perm[pb + lane] : 0u;
-    const uint64_t qbl = act ? ra.q_off[ql] : 0ull;
-    const uint32_t lenl = act ? (uint32_t)(ra.q_off[ql + 1] - qbl) : 0u;
-    const uint32_t incl = warp_incl_scan(lenl);  // lanes >= nr hold the total
-    const uint32_t excl = incl - lenl;
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t len0 = __shfl_sync(0xffffffffu, incl, 0);  // query 0 owns positions [0, len0)
-    if (act) s.qid[lane] = ql;
-    uint32_t e = 0, nd = 0, eb = 0;  // gathered entries / query 0's dense terms so far (uniform); entries before query `lane`
-    for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
-      const uint32_t p = p0 + lane;
-      uint32_t r = 0;  // the query owning position p
-      for (uint32_t a = 0; a + 1 < nr; ++a) r += p >= __shfl_sync(0xffffffffu, incl, a) ? 1u : 0u;
-      const uint64_t qb = __shfl_sync(0xffffffffu, qbl, r);
-      const uint32_t ex = __shfl_sync(0xffffffffu, excl, r);
-      uint32_t t = 0xFFFFFFFFu;
-      if (p < tot) t = ra.q_tok[qb + (p - ex)];
-      bool ok = p < tot && t < ix.V;
-      uint32_t dfv = 0;
-      uint64_t rb = 0, re = 0;
-      int32_t info = 0;
-      if (ok) {
-        dfv = ix.df_global[t];
-        rb = ix.indptr[t];
-        re = ix.indptr[t + 1];
-        info = ix.tokinfo[t];
-      }
-      ok = ok && dfv != 0 && rb != re;  // OOV drop (SPEC tokenizer decisions); no local postings
-      const bool isg = ok && info < 0, isd = ok && info >= 0 && p < len0;
-      const uint32_t ms = __ballot_sync(0xffffffffu, isg), md = __ballot_sync(0xffffffffu, isd);
-      if (isg) {
-        const uint32_t ee = e + __popc(ms & lanemask_lt());
-        if (ee < 32) {
-          s.row_start[ee] = rb;
-          s.row_len[ee] = (uint32_t)(re - rb);
-          s.skip[ee] = info <= -2 ? -2 - info : -1;
-          if (PRUNE) s.rmax[ee] = ix.rowmax[t];
-        }
-      }
-      if (isd) {  // identical multiset for every query of the run: query 0's
-        const uint32_t di = nd + __popc(md & lanemask_lt());
-        if (di < (uint32_t)NDMAX) s.dslot[di] = info;
-      }
-      const uint32_t w = excl > p0 ? min(excl - p0, 32u) : 0u;  // this chunk's positions before query `lane`
-      eb += __popc(ms & (w >= 32u ? 0xffffffffu : (1u << w) - 1u));
-      e += __popc(ms);
-      nd += __popc(md);
-    }
-    if (act) s.ebeg[lane] = (int32_t)min(eb, 32u);
-    if (lane == 0) s.ebeg[nr] = (int32_t)min(e, 32u);
-    __syncwarp();
-#else
-  // ---- setup: lane r classifies query r's tokens; gathered rows are concatenated
-  {
-    const bool act = (uint32_t)lane < nr;
-    const uint32_t q = act ? ra.perm[pb + lane] : 0u;
-    if (act) s.qid[lane] = q;
-    const uint64_t qb = act ? ra.q_off[q] : 0, qe = act ? ra.q_off[q + 1] : 0;
-    uint32_t ns = 0, nd = 0;
-    for (uint64_t j = qb; j < qe; ++j) {
-      const uint32_t t = ra.q_tok[j];
-      if (t >= ix.V || ix.df_global[t] == 0 || ix.indptr[t] == ix.indptr[t + 1]) continue;
-      if (ix.tokinfo[t] >= 0) ++nd; else ++ns;
-    }
-    const uint32_t incl = warp_incl_scan(ns);
-    uint32_t e = incl - ns;
-    if (act) s.ebeg[lane] = (int32_t)e;
-    if (lane == 31) s.ebeg[nr] = (int32_t)min(incl, 32u);
-    nd = 0;
-    for (uint64_t j = qb; j < qe; ++j) {
-      const uint32_t t = ra.q_tok[j];
-      if (t >= ix.V || ix.df_global[t] == 0) continue;  // OOV drop (SPEC tokenizer decisions)
-      const uint64_t rb = ix.indptr[t], re = ix.indptr[t + 1];
-      if (rb == re) continue;                           // no local postings
-      const int32_t info = ix.tokinfo[t];
-      if (info >= 0) {
-        if (lane == 0 && nd < NDMAX) s.dslot[nd] = info;  // identical multiset for every query of the run
-        ++nd;
-      } else if (e < 32) {
-#ifdef SL_DEBUG_CHECKS
-        if (e >= 32u) {
-          printf("entry overflow: run %u lane %d nr %u R %u qmax %u e %u incl %u ns %u q %u qlen %llu\n", run, lane, nr,
-                 ra.R, ra.qmax, e, incl, ns, q, (unsigned long long)(qe - qb));
-          __trap();
-        }
-#endif
-        s.row_start[e] = rb;
-        s.row_len[e] = (uint32_t)(re - rb);
-        s.skip[e] = info <= -2 ? -2 - info : -1;
-        if (PRUNE) s.rmax[e] = ix.rowmax[t];
-        ++e;
-      }
-    }
-#endif
-    if (act) {
+    const int e1 = __shfl_down_sync(0xffffffffu, eb, 1);
+    if ((uint32_t)lane < nr) {
+      s.qid[lane] = qm;
       s.n_kept[lane] = 0;
       s.tau[lane] = 0;
       s.tauf[lane] = -INFINITY;
+      s.emask[lane] = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << eb) - 1u);
+      s.keptp[lane] = ra.cand + ((uint64_t)qm * ra.n_splits + split) * ra.C;
     }
-    if (lane == 0) {
-      for (uint32_t a = 1; a < nd; ++a) {  // canonical (ascending slot) order of the dense terms
-        const int32_t x = s.dslot[a];
-        int b = (int)a - 1;
-        while (b >= 0 && s.dslot[b] > x) {
-          s.dslot[b + 1] = s.dslot[b];
-          --b;
-        }
-        s.dslot[b + 1] = x;
-      }
-      // a signature led by two slots with a pair row starts from it (one dense row fewer)
-      // (a repeated token repeats its slot: equal leading slots have no pair row)
-      if (!PRUNE && nd >= 3 && nd <= (uint32_t)NDMAX && (uint32_t)s.dslot[2] < ix.triple_m &&
-          s.dslot[0] < s.dslot[1] && s.dslot[1] < s.dslot[2]) {  // three leading slots: a triple row
-        s.dslot[0] = (int32_t)dense_triple_row(ix.n_dense, ix.pair_m, (uint32_t)s.dslot[0], (uint32_t)s.dslot[1],
-                                               (uint32_t)s.dslot[2]);
-        for (uint32_t a = 1; a + 2 < nd; ++a) s.dslot[a] = s.dslot[a + 2];
-        nd -= 2;
-      } else if (!PRUNE && nd >= 2 && nd <= (uint32_t)NDMAX && (uint32_t)s.dslot[1] < ix.pair_m &&
-                 s.dslot[0] < s.dslot[1]) {
-        s.dslot[0] = (int32_t)dense_pair_row(ix.n_dense, ix.pair_m, (uint32_t)s.dslot[0], (uint32_t)s.dslot[1]);
-        for (uint32_t a = 1; a + 1 < nd; ++a) s.dslot[a] = s.dslot[a + 1];
-        --nd;
-      }
-      s.nd[0] = (int32_t)nd;
-    }
+    if (PRUNE && (uint32_t)lane <= nr) s.ebeg[lane] = eb;
   }
   __syncwarp();
-  if ((uint32_t)lane < nr) {
-    const int e0 = s.ebeg[lane], e1 = s.ebeg[lane + 1];
-    s.emask[lane] = (e1 >= 32 ? 0xffffffffu : ((1u << e1) - 1u)) & ~((1u << e0) - 1u);
-    s.keptp[lane] = ra.cand + ((uint64_t)s.qid[lane] * ra.n_splits + split) * ra.C;
-  }
-  __syncwarp();
-  const int E = s.ebeg[nr];
-  const int nd = s.nd[0];
 #ifdef SL_DEBUG_CHECKS
   if (lane == 0 && (nr > ra.R || nr == 0 || (uint32_t)E > 32u || (uint32_t)nd > ra.qmax)) {
-    printf("k_score_runs invariant: run %u nr %u R %u E %d qmax %u nd %d\n", run, nr, ra.R, E, ra.qmax, nd);
+    printf("k_score_runs invariant: item %u nr %u R %u E %d qmax %u nd %d\n", ridx, nr, ra.R, E, ra.qmax, nd);
     __trap();
   }
 #endif
-  // ---- per-lane entry state (registers)
-  const bool ent = lane < E;
-  const uint64_t rstart = ent ? s.row_start[lane] : 0ull;
-  const uint32_t rlen = ent ? s.row_len[lane] : 0u;
-  const int32_t sk = ent ? s.skip[lane] : -1;
-  const float rmx = PRUNE && ent ? s.rmax[lane] : 0.f;
   const uint32_t* tab = ix.skiptab + (uint64_t)(sk < 0 ? 0 : sk) * (ix.num_tiles + 1);
   uint32_t cursor = 0, nextdoc = 0xFFFFFFFFu;  // short rows
   uint32_t nsb = 0, nse = 0;                   // skip rows: slice [nsb, nse) of the current tile
@@ -1012,7 +900,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           lmax = fmaxf(lmax, apply_slices(ix, emask, cnt, rbase, buf, d0));
       }
       if constexpr (MODE == GM_DENSE) {
-        const double qc = ra.qconst[ra.perm[pb + r]];
+        const double qc = ra.qconst[q];
         for (uint32_t i = lane; i < nvalid; i += 32) ra.dense_out[d0 + i] = __double2float_rn((double)buf[i] + qc);
         __syncwarp();
       } else {
@@ -1378,6 +1266,112 @@ __global__ void k_run_order(const uint32_t* __restrict__ run_begin, const uint32
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < R; r += blockDim.x)
     rorder[atomicAdd(&off[run_bucket(run_begin, perm, qpost, nden, r, n_docs)], 1u)] = r;
+}
+
+// Descriptor of every run in work order (one warp per run; see RunDesc). A lane per query token:
+// the tokens of the run's queries, concatenated in query order, are classified 32 at a time (each
+// lane's df / indptr / tokinfo loads in flight together) and ballots place the gathered rows
+// (query order, then token order) and query 0's dense slots — every query of a run has the same
+// dense multiset. The dense signature is put in canonical (ascending slot) order; a signature led
+// by two (three) slots with a pair (triple) row starts from that row.
+constexpr int kDescWarps = 4;
+__global__ void __launch_bounds__(kDescWarps * 32) k_run_desc(IndexView ix, const uint32_t* __restrict__ rorder,
+                                                              const uint32_t* __restrict__ run_begin,
+                                                              const uint32_t* __restrict__ n_runs,
+                                                              const uint32_t* __restrict__ perm,
+                                                              const uint64_t* __restrict__ q_off,
+                                                              const uint32_t* __restrict__ q_tok, uint32_t prune,
+                                                              RunDesc* __restrict__ rdesc) {
+  __shared__ RunDesc sd[kDescWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t i = blockIdx.x * kDescWarps + warp;
+  if (i >= *n_runs) return;
+  RunDesc& d = sd[warp];
+  const uint32_t run = rorder ? rorder[i] : i;
+  const uint32_t pb = run_begin[run];
+  const uint32_t nr = min(run_begin[run + 1] - pb, (uint32_t)RMAX);
+  const bool act = (uint32_t)lane < nr;
+  const uint32_t ql = act ? perm[pb + lane] : 0xFFFFFFFFu;
+  const uint64_t qbl = act ? q_off[ql] : 0ull;
+  const uint32_t lenl = act ? (uint32_t)(q_off[ql + 1] - qbl) : 0u;
+  const uint32_t incl = warp_incl_scan(lenl);  // lanes >= nr hold the total
+  const uint32_t excl = incl - lenl;
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t len0 = __shfl_sync(0xffffffffu, incl, 0);  // query 0 owns positions [0, len0)
+  if (lane < RMAX) d.qid[lane] = ql;
+  uint32_t e = 0, nd = 0, eb = 0;  // gathered entries / query 0's dense terms so far (uniform); entries before query `lane`
+  for (uint32_t p0 = 0; p0 < tot; p0 += 32) {
+    const uint32_t p = p0 + lane;
+    uint32_t r = 0;  // the query owning position p
+    for (uint32_t a = 0; a + 1 < nr; ++a) r += p >= __shfl_sync(0xffffffffu, incl, a) ? 1u : 0u;
+    const uint64_t qb = __shfl_sync(0xffffffffu, qbl, r);
+    const uint32_t ex = __shfl_sync(0xffffffffu, excl, r);
+    uint32_t t = 0xFFFFFFFFu;
+    if (p < tot) t = q_tok[qb + (p - ex)];
+    bool ok = p < tot && t < ix.V;
+    uint32_t dfv = 0;
+    uint64_t rb = 0, re = 0;
+    int32_t info = 0;
+    if (ok) {
+      dfv = ix.df_global[t];
+      rb = ix.indptr[t];
+      re = ix.indptr[t + 1];
+      info = ix.tokinfo[t];
+    }
+    ok = ok && dfv != 0 && rb != re;  // OOV drop (SPEC tokenizer decisions); no local postings
+    const bool isg = ok && info < 0, isd = ok && info >= 0 && p < len0;
+    const uint32_t ms = __ballot_sync(0xffffffffu, isg), md = __ballot_sync(0xffffffffu, isd);
+    if (isg) {
+      const uint32_t ee = e + __popc(ms & lanemask_lt());
+      if (ee < 32) {
+        d.row_start[ee] = rb;
+        d.row_len[ee] = (uint32_t)(re - rb);
+        d.skip[ee] = info <= -2 ? -2 - info : -1;
+        d.rmax[ee] = ix.rowmax ? ix.rowmax[t] : 0.f;
+      }
+    }
+    if (isd) {
+      const uint32_t di = nd + __popc(md & lanemask_lt());
+      if (di < (uint32_t)NDMAX) d.dslot[di] = info;
+    }
+    const uint32_t w = excl > p0 ? min(excl - p0, 32u) : 0u;  // this chunk's positions before query `lane`
+    eb += __popc(ms & (w >= 32u ? 0xffffffffu : (1u << w) - 1u));
+    e += __popc(ms);
+    nd += __popc(md);
+  }
+  if (lane <= RMAX) d.ebeg[lane] = (int32_t)min((uint32_t)lane < nr ? eb : e, 32u);
+  __syncwarp();
+  if (lane == 0) {
+    for (uint32_t a = 1; a < nd && a < (uint32_t)NDMAX; ++a) {  // canonical (ascending slot) order of the dense terms
+      const int32_t x = d.dslot[a];
+      int b = (int)a - 1;
+      while (b >= 0 && d.dslot[b] > x) {
+        d.dslot[b + 1] = d.dslot[b];
+        --b;
+      }
+      d.dslot[b + 1] = x;
+    }
+    // (a repeated token repeats its slot: equal leading slots have no pair row; block-max
+    // pruning has bounds for the plain rows only)
+    if (!prune && nd >= 3 && nd <= (uint32_t)NDMAX && (uint32_t)d.dslot[2] < ix.triple_m &&
+        d.dslot[0] < d.dslot[1] && d.dslot[1] < d.dslot[2]) {
+      d.dslot[0] = (int32_t)dense_triple_row(ix.n_dense, ix.pair_m, (uint32_t)d.dslot[0], (uint32_t)d.dslot[1],
+                                             (uint32_t)d.dslot[2]);
+      for (uint32_t a = 1; a + 2 < nd; ++a) d.dslot[a] = d.dslot[a + 2];
+      nd -= 2;
+    } else if (!prune && nd >= 2 && nd <= (uint32_t)NDMAX && (uint32_t)d.dslot[1] < ix.pair_m &&
+               d.dslot[0] < d.dslot[1]) {
+      d.dslot[0] = (int32_t)dense_pair_row(ix.n_dense, ix.pair_m, (uint32_t)d.dslot[0], (uint32_t)d.dslot[1]);
+      for (uint32_t a = 1; a + 1 < nd; ++a) d.dslot[a] = d.dslot[a + 1];
+      --nd;
+    }
+    d.nd = (int32_t)nd;
+  }
+  __syncwarp();
+  // descriptor out, 16 bytes per lane and step (entries past the run's counts are never read)
+  const uint4* src = reinterpret_cast<const uint4*>(&d);
+  uint4* dst = reinterpret_cast<uint4*>(rdesc + i);
+  for (uint32_t w = lane; w < sizeof(RunDesc) / 16; w += 32) dst[w] = src[w];
 }
 
 // top-k over an arbitrary f32 vector (SPEC top_k on its own): CTA per split of tiles,
@@ -2027,6 +2021,13 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
     SL_TRY(scr.alloc(&rorder, B));
     k_run_order<<<1, 1024, 0, st>>>(run_begin, n_runs, perm, qpost, nden, ix->N, rorder); ++t_launches;
   }
+  // every run's descriptor in work order (members, gathered-row entries, dense signature)
+  const uint32_t prune = have_bounds && env_int("SL_PRUNE", 0) ? 1u : 0u;  // opt-in
+  RunDesc* rdesc;
+  SL_TRY(scr.alloc(&rdesc, std::max<uint64_t>(B, 1)));
+  k_run_desc<<<std::max(1u, (B + kDescWarps - 1) / kDescWarps), kDescWarps * 32, 0, st>>>(
+      v, rorder, run_begin, n_runs, perm, d_off, d_tok, prune, rdesc);
+  ++t_launches;
   tr.mark("groups+runs");
   SL_CUDA_TRY(cudaGetLastError());
   RunArgs ra{};
@@ -2037,6 +2038,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   ra.run_begin = run_begin;
   ra.n_runs = n_runs;
   ra.rorder = rorder;
+  ra.rdesc = rdesc;
   ra.work = n_runs + 1;
   ra.k = k;
   ra.C = plan.C;
@@ -2046,7 +2048,7 @@ int32_t score_chunk(const sl_index* ix, StreamCache* sc, const uint64_t* d_off, 
   ra.wpc = plan.wpc;
   ra.debug_skip = (uint32_t)env_int("SL_DEBUG_SKIP", 0);
   ra.split_major = (uint32_t)env_int("SL_SPLIT_MAJOR", 1);
-  ra.prune = have_bounds && env_int("SL_PRUNE", 0) ? 1u : 0u;  // opt-in
+  ra.prune = prune;
   uint64_t* cand;
   SL_TRY(scr.alloc(&cand, (uint64_t)B * plan.n_splits * plan.C));
   ra.cand = cand;
