@@ -331,6 +331,9 @@ constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) hand
 #define SL_UNROLL 4
 #endif
 constexpr int UNROLL = SL_UNROLL;  // gather rounds whose loads are issued together
+#ifndef SL_ONE_FILTER
+#define SL_ONE_FILTER 1  // one filter instantiation (the partial last tile padded with -inf): ~25% less code
+#endif
 
 constexpr int NDMAX = 64;   // dense rows per query in the warp kernel
 
@@ -410,6 +413,9 @@ struct __align__(16) WarpSmem {
 #endif
 };
 
+
+// four resident CTAs per SM: 228 KB of shared memory per SM, 1 KB reserved per CTA
+static_assert(SL_MINB * (WPC * sizeof(WarpSmem) + 1024) <= 228 * 1024, "WarpSmem exceeds the per-SM shared memory at SL_MINB CTAs");
 
 // Add the tile slices of the query owning lanes [e0, e1) (lane = gathered-row entry, in
 // query order) to buf. Work is cut into rounds of <= 32 postings of ONE entry (doc ids are
@@ -776,6 +782,14 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // (2) dense signature of the run, ascending slot order, all loads in flight
     // register passes of DCH float4 per lane, so the tile size does not set the register
     // footprint; returns the lane max of its sums (padding docs included: an upper bound)
+    // the corpus's last tile: -inf past its last document, so the filter needs no per-document
+    // bound checks (the strict pre-test x > tau_f never passes -inf)
+    auto pad_tail = [&]() {
+      if (nvalid != (uint32_t)TILE) {
+        __syncwarp();
+        for (uint32_t i = nvalid + lane; i < (uint32_t)TILE; i += 32) s.dsum[i] = -INFINITY;
+      }
+    };
 #if SL_DENSE_ASYNC
     // The first dense row is copied global -> shared with cp.async (no registers: the whole row
     // in flight at once, one L2 round trip); later rows are added chunk by chunk in registers,
@@ -788,6 +802,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       if (nd == 0) {
 #pragma unroll
         for (int rr = 0; rr < F4L; ++rr) dsum4[lane + 32 * rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        pad_tail();
         return 0.f;
       }
 #if SL_DENSE_TMA
@@ -836,6 +851,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           m = fmaxf(m, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
         }
       }
+      pad_tail();
       return m;
     };
 #else
@@ -867,13 +883,20 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           m = fmaxf(m, fmaxf(fmaxf(a[rr].x, a[rr].y), fmaxf(a[rr].z, a[rr].w)));
         }
       }
+      pad_tail();
       return m;
     };
 #endif
-    const float dm = (ra.debug_skip & 4) ? INFINITY : dense_pass(SL_TMA_EARLY && SL_DENSE_TMA);
-    __syncwarp();
-    // (3) per query: gathered rows, then the running top-k
+    // (3) per query: gathered rows, then the running top-k. The dense pass has ONE inlined site:
+    // before member 0, and again before a member whose predecessor's gather outgrew the undo log
+    float dm = INFINITY;
+    bool redo = true;
     for (uint32_t r = 0; r < nr; ++r) {
+      if (redo) {
+        if (!(ra.debug_skip & 4)) dm = dense_pass(r == 0 && SL_TMA_EARLY && SL_DENSE_TMA);
+        __syncwarp();
+        redo = false;
+      }
       if (PRUNE && !((live >> r) & 1u)) continue;
       const uint32_t emask = s.emask[r];
       float* buf = s.dsum;
@@ -906,10 +929,16 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
       } else {
         uint64_t* kept = s.keptp[r];
         if (!(ra.debug_skip & 2)) {
+          // one instantiation: the corpus's last, partial tile holds -inf past its documents
+          // (dense_pass), which the strict pre-test never passes
+#if SL_ONE_FILTER
+          filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
+#else
           if (nvalid == TILE)
             filter_tile<true>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
           else
             filter_tile<false>(s, r, ra.k, ra.C, ix.doc_base + d0, nvalid, buf, kept, gp, lmax, gv);
+#endif
         }
       }
 #if SL_RMAX_CT > 1
@@ -921,9 +950,7 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
           __syncwarp();
         }
       } else if (undo == 2) {
-        __syncwarp();
-        dense_pass(false);
-        __syncwarp();
+        redo = true;  // recomputed at the top of the next member's iteration
       }
 #endif
     }
@@ -1824,6 +1851,7 @@ int32_t plan_runs(const sl_index* ix, uint32_t B, uint32_t k, uint32_t qmax, Run
   }
   SL_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score_runs<GM_TOPK, false>, NT, p->smem));
   p->per_sm = (uint32_t)std::max(1, per_sm);
+  if (env_int("SL_PLAN_TRACE", 0)) fprintf(stderr, "[plan] k_score_runs: %d CTAs/SM, %zu B shared per CTA\n", per_sm, p->smem);
   const uint64_t warps = (uint64_t)std::max(1, per_sm) * p->wpc * num_sms(ix->device);
   const uint64_t items = std::max<uint64_t>(1, (uint64_t)B / std::max(1u, p->R / 2 + 1));  // expected runs
   uint32_t ns = (uint32_t)env_int("SL_SPLITS", 0);
