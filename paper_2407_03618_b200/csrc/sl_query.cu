@@ -331,6 +331,12 @@ constexpr int RMAX = SL_RMAX_CT;  // queries per run (same dense signature) hand
 #define SL_UNROLL 4
 #endif
 constexpr int UNROLL = SL_UNROLL;  // gather rounds whose loads are issued together
+#ifndef SL_PIN_IDS
+#define SL_PIN_IDS 3  // lane / warp ids held in registers (bit 0: lane, bit 1: warp); 3: +1.7% at c2, lane alone -4.5%
+#endif
+#ifndef SL_PROXY_FENCE
+#define SL_PROXY_FENCE 1  // fence.proxy.async before the first dense row's bulk copy overwrites the warp's dense sum (0: +0.5%, not taken: the generic writes of the previous tile must be ordered before the async-proxy write)
+#endif
 #ifndef SL_ONE_FILTER
 #define SL_ONE_FILTER 1  // one filter instantiation (the partial last tile padded with -inf): ~25% less code
 #endif
@@ -619,7 +625,19 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
 #else
   __shared__ WarpSmem wsm[WPC];
 #endif
+#if SL_PIN_IDS
+  // lane / warp as opaque register values: otherwise they are rematerialised from S2R tid at
+  // every use (~6% of the kernel's instructions, with the S2R latency exposed)
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if SL_PIN_IDS & 1
+  asm volatile("" : "+r"(lane));
+#endif
+#if SL_PIN_IDS & 2
+  asm volatile("" : "+r"(warp));
+#endif
+#else
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#endif
   const uint32_t n_runs = *ra.n_runs;
   const uint32_t total = n_runs * ra.n_splits;
   WarpSmem& s = wsm[warp];
@@ -707,7 +725,9 @@ __global__ void __launch_bounds__(NT, SL_MINB) k_score_runs(IndexView ix, RunArg
     // the whole 4 KB first-row tile by one bulk copy: order this warp's earlier generic accesses
     // to the buffer before the async-proxy write, then lane 0 arms the barrier and starts the copy
     auto issue_first_row = [&]() {
+#if SL_PROXY_FENCE
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
       __syncwarp();
       if (lane == 0) bulk_copy_g2s(s.dsum, ix.dense + (uint64_t)s.dslot[0] * ix.n_pad + d0, TILE * 4u, s.mbar);
     };
