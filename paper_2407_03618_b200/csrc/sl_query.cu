@@ -322,7 +322,10 @@ __device__ __forceinline__ float f4c(const float4& v, int c) {
 
 enum GroupMode { GM_TOPK = 0, GM_DENSE = 1 };
 
-constexpr int ULOG = 8;  // undo-log capacity in gather slots
+#ifndef SL_ULOG
+#define SL_ULOG 8
+#endif
+constexpr int ULOG = SL_ULOG;  // undo-log capacity in gather slots
 #ifndef SL_RMAX_CT
 #define SL_RMAX_CT 4  // up to four queries of one dense signature per warp item (all but the last via the undo log)
 #endif
